@@ -1,0 +1,282 @@
+// st_api.cu -- the C-ABI (include/sinkattn.h): argument checks, workspace
+// carving and the stream-ordered orchestration of the sm_100a kernels.
+//
+// Orchestration of st_forward (run_surrogate, sinkhorn.hpp:288-302):
+//   scores -> for t = 1..T+R: u half-step, v half-step -> O = P V -> gauges
+// The duals run raw (uncentered); the ledger gauge mean_valid(u_raw) is
+// recorded for the three tail steps, so the reference's centered trace is
+// u_c = u_raw - C, v_c = v_raw + C (gauge equivariance, test_sinkhorn.cpp:269-304)
+// and every output/gradient is gauge invariant (test_adjoint.cpp:355-376).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sinkattn.h"
+#include "st_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+st_status fail(st_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Dims {
+    long BH, Lq, Lk, Lrq, Lrk, d, w, Wf;
+};
+
+st_status check_desc(const st_desc* d, Dims& o) {
+    if (d == nullptr) return fail(ST_INVALID_ARGUMENT, "null descriptor");
+    if (d->batch < 1 || d->heads < 1 || d->seq_q < 1 || d->seq_k < 1 || d->head_dim < 1)
+        return fail(ST_INVALID_ARGUMENT, "support dimensions must be >= 1");
+    if (d->half_band < 0) return fail(ST_INVALID_ARGUMENT, "half band width must be >= 0");
+    if (!(d->epsilon > 0.0) || !std::isfinite(d->epsilon)) return fail(ST_INVALID_TEMPERATURE, "epsilon must be > 0");
+    if (d->base_depth < 0 || d->tail_depth < 0) return fail(ST_INVALID_ARGUMENT, "depths must be >= 0");
+    if (d->dtype != ST_F32 && d->dtype != ST_BF16) return fail(ST_INVALID_ARGUMENT, "dtype must be ST_F32 or ST_BF16");
+    if (d->dustbin != 0 && d->dustbin != 1) return fail(ST_INVALID_ARGUMENT, "dustbin must be 0 or 1");
+    if (d->head_dim > 128) return fail(ST_NOT_SUPPORTED, "head_dim > 128 is not implemented");
+    o.BH = d->batch * d->heads;
+    o.Lq = d->seq_q;
+    o.Lk = d->seq_k;
+    o.Lrq = d->seq_q + d->dustbin;
+    o.Lrk = d->seq_k + d->dustbin;
+    o.d = d->head_dim;
+    o.w = std::min<long>(d->half_band, std::max(d->seq_q, d->seq_k));  // wider bands change nothing
+    o.Wf = 2 * o.w + 1;
+    if ((double)o.BH * o.Lq * o.Wf > 4.0e9 || o.Lrq > (1L << 30) || o.Lrk > (1L << 30))
+        return fail(ST_SIZE_CAP_EXCEEDED, "problem exceeds the 32-bit index space of the kernels");
+    return ST_OK;
+}
+
+st::Geo make_geo(const st_desc* d, const Dims& m, const uint8_t* rm, const uint8_t* cm) {
+    st::Geo g;
+    g.BH = (int)m.BH;
+    g.H = (int)d->heads;
+    g.Lq = (int)m.Lq;
+    g.Lk = (int)m.Lk;
+    g.Lrq = (int)m.Lrq;
+    g.Lrk = (int)m.Lrk;
+    g.d = (int)m.d;
+    g.w = (int)m.w;
+    g.Wf = (int)m.Wf;
+    g.dustbin = d->dustbin;
+    g.eps = (float)d->epsilon;
+    g.c2 = (float)(1.4426950408889634 / (std::sqrt((double)m.d) * d->epsilon));
+    g.inv_qk = (float)(1.0 / (std::sqrt((double)m.d) * d->epsilon));
+    g.sd2 = (float)(-d->dustbin_cost * 1.4426950408889634 / d->epsilon);
+    g.row_mask = rm;
+    g.col_mask = cm;
+    return g;
+}
+
+// saved-state layout (fp32, base-2 raw duals): u[3][BH][Lrq] | v[3][BH][Lrk] | gauge[3][BH] | status int
+struct SavedLayout {
+    size_t u, v, gauge, status, bytes;
+};
+SavedLayout saved_layout(const Dims& m) {
+    SavedLayout s;
+    s.u = 0;
+    s.v = align_up(s.u + sizeof(float) * 3 * m.BH * m.Lrq);
+    s.gauge = align_up(s.v + sizeof(float) * 3 * m.BH * m.Lrk);
+    s.status = align_up(s.gauge + sizeof(float) * 3 * m.BH);
+    s.bytes = align_up(s.status + sizeof(int));
+    return s;
+}
+
+struct WsLayout {
+    size_t S2, u, v, g_u, u2b, u1b, deps, g_v, v1b, v0b, err, bytes;
+};
+WsLayout ws_layout(const Dims& m) {
+    WsLayout w;
+    size_t o = 0;
+    auto take = [&](size_t n) {
+        const size_t at = o;
+        o = align_up(o + n);
+        return at;
+    };
+    const size_t rq = sizeof(float) * m.BH * m.Lrq, rk = sizeof(float) * m.BH * m.Lrk;
+    w.S2 = take(sizeof(float) * (size_t)m.BH * m.Lq * m.Wf);
+    w.u = take(rq);
+    w.v = take(rk);
+    w.g_u = take(rq);
+    w.u2b = take(rq);
+    w.u1b = take(rq);
+    w.deps = take(rq);
+    w.g_v = take(rk);
+    w.v1b = take(rk);
+    w.v0b = take(rk);
+    w.err = take(sizeof(int));
+    w.bytes = o;
+    return w;
+}
+
+#define ST_CUDA(call)                                                                  \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess) return fail(ST_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+}  // namespace
+
+extern "C" {
+
+const char* st_last_error(void) { return g_err.c_str(); }
+
+int64_t st_launch_count(int32_t reset) { return (int64_t)st::launch_count(reset != 0); }
+
+size_t st_saved_bytes(const st_desc* desc) {
+    Dims m;
+    if (check_desc(desc, m) != ST_OK) return 0;
+    return saved_layout(m).bytes;
+}
+
+size_t st_workspace_bytes(const st_desc* desc) {
+    Dims m;
+    if (check_desc(desc, m) != ST_OK) return 0;
+    return ws_layout(m).bytes;
+}
+
+st_status st_forward(const st_desc* desc, const void* Q, const void* K, const void* V, const uint8_t* row_mask,
+                     const uint8_t* col_mask, float* O, void* saved, void* workspace, size_t workspace_bytes,
+                     void* stream) {
+    Dims m;
+    st_status s = check_desc(desc, m);
+    if (s != ST_OK) return s;
+    if (!Q || !K || !V || !O) return fail(ST_INVALID_ARGUMENT, "null tensor pointer");
+    const WsLayout wl = ws_layout(m);
+    if (workspace == nullptr || workspace_bytes < wl.bytes)
+        return fail(ST_WORKSPACE_TOO_SMALL, "workspace smaller than st_workspace_bytes()");
+    cudaStream_t st = (cudaStream_t)stream;
+    char* ws = (char*)workspace;
+    const st::Geo g = make_geo(desc, m, row_mask, col_mask);
+    float* S2 = (float*)(ws + wl.S2);
+    float* u_ws = (float*)(ws + wl.u);
+    float* v_ws = (float*)(ws + wl.v);
+    int* err = (int*)(ws + wl.err);
+
+    const SavedLayout sl = saved_layout(m);
+    char* sv = (char*)saved;
+    float* su = sv ? (float*)(sv + sl.u) : nullptr;
+    float* svv = sv ? (float*)(sv + sl.v) : nullptr;
+    if (sv) err = (int*)(sv + sl.status);  // the status word travels with the saved state
+    ST_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+    ST_CUDA(cudaMemsetAsync(u_ws, 0, sizeof(float) * m.BH * m.Lrq, st));
+    ST_CUDA(cudaMemsetAsync(v_ws, 0, sizeof(float) * m.BH * m.Lrk, st));
+    ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));
+
+    const long T = desc->base_depth, R = desc->tail_depth;
+    auto slot_u = [&](long r) { return su + (size_t)r * m.BH * m.Lrq; };
+    auto slot_v = [&](long r) { return svv + (size_t)r * m.BH * m.Lrk; };
+    const float* u_prev = u_ws;
+    const float* v_prev = v_ws;
+    if (sv && T == 0) {  // the stopped pair is the cold start
+        ST_CUDA(cudaMemsetAsync(slot_u(0), 0, sizeof(float) * m.BH * m.Lrq, st));
+        ST_CUDA(cudaMemsetAsync(slot_v(0), 0, sizeof(float) * m.BH * m.Lrk, st));
+    }
+    for (long t = 1; t <= T + R; ++t) {
+        const long r = t - T;
+        float* u_out = (sv && r >= 0 && r <= 2) ? slot_u(r) : u_ws;
+        float* v_out = (sv && r >= 0 && r <= 2) ? slot_v(r) : v_ws;
+        ST_CUDA(st::launch_row_step(g, t == 1, S2, v_prev, u_prev, u_out, err, st));
+        ST_CUDA(st::launch_col_step(g, t == 1, S2, u_out, v_prev, v_out, err, st));
+        u_prev = u_out;
+        v_prev = v_out;
+    }
+    ST_CUDA(st::launch_output(g, desc->dtype, S2, u_prev, v_prev, V, O, st));
+    if (sv) {
+        const int nslots = (int)std::min<long>(R, 2) + 1;
+        ST_CUDA(st::launch_gauges(g, su, nslots, (float*)(sv + sl.gauge), st));
+    }
+    return ST_OK;
+}
+
+st_status st_backward(const st_desc* desc, const void* saved, const void* Q, const void* K, const void* V,
+                      const void* dO, const uint8_t* row_mask, const uint8_t* col_mask, float* dQ, float* dK,
+                      float* dV, float* d_eps, float* eta_v, int32_t mode, void* workspace, size_t workspace_bytes,
+                      void* stream) {
+    Dims m;
+    st_status s = check_desc(desc, m);
+    if (s != ST_OK) return s;
+    if (desc->tail_depth != 2) return fail(ST_UNSUPPORTED_DEPTH, "r2_backward requires a tail of depth 2");
+    if (saved == nullptr) return fail(ST_MISSING_BASE_TRACE, "backward needs the forward's saved state");
+    if (!Q || !K || !V || !dO || !dQ || !dK || !dV) return fail(ST_INVALID_ARGUMENT, "null tensor pointer");
+    if (mode != ST_ONE_REFERENCE && mode != ST_DIRECT_FOUR_PLAN) return fail(ST_INVALID_ARGUMENT, "unknown mode");
+    const WsLayout wl = ws_layout(m);
+    if (workspace == nullptr || workspace_bytes < wl.bytes)
+        return fail(ST_WORKSPACE_TOO_SMALL, "workspace smaller than st_workspace_bytes()");
+    cudaStream_t st = (cudaStream_t)stream;
+    char* ws = (char*)workspace;
+    const st::Geo g = make_geo(desc, m, row_mask, col_mask);
+    const SavedLayout sl = saved_layout(m);
+    const float* su = (const float*)((const char*)saved + sl.u);
+    const float* svv = (const float*)((const char*)saved + sl.v);
+    st::BwdPtrs p;
+    p.S2 = (float*)(ws + wl.S2);
+    p.u1 = su + (size_t)1 * m.BH * m.Lrq;
+    p.u2 = su + (size_t)2 * m.BH * m.Lrq;
+    p.v0 = svv;
+    p.v1 = svv + (size_t)1 * m.BH * m.Lrk;
+    p.v2 = svv + (size_t)2 * m.BH * m.Lrk;
+    p.g_u = (float*)(ws + wl.g_u);
+    p.u2b = (float*)(ws + wl.u2b);
+    p.u1b = (float*)(ws + wl.u1b);
+    p.deps_part = (float*)(ws + wl.deps);
+    p.g_v = (float*)(ws + wl.g_v);
+    p.v1b = (float*)(ws + wl.v1b);
+    p.v0b = eta_v ? eta_v : (float*)(ws + wl.v0b);
+    p.Q = Q;
+    p.K = K;
+    p.V = V;
+    p.dO = dO;
+    p.dQ = dQ;
+    p.dK = dK;
+    p.dV = dV;
+    ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, (float*)p.S2, st));
+    ST_CUDA(st::launch_backward(g, desc->dtype, p, mode == ST_DIRECT_FOUR_PLAN, st));
+    if (d_eps) ST_CUDA(st::launch_deps_reduce(g, p.deps_part, d_eps, st));
+    return ST_OK;
+}
+
+st_status st_saved_duals(const st_desc* desc, const void* saved, const uint8_t* row_mask_host,
+                         const uint8_t* col_mask_host, double* u, double* v, double* gauge, void* stream) {
+    Dims m;
+    st_status s = check_desc(desc, m);
+    if (s != ST_OK) return s;
+    if (saved == nullptr) return fail(ST_MISSING_BASE_TRACE, "null saved state");
+    const SavedLayout sl = saved_layout(m);
+    std::vector<char> h(sl.bytes);
+    ST_CUDA(cudaMemcpyAsync(h.data(), saved, sl.bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    ST_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    const float* hu = (const float*)(h.data() + sl.u);
+    const float* hv = (const float*)(h.data() + sl.v);
+    const float* hg = (const float*)(h.data() + sl.gauge);
+    const int status = *(const int*)(h.data() + sl.status);
+    const double ln2 = 0.6931471805599453;
+    const long H = desc->heads;
+    for (int r = 0; r < 3; ++r)
+        for (long bh = 0; bh < m.BH; ++bh) {
+            const long b = bh / H;
+            const double C = desc->centered ? (double)hg[r * m.BH + bh] * ln2 : 0.0;
+            if (gauge) gauge[r * m.BH + bh] = (double)hg[r * m.BH + bh] * ln2;
+            for (long i = 0; i < m.Lrq; ++i) {
+                const bool on = i >= m.Lq || !row_mask_host || row_mask_host[b * m.Lq + i];
+                const size_t k = ((size_t)r * m.BH + bh) * m.Lrq + i;
+                if (u) u[k] = on ? (double)hu[k] * ln2 - C : 0.0;
+            }
+            for (long j = 0; j < m.Lrk; ++j) {
+                const bool on = j >= m.Lk || !col_mask_host || col_mask_host[b * m.Lk + j];
+                const size_t k = ((size_t)r * m.BH + bh) * m.Lrk + j;
+                if (v) v[k] = on ? (double)hv[k] * ln2 + C : 0.0;
+            }
+        }
+    if (status != 0) return fail(ST_INFEASIBLE_SUPPORT, "an active row or column had an empty reduction");
+    return ST_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+"""ctypes access to the CPU oracle (oracle/build/libstoc.so) -- the checker.
+
+TEST INFRASTRUCTURE: imported only by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs.  Never by the product.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_DIR = os.path.join(ROOT, "oracle")
+LIB = os.path.join(ORACLE_DIR, "build", "libstoc.so")
+KAT = os.path.join(ORACLE_DIR, "build", "kat_tests")
+
+
+def build() -> None:
+    subprocess.run(["make", "-s", "-C", ORACLE_DIR], check=True)
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            build()
+        L = ctypes.CDLL(LIB)
+        D = ctypes.POINTER(ctypes.c_double)
+        U8 = ctypes.c_void_p
+        I64 = ctypes.c_int64
+        L.stoc_run_batch.argtypes = [I64, I64, I64, I64, I64, I64, I64, ctypes.c_double, ctypes.c_int,
+                                     ctypes.c_double, D, D, D, D, U8, U8, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int, I64, I64, D, D, D, D, D, D, D, D]
+        L.stoc_run_batch.restype = ctypes.c_int
+        L.stoc_normal_fill.argtypes = [ctypes.c_uint64, ctypes.c_char_p, ctypes.c_uint64, I64, ctypes.c_double, D]
+        L.stoc_normal_fill.restype = None
+        L.stoc_last_error.restype = ctypes.c_char_p
+        L.stoc_banded_entry_count.argtypes = [I64, I64]
+        L.stoc_banded_entry_count.restype = I64
+        _lib = L
+    return _lib
+
+
+def normal_fill(seed, tag, start, n, scale=1.0):
+    out = np.empty(n, dtype=np.float64)
+    lib().stoc_normal_fill(seed, tag.encode(), start, n, scale, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    return out
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"oracle status {code}: {msg}")
+        self.code = code
+
+
+def run(cfg, Q, K, V, G, row_mask=None, col_mask=None, *, heads=None, precision=64, mode=0, backward=True,
+        threads=None, tile_block=128, centered=True):
+    """Reference path per head: run_surrogate + r2_backward (inc/validation.hpp:102-114).
+
+    Q, K, V, G: [nh, L', d] arrays of the heads `heads` (global b*H+h indices,
+    default 0..nh-1; any float dtype, upcast exactly to double).
+    row_mask/col_mask: [B, L] uint8 of the whole batch.  Returns float64 arrays.
+    """
+    Q, K, V, G = (np.ascontiguousarray(x, dtype=np.float64) for x in (Q, K, V, G))
+    nh, Lr, d = Q.shape
+    heads = range(nh) if heads is None else heads
+    Lreal = cfg.L
+    # one pseudo-example per head so that any head subset maps onto its own mask row
+    Hh, Bb = 1, nh
+    sel = np.array([h // cfg.H for h in heads], dtype=np.int64)
+    if row_mask is not None:
+        row_mask = np.asarray(row_mask)[sel]
+    if col_mask is not None:
+        col_mask = np.asarray(col_mask)[sel]
+    out = {k: np.zeros_like(Q) for k in ("O", "dQ", "dK", "dV")}
+    out["d_eps"] = np.zeros(nh)
+    out["eta_v"] = np.zeros((nh, Lr))
+    out["duals"] = np.zeros((nh, 6, Lr))
+    out["gauges"] = np.zeros((nh, 3))
+    P = ctypes.POINTER(ctypes.c_double)
+    p = lambda a: a.ctypes.data_as(P)
+    rm = None if row_mask is None else np.ascontiguousarray(row_mask, dtype=np.uint8)
+    cm = None if col_mask is None else np.ascontiguousarray(col_mask, dtype=np.uint8)
+    code = lib().stoc_run_batch(
+        Bb, Hh, Lreal, d, cfg.w, cfg.T, cfg.R, cfg.eps, cfg.dustbin, cfg.dustbin_cost,
+        p(Q), p(K), p(V), p(G), None if rm is None else rm.ctypes.data, None if cm is None else cm.ctypes.data,
+        precision, mode, tile_block, 1 if centered else 0, threads or os.cpu_count() or 1, 0, nh,
+        p(out["O"]), p(out["dQ"]) if backward else None, p(out["dK"]), p(out["dV"]), p(out["d_eps"]),
+        p(out["eta_v"]), p(out["duals"]), p(out["gauges"]))
+    if code != 0:
+        raise OracleError(code, lib().stoc_last_error().decode())
+    return out

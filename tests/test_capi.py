@@ -1,0 +1,119 @@
+"""CPU-side checks of the C-ABI library: loads, exports every declared symbol,
+bit-exact RNG against the oracle, host validation and error contract (no kernels run)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle_ref
+from paper_2605_08123_b200 import _lib, band, configs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "sinkattn.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(st_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    syms = declared_symbols()
+    assert len(syms) >= 10
+    for s in syms:
+        assert hasattr(_lib.lib, s), s
+    assert set(syms) == set(_lib.EXPORTED)
+
+
+def test_library_is_sm100a():
+    out = os.popen(f"cuobjdump --list-elf {_lib.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out, out
+
+
+@pytest.mark.parametrize("tag,start,n,scale", [("Q", 0, 1000, 1.0), ("G", 123456789, 777, 0.5), ("dustbin_v", 5, 64, 1.0)])
+def test_rng_bit_exact_with_reference_generator(tag, start, n, scale):
+    a = configs.normal_fill(7, tag, start, n, scale)
+    b = oracle_ref.normal_fill(7, tag, start, n, scale)
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def test_rng_flat_index_identity():
+    # test_io.cpp:68-81: entry (i, j) of a wider draw equals the same flat index
+    a = configs.normal_fill(5, "Q", 0, 32).reshape(8, 4)
+    wide = configs.normal_fill(5, "Q", 0, 32).reshape(4, 8)
+    assert wide[0, 5] == a[1, 1]
+
+
+def _spec(**kw):
+    base = dict(batch=1, heads=1, seq_q=8, seq_k=8, head_dim=4, half_band=1, base_depth=3, tail_depth=2,
+                epsilon=1.0)
+    base.update(kw)
+    return band.BandSpec(**base)
+
+
+def test_validate_support_matches_reference_cases():
+    # test_support.cpp:72-79
+    band.validate_support(_spec(seq_q=3, seq_k=3, half_band=0), None, None)
+    with pytest.raises(band.InfeasibleSupport):
+        band.validate_support(_spec(seq_q=3, seq_k=3, half_band=0), None, np.array([[0, 1, 1]], np.uint8))
+    with pytest.raises(band.InfeasibleSupport):
+        band.validate_support(_spec(seq_q=3, seq_k=3, half_band=0), np.array([[1, 1, 0]], np.uint8), None)
+    # rectangular: half band 2 leaves far columns unreachable (test_support.cpp:47-54)
+    with pytest.raises(band.InfeasibleSupport):
+        band.validate_support(_spec(seq_q=4, seq_k=7, half_band=2), None, None)
+    band.validate_support(_spec(seq_q=4, seq_k=7, half_band=3), None, None)
+    # the dustbin spoke makes every active row/col feasible
+    band.validate_support(_spec(seq_q=3, seq_k=3, half_band=0, dustbin=1), None, np.array([[0, 1, 1]], np.uint8))
+
+
+def _status(fn, *args):
+    return fn(*args)
+
+
+def test_error_contract_without_gpu():
+    lib = _lib.lib
+    d = _spec(epsilon=0.0).desc()
+    assert lib.st_forward(ctypes.byref(d), 1, 1, 1, None, None, 1, None, None, 0, None) == _lib.ST_INVALID_TEMPERATURE
+    d = _spec(tail_depth=1).desc()
+    assert lib.st_backward(ctypes.byref(d), 1, 1, 1, 1, 1, None, None, 1, 1, 1, None, None, 0, None, 0,
+                           None) == _lib.ST_UNSUPPORTED_DEPTH
+    d = _spec().desc()
+    assert lib.st_backward(ctypes.byref(d), None, 1, 1, 1, 1, None, None, 1, 1, 1, None, None, 0, None, 0,
+                           None) == _lib.ST_MISSING_BASE_TRACE
+    assert lib.st_forward(ctypes.byref(d), 1, 1, 1, None, None, 1, None, None, 0, None) == _lib.ST_WORKSPACE_TOO_SMALL
+    d = _spec(head_dim=256).desc()
+    assert lib.st_forward(ctypes.byref(d), 1, 1, 1, None, None, 1, None, None, 0, None) == _lib.ST_NOT_SUPPORTED
+    d = _spec(seq_q=0).desc()
+    assert lib.st_workspace_bytes(ctypes.byref(d)) == 0
+    assert b"dimensions" in lib.st_last_error() or lib.st_last_error() != b""
+
+
+def test_saved_state_is_O_of_L():
+    s = _spec(batch=8, heads=4, seq_q=2048, seq_k=2048, head_dim=64, half_band=64)
+    # 6 vectors of L per head + gauges: never the L x W plan
+    assert s.saved_bytes() < 8 * 4 * (6 * 2048 * 4 + 4096)
+    assert s.workspace_bytes() >= 8 * 4 * 2048 * 129 * 4
+
+
+def test_config_table_matches_baseline():
+    c = configs.CONFIGS
+    assert (c[1].B, c[1].H, c[1].L, c[1].d, c[1].Wf, c[1].eps, c[1].T, c[1].R) == (1, 1, 256, 32, 33, 0.1, 20, 2)
+    assert (c[2].B, c[2].H, c[2].L, c[2].d, c[2].Wf, c[2].eps, c[2].T) == (8, 4, 2048, 64, 129, 0.05, 50)
+    assert (c[3].B, c[3].H, c[3].L, c[3].d, c[3].Wf, c[3].eps, c[3].T, c[3].dustbin) == (16, 8, 1024, 64, 65, 0.1, 30, 1)
+    assert (c[4].B, c[4].H, c[4].L, c[4].d, c[4].Wf, c[4].eps, c[4].T, c[4].dtype) == (4, 8, 32768, 128, 257, 0.05, 100, "bf16")
+    assert (c[5].B, c[5].H, c[5].L, c[5].d, c[5].Wf, c[5].eps, c[5].T, c[5].dtype) == (1, 16, 131072, 64, 513, 0.05, 50, "bf16")
+    ls = configs.lengths(c[2])
+    assert ls.min() >= 1024 and ls.max() <= 2048
+    l3 = configs.lengths(c[3])
+    assert l3.min() >= 64 and l3.max() <= 1024
+
+
+def test_bf16_rounding_is_rne():
+    x = np.array([1.0, 1.00390625, 1.005859375, -2.0000001, 3.14159265], dtype=np.float64)
+    bits = configs.to_bf16_bits(x)
+    back = configs.bf16_bits_to_f32(bits)
+    assert back[0] == 1.0 and back[1] == 1.0  # tie to even
+    assert back[2] == 1.0078125
+    assert abs(back[4] - 3.140625) < 1e-7

@@ -1,0 +1,32 @@
+"""Quick per-config timing of the CUDA path (development helper, not the bench)."""
+import sys, time
+import numpy as np, torch
+sys.path.insert(0, '.')
+from paper_2605_08123_b200 import band, configs
+
+def bench(cid, iters=3, L=None):
+    cfg = configs.CONFIGS[cid]
+    if L: cfg = cfg.replace(L=L)
+    inp = configs.make_inputs(cfg)
+    spec = band.BandSpec(batch=cfg.B, heads=cfg.H, seq_q=cfg.L, seq_k=cfg.L, head_dim=cfg.d, half_band=cfg.w,
+                         base_depth=cfg.T, tail_depth=cfg.R, epsilon=cfg.eps, dtype=cfg.dtype, dustbin=cfg.dustbin)
+    shp = (cfg.B, cfg.H, cfg.rows, cfg.d)
+    b = inp.bits or {}
+    dev = lambda x, k: (torch.from_numpy(b[k].astype(np.int16)).view(torch.bfloat16) if k in b else torch.from_numpy(x)).cuda().reshape(shp)
+    Q, K, V, G = dev(inp.Q, 'Q'), dev(inp.K, 'K'), dev(inp.V, 'V'), dev(inp.G, 'G')
+    rm = None if inp.row_mask is None else torch.from_numpy(inp.row_mask).cuda()
+    run = band.run_surrogate(Q, K, V, spec, rm, rm)
+    band.r2_backward(run, G)
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    tf, tb = [], []
+    for _ in range(iters):
+        e[0].record(); run = band.run_surrogate(Q, K, V, spec, rm, rm, validate=False, saved=run.saved, out=run.output)
+        e[1].record(); band.r2_backward(run, G); e[2].record(); torch.cuda.synchronize()
+        tf.append(e[0].elapsed_time(e[1])); tb.append(e[1].elapsed_time(e[2]))
+    cells = cfg.nominal_cell_steps()
+    t = min(tf) + min(tb)
+    print(f"config {cid} L={cfg.L}: fwd {min(tf):.3f} ms bwd {min(tb):.3f} ms -> {cells/(t*1e-3):.3e} band-cells/s", flush=True)
+
+for cid in [int(x) for x in sys.argv[1:]]:
+    bench(cid)
