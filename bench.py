@@ -85,7 +85,7 @@ def run_reference(args, cfg):
         "cpu_baseline": {"value": v, "unit": "band-cells/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "band-cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line, default=lambda o: o.item() if hasattr(o, "item") else str(o)), flush=True)
     return 0
 
 
@@ -361,7 +361,7 @@ def main():
             "gpu_launches": int(launches_per_step * args.steps), "clocks": clk.summary(),
             "ms_per_step_all": [round(x, 4) for x in ts],
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line, default=lambda o: o.item() if hasattr(o, "item") else str(o)), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -197,4 +197,4 @@ def active_cells(cfg: Config, seed: int = 0) -> int:
         band = l * (2 * w + 1) - w * (w + 1)
         spokes = (2 * l + 1) if cfg.dustbin else 0
         tot += (band + spokes) * cfg.H
-    return tot
+    return int(tot)
