@@ -71,8 +71,10 @@ typedef struct st_desc {
     int32_t dustbin;      /* 0, or 1 = one active dustbin token per side on the spoke support */
     double dustbin_cost;  /* constant cost on every dustbin edge (score = -cost / epsilon) */
     int32_t centered;     /* 1 = reference default: report the centered gauge ledger in saved */
-    int32_t reserved;
+    int32_t flags;        /* 0 = auto; ST_FLAG_GENERIC forces the generic (non-tensor-core) kernels */
 } st_desc;
+
+#define ST_FLAG_GENERIC 1
 
 /* Device bytes of the opaque saved state written by st_forward and read by
  * st_backward: fp32 tail duals u, v at steps T, T+1, T+2 plus the per-head

@@ -26,6 +26,7 @@ ST_NOT_SUPPORTED = 9
 
 ST_F32 = 0
 ST_BF16 = 1
+ST_FLAG_GENERIC = 1
 ST_ONE_REFERENCE = 0
 ST_DIRECT_FOUR_PLAN = 1
 
@@ -42,7 +43,7 @@ class StDesc(ctypes.Structure):
         ("seq_k", ctypes.c_int64), ("head_dim", ctypes.c_int64), ("half_band", ctypes.c_int64),
         ("base_depth", ctypes.c_int64), ("tail_depth", ctypes.c_int64), ("epsilon", ctypes.c_double),
         ("dtype", ctypes.c_int32), ("dustbin", ctypes.c_int32), ("dustbin_cost", ctypes.c_double),
-        ("centered", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("centered", ctypes.c_int32), ("flags", ctypes.c_int32),
     ]
 
 

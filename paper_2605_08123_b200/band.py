@@ -89,12 +89,14 @@ class BandSpec:
     dustbin: int = 0
     dustbin_cost: float = 1.0
     centered: bool = True
+    generic: bool = False       # force the generic (non-tensor-core) kernels (testing / ablation)
 
     def desc(self) -> _lib.StDesc:
         return _lib.StDesc(self.batch, self.heads, self.seq_q, self.seq_k, self.head_dim, self.half_band,
                            self.base_depth, self.tail_depth, float(self.epsilon),
                            _lib.ST_BF16 if self.dtype == "bf16" else _lib.ST_F32, int(self.dustbin),
-                           float(self.dustbin_cost), int(bool(self.centered)), 0)
+                           float(self.dustbin_cost), int(bool(self.centered)),
+                           _lib.ST_FLAG_GENERIC if self.generic else 0)
 
     @property
     def rows(self) -> int:

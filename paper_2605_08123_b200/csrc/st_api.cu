@@ -9,12 +9,14 @@
 // and every output/gradient is gauge invariant (test_adjoint.cpp:355-376).
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/sinkattn.h"
 #include "st_kernels.cuh"
+#include "st_phase.cuh"
 
 namespace {
 
@@ -89,10 +91,58 @@ SavedLayout saved_layout(const Dims& m) {
     return s;
 }
 
-struct WsLayout {
-    size_t S2, u, v, g_u, u2b, u1b, deps, g_v, v1b, v0b, err, bytes;
+// Tensor-core (tcgen05) forward plan: eligibility and SMEM geometry of k_phase.
+struct TcPlan {
+    bool ok = false;
+    int npl, CR, shift, NA, NSK, row_bytes, maxwin, Lpq, Lpk, NBq, NBk;
+    size_t smem;
 };
-WsLayout ws_layout(const Dims& m) {
+TcPlan tc_plan(const st_desc* d, const Dims& m) {
+    TcPlan p;
+    if (d->flags & ST_FLAG_GENERIC) return p;
+    if (m.d % 16 != 0 || m.d > 128) return p;  // MMA-K slices of 16 bf16
+    // fp32 inputs stay on the stored-score path: the tensor core's fp32 accumulation of
+    // large dot products (config 3: |s2| ~ 115) drifts ~1e-4 from the exact scores, which
+    // breaks the 1e-5 parity bound (the 3-plane split below is kept for ST_TC_FP32=1 studies).
+    if (d->dtype != ST_BF16 && !getenv("ST_TC_FP32")) return p;
+    p.npl = d->dtype == ST_BF16 ? 1 : 3;        // fp32 -> bf16 hi/mid/lo planes
+    p.row_bytes = (int)m.d * 2;
+    p.CR = m.w >= 64 ? 128 : 64;
+    p.shift = (int)(m.w % p.CR);
+    if (p.shift % 8 != 0) return p;             // packed 8-row core-matrix groups
+    p.NBq = (int)((m.Lq + 127) / 128);
+    p.NBk = (int)((m.Lk + 127) / 128);
+    p.Lpq = (p.NBq + (p.shift ? 1 : 0)) * 128;
+    p.Lpk = (p.NBk + (p.shift ? 1 : 0)) * 128;
+    const int nchunk = (int)((128 + 2 * m.w + p.CR - 1) / p.CR);  // window chunks of one block
+    p.maxwin = nchunk * p.CR;
+    const size_t kMax = 227 * 1024;
+    for (int NA = 2; NA >= 1; --NA)
+        for (int extra = 128 / p.CR + 1; extra >= 0; --extra) {
+            st::PhaseArgs a{};
+            a.CR = p.CR;
+            a.NA = NA;
+            a.NSK = nchunk + extra;
+            a.npl = p.npl;
+            a.row_bytes = p.row_bytes;
+            a.maxwin = p.maxwin;
+            const size_t sm = st::phase_smem_bytes(a);
+            if (sm <= kMax) {
+                p.NA = NA;
+                p.NSK = a.NSK;
+                p.smem = sm;
+                p.ok = true;
+                return p;
+            }
+        }
+    return p;
+}
+
+struct WsLayout {
+    size_t S2, u, v, g_u, u2b, u1b, deps, g_v, v1b, v0b, err;
+    size_t qp[3], kp[3], flags, work_q, work_k, cnt, bytes;
+};
+WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
     WsLayout w;
     size_t o = 0;
     auto take = [&](size_t n) {
@@ -112,8 +162,32 @@ WsLayout ws_layout(const Dims& m) {
     w.v1b = take(rk);
     w.v0b = take(rk);
     w.err = take(sizeof(int));
+    for (int p = 0; p < 3; ++p) w.qp[p] = w.kp[p] = 0;
+    w.flags = w.work_q = w.work_k = w.cnt = 0;
+    if (tp.ok) {
+        for (int p = 0; p < tp.npl; ++p) {
+            w.qp[p] = take((size_t)m.BH * tp.Lpq * tp.row_bytes);
+            w.kp[p] = take((size_t)m.BH * tp.Lpk * tp.row_bytes);
+        }
+        const size_t nbmax = (size_t)m.BH * std::max(tp.NBq, tp.NBk);
+        w.flags = take(sizeof(int) * nbmax);
+        w.work_q = take(sizeof(int) * (size_t)m.BH * tp.NBq);
+        w.work_k = take(sizeof(int) * (size_t)m.BH * tp.NBk);
+        w.cnt = take(sizeof(int) * 2);
+    }
     w.bytes = o;
     return w;
+}
+
+int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
 }
 
 #define ST_CUDA(call)                                                                  \
@@ -128,7 +202,9 @@ extern "C" {
 
 const char* st_last_error(void) { return g_err.c_str(); }
 
-int64_t st_launch_count(int32_t reset) { return (int64_t)st::launch_count(reset != 0); }
+int64_t st_launch_count(int32_t reset) {
+    return (int64_t)(st::launch_count(reset != 0) + st::phase_launch_count(reset != 0));
+}
 
 size_t st_saved_bytes(const st_desc* desc) {
     Dims m;
@@ -139,7 +215,7 @@ size_t st_saved_bytes(const st_desc* desc) {
 size_t st_workspace_bytes(const st_desc* desc) {
     Dims m;
     if (check_desc(desc, m) != ST_OK) return 0;
-    return ws_layout(m).bytes;
+    return ws_layout(m, tc_plan(desc, m)).bytes;
 }
 
 st_status st_forward(const st_desc* desc, const void* Q, const void* K, const void* V, const uint8_t* row_mask,
@@ -149,7 +225,8 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
     st_status s = check_desc(desc, m);
     if (s != ST_OK) return s;
     if (!Q || !K || !V || !O) return fail(ST_INVALID_ARGUMENT, "null tensor pointer");
-    const WsLayout wl = ws_layout(m);
+    const TcPlan tp = tc_plan(desc, m);
+    const WsLayout wl = ws_layout(m, tp);
     if (workspace == nullptr || workspace_bytes < wl.bytes)
         return fail(ST_WORKSPACE_TOO_SMALL, "workspace smaller than st_workspace_bytes()");
     cudaStream_t st = (cudaStream_t)stream;
@@ -168,8 +245,6 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
     ST_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
     ST_CUDA(cudaMemsetAsync(u_ws, 0, sizeof(float) * m.BH * m.Lrq, st));
     ST_CUDA(cudaMemsetAsync(v_ws, 0, sizeof(float) * m.BH * m.Lrk, st));
-    ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));
-
     const long T = desc->base_depth, R = desc->tail_depth;
     auto slot_u = [&](long r) { return su + (size_t)r * m.BH * m.Lrq; };
     auto slot_v = [&](long r) { return svv + (size_t)r * m.BH * m.Lrk; };
@@ -179,14 +254,116 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
         ST_CUDA(cudaMemsetAsync(slot_u(0), 0, sizeof(float) * m.BH * m.Lrq, st));
         ST_CUDA(cudaMemsetAsync(slot_v(0), 0, sizeof(float) * m.BH * m.Lrk, st));
     }
-    for (long t = 1; t <= T + R; ++t) {
-        const long r = t - T;
-        float* u_out = (sv && r >= 0 && r <= 2) ? slot_u(r) : u_ws;
-        float* v_out = (sv && r >= 0 && r <= 2) ? slot_v(r) : v_ws;
-        ST_CUDA(st::launch_row_step(g, t == 1, S2, v_prev, u_prev, u_out, err, st));
-        ST_CUDA(st::launch_col_step(g, t == 1, S2, u_out, v_prev, v_out, err, st));
-        u_prev = u_out;
-        v_prev = v_out;
+    if (tp.ok) {
+        // ---- tensor-core path: pack Q/K once, then 2 tcgen05 half-step launches per step
+        uint8_t* qp[3] = {nullptr, nullptr, nullptr};
+        uint8_t* kp[3] = {nullptr, nullptr, nullptr};
+        for (int p = 0; p < tp.npl; ++p) {
+            qp[p] = (uint8_t*)(ws + wl.qp[p]);
+            kp[p] = (uint8_t*)(ws + wl.kp[p]);
+        }
+        int* flags = (int*)(ws + wl.flags);
+        int* work_q = (int*)(ws + wl.work_q);
+        int* work_k = (int*)(ws + wl.work_k);
+        int* cnt = (int*)(ws + wl.cnt);
+        ST_CUDA(st::launch_pack(desc->dtype, Q, g.BH, g.Lq, g.Lrq, tp.Lpq, g.d, tp.shift, qp[0], qp[1], qp[2], st));
+        ST_CUDA(st::launch_pack(desc->dtype, K, g.BH, g.Lk, g.Lrk, tp.Lpk, g.d, tp.shift, kp[0], kp[1], kp[2], st));
+        ST_CUDA(st::launch_worklist(row_mask, g.H, g.BH, g.Lq, tp.NBq, flags, work_q, cnt, st));
+        ST_CUDA(st::launch_worklist(col_mask, g.H, g.BH, g.Lk, tp.NBk, flags, work_k, cnt + 1, st));
+        st::PhaseArgs pr{};
+        pr.npl = tp.npl;
+        pr.CR = tp.CR;
+        pr.shift = tp.shift;
+        pr.NA = tp.NA;
+        pr.NSK = tp.NSK;
+        pr.row_bytes = tp.row_bytes;
+        pr.maxwin = tp.maxwin;
+        pr.H = g.H;
+        pr.w = g.w;
+        pr.dustbin = g.dustbin;
+        pr.c2 = g.c2;
+        pr.sd2 = g.sd2;
+        pr.err = err;
+        st::PhaseArgs pc = pr;
+        // row phase: own = queries (A = Q block), other = keys (B = K window)
+        pr.NB = tp.NBq;
+        pr.L_own = g.Lq; pr.L_other = g.Lk; pr.Lr_own = g.Lrq; pr.Lr_other = g.Lrk;
+        pr.Lp_own = tp.Lpq; pr.Lp_other = tp.Lpk;
+        pr.mask_own = row_mask; pr.mask_other = col_mask;
+        for (int p = 0; p < 3; ++p) { pr.A_pack[p] = qp[p]; pr.B_pack[p] = kp[p]; }
+        pr.work = work_q; pr.nwork = cnt;
+        // column phase: own = keys (A = K block), other = queries (B = Q window)
+        pc.NB = tp.NBk;
+        pc.L_own = g.Lk; pc.L_other = g.Lq; pc.Lr_own = g.Lrk; pc.Lr_other = g.Lrq;
+        pc.Lp_own = tp.Lpk; pc.Lp_other = tp.Lpq;
+        pc.mask_own = col_mask; pc.mask_other = row_mask;
+        for (int p = 0; p < 3; ++p) { pc.A_pack[p] = kp[p]; pc.B_pack[p] = qp[p]; }
+        pc.work = work_k; pc.nwork = cnt + 1;
+        st::DustArgs dr{}, dc{};
+        dr.H = dc.H = g.H;
+        dr.sd2 = dc.sd2 = g.sd2;
+        dr.err = dc.err = err;
+        dr.L_own = g.Lq; dr.L_other = g.Lk; dr.Lr_own = g.Lrq; dr.Lr_other = g.Lrk; dr.mask_other = col_mask;
+        dc.L_own = g.Lk; dc.L_other = g.Lq; dc.Lr_own = g.Lrk; dc.Lr_other = g.Lrq; dc.mask_other = row_mask;
+        const int grid = std::min(num_sms(), (int)(m.BH * std::max(tp.NBq, tp.NBk)));
+        // ST_TRACE_PHASE=t: dump the device timeline of the row phase of step t (debug only)
+        static const long trace_step = getenv("ST_TRACE_PHASE") ? atol(getenv("ST_TRACE_PHASE")) : -1;
+        unsigned long long* trace = nullptr;
+        if (trace_step >= 1) {
+            cudaMalloc(&trace, 16 * 64 * sizeof(unsigned long long));
+            cudaMemsetAsync(trace, 0, 16 * 64 * sizeof(unsigned long long), st);
+        }
+        for (long t = 1; t <= T + R; ++t) {
+            const long r = t - T;
+            float* u_out = (sv && r >= 0 && r <= 2) ? slot_u(r) : u_ws;
+            float* v_out = (sv && r >= 0 && r <= 2) ? slot_v(r) : v_ws;
+            pr.dual_other = v_prev; pr.off_own = u_prev; pr.out_own = u_out;
+            pr.trace = (t == trace_step) ? trace : nullptr;
+            ST_CUDA(st::launch_phase(pr, t == 1, grid, st));
+            if (t == trace_step) {
+                unsigned long long h[16 * 64];
+                cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                for (int c = 0; c < 16; ++c) {
+                    const unsigned long long t0 = h[c * 64];
+                    fprintf(stderr, "cta %2d nblk %llu:", c, h[c * 64 + 42]);
+                    auto pr_ = [&](const char* nm, int base, int n) {
+                        fprintf(stderr, " %s", nm);
+                        for (int k = 0; k < n; ++k)
+                            if (h[c * 64 + base + k]) fprintf(stderr, " %.2f", (h[c * 64 + base + k] - t0) * 1e-3);
+                    };
+                    pr_("prodA", 1, 8); pr_("| mmaA", 9, 8); pr_("| mmaEnd", 17, 8); pr_("| epiS", 25, 8);
+                    pr_("| epiE", 33, 8); pr_("| end", 41, 1); pr_("\n      kfull/tempty b0", 43, 10); pr_("b1", 53, 10);
+                    fprintf(stderr, "\n");
+                }
+                cudaFree(trace);
+                trace = nullptr;
+            }
+            if (g.dustbin) {
+                dr.dual_other = v_prev; dr.off_own = u_prev; dr.out_own = u_out;
+                ST_CUDA(st::launch_dustbin(dr, t == 1, g.BH, st));
+            }
+            pc.dual_other = u_out; pc.off_own = v_prev; pc.out_own = v_out;
+            ST_CUDA(st::launch_phase(pc, t == 1, grid, st));
+            if (g.dustbin) {
+                dc.dual_other = u_out; dc.off_own = v_prev; dc.out_own = v_out;
+                ST_CUDA(st::launch_dustbin(dc, t == 1, g.BH, st));
+            }
+            u_prev = u_out;
+            v_prev = v_out;
+        }
+        ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));  // transport application (generic kernel)
+    } else {
+        ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));
+        for (long t = 1; t <= T + R; ++t) {
+            const long r = t - T;
+            float* u_out = (sv && r >= 0 && r <= 2) ? slot_u(r) : u_ws;
+            float* v_out = (sv && r >= 0 && r <= 2) ? slot_v(r) : v_ws;
+            ST_CUDA(st::launch_row_step(g, t == 1, S2, v_prev, u_prev, u_out, err, st));
+            ST_CUDA(st::launch_col_step(g, t == 1, S2, u_out, v_prev, v_out, err, st));
+            u_prev = u_out;
+            v_prev = v_out;
+        }
     }
     ST_CUDA(st::launch_output(g, desc->dtype, S2, u_prev, v_prev, V, O, st));
     if (sv) {
@@ -207,7 +384,7 @@ st_status st_backward(const st_desc* desc, const void* saved, const void* Q, con
     if (saved == nullptr) return fail(ST_MISSING_BASE_TRACE, "backward needs the forward's saved state");
     if (!Q || !K || !V || !dO || !dQ || !dK || !dV) return fail(ST_INVALID_ARGUMENT, "null tensor pointer");
     if (mode != ST_ONE_REFERENCE && mode != ST_DIRECT_FOUR_PLAN) return fail(ST_INVALID_ARGUMENT, "unknown mode");
-    const WsLayout wl = ws_layout(m);
+    const WsLayout wl = ws_layout(m, tc_plan(desc, m));
     if (workspace == nullptr || workspace_bytes < wl.bytes)
         return fail(ST_WORKSPACE_TOO_SMALL, "workspace smaller than st_workspace_bytes()");
     cudaStream_t st = (cudaStream_t)stream;

@@ -1,0 +1,623 @@
+// st_phase.cu -- the tcgen05 half-step ("phase") kernel of the Sinkhorn forward.
+//
+// One launch = one half-step for every head:
+//   row phase:  u_i <- o_i - lg2 sum_{j in band(i)} 2^( s2_ij + v_j + o_i )      (row_half_step,  sinkhorn.hpp:15-61)
+//   col phase:  v_j <- o_j - lg2 sum_{i in band(j)} 2^( s2_ij + u_i + o_j )      (col_half_step,  sinkhorn.hpp:64-107)
+// with s2 = (q.k) * log2(e)/(sqrt(d) eps) RECOMPUTED on the tensor cores for
+// every 128-row block and never stored (O(L) extra HBM).  The column phase is
+// the row phase of the transposed problem (A = K block, B = Q window), so one
+// kernel serves both and every log-sum-exp is an in-thread TMEM-lane reduction.
+//
+// Persistent CTA (one per SM), warp-specialised:
+//   warp 0      producer: 1-D bulk async copies (TMA engine, UBLKCP) of the packed
+//               A block and of the B window in CR-row chunks into an SMEM ring;
+//               chunks shared by consecutive blocks of a head are loaded once
+//   warp 1      MMA issuer: tcgen05.mma kind::f16 (BF16) M=128, N=CR, K=16, two
+//               window chunks interleaved (independent accumulators hide the
+//               ~80 ns dependent-MMA latency); fp32 inputs use a 3-plane bf16
+//               split (hi, mid, lo) with the 6 products of order <= 2^-16,
+//               i.e. fp32-accurate scores at bf16 tensor rate
+//   warps 2..9  epilogue: two warps per TMEM lane quadrant (each owns half of
+//               every chunk's columns): tcgen05.ld, FFMA scale + window dual,
+//               MUFU.EX2, in-thread sums, lg2; window duals prefetched one
+//               block ahead into a double-buffered SMEM slot
+// Offsets: cold start uses an online running max; every later step uses the
+// previous dual of the same row (terms <= 1, sums in [1/W, W]).
+#include <cstdio>
+
+#include "st_common.cuh"
+#include "st_phase.cuh"
+#include "st_sm100.cuh"
+
+namespace st {
+
+using namespace sm100;
+
+namespace {
+
+struct Smem {
+    uint8_t* A;       // [NA][npl][128 * row_bytes]
+    uint8_t* K;       // [NSK][npl][CR * row_bytes]
+    float* vwin;      // [2][maxwin]
+    float* part;      // [256] partial (sum, max) of the second column half
+    uint64_t* a_full;
+    uint64_t* a_empty;
+    uint64_t* k_full;
+    uint64_t* k_empty;
+    uint64_t* t_full;
+    uint64_t* t_empty;
+    uint32_t* tmem_base;
+};
+
+__device__ __forceinline__ Smem carve(uint8_t* base, const PhaseArgs& a, int nst) {
+    Smem s;
+    const size_t blk = (size_t)128 * a.row_bytes, chk = (size_t)a.CR * a.row_bytes;
+    s.A = base;
+    s.K = s.A + (size_t)a.NA * a.npl * blk;
+    s.vwin = (float*)(s.K + (size_t)a.NSK * a.npl * chk);
+    s.part = s.vwin + 2 * a.maxwin;
+    uint64_t* bars = (uint64_t*)(s.part + 256);
+    s.a_full = bars;
+    s.a_empty = bars + 2;
+    s.k_full = bars + 4;
+    s.k_empty = s.k_full + a.NSK;
+    s.t_full = s.k_empty + a.NSK;
+    s.t_empty = s.t_full + nst;
+    s.tmem_base = (uint32_t*)(s.t_empty + nst);
+    return s;
+}
+
+// A 128-row block of the own side and its window chunks [q0, q1] of the other side.
+// Chunk q = packed rows [q*CR, (q+1)*CR) = original rows [q*CR - shift, ...).
+struct Blk {
+    int bh, i0, q0, q1;
+};
+__device__ __forceinline__ Blk block_of(const PhaseArgs& a, int g) {
+    Blk b;
+    b.bh = g / a.NB;
+    b.i0 = (g % a.NB) * 128;
+    const int nq = a.Lp_other / a.CR;
+    b.q0 = max(0, (b.i0 - a.w + a.shift) / a.CR);  // exact: shift = w mod CR, CR | 128
+    b.q1 = min(nq - 1, (b.i0 + 128 + a.w + a.shift + a.CR - 1) / a.CR - 1);
+    return b;
+}
+
+__device__ __forceinline__ bool on_mask(const uint8_t* m, int H, int L, int bh, int i) {
+    return m == nullptr || m[(size_t)(bh / H) * L + i] != 0;
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// debug timeline: trace[cta][slot] for the first 16 CTAs (ST_TRACE_PHASE, st_api.cu)
+#define ST_TRACE(slot)                                                                                \
+    do {                                                                                              \
+        if (a.trace && blockIdx.x < 16 && (slot) < 64) a.trace[blockIdx.x * 64 + (slot)] = gtimer(); \
+    } while (0)
+
+__device__ __forceinline__ float window_dual(const PhaseArgs& a, int bh, int j) {
+    if (j < 0 || j >= a.L_other || !on_mask(a.mask_other, a.H, a.L_other, bh, j)) return -INFINITY;
+    return a.dual_other[(size_t)bh * a.Lr_other + j];
+}
+
+}  // namespace
+
+template <int kNPL, int kCR, bool kFirst>
+__global__ void __launch_bounds__(320, 1) k_phase(PhaseArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    constexpr int NST = 512 / kCR;  // TMEM accumulator slots
+    const Smem s = carve(smem_raw, a, NST);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t blk_bytes = 128u * a.row_bytes, chk_bytes = (uint32_t)kCR * a.row_bytes;
+
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 2; ++k) {
+            mbar_init(&s.a_full[k], 1);
+            mbar_init(&s.a_empty[k], 1);
+        }
+        for (int k = 0; k < a.NSK; ++k) {
+            mbar_init(&s.k_full[k], 1);
+            mbar_init(&s.k_empty[k], 1);
+        }
+        for (int k = 0; k < NST; ++k) {
+            mbar_init(&s.t_full[k], 1);
+            mbar_init(&s.t_empty[k], 8);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        tc_alloc(s.tmem_base, 512);
+        tc_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = *s.tmem_base;
+    if (threadIdx.x == 0) ST_TRACE(0);
+
+    const int n = *a.nwork;
+    const int g_begin = (int)((long long)n * blockIdx.x / gridDim.x);
+    const int g_end = (int)((long long)n * (blockIdx.x + 1) / gridDim.x);
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer (warp-uniform loop)
+        int last_bh = -1, last_q = -1;
+        uint32_t kseq = 0;
+        for (int gi = g_begin; gi < g_end; ++gi) {
+            const Blk b = block_of(a, a.work[gi]);
+            const int ab = (gi - g_begin) % a.NA;
+            const uint32_t an = (gi - g_begin) / a.NA;
+            mbar_wait(&s.a_empty[ab], (an & 1) ^ 1);
+            if (elect_one()) {
+                ST_TRACE(1 + min(gi - g_begin, 7));
+                mbar_arrive_expect_tx(&s.a_full[ab], blk_bytes * kNPL);
+#pragma unroll
+                for (int p = 0; p < kNPL; ++p)
+                    bulk_g2s(s.A + ((size_t)ab * kNPL + p) * blk_bytes,
+                             a.A_pack[p] + ((size_t)b.bh * a.Lp_own + b.i0 + a.shift) * a.row_bytes, blk_bytes,
+                             &s.a_full[ab]);
+            }
+            __syncwarp();
+            const int qstart = (b.bh == last_bh) ? max(b.q0, last_q + 1) : b.q0;
+            for (int q = qstart; q <= b.q1; ++q) {
+                const int sl = kseq % a.NSK;
+                const uint32_t kn = kseq / a.NSK;
+                mbar_wait(&s.k_empty[sl], (kn & 1) ^ 1);
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(&s.k_full[sl], chk_bytes * kNPL);
+#pragma unroll
+                    for (int p = 0; p < kNPL; ++p)
+                        bulk_g2s(s.K + ((size_t)sl * kNPL + p) * chk_bytes,
+                                 a.B_pack[p] + ((size_t)b.bh * a.Lp_other + (size_t)q * kCR) * a.row_bytes, chk_bytes,
+                                 &s.k_full[sl]);
+                }
+                __syncwarp();
+                ++kseq;
+            }
+            if (b.bh != last_bh) last_q = -1;
+            last_q = max(last_q, b.q1);
+            last_bh = b.bh;
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer (warp-uniform loop)
+        const uint32_t idesc = make_idesc(128, kCR, 1u);            // BF16 x BF16 -> F32
+        const uint32_t sbo = (uint32_t)(a.row_bytes / 16) * 128u;   // bytes between 8-row groups
+        const int ksteps = a.row_bytes / 32;                         // MMA-K slices of 32 bytes (16 bf16)
+        const uint64_t a_plane = (uint64_t)(blk_bytes >> 4), b_plane = (uint64_t)(chk_bytes >> 4);
+        // products (plane of A, plane of B): exact for bf16 inputs; fp32 = hi+mid+lo with the
+        // 6 products hh, hm, mh, hl, mm, lh (omitted terms are below 2^-24 relative)
+        constexpr int kNP = (kNPL == 1) ? 1 : 6;
+        constexpr int pa_[6] = {0, 0, 1, 0, 1, 2};
+        constexpr int pb_[6] = {0, 1, 0, 2, 1, 0};
+        int last_bh = -1, last_q = -1;
+        uint32_t last_seq = 0, rel_seq = 0, tseq = 0;
+        bool have = false;
+        for (int gi = g_begin; gi < g_end; ++gi) {
+            const Blk b = block_of(a, a.work[gi]);
+            const int ab = (gi - g_begin) % a.NA;
+            const uint32_t an = (gi - g_begin) / a.NA;
+            mbar_wait(&s.a_full[ab], an & 1);
+            if (lane == 0) ST_TRACE(9 + min(gi - g_begin, 7));
+            tc_fence_after();
+            const uint64_t ad0 = make_desc(smem_u32(s.A + (size_t)ab * kNPL * blk_bytes), 128, sbo);
+            const bool same = have && b.bh == last_bh;
+            const int new_start = same ? max(b.q0, last_q + 1) : b.q0;
+            const uint32_t next_seq = have ? last_seq + 1 : 0;
+            constexpr int kG = 2;  // chunks per MMA group (independent accumulators)
+            for (int q0 = b.q0; q0 <= b.q1; q0 += kG) {
+                const int ng = min(kG, b.q1 - q0 + 1);
+                uint64_t bd[kG];
+                uint32_t dt[kG];
+#pragma unroll
+                for (int c = 0; c < kG; ++c) {
+                    if (c < ng) {
+                        const int q = q0 + c;
+                        const uint32_t seq = (same && q <= last_q) ? last_seq - (uint32_t)(last_q - q)
+                                                                   : next_seq + (uint32_t)(q - new_start);
+                        const int sl = seq % a.NSK;
+                        mbar_wait(&s.k_full[sl], (seq / a.NSK) & 1);
+                        const uint32_t tq = tseq + c;
+                        mbar_wait(&s.t_empty[tq % NST], ((tq / NST) & 1) ^ 1);
+                        bd[c] = make_desc(smem_u32(s.K + (size_t)sl * kNPL * chk_bytes), 128, sbo);
+                        dt[c] = tbase + (uint32_t)((tq % NST) * kCR);
+                    }
+                }
+                tc_fence_after();
+                if (elect_one()) {
+#pragma unroll
+                    for (int pr = 0; pr < kNP; ++pr)
+                        for (int kk = 0; kk < ksteps; ++kk) {
+                            const uint64_t adk = ad0 + (uint64_t)pa_[pr] * a_plane + (uint64_t)(kk * 16);
+#pragma unroll
+                            for (int c = 0; c < kG; ++c)
+                                if (c < ng)
+                                    mma_bf16(dt[c], adk, bd[c] + (uint64_t)pb_[pr] * b_plane + (uint64_t)(kk * 16),
+                                             idesc, (pr | kk) > 0);
+                        }
+#pragma unroll
+                    for (int c = 0; c < kG; ++c)
+                        if (c < ng) tc_commit(&s.t_full[(tseq + c) % NST]);
+                }
+                __syncwarp();
+                tseq += ng;
+            }
+            if (elect_one()) tc_commit(&s.a_empty[ab]);  // A is free once this block's MMAs completed
+            __syncwarp();
+            if (lane == 0) ST_TRACE(17 + min(gi - g_begin, 7));
+            // chunk bookkeeping (mirrors the producer)
+            if (b.q1 >= new_start) last_seq = next_seq + (uint32_t)(b.q1 - new_start);
+            if (!same) last_q = -1;
+            last_q = max(last_q, b.q1);
+            last_bh = b.bh;
+            have = true;
+            // release ring slots the next block of this CTA does not need
+            uint32_t keep_from = last_seq + 1;
+            if (gi + 1 < g_end) {
+                const Blk nb = block_of(a, a.work[gi + 1]);
+                if (nb.bh == last_bh && nb.q0 <= last_q) keep_from = last_seq - (uint32_t)(last_q - nb.q0);
+            }
+            if (elect_one()) {
+                for (uint32_t r = rel_seq; r < keep_from; ++r) tc_commit(&s.k_empty[r % a.NSK]);
+            }
+            __syncwarp();
+            rel_seq = max(rel_seq, keep_from);
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue (warps 2..9)
+        constexpr int HC = kCR / 2;               // columns per warp per chunk
+        const int ew = warp - 2;                  // 0..7
+        const int qd = warp & 3;                  // TMEM lane quadrant (warp_id % 4)
+        const int half = ew >> 2;
+        const int r = qd * 32 + lane;             // row inside the 128-row block
+        const int et = threadIdx.x - 64;          // 0..255
+        uint32_t tseq = 0;
+        if (g_begin < g_end) {  // window duals of the first block (later ones are prefetched)
+            const Blk b = block_of(a, a.work[g_begin]);
+            const int wbase = b.q0 * kCR - a.shift, nwin = (b.q1 - b.q0 + 1) * kCR;
+            for (int c = et; c < nwin; c += 256) s.vwin[c] = window_dual(a, b.bh, wbase + c);
+        }
+        for (int gi = g_begin; gi < g_end; ++gi) {
+            const Blk b = block_of(a, a.work[gi]);
+            const float* vw = s.vwin + ((gi - g_begin) & 1) * a.maxwin;
+            const int wbase = b.q0 * kCR - a.shift;   // original column of window column 0
+            named_bar(1, 256);  // vw complete; previous block fully consumed
+            if (et == 0) ST_TRACE(25 + min(gi - g_begin, 7));
+            // prefetch the next block's window duals into registers (parked in SMEM after this block)
+            constexpr int kPre = 4;
+            float pre[kPre];
+            Blk nb{};
+            const bool has_next = gi + 1 < g_end;
+            int nwin_next = 0;
+            if (has_next) {
+                nb = block_of(a, a.work[gi + 1]);
+                nwin_next = (nb.q1 - nb.q0 + 1) * kCR;
+#pragma unroll
+                for (int k = 0; k < kPre; ++k) {
+                    const int c = et + 256 * k;
+                    pre[k] = (c < nwin_next) ? window_dual(a, nb.bh, nb.q0 * kCR - a.shift + c) : -INFINITY;
+                }
+            }
+            const int i = b.i0 + r;
+            const bool active = i < a.L_own && on_mask(a.mask_own, a.H, a.L_own, b.bh, i);
+            float o = 0.f, acc0 = 0.f, acc1 = 0.f, M = -INFINITY;
+            if (!kFirst && active) o = a.off_own[(size_t)b.bh * a.Lr_own + i];
+            const int lo = i - a.w - wbase;               // band of this lane, window coordinates
+            const int wlo = b.i0 + qd * 32 - a.w - wbase; // union over the warp
+            const int whi = wlo + 31 + 2 * a.w;
+            const int ilo = wlo + 31, ihi = wlo + 2 * a.w; // intersection over the warp
+            for (int q = b.q0; q <= b.q1; ++q) {
+                const int ts = tseq % NST;
+                mbar_wait(&s.t_full[ts], (tseq / NST) & 1);
+                tc_fence_after();
+                const int c0 = (q - b.q0) * kCR + half * HC;
+                const bool any = !(whi < c0 || wlo > c0 + HC - 1);
+                const bool inner = (c0 >= ilo) && (c0 + HC - 1 <= ihi);
+                float v[HC];
+                if (any) {
+                    const uint32_t taddr = tbase + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ts * kCR + half * HC);
+#pragma unroll
+                    for (int h = 0; h < HC / 32; ++h) tc_ld32(taddr + 32 * h, *reinterpret_cast<float(*)[32]>(v + 32 * h));
+                    tc_wait_ld();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s.t_empty[ts]);
+                ++tseq;
+                if (!any || !active) continue;
+                if (kFirst) {
+                    float m = -INFINITY;
+#pragma unroll
+                    for (int cc = 0; cc < HC; ++cc) {
+                        const int c = c0 + cc;
+                        const float x = fmaf(v[cc], a.c2, vw[c]);
+                        v[cc] = ((unsigned)(c - lo) <= (unsigned)(2 * a.w)) ? x : -INFINITY;
+                        m = fmaxf(m, v[cc]);
+                    }
+                    if (m > M) {
+                        acc0 = (M == -INFINITY) ? 0.f : acc0 * ex2(M - m);
+                        M = m;
+                    }
+                    if (M != -INFINITY) {
+#pragma unroll
+                        for (int cc = 0; cc < HC; ++cc) acc0 += ex2(v[cc] - M);
+                    }
+                } else if (inner) {
+#pragma unroll
+                    for (int cc = 0; cc < HC; cc += 4) {
+                        const float4 w4 = *reinterpret_cast<const float4*>(vw + c0 + cc);
+                        acc0 += ex2(fmaf(v[cc + 0], a.c2, w4.x) + o);
+                        acc1 += ex2(fmaf(v[cc + 1], a.c2, w4.y) + o);
+                        acc0 += ex2(fmaf(v[cc + 2], a.c2, w4.z) + o);
+                        acc1 += ex2(fmaf(v[cc + 3], a.c2, w4.w) + o);
+                    }
+                } else {
+#pragma unroll
+                    for (int cc = 0; cc < HC; ++cc) {
+                        const int c = c0 + cc;
+                        float x = fmaf(v[cc], a.c2, vw[c]) + o;
+                        x = ((unsigned)(c - lo) <= (unsigned)(2 * a.w)) ? x : -INFINITY;
+                        if (cc & 1) acc1 += ex2(x);
+                        else acc0 += ex2(x);
+                    }
+                }
+            }
+            float acc_s = acc0 + acc1;
+            if (has_next) {  // park the prefetched window duals for the next block
+                float* nvw = s.vwin + ((gi + 1 - g_begin) & 1) * a.maxwin;
+#pragma unroll
+                for (int k = 0; k < kPre; ++k)
+                    if (et + 256 * k < nwin_next) nvw[et + 256 * k] = pre[k];
+                for (int c = et + 256 * kPre; c < nwin_next; c += 256)
+                    nvw[c] = window_dual(a, nb.bh, nb.q0 * kCR - a.shift + c);
+            }
+            if (et == 0) ST_TRACE(33 + min(gi - g_begin, 7));
+            // combine the two column halves of every row
+            if (half == 1) {
+                s.part[r] = acc_s;
+                s.part[128 + r] = M;
+            }
+            named_bar(2, 256);
+            if (half == 0 && i < a.L_own) {
+                const float s1 = s.part[r];
+                float u = 0.f;
+                if (kFirst) {
+                    const float M1 = s.part[128 + r];
+                    const float Mx = fmaxf(M, M1);
+                    acc_s = (M == -INFINITY ? 0.f : acc_s * ex2(M - Mx)) + (M1 == -INFINITY ? 0.f : s1 * ex2(M1 - Mx));
+                    M = Mx;
+                } else {
+                    acc_s += s1;
+                }
+                if (active) {
+                    if (a.dustbin) {  // the spoke cell (i, dustbin) with constant score sd2
+                        const float x = a.sd2 + a.dual_other[(size_t)b.bh * a.Lr_other + a.L_other];
+                        if (kFirst) {
+                            if (x > M) {
+                                acc_s = (M == -INFINITY) ? 0.f : acc_s * ex2(M - x);
+                                M = x;
+                            }
+                            acc_s += ex2(x - M);
+                        } else {
+                            acc_s += ex2(x + o);
+                        }
+                    }
+                    u = kFirst ? (-M - lg2(acc_s)) : (o - lg2(acc_s));
+                    if (!(acc_s > 0.f) || !isfinite(u)) {
+                        atomicOr(a.err, 4);
+                        u = 0.f;
+                    }
+                }
+                a.out_own[(size_t)b.bh * a.Lr_own + i] = u;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ST_TRACE(41);
+        if (a.trace && blockIdx.x < 16) a.trace[blockIdx.x * 64 + 42] = (unsigned long long)(g_end - g_begin);
+    }
+    if (warp == 1) {
+        tc_fence_after();
+        tc_dealloc(tbase, 512);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Dustbin row/column (spoke support): u_L <- o - lg2( sum_{j active} 2^(sd2 + v_j + o) + 2^(sd2 + v_L + o) )
+// one CTA per head, fixed-order block reduction.
+// ---------------------------------------------------------------------------
+template <bool kFirst>
+__global__ void __launch_bounds__(256) k_dustbin(DustArgs a) {
+    const int bh = blockIdx.x;
+    const float* dual = a.dual_other + (size_t)bh * a.Lr_other;
+    const int n = a.L_other + 1;
+    __shared__ float red[256];
+    float off;
+    if (kFirst) {
+        float m = -INFINITY;
+        for (int j = threadIdx.x; j < n; j += 256)
+            if (j == a.L_other || on_mask(a.mask_other, a.H, a.L_other, bh, j)) m = fmaxf(m, a.sd2 + dual[j]);
+        red[threadIdx.x] = m;
+        __syncthreads();
+        for (int o = 128; o > 0; o >>= 1) {
+            if (threadIdx.x < o) red[threadIdx.x] = fmaxf(red[threadIdx.x], red[threadIdx.x + o]);
+            __syncthreads();
+        }
+        off = -red[0];
+        __syncthreads();
+    } else {
+        off = a.off_own[(size_t)bh * a.Lr_own + a.L_own];
+    }
+    float sum = 0.f;
+    for (int j = threadIdx.x; j < n; j += 256)
+        if (j == a.L_other || on_mask(a.mask_other, a.H, a.L_other, bh, j)) sum += ex2(a.sd2 + dual[j] + off);
+    red[threadIdx.x] = sum;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        float u = off - lg2(red[0]);
+        if (!(red[0] > 0.f) || !isfinite(u)) {
+            atomicOr(a.err, 8);
+            u = 0.f;
+        }
+        a.out_own[(size_t)bh * a.Lr_own + a.L_own] = u;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Packing: one thread per (head, packed row, 16-byte K chunk of 8 elements).
+// bf16 input -> 1 plane (verbatim); fp32 input -> 3 bf16 planes
+//   hi = bf16(x), mid = bf16(x - hi), lo = bf16(x - hi - mid)   (x - hi and x - hi - mid are exact in fp32)
+// Packed row p holds original row p - shift (zero outside [0, L)).
+// ---------------------------------------------------------------------------
+template <class TIn>
+__global__ void k_pack(const TIn* __restrict__ X, int BH, int L, int Lr, int Lp, int d, int shift,
+                       uint8_t* __restrict__ p0, uint8_t* __restrict__ p1, uint8_t* __restrict__ p2) {
+    const int kc_n = d / 8;
+    const long total = (long)BH * Lp * kc_n;
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= total) return;
+    const int kc = (int)(t % kc_n);
+    const long rowg = t / kc_n;
+    const int p = (int)(rowg % Lp);
+    const int bh = (int)(rowg / Lp);
+    const int r = p - shift;
+    const size_t row_bytes = (size_t)d * 2;
+    const size_t off = ((size_t)bh * Lp + (p & ~7)) * row_bytes + (size_t)kc * 128 + (p & 7) * 16;
+    if (sizeof(TIn) == 2) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (r >= 0 && r < L) v = *reinterpret_cast<const uint4*>(X + ((size_t)bh * Lr + r) * d + kc * 8);
+        *reinterpret_cast<uint4*>(p0 + off) = v;
+    } else {
+        float x[8];
+        if (r >= 0 && r < L) {
+            const float4* src = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(X) +
+                                                                ((size_t)bh * Lr + r) * d + kc * 8);
+            const float4 a = src[0], b = src[1];
+            x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) x[k] = 0.f;
+        }
+        __align__(16) __nv_bfloat16 h[8], m[8], l[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            h[k] = __float2bfloat16_rn(x[k]);
+            const float r1 = x[k] - __bfloat162float(h[k]);
+            m[k] = __float2bfloat16_rn(r1);
+            l[k] = __float2bfloat16_rn(r1 - __bfloat162float(m[k]));
+        }
+        *reinterpret_cast<uint4*>(p0 + off) = *reinterpret_cast<const uint4*>(h);
+        *reinterpret_cast<uint4*>(p1 + off) = *reinterpret_cast<const uint4*>(m);
+        *reinterpret_cast<uint4*>(p2 + off) = *reinterpret_cast<const uint4*>(l);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Work lists: active 128-row blocks (any active row) in (head, block) order.
+// ---------------------------------------------------------------------------
+__global__ void k_block_flags(const uint8_t* __restrict__ mask, int H, int BH, int L, int NB, int* __restrict__ flags) {
+    const int g = blockIdx.x;
+    if (g >= BH * NB) return;
+    const int bh = g / NB, b = g % NB;
+    int any = 0;
+    for (int r = threadIdx.x; r < 128; r += blockDim.x) {
+        const int i = b * 128 + r;
+        if (i < L && on_mask(mask, H, L, bh, i)) any = 1;
+    }
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) flags[g] = any;
+}
+
+__global__ void __launch_bounds__(1024) k_compact(const int* __restrict__ flags, int n, int* __restrict__ work,
+                                                  int* __restrict__ count) {
+    __shared__ int base;
+    __shared__ int warp_tot[32];
+    if (threadIdx.x == 0) base = 0;
+    __syncthreads();
+    for (int c0 = 0; c0 < n; c0 += 1024) {
+        const int g = c0 + threadIdx.x;
+        const int f = (g < n) ? flags[g] : 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        const int pre = __popc(bal & ((1u << lane) - 1));
+        if (lane == 0) warp_tot[wid] = __popc(bal);
+        __syncthreads();
+        int woff = 0;
+        for (int k = 0; k < wid; ++k) woff += warp_tot[k];
+        if (f) work[base + woff + pre] = g;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int k = 0; k < 32; ++k) tot += warp_tot[k];
+            base += tot;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *count = base;
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+static thread_local long long g_phase_launches = 0;
+long long phase_launch_count(bool reset) {
+    const long long c = g_phase_launches;
+    if (reset) g_phase_launches = 0;
+    return c;
+}
+
+size_t phase_smem_bytes(const PhaseArgs& a) {
+    const int nst = 512 / a.CR;
+    return (size_t)a.NA * a.npl * 128 * a.row_bytes + (size_t)a.NSK * a.npl * a.CR * a.row_bytes +
+           (size_t)(2 * a.maxwin + 256) * 4 + (size_t)(4 + 2 * a.NSK + 2 * nst) * 8 + 16;
+}
+
+template <int kNPL, int kCR>
+static cudaError_t launch_phase_t(const PhaseArgs& a, bool first, int grid, cudaStream_t s) {
+    const size_t smem = phase_smem_bytes(a);
+    auto k = first ? k_phase<kNPL, kCR, true> : k_phase<kNPL, kCR, false>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k<<<grid, 320, smem, s>>>(a);
+    ++g_phase_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_phase(const PhaseArgs& a, bool first, int grid, cudaStream_t s) {
+    if (a.npl == 1) return a.CR == 128 ? launch_phase_t<1, 128>(a, first, grid, s) : launch_phase_t<1, 64>(a, first, grid, s);
+    return a.CR == 128 ? launch_phase_t<3, 128>(a, first, grid, s) : launch_phase_t<3, 64>(a, first, grid, s);
+}
+
+cudaError_t launch_dustbin(const DustArgs& a, bool first, int BH, cudaStream_t s) {
+    if (first) k_dustbin<true><<<BH, 256, 0, s>>>(a);
+    else k_dustbin<false><<<BH, 256, 0, s>>>(a);
+    ++g_phase_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack(int dtype, const void* X, int BH, int L, int Lr, int Lp, int d, int shift, uint8_t* p0,
+                        uint8_t* p1, uint8_t* p2, cudaStream_t s) {
+    const long total = (long)BH * Lp * (d / 8);
+    const unsigned nb = (unsigned)((total + 255) / 256);
+    if (dtype == 0) k_pack<float><<<nb, 256, 0, s>>>((const float*)X, BH, L, Lr, Lp, d, shift, p0, p1, p2);
+    else k_pack<__nv_bfloat16><<<nb, 256, 0, s>>>((const __nv_bfloat16*)X, BH, L, Lr, Lp, d, shift, p0, p1, p2);
+    ++g_phase_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_worklist(const uint8_t* mask, int H, int BH, int L, int NB, int* flags, int* work, int* count,
+                            cudaStream_t s) {
+    k_block_flags<<<BH * NB, 128, 0, s>>>(mask, H, BH, L, NB, flags);
+    k_compact<<<1, 1024, 0, s>>>(flags, BH * NB, work, count);
+    g_phase_launches += 2;
+    return cudaGetLastError();
+}
+
+}  // namespace st

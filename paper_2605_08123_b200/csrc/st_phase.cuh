@@ -1,0 +1,56 @@
+// st_phase.cuh -- host interface of the tcgen05 half-step kernels (st_phase.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace st {
+
+// One half-step.  "own" = the side whose dual is updated (rows of the MMA
+// tile, one TMEM lane each); "other" = the window side (MMA N dimension).
+struct PhaseArgs {
+    int npl;            // operand planes: 1 (bf16 inputs) or 3 (fp32 inputs split into bf16 hi/mid/lo)
+    int CR;             // window chunk rows = MMA N (64 or 128)
+    int shift;          // packed row = row + shift: aligns the chunk grid with every band window
+    int NA, NSK;        // A buffers (1-2), B chunk ring slots
+    int row_bytes;      // d * 2 (one bf16 plane)
+    int maxwin;         // floats reserved per window-dual buffer
+    int H, NB;          // heads per example, 128-row blocks per head (own side)
+    int L_own, L_other, Lr_own, Lr_other, Lp_own, Lp_other;
+    int w, dustbin;
+    float c2, sd2;
+    const uint8_t* mask_own;    // [B, L_own] or null
+    const uint8_t* mask_other;  // [B, L_other] or null
+    const uint8_t* A_pack[3];   // packed planes of the own side  [BH][Lp_own][d] bf16
+    const uint8_t* B_pack[3];   // packed planes of the other side
+    const float* dual_other;    // [BH][Lr_other]
+    const float* off_own;       // [BH][Lr_own] previous dual of the own side
+    float* out_own;             // [BH][Lr_own]
+    const int* work;            // active (head, block) list
+    const int* nwork;
+    int* err;
+    unsigned long long* trace;  // debug timeline (null in production)
+};
+
+struct DustArgs {
+    int H, L_own, L_other, Lr_own, Lr_other;
+    float sd2;
+    const uint8_t* mask_other;
+    const float* dual_other;
+    const float* off_own;
+    float* out_own;
+    int* err;
+};
+
+long long phase_launch_count(bool reset);
+size_t phase_smem_bytes(const PhaseArgs& a);
+cudaError_t launch_phase(const PhaseArgs& a, bool first, int grid, cudaStream_t s);
+cudaError_t launch_dustbin(const DustArgs& a, bool first, int BH, cudaStream_t s);
+// [BH][Lr][d] (f32 or bf16) -> npl bf16 planes [BH][Lp][d] in the K-major core-matrix
+// layout, row r stored at packed row r + shift (other packed rows zero).
+cudaError_t launch_pack(int dtype, const void* X, int BH, int L, int Lr, int Lp, int d, int shift, uint8_t* p0,
+                        uint8_t* p1, uint8_t* p2, cudaStream_t s);
+cudaError_t launch_worklist(const uint8_t* mask, int H, int BH, int L, int NB, int* flags, int* work, int* count,
+                            cudaStream_t s);
+
+}  // namespace st
