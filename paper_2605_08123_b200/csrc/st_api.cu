@@ -64,6 +64,8 @@ st::Geo make_geo(const st_desc* d, const Dims& m, const uint8_t* rm, const uint8
     g.Lk = (int)m.Lk;
     g.Lrq = (int)m.Lrq;
     g.Lrk = (int)m.Lrk;
+    g.Lqp = (int)((m.Lq + 127) / 128 * 128);
+    g.Lkp = (int)((m.Lk + 127) / 128 * 128);
     g.d = (int)m.d;
     g.w = (int)m.w;
     g.Wf = (int)m.Wf;
@@ -139,7 +141,8 @@ TcPlan tc_plan(const st_desc* d, const Dims& m) {
 }
 
 struct WsLayout {
-    size_t S2, u, v, g_u, u2b, u1b, deps, g_v, v1b, v0b, err;
+    size_t Z, ZT, Zd, ZdT;  // tile backward bands
+    size_t S2, S2T, u, v, g_u, u2b, u1b, deps, g_v, v1b, v0b, err;
     size_t qp[3], kp[3], flags, work_q, work_k, cnt, bytes;
 };
 WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
@@ -151,7 +154,20 @@ WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
         return at;
     };
     const size_t rq = sizeof(float) * m.BH * m.Lrq, rk = sizeof(float) * m.BH * m.Lrk;
-    w.S2 = take(sizeof(float) * (size_t)m.BH * m.Lq * m.Wf);
+    const size_t Lqp = (m.Lq + 127) / 128 * 128, Lkp = (m.Lk + 127) / 128 * 128;
+    w.S2 = take(sizeof(float) * (size_t)m.BH * Lqp * m.Wf);
+    // transposed band (fp32 tile forward and the tile backward) and the cotangent bands
+    st::Geo gg{};
+    gg.d = (int)m.d;
+    gg.w = (int)m.w;
+    gg.Wf = (int)m.Wf;
+    const bool bt = st::bwdT_supported(gg);
+    const size_t band_q = sizeof(float) * (size_t)m.BH * Lqp * m.Wf, band_k = sizeof(float) * (size_t)m.BH * Lkp * m.Wf;
+    w.S2T = (!tp.ok || bt) ? take(band_k) : 0;
+    w.Z = bt ? take(band_q) : 0;
+    w.ZT = bt ? take(band_k) : 0;
+    w.Zd = bt ? take(sizeof(float) * (size_t)m.BH * Lqp) : 0;
+    w.ZdT = bt ? take(sizeof(float) * (size_t)m.BH * Lkp) : 0;
     w.u = take(rq);
     w.v = take(rk);
     w.g_u = take(rq);
@@ -355,12 +371,36 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
         ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));  // transport application (generic kernel)
     } else {
         ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));
+        const bool tile = st::stepT_smem_bytes(g) <= 227 * 1024;
+        float* S2T = (float*)(ws + wl.S2T);
+        if (tile) ST_CUDA(st::launch_transpose_band(g, S2, S2T, st, -INFINITY));
+        const st::Geo gt = st::transposed(g);
+        st::DustArgs dr{}, dc{};
+        dr.H = dc.H = g.H;
+        dr.sd2 = dc.sd2 = g.sd2;
+        dr.err = dc.err = err;
+        dr.L_own = g.Lq; dr.L_other = g.Lk; dr.Lr_own = g.Lrq; dr.Lr_other = g.Lrk; dr.mask_other = col_mask;
+        dc.L_own = g.Lk; dc.L_other = g.Lq; dc.Lr_own = g.Lrk; dc.Lr_other = g.Lrq; dc.mask_other = row_mask;
         for (long t = 1; t <= T + R; ++t) {
             const long r = t - T;
             float* u_out = (sv && r >= 0 && r <= 2) ? slot_u(r) : u_ws;
             float* v_out = (sv && r >= 0 && r <= 2) ? slot_v(r) : v_ws;
-            ST_CUDA(st::launch_row_step(g, t == 1, S2, v_prev, u_prev, u_out, err, st));
-            ST_CUDA(st::launch_col_step(g, t == 1, S2, u_out, v_prev, v_out, err, st));
+            if (tile) {
+                // fp32 path: bulk-copied band tiles, in-thread reductions; columns via the transposed band
+                ST_CUDA(st::launch_stepT(g, t == 1, S2, v_prev, u_prev, u_out, err, st));
+                if (g.dustbin) {
+                    dr.dual_other = v_prev; dr.off_own = u_prev; dr.out_own = u_out;
+                    ST_CUDA(st::launch_dustbin(dr, t == 1, g.BH, st));
+                }
+                ST_CUDA(st::launch_stepT(gt, t == 1, S2T, u_out, v_prev, v_out, err, st));
+                if (g.dustbin) {
+                    dc.dual_other = u_out; dc.off_own = v_prev; dc.out_own = v_out;
+                    ST_CUDA(st::launch_dustbin(dc, t == 1, g.BH, st));
+                }
+            } else {
+                ST_CUDA(st::launch_row_step(g, t == 1, S2, v_prev, u_prev, u_out, err, st));
+                ST_CUDA(st::launch_col_step(g, t == 1, S2, u_out, v_prev, v_out, err, st));
+            }
             u_prev = u_out;
             v_prev = v_out;
         }
@@ -415,7 +455,26 @@ st_status st_backward(const st_desc* desc, const void* saved, const void* Q, con
     p.dK = dK;
     p.dV = dV;
     ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, (float*)p.S2, st));
-    ST_CUDA(st::launch_backward(g, desc->dtype, p, mode == ST_DIRECT_FOUR_PLAN, st));
+    if (st::bwdT_supported(g) && !(desc->flags & ST_FLAG_GENERIC)) {
+        // tile backward: score band + transposes, cotangent band Z = dO V^T + transpose
+        st::BwdTPtrs t;
+        float* S2T = (float*)(ws + wl.S2T);
+        float* Z = (float*)(ws + wl.Z);
+        float* ZT = (float*)(ws + wl.ZT);
+        t.S2T = S2T;
+        t.Z = Z;
+        t.ZT = ZT;
+        t.Zd = (float*)(ws + wl.Zd);
+        t.ZdT = (float*)(ws + wl.ZdT);
+        ST_CUDA(st::launch_transpose_band(g, p.S2, S2T, st, -INFINITY));
+        ST_CUDA(st::launch_zband(g, desc->dtype, dO, V, Z, st));
+        ST_CUDA(st::launch_transpose_band(g, Z, ZT, st, 0.f));
+        long long nl = 0;
+        ST_CUDA(st::launch_backward_tile(g, desc->dtype, p, t, mode == ST_DIRECT_FOUR_PLAN, st, nl));
+        st::add_launches(nl);
+    } else {
+        ST_CUDA(st::launch_backward(g, desc->dtype, p, mode == ST_DIRECT_FOUR_PLAN, st));
+    }
     if (d_eps) ST_CUDA(st::launch_deps_reduce(g, p.deps_part, d_eps, st));
     return ST_OK;
 }

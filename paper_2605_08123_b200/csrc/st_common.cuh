@@ -23,6 +23,7 @@ struct Geo {
     int BH, H;       // heads = B*H, heads per example
     int Lq, Lk;      // rows / cols without the dustbin token
     int Lrq, Lrk;    // rows / cols of the stored tensors (+1 with the dustbin)
+    int Lqp, Lkp;    // rows / cols of the stored score bands (multiples of 128)
     int d, w, Wf;    // head dim, half band, full band 2w+1
     int dustbin;     // 0 / 1
     float sd2;       // base-2 dustbin score: -cost * log2(e) / eps
@@ -57,6 +58,21 @@ __device__ __forceinline__ float warp_max(float x) {
 __device__ __forceinline__ float ldf(const float* p) { return *p; }
 __device__ __forceinline__ float ldf(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 
+// the same geometry seen from the key side (rows <-> columns): the column
+// half-step is the row half-step of the transposed band
+__host__ __device__ inline Geo transposed(const Geo& g) {
+    Geo t = g;
+    t.Lq = g.Lk;
+    t.Lk = g.Lq;
+    t.Lrq = g.Lrk;
+    t.Lrk = g.Lrq;
+    t.Lqp = g.Lkp;
+    t.Lkp = g.Lqp;
+    t.row_mask = g.col_mask;
+    t.col_mask = g.row_mask;
+    return t;
+}
+
 __device__ __forceinline__ bool row_on(const Geo& g, int bh, int i) {
     if (i >= g.Lq) return true;  // the dustbin row (exists only when g.dustbin)
     return g.row_mask == nullptr || g.row_mask[(size_t)(bh / g.H) * g.Lq + i] != 0;
@@ -78,7 +94,7 @@ __device__ __forceinline__ void row_cell(const Geo& g, const float* __restrict__
             const int jj = i - g.w + k;
             if (jj >= 0 && jj < g.Lk) {
                 j = jj;
-                s2 = S2[((size_t)bh * g.Lq + i) * g.Wf + k];
+                s2 = S2[((size_t)bh * g.Lqp + i) * g.Wf + k];
             } else {
                 j = 0;
                 s2 = -INFINITY;
@@ -100,7 +116,7 @@ __device__ __forceinline__ void col_cell(const Geo& g, const float* __restrict__
             const int ii = j - g.w + k;
             if (ii >= 0 && ii < g.Lq) {
                 i = ii;
-                s2 = S2[((size_t)bh * g.Lq + ii) * g.Wf + (2 * g.w - k)];
+                s2 = S2[((size_t)bh * g.Lqp + ii) * g.Wf + (2 * g.w - k)];
             } else {
                 i = 0;
                 s2 = -INFINITY;

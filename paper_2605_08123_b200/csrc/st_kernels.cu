@@ -14,6 +14,7 @@
 
 #include "st_common.cuh"
 #include "st_kernels.cuh"
+#include "st_sm100.cuh"
 
 namespace st {
 
@@ -28,9 +29,10 @@ namespace st {
 constexpr int kScoreRows = 64;
 constexpr int kScoreChunk = 64;
 
-template <class TIn, bool kF64Acc>
+template <class TIn, bool kF64Acc, bool kZ>
 __global__ void __launch_bounds__(256) k_scores(Geo g, const TIn* __restrict__ Q, const TIn* __restrict__ K,
                                                 float* __restrict__ S2) {
+    // kZ: the output-cotangent band Z_ij = dO_i . V_j (Q := dO, K := V), unscaled, 0 off support
     extern __shared__ float smem[];
     const int dp = g.d + 1;  // padded row pitch: conflict-free column walks
     float* sq = smem;                          // [64][dp]
@@ -65,13 +67,13 @@ __global__ void __launch_bounds__(256) k_scores(Geo g, const TIn* __restrict__ Q
             if (kF64Acc) {
                 double acc = 0.0;
                 for (int x = 0; x < g.d; ++x) acc = fma((double)qa[x], (double)kb[x], acc);
-                val = (float)(acc * (double)g.c2);
+                val = kZ ? (float)acc : (float)(acc * (double)g.c2);
             } else {
                 float acc = 0.f;
                 for (int x = 0; x < g.d; ++x) acc = fmaf(qa[x], kb[x], acc);
-                val = acc * g.c2;
+                val = kZ ? acc : acc * g.c2;
             }
-            S2[((size_t)bh * g.Lq + i) * g.Wf + (j - i + g.w)] = val;
+            S2[((size_t)bh * g.Lqp + i) * g.Wf + (j - i + g.w)] = val;
         }
     }
     // off-support cells of this CTA's rows -> -inf (disjoint from the cells written above)
@@ -81,8 +83,97 @@ __global__ void __launch_bounds__(256) k_scores(Geo g, const TIn* __restrict__ Q
         if (ii >= g.Lq) continue;
         const int j = ii - g.w + k;
         const bool on = row_on(g, bh, ii) && j >= 0 && j < g.Lk && col_on(g, bh, j);
-        if (!on) S2[((size_t)bh * g.Lq + ii) * g.Wf + k] = -INFINITY;
+        if (!on) S2[((size_t)bh * g.Lqp + ii) * g.Wf + k] = kZ ? 0.f : -INFINITY;
     }
+}
+
+// ---------------------------------------------------------------------------
+// S2T[bh][j][k'] = S2[bh][j - w + k'][2w - k']  (the band seen from the key side;
+// -inf where the row is outside [0, Lq)).  Coalesced writes, L2-served gathers.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_transpose_band(Geo g, const float* __restrict__ S2, float* __restrict__ S2T,
+                                                        float fill) {
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long total = (long)g.BH * g.Lkp * g.Wf;
+    if (t >= total) return;
+    const int kp = (int)(t % g.Wf);
+    const long rj = t / g.Wf;
+    const int j = (int)(rj % g.Lkp), bh = (int)(rj / g.Lkp);
+    const int i = j - g.w + kp;
+    float v = fill;
+    if (j < g.Lk && i >= 0 && i < g.Lq) v = S2[((size_t)bh * g.Lqp + i) * g.Wf + (2 * g.w - kp)];
+    S2T[t] = v;
+}
+
+// ---------------------------------------------------------------------------
+// Tile half-step over a stored band (fp32 path).  One CTA = 128 rows of one
+// head: the 128 x Wf band tile is contiguous in HBM/L2 and lands in SMEM with a
+// single bulk async copy (TMA engine); the window duals land beside it; thread
+// r owns row i0 + r and reduces in-thread (stride Wf is odd: conflict-free).
+// The column half-step runs this kernel on the transposed band.
+// ---------------------------------------------------------------------------
+template <bool kFirst>
+__global__ void __launch_bounds__(128) k_stepT(Geo g, const float* __restrict__ S2, const float* __restrict__ dual_other,
+                                               const float* off_own, float* out_own, int* err) {
+    extern __shared__ __align__(16) float smf[];
+    __shared__ __align__(8) uint64_t bar;
+    const int bh = blockIdx.y, i0 = blockIdx.x * 128, r = threadIdx.x, i = i0 + r;
+    const bool active = i < g.Lq && row_on(g, bh, i);
+    if (!__syncthreads_or(active)) {
+        if (i < g.Lq) out_own[(size_t)bh * g.Lrq + i] = 0.f;
+        return;
+    }
+    float* tile = smf;
+    float* vw = smf + 128 * g.Wf;
+    if (threadIdx.x == 0) {
+        sm100::mbar_init(&bar, 1);
+        sm100::fence_mbar_init();
+    }
+    __syncthreads();
+    const uint32_t bytes = 128u * (uint32_t)g.Wf * 4u;
+    if (threadIdx.x == 0) {
+        sm100::mbar_arrive_expect_tx(&bar, bytes);
+        sm100::bulk_g2s(tile, S2 + ((size_t)bh * g.Lqp + i0) * g.Wf, bytes, &bar);
+    }
+    const float* dual = dual_other + (size_t)bh * g.Lrk;
+    for (int c = threadIdx.x; c < 128 + 2 * g.w; c += 128) {
+        const int j = i0 - g.w + c;
+        vw[c] = (j >= 0 && j < g.Lk && col_on(g, bh, j)) ? dual[j] : -INFINITY;
+    }
+    __syncthreads();
+    sm100::mbar_wait(&bar, 0);
+    if (i >= g.Lq) return;
+    float u = 0.f;
+    if (active) {
+        const float* trow = tile + r * g.Wf;
+        const float* vr = vw + r;
+        const float xd = g.dustbin ? g.sd2 + dual[g.Lk] : -INFINITY;  // spoke cell (i, dustbin)
+        float o;
+        if (kFirst) {
+            float m = xd;
+            for (int k = 0; k < g.Wf; ++k) m = fmaxf(m, trow[k] + vr[k]);
+            o = -m;
+        } else {
+            o = off_own[(size_t)bh * g.Lrq + i];
+        }
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        int k = 0;
+        for (; k + 4 <= g.Wf; k += 4) {
+            s0 += ex2(trow[k] + vr[k] + o);
+            s1 += ex2(trow[k + 1] + vr[k + 1] + o);
+            s2 += ex2(trow[k + 2] + vr[k + 2] + o);
+            s3 += ex2(trow[k + 3] + vr[k + 3] + o);
+        }
+        for (; k < g.Wf; ++k) s0 += ex2(trow[k] + vr[k] + o);
+        float s = (s0 + s1) + (s2 + s3);
+        if (g.dustbin) s += ex2(xd + o);
+        u = o - lg2(s);
+        if (!(s > 0.f) || !isfinite(u)) {
+            atomicOr(err, 16);
+            u = 0.f;
+        }
+    }
+    out_own[(size_t)bh * g.Lrq + i] = u;
 }
 
 // ---------------------------------------------------------------------------
@@ -288,12 +379,12 @@ enum { RB_GU = 0, RB_U2B = 1, RB_U1B = 2, RB_DQ = 3 };
 enum { CB_GV = 0, CB_V1B = 1, CB_V0B = 2, CB_DK = 3 };
 
 template <int kOp, bool kDirect, class TIn>
-__global__ void __launch_bounds__(256) k_bwd_row(Geo g, BwdArgs<TIn> a) {
+__global__ void __launch_bounds__(256) k_bwd_row(Geo g, BwdArgs<TIn> a, int last_only) {
     __shared__ float sh_vec[8][128];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const long gw = (long)blockIdx.x * 8 + wid;
-    if (gw >= (long)g.BH * g.Lrq) return;
-    const int bh = (int)(gw / g.Lrq), i = (int)(gw % g.Lrq);
+    if (gw >= (long)g.BH * (last_only ? 1 : g.Lrq)) return;
+    const int bh = last_only ? (int)gw : (int)(gw / g.Lrq), i = last_only ? g.Lrq - 1 : (int)(gw % g.Lrq);
     const size_t ri = (size_t)bh * g.Lrq + i;
     const size_t cbase = (size_t)bh * g.Lrk;
     const bool on = row_on(g, bh, i);
@@ -384,12 +475,12 @@ __global__ void __launch_bounds__(256) k_bwd_row(Geo g, BwdArgs<TIn> a) {
 }
 
 template <int kOp, bool kDirect, class TIn>
-__global__ void __launch_bounds__(256) k_bwd_col(Geo g, BwdArgs<TIn> a) {
+__global__ void __launch_bounds__(256) k_bwd_col(Geo g, BwdArgs<TIn> a, int last_only) {
     __shared__ float sh_vec[8][128];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const long gw = (long)blockIdx.x * 8 + wid;
-    if (gw >= (long)g.BH * g.Lrk) return;
-    const int bh = (int)(gw / g.Lrk), j = (int)(gw % g.Lrk);
+    if (gw >= (long)g.BH * (last_only ? 1 : g.Lrk)) return;
+    const int bh = last_only ? (int)gw : (int)(gw / g.Lrk), j = last_only ? g.Lrk - 1 : (int)(gw % g.Lrk);
     const size_t cj = (size_t)bh * g.Lrk + j;
     const size_t rbase = (size_t)bh * g.Lrq;
     const bool on = col_on(g, bh, j);
@@ -504,6 +595,7 @@ __global__ void k_scale(const float* __restrict__ src, float* __restrict__ dst, 
 // Launchers
 // ---------------------------------------------------------------------------
 static thread_local long long g_launches = 0;
+void add_launches(long long n) { g_launches += n; }
 long long launch_count(bool reset) {
     const long long c = g_launches;
     if (reset) g_launches = 0;
@@ -515,13 +607,29 @@ cudaError_t launch_scores(const Geo& g, int dtype, const void* Q, const void* K,
     const size_t smem = (size_t)2 * kScoreRows * (g.d + 1) * sizeof(float);
     dim3 grid((g.Lq + kScoreRows - 1) / kScoreRows, g.BH);
     if (dtype == 0) {
-        auto kern = k_scores<float, true>;
+        auto kern = k_scores<float, true, false>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, 256, smem, s>>>(g, (const float*)Q, (const float*)K, S2);
     } else {
-        auto kern = k_scores<__nv_bfloat16, false>;
+        auto kern = k_scores<__nv_bfloat16, false, false>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, 256, smem, s>>>(g, (const __nv_bfloat16*)Q, (const __nv_bfloat16*)K, S2);
+    }
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_zband(const Geo& g, int dtype, const void* dO, const void* V, float* Z, cudaStream_t s) {
+    const size_t smem = (size_t)2 * kScoreRows * (g.d + 1) * sizeof(float);
+    dim3 grid((g.Lq + kScoreRows - 1) / kScoreRows, g.BH);
+    if (dtype == 0) {
+        auto kern = k_scores<float, false, true>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, 256, smem, s>>>(g, (const float*)dO, (const float*)V, Z);
+    } else {
+        auto kern = k_scores<__nv_bfloat16, false, true>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, 256, smem, s>>>(g, (const __nv_bfloat16*)dO, (const __nv_bfloat16*)V, Z);
     }
     ++g_launches;
     return cudaGetLastError();
@@ -532,6 +640,31 @@ cudaError_t launch_row_step(const Geo& g, bool first, const float* S2, const flo
     const unsigned nb = nblocks((long)g.BH * g.Lrq, 8);
     if (first) k_row_step<true><<<nb, 256, 0, s>>>(g, S2, v, u_prev, u_out, err);
     else k_row_step<false><<<nb, 256, 0, s>>>(g, S2, v, u_prev, u_out, err);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_transpose_band(const Geo& g, const float* S2, float* S2T, cudaStream_t s, float fill) {
+    const long total = (long)g.BH * g.Lkp * g.Wf;
+    k_transpose_band<<<nblocks(total, 256), 256, 0, s>>>(g, S2, S2T, fill);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+size_t stepT_smem_bytes(const Geo& g) { return (size_t)128 * g.Wf * 4 + (size_t)(128 + 2 * g.w) * 4 + 16; }
+
+cudaError_t launch_stepT(const Geo& g, bool first, const float* S2, const float* dual_other, const float* off_own,
+                         float* out_own, int* err, cudaStream_t s) {
+    const size_t smem = stepT_smem_bytes(g);
+    auto k = first ? k_stepT<true> : k_stepT<false>;
+    static size_t set_true = 0, set_false = 0;
+    size_t& cur = first ? set_true : set_false;
+    if (smem > cur) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        cur = smem;
+    }
+    k<<<dim3((g.Lq + 127) / 128, g.BH), 128, smem, s>>>(g, S2, dual_other, off_own, out_own, err);
     ++g_launches;
     return cudaGetLastError();
 }
@@ -590,37 +723,92 @@ static cudaError_t run_backward_t(const Geo& g, const BwdPtrs& p, bool direct, c
         ++g_launches;                            \
         if ((e = cudaGetLastError()) != cudaSuccess) return e; \
     } while (0)
-    k_bwd_row<RB_GU, false, TIn><<<nr, 256, 0, s>>>(g, a);
+    k_bwd_row<RB_GU, false, TIn><<<nr, 256, 0, s>>>(g, a, 0);
     ST_CHECK_LAUNCH();
-    k_bwd_col<CB_GV, false, TIn><<<nc, 256, 0, s>>>(g, a);
+    k_bwd_col<CB_GV, false, TIn><<<nc, 256, 0, s>>>(g, a, 0);
     ST_CHECK_LAUNCH();
-    k_bwd_row<RB_U2B, false, TIn><<<nr, 256, 0, s>>>(g, a);
+    k_bwd_row<RB_U2B, false, TIn><<<nr, 256, 0, s>>>(g, a, 0);
     ST_CHECK_LAUNCH();
     if (direct) {
-        k_bwd_col<CB_V1B, true, TIn><<<nc, 256, 0, s>>>(g, a);
+        k_bwd_col<CB_V1B, true, TIn><<<nc, 256, 0, s>>>(g, a, 0);
         ST_CHECK_LAUNCH();
-        k_bwd_row<RB_U1B, true, TIn><<<nr, 256, 0, s>>>(g, a);
+        k_bwd_row<RB_U1B, true, TIn><<<nr, 256, 0, s>>>(g, a, 0);
         ST_CHECK_LAUNCH();
-        k_bwd_col<CB_V0B, true, TIn><<<nc, 256, 0, s>>>(g, a);
+        k_bwd_col<CB_V0B, true, TIn><<<nc, 256, 0, s>>>(g, a, 0);
         ST_CHECK_LAUNCH();
-        k_bwd_row<RB_DQ, true, TIn><<<nr, 256, 0, s>>>(g, a);
+        k_bwd_row<RB_DQ, true, TIn><<<nr, 256, 0, s>>>(g, a, 0);
         ST_CHECK_LAUNCH();
-        k_bwd_col<CB_DK, true, TIn><<<nc, 256, 0, s>>>(g, a);
+        k_bwd_col<CB_DK, true, TIn><<<nc, 256, 0, s>>>(g, a, 0);
         ST_CHECK_LAUNCH();
     } else {
-        k_bwd_col<CB_V1B, false, TIn><<<nc, 256, 0, s>>>(g, a);
+        k_bwd_col<CB_V1B, false, TIn><<<nc, 256, 0, s>>>(g, a, 0);
         ST_CHECK_LAUNCH();
-        k_bwd_row<RB_U1B, false, TIn><<<nr, 256, 0, s>>>(g, a);
+        k_bwd_row<RB_U1B, false, TIn><<<nr, 256, 0, s>>>(g, a, 0);
         ST_CHECK_LAUNCH();
-        k_bwd_col<CB_V0B, false, TIn><<<nc, 256, 0, s>>>(g, a);
+        k_bwd_col<CB_V0B, false, TIn><<<nc, 256, 0, s>>>(g, a, 0);
         ST_CHECK_LAUNCH();
-        k_bwd_row<RB_DQ, false, TIn><<<nr, 256, 0, s>>>(g, a);
+        k_bwd_row<RB_DQ, false, TIn><<<nr, 256, 0, s>>>(g, a, 0);
         ST_CHECK_LAUNCH();
-        k_bwd_col<CB_DK, false, TIn><<<nc, 256, 0, s>>>(g, a);
+        k_bwd_col<CB_DK, false, TIn><<<nc, 256, 0, s>>>(g, a, 0);
         ST_CHECK_LAUNCH();
     }
 #undef ST_CHECK_LAUNCH
     return cudaSuccess;
+}
+
+template <class TIn>
+static BwdArgs<TIn> bwd_args(const BwdPtrs& p) {
+    BwdArgs<TIn> a;
+    a.S2 = p.S2;
+    a.u1 = p.u1;
+    a.u2 = p.u2;
+    a.v0 = p.v0;
+    a.v1 = p.v1;
+    a.v2 = p.v2;
+    a.g_u = p.g_u;
+    a.g_v = p.g_v;
+    a.u2b = p.u2b;
+    a.v1b = p.v1b;
+    a.u1b = p.u1b;
+    a.v0b = p.v0b;
+    a.Q = (const TIn*)p.Q;
+    a.K = (const TIn*)p.K;
+    a.V = (const TIn*)p.V;
+    a.dO = (const TIn*)p.dO;
+    a.dQ = p.dQ;
+    a.dK = p.dK;
+    a.dV = p.dV;
+    a.deps_part = p.deps_part;
+    return a;
+}
+
+template <class TIn, bool kD>
+static cudaError_t dust_stage_t(const Geo& g, const BwdPtrs& p, int stage, cudaStream_t s) {
+    const BwdArgs<TIn> a = bwd_args<TIn>(p);
+    const unsigned nb = nblocks(g.BH, 8);
+    switch (stage) {
+        case 0:
+            k_bwd_row<RB_GU, kD, TIn><<<nb, 256, 0, s>>>(g, a, 1);
+            k_bwd_col<CB_GV, kD, TIn><<<nb, 256, 0, s>>>(g, a, 1);
+            g_launches += 2;
+            break;
+        case 1: k_bwd_row<RB_U2B, kD, TIn><<<nb, 256, 0, s>>>(g, a, 1); ++g_launches; break;
+        case 2: k_bwd_col<CB_V1B, kD, TIn><<<nb, 256, 0, s>>>(g, a, 1); ++g_launches; break;
+        case 3: k_bwd_row<RB_U1B, kD, TIn><<<nb, 256, 0, s>>>(g, a, 1); ++g_launches; break;
+        case 4: k_bwd_col<CB_V0B, kD, TIn><<<nb, 256, 0, s>>>(g, a, 1); ++g_launches; break;
+        default:
+            k_bwd_row<RB_DQ, kD, TIn><<<nb, 256, 0, s>>>(g, a, 1);
+            k_bwd_col<CB_DK, kD, TIn><<<nb, 256, 0, s>>>(g, a, 1);
+            g_launches += 2;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_backward_dustbin_stage(const Geo& g, int dtype, const BwdPtrs& p, bool direct, int stage,
+                                          cudaStream_t s) {
+    if (dtype == 0) return direct ? dust_stage_t<float, true>(g, p, stage, s) : dust_stage_t<float, false>(g, p, stage, s);
+    return direct ? dust_stage_t<__nv_bfloat16, true>(g, p, stage, s)
+                  : dust_stage_t<__nv_bfloat16, false>(g, p, stage, s);
 }
 
 cudaError_t launch_backward(const Geo& g, int dtype, const BwdPtrs& p, bool direct, cudaStream_t s) {

@@ -15,11 +15,30 @@ struct BwdPtrs {
     float *dQ, *dK, *dV, *deps_part;
 };
 
+// extra bands of the tile backward (st_bwd.cu)
+struct BwdTPtrs {
+    const float *S2T, *Z, *ZT;
+    float *Zd, *ZdT;
+};
+
 long long launch_count(bool reset);
+void add_launches(long long n);
+size_t bwdT_smem_bytes(const Geo& g);
+bool bwdT_supported(const Geo& g);
+cudaError_t launch_backward_tile(const Geo& g, int dtype, const BwdPtrs& p, const BwdTPtrs& t, bool direct,
+                                 cudaStream_t s, long long& launches);
+// the dustbin row / column of one backward stage through the generic sweeps
+cudaError_t launch_backward_dustbin_stage(const Geo& g, int dtype, const BwdPtrs& p, bool direct, int stage,
+                                          cudaStream_t s);
 
 cudaError_t launch_scores(const Geo& g, int dtype, const void* Q, const void* K, float* S2, cudaStream_t s);
 cudaError_t launch_row_step(const Geo& g, bool first, const float* S2, const float* v, const float* u_prev,
                             float* u_out, int* err, cudaStream_t s);
+cudaError_t launch_transpose_band(const Geo& g, const float* S2, float* S2T, cudaStream_t s, float fill);
+cudaError_t launch_zband(const Geo& g, int dtype, const void* dO, const void* V, float* Z, cudaStream_t s);
+size_t stepT_smem_bytes(const Geo& g);
+cudaError_t launch_stepT(const Geo& g, bool first, const float* S2, const float* dual_other, const float* off_own,
+                         float* out_own, int* err, cudaStream_t s);
 cudaError_t launch_col_step(const Geo& g, bool first, const float* S2, const float* u, const float* v_prev,
                             float* v_out, int* err, cudaStream_t s);
 cudaError_t launch_output(const Geo& g, int dtype, const float* S2, const float* u, const float* v, const void* V,
