@@ -143,8 +143,20 @@ TcPlan tc_plan(const st_desc* d, const Dims& m) {
 struct WsLayout {
     size_t Z, ZT, Zd, ZdT;  // tile backward bands
     size_t S2, S2T, u, v, g_u, u2b, u1b, deps, g_v, v1b, v0b, err;
-    size_t qp[3], kp[3], flags, work_q, work_k, cnt, bytes;
+    size_t qp[3], kp[3], flags, work_q, work_k, cnt;
+    size_t vb2, part[2], partm;  // fused-step ping-pong duals and column partials
+    size_t bytes;
 };
+
+// fused full-step forward (k_fstep): fp32 stored band, square, no dustbin
+bool fused_ok(const st_desc* d, const Dims& m) {
+    if (d->flags & ST_FLAG_GENERIC) return false;
+    if (d->dustbin || m.Lq != m.Lk) return false;
+    st::Geo g{};
+    g.w = (int)m.w;
+    g.Wf = (int)m.Wf;
+    return st::fstep_smem_bytes(g) <= 227 * 1024 && !getenv("ST_NO_FUSED");
+}
 WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
     WsLayout w;
     size_t o = 0;
@@ -180,6 +192,13 @@ WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
     w.err = take(sizeof(int));
     for (int p = 0; p < 3; ++p) w.qp[p] = w.kp[p] = 0;
     w.flags = w.work_q = w.work_k = w.cnt = 0;
+    w.vb2 = take(rk);
+    {
+        const size_t np = sizeof(float) * (size_t)m.BH * ((m.Lq + 127) / 128) * (128 + 2 * m.w);
+        w.part[0] = take(np);
+        w.part[1] = take(np);
+        w.partm = take(np);
+    }
     if (tp.ok) {
         for (int p = 0; p < tp.npl; ++p) {
             w.qp[p] = take((size_t)m.BH * tp.Lpq * tp.row_bytes);
@@ -371,6 +390,39 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
         ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));  // transport application (generic kernel)
     } else {
         ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));
+        if (fused_ok(desc, m) && T + R >= 1) {
+            // one launch per full step; the column half-step rides on the row exponentials
+            float* vbuf[2] = {v_ws, (float*)(ws + wl.vb2)};
+            float* part[2] = {(float*)(ws + wl.part[0]), (float*)(ws + wl.part[1])};
+            float* partm = (float*)(ws + wl.partm);
+            st::FStepPtrs p{};
+            p.S2 = S2;
+            p.err = err;
+            for (long t = 1; t <= T + R; ++t) {
+                const long r = t - T;
+                float* u_out = (sv && r >= 0 && r <= 2) ? slot_u(r) : u_ws;
+                p.u_prev = u_prev;
+                p.u_out = u_out;
+                p.v_pp = (t >= 3) ? vbuf[(t - 2) & 1] : nullptr;
+                p.v_p_out = (t >= 2) ? vbuf[(t - 1) & 1] : nullptr;
+                const long rv = t - 1 - T;
+                p.v_p_slot = (t >= 2 && sv && rv >= 0 && rv <= 2) ? slot_v(rv) : nullptr;
+                p.part_in = (t >= 2) ? part[(t - 1) & 1] : nullptr;
+                p.partm_in = partm;
+                p.part_out = part[t & 1];
+                p.partm_out = partm;
+                ST_CUDA(st::launch_fstep(g, (int)t, p, st));
+                u_prev = u_out;
+            }
+            const long tl = T + R;
+            p.v_pp = (tl >= 2) ? vbuf[(tl - 1) & 1] : nullptr;
+            p.v_p_out = vbuf[tl & 1];
+            p.v_p_slot = (sv && R <= 2) ? slot_v(R) : nullptr;
+            p.part_in = part[tl & 1];
+            p.partm_in = partm;
+            ST_CUDA(st::launch_ffinal(g, (int)tl, p, st));
+            v_prev = vbuf[tl & 1];
+        } else {
         const bool tile = st::stepT_smem_bytes(g) <= 227 * 1024;
         float* S2T = (float*)(ws + wl.S2T);
         if (tile) ST_CUDA(st::launch_transpose_band(g, S2, S2T, st, -INFINITY));
@@ -404,8 +456,14 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
             u_prev = u_out;
             v_prev = v_out;
         }
+        }
     }
-    ST_CUDA(st::launch_output(g, desc->dtype, S2, u_prev, v_prev, V, O, st));
+    if (st::bwdT_supported(g) && !(desc->flags & ST_FLAG_GENERIC)) {
+        ST_CUDA(st::launch_output_tile(g, desc->dtype, S2, u_prev, v_prev, V, O, st));
+        if (g.dustbin) ST_CUDA(st::launch_output(g, desc->dtype, S2, u_prev, v_prev, V, O, st, 1));
+    } else {
+        ST_CUDA(st::launch_output(g, desc->dtype, S2, u_prev, v_prev, V, O, st));
+    }
     if (sv) {
         const int nslots = (int)std::min<long>(R, 2) + 1;
         ST_CUDA(st::launch_gauges(g, su, nslots, (float*)(sv + sl.gauge), st));

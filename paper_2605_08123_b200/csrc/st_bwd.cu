@@ -14,6 +14,8 @@
 // The band tile of each CTA is contiguous in memory and arrives with one 1-D
 // bulk async copy per band; window vectors and operand rows are staged beside it.
 // The dustbin row / column (full-length reductions) run in the generic kernels.
+#include <type_traits>
+
 #include "st_common.cuh"
 #include "st_kernels.cuh"
 #include "st_sm100.cuh"
@@ -30,9 +32,10 @@ struct BT {
     float *g_u, *g_v, *u2b, *v1b, *u1b, *v0b;
     const TIn *Q, *K, *V, *dO;
     float *dQ, *dK, *dV, *deps_part;
+    float* O;  // transport output (RO)
 };
 
-enum { R1 = 0, R2 = 1, R4 = 2, R6 = 3, C1 = 10, C3 = 11, C5 = 12, C6 = 13 };
+enum { R1 = 0, R2 = 1, R4 = 2, R6 = 3, RO = 4, C1 = 10, C3 = 11, C5 = 12, C6 = 13 };
 
 __device__ __forceinline__ float sbar_of(bool direct, float s2, float p22, float z, float u1i, float u2i,
                                          float v0j, float v1j, float v2j, float u2bi, float u1bi, float v2bj,
@@ -55,7 +58,7 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
     __shared__ __align__(8) uint64_t bar;
     constexpr bool kRow = kOp < 10;
     constexpr bool kNeedZ = (kOp == R1 || kOp == R6 || kOp == C1 || kOp == C6);
-    constexpr bool kVec = (kOp == R6 || kOp == C1 || kOp == C6);
+    constexpr bool kVec = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RO);
     // own = rows (row stages) or columns (column stages)
     const int Lo = kRow ? g.Lq : g.Lk, Lx = kRow ? g.Lk : g.Lq;
     const int Lro = kRow ? g.Lrq : g.Lrk, Lrx = kRow ? g.Lrk : g.Lrq;
@@ -77,7 +80,7 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
             if (kOp == C1) a.g_v[bo + i] = 0.f;
             if (kOp == C3) a.v1b[bo + i] = 0.f;
             if (kOp == C5) a.v0b[bo + i] = 0.f;
-            float* vo = kOp == R6 ? a.dQ : kOp == C1 ? a.dV : kOp == C6 ? a.dK : nullptr;
+            float* vo = kOp == R6 ? a.dQ : kOp == C1 ? a.dV : kOp == C6 ? a.dK : kOp == RO ? a.O : nullptr;
             if (kVec)
                 for (int x = 0; x < g.d; ++x) vo[(bo + i) * g.d + x] = 0.f;
         }
@@ -127,7 +130,7 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
         wv[3 * Nw + c] = w3;
         wv[4 * Nw + c] = w4;
         if (kVec) {
-            const TIn* src = (kOp == R6) ? a.K : (kOp == C1) ? a.dO : a.Q;
+            const TIn* src = (kOp == R6) ? a.K : (kOp == C1) ? a.dO : (kOp == RO) ? a.V : a.Q;
             for (int e = 0; e < D; ++e)
                 ops[c * (D + 4) + e] = (x >= 0 && x < Lx && e < g.d) ? ldf(src + (bx + x) * g.d + e) : 0.f;
         }
@@ -143,7 +146,7 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
         if (kOp == C1) a.g_v[bo + i] = 0.f;
         if (kOp == C3) a.v1b[bo + i] = 0.f;
         if (kOp == C5) a.v0b[bo + i] = 0.f;
-        float* vo = kOp == R6 ? a.dQ : kOp == C1 ? a.dV : kOp == C6 ? a.dK : nullptr;
+        float* vo = kOp == R6 ? a.dQ : kOp == C1 ? a.dV : kOp == C6 ? a.dK : kOp == RO ? a.O : nullptr;
         if (kVec)
             for (int x = 0; x < g.d; ++x) vo[(bo + i) * g.d + x] = 0.f;
         return;
@@ -182,6 +185,8 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
         if (kOp == R1 || kOp == C1) {
             acc += p * tz[k];
             wgt = p;
+        } else if (kOp == RO) {
+            wgt = p;
         } else if (kOp == R2) {
             acc += p * wv[3 * Nw + c];
         } else if (kOp == R4) {
@@ -216,8 +221,11 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
         const float x2 = kRow ? a.v2[bx + xd] : a.u2[bx + xd];
         const float x1 = kRow ? a.v1[bx + xd] : a.u1[bx + xd];
         const float p = ex2(s2 + o2 + x2);
-        const float z = kRow ? a.Zd[(size_t)bh * g.Lqp + i] : a.ZdT[(size_t)bh * g.Lkp + i];
-        if (kOp == R1 || kOp == C1) {
+        const float z = (kOp == RO) ? 0.f : kRow ? a.Zd[(size_t)bh * g.Lqp + i] : a.ZdT[(size_t)bh * g.Lkp + i];
+        if (kOp == RO) {  // O_i += p * V_dustbin
+#pragma unroll
+            for (int e = 0; e < (kVec ? D : 1); ++e) vacc[e] = fmaf(p, ldf(a.V + (bx + xd) * g.d + e), vacc[e]);
+        } else if (kOp == R1 || kOp == C1) {
             acc += p * z;
             if (kOp == C1) {  // dV_j += p * dO_dustbin
 #pragma unroll
@@ -246,8 +254,8 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
     if (kOp == C5) a.v0b[bo + i] = kDirect ? -acc : -ex2(o0 - o2) * acc;
     if (kOp == R6) a.deps_part[bo + i] = dacc;
     if (kVec) {
-        float* vo = kOp == R6 ? a.dQ : kOp == C1 ? a.dV : a.dK;
-        const float sc = kOp == C1 ? 1.f : g.inv_qk;
+        float* vo = kOp == R6 ? a.dQ : kOp == C1 ? a.dV : kOp == RO ? a.O : a.dK;
+        const float sc = (kOp == C1 || kOp == RO) ? 1.f : g.inv_qk;
 #pragma unroll
         for (int e = 0; e < (kVec ? D : 1); ++e) vo[(bo + i) * g.d + e] = vacc[e] * sc;
     }
@@ -361,6 +369,31 @@ static cudaError_t run_all(const Geo& g, const BwdPtrs& p, const BwdTPtrs& t, in
 #undef ST_RUN
 #undef ST_DUST
     return cudaSuccess;
+}
+
+// O = P^(T+R,T+R) V on the stored band (apply_transport, sinkhorn.hpp:262-277): the RO row stage
+cudaError_t launch_output_tile(const Geo& g, int dtype, const float* S2, const float* u, const float* v, const void* V,
+                               float* O, cudaStream_t s) {
+    auto go = [&](auto tag, auto dtag) -> cudaError_t {
+        using TIn = decltype(tag);
+        constexpr int D = decltype(dtag)::value;
+        BT<TIn> a{};
+        a.S2 = S2;
+        a.u2 = u;
+        a.u1 = u;
+        a.v2 = v;
+        a.v1 = v;
+        a.v0 = v;
+        a.V = (const TIn*)V;
+        a.O = O;
+        return run_op<RO, false, D, TIn>(g, a, s);
+    };
+    cudaError_t e;
+    if (g.d == 32) e = dtype == 0 ? go(float{}, std::integral_constant<int, 32>{}) : go(__nv_bfloat16{}, std::integral_constant<int, 32>{});
+    else if (g.d == 64) e = dtype == 0 ? go(float{}, std::integral_constant<int, 64>{}) : go(__nv_bfloat16{}, std::integral_constant<int, 64>{});
+    else e = dtype == 0 ? go(float{}, std::integral_constant<int, 128>{}) : go(__nv_bfloat16{}, std::integral_constant<int, 128>{});
+    add_launches(1);
+    return e;
 }
 
 cudaError_t launch_backward_tile(const Geo& g, int dtype, const BwdPtrs& p, const BwdTPtrs& t, bool direct,

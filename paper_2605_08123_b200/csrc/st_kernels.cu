@@ -11,6 +11,7 @@
 // Every reduction is owned by one warp (one row or one column), so results are
 // deterministic and independent of launch geometry.
 #include <cstdio>
+#include <type_traits>
 
 #include "st_common.cuh"
 #include "st_kernels.cuh"
@@ -19,71 +20,197 @@
 namespace st {
 
 // ---------------------------------------------------------------------------
-// Scores: S2[bh][i][k] for j = i - w + k.  One CTA = 64 query rows x one head;
-// the key window [i0-w, i0+63+w] streams through shared memory in 64-row
-// chunks.  fp32 inputs accumulate in f64 (products of floats are exact in
-// f64), so the stored score is the correctly rounded fp32 value; bf16 inputs
-// accumulate in fp32 (bf16 products are exact in fp32), the tensor-core
-// contract.
+// Band dot products: S2[bh][i][k] = (q_i . k_j) * c2 for j = i - w + k (kZ: the
+// cotangent band Z = dO_i . V_j, unscaled).  One CTA = 64 rows x one head; the
+// row tile and the column window [i0-w, i0+63+w] sit K-major in SMEM (x-major,
+// float4 reads), 256 threads each own a 4 x 4 micro-tile per 64-column block.
+// fp32 inputs accumulate in f64 (products of floats are exact in f64, so the
+// stored score is the correctly rounded fp32 value); bf16 inputs accumulate in
+// fp32 (bf16 products are exact in fp32), the tensor-core contract.
+// Off-support cells: -inf (scores) / 0 (Z).
 // ---------------------------------------------------------------------------
 constexpr int kScoreRows = 64;
-constexpr int kScoreChunk = 64;
 
-template <class TIn, bool kF64Acc, bool kZ>
+template <class TIn, class TAcc, bool kZ>
 __global__ void __launch_bounds__(256) k_scores(Geo g, const TIn* __restrict__ Q, const TIn* __restrict__ K,
                                                 float* __restrict__ S2) {
-    // kZ: the output-cotangent band Z_ij = dO_i . V_j (Q := dO, K := V), unscaled, 0 off support
-    extern __shared__ float smem[];
-    const int dp = g.d + 1;  // padded row pitch: conflict-free column walks
-    float* sq = smem;                          // [64][dp]
-    float* sk = smem + kScoreRows * dp;        // [64][dp]
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* smem = reinterpret_cast<float*>(smem_raw);
     const int bh = blockIdx.y;
     const int i0 = blockIdx.x * kScoreRows;
+    const int ncol = ((kScoreRows + 2 * g.w + 63) / 64) * 64;  // window columns, padded to 64
+    const int c0 = i0 - g.w;                                     // original column of window column 0
+    const int dp = g.d + 1;                                      // odd pitch: conflict-free column walks
+    float* sq = smem;                                            // [64][dp]
+    float* sk = smem + kScoreRows * dp;                          // [ncol][dp]
     const int tid = threadIdx.x;
     const TIn* Qh = Q + (size_t)bh * g.Lrq * g.d;
     const TIn* Kh = K + (size_t)bh * g.Lrk * g.d;
-    for (int e = tid; e < kScoreRows * g.d; e += blockDim.x) {
+    for (int e = tid; e < kScoreRows * g.d; e += 256) {
         const int r = e / g.d, x = e % g.d;
-        sq[r * dp + x] = (i0 + r < g.Lq) ? ldf(Qh + (size_t)(i0 + r) * g.d + x) : 0.f;
+        sq[r * dp + x] = ((i0 + r < g.Lq) ? ldf(Qh + (size_t)(i0 + r) * g.d + x) : 0.f);
     }
-    const int jlo = max(0, i0 - g.w), jhi = min(g.Lk - 1, i0 + kScoreRows - 1 + g.w);
-    const int r = tid >> 2;          // 4 threads per row
-    const int i = i0 + r;
-    const bool row_ok = i < g.Lq && row_on(g, bh, i);
-    for (int c0 = jlo; c0 <= jhi; c0 += kScoreChunk) {
-        __syncthreads();
-        for (int e = tid; e < kScoreChunk * g.d; e += blockDim.x) {
-            const int rr = e / g.d, x = e % g.d;
-            sk[rr * dp + x] = (c0 + rr <= jhi) ? ldf(Kh + (size_t)(c0 + rr) * g.d + x) : 0.f;
+    for (int e = tid; e < ncol * g.d; e += 256) {
+        const int c = e / g.d, x = e % g.d;
+        const int j = c0 + c;
+        sk[c * dp + x] = ((j >= 0 && j < g.Lk) ? ldf(Kh + (size_t)j * g.d + x) : 0.f);
+    }
+    __syncthreads();
+    // thread (ty, tx) owns rows ty + 16a and columns cb + tx + 16b (a, b < 4) of each 64-column block
+    const int ty = tid >> 4, tx = tid & 15;
+    for (int cb = 0; cb < ncol; cb += 64) {
+        TAcc acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = TAcc(0);
+        const float* qr = sq + ty * dp;
+        const float* kr = sk + (cb + tx) * dp;
+#pragma unroll 4
+        for (int x = 0; x < g.d; ++x) {
+            TAcc q4[4], k4[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) q4[a] = (TAcc)qr[16 * a * dp + x];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) k4[b] = (TAcc)kr[16 * b * dp + x];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = fma(q4[a], k4[b], acc[a][b]);
         }
-        __syncthreads();
-        if (!row_ok) continue;
-        for (int c = (tid & 3); c < kScoreChunk; c += 4) {
-            const int j = c0 + c;
-            if (j > jhi || j < i - g.w || j > i + g.w || !col_on(g, bh, j)) continue;
-            const float* qa = sq + r * dp;
-            const float* kb = sk + c * dp;
-            float val;
-            if (kF64Acc) {
-                double acc = 0.0;
-                for (int x = 0; x < g.d; ++x) acc = fma((double)qa[x], (double)kb[x], acc);
-                val = kZ ? (float)acc : (float)(acc * (double)g.c2);
-            } else {
-                float acc = 0.f;
-                for (int x = 0; x < g.d; ++x) acc = fmaf(qa[x], kb[x], acc);
-                val = kZ ? acc : acc * g.c2;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int i = i0 + ty + 16 * a;
+            if (i >= g.Lq) continue;
+            const bool ron = row_on(g, bh, i);
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int j = c0 + cb + tx + 16 * b;
+                const int k = j - i + g.w;
+                if (k < 0 || k >= g.Wf) continue;
+                const bool on = ron && j >= 0 && j < g.Lk && col_on(g, bh, j);
+                float val;
+                if (kZ) val = on ? (float)acc[a][b] : 0.f;
+                else val = on ? (float)(acc[a][b] * (TAcc)g.c2) : -INFINITY;
+                S2[((size_t)bh * g.Lqp + i) * g.Wf + k] = val;
             }
-            S2[((size_t)bh * g.Lqp + i) * g.Wf + (j - i + g.w)] = val;
         }
     }
-    // off-support cells of this CTA's rows -> -inf (disjoint from the cells written above)
-    for (int e = tid; e < kScoreRows * g.Wf; e += blockDim.x) {
-        const int rr = e / g.Wf, k = e % g.Wf;
-        const int ii = i0 + rr;
-        if (ii >= g.Lq) continue;
-        const int j = ii - g.w + k;
-        const bool on = row_on(g, bh, ii) && j >= 0 && j < g.Lk && col_on(g, bh, j);
-        if (!on) S2[((size_t)bh * g.Lqp + ii) * g.Wf + k] = kZ ? 0.f : -INFINITY;
+}
+
+// ---------------------------------------------------------------------------
+// Band dot products on the FP64 tensor cores (mma.sync m8n8k4 .f64): the same
+// field as k_scores, exact products and f64 accumulation, rounded once to fp32.
+// CTA = 128 rows of one head; warp = RT 8-row tiles, its A fragments (query
+// rows, converted to f64) register-resident; the key window [i0-w, ...) sits
+// in SMEM as fp32 with pitch D+4 (B fragment loads are bank-conflict free).
+// A warp visits only the 8-column tiles its rows' bands touch (~1.1x the band).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <int D>
+struct BandMma {
+    static constexpr int CP = D <= 64 ? 2 : 1;   // key column tiles per warp pass (B fragments in registers)
+    static constexpr int NWARP = 8;
+    static constexpr int P = D + 4;               // SMEM pitch (doubles): conflict-free A fragment loads
+    static size_t smem() { return (size_t)128 * P * 8; }
+};
+
+// Warp pass = CP key column tiles (8 keys each, B fragments converted to f64
+// once, register-resident); it walks the query row tiles whose bands touch
+// those columns, A fragments (f64) streamed from SMEM: one LDS.64 feeds CP
+// DMMAs and the inner loop has no conversions.
+template <class TIn, bool kZ, int D>
+__global__ void __launch_bounds__(256) k_band_mma(Geo g, const TIn* __restrict__ A, const TIn* __restrict__ B,
+                                                  float* __restrict__ out) {
+    using M = BandMma<D>;
+    constexpr int CP = M::CP, P = M::P, KS = D / 4;
+    extern __shared__ __align__(16) double sqa[];  // [128][P] query rows of the block, f64
+    const int bh = blockIdx.y, i0 = blockIdx.x * 128, j0 = i0 - g.w;
+    const TIn* Ah = A + (size_t)bh * g.Lrq * D;
+    const TIn* Bh = B + (size_t)bh * g.Lrk * D;
+    for (int e = threadIdx.x; e < 128 * (D / 4); e += 256) {
+        const int r = e / (D / 4), x = (e % (D / 4)) * 4;
+        const int i = i0 + r;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < g.Lq) {
+            const TIn* src = Ah + (size_t)i * D + x;
+            if constexpr (sizeof(TIn) == 4) {
+                v = *reinterpret_cast<const float4*>(src);
+            } else {
+                v.x = ldf(src); v.y = ldf(src + 1); v.z = ldf(src + 2); v.w = ldf(src + 3);
+            }
+        }
+        double* dst = sqa + r * P + x;
+        dst[0] = v.x;
+        dst[1] = v.y;
+        dst[2] = v.z;
+        dst[3] = v.w;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
+    const int CT = (7 + 2 * g.w) / 8 + 1;     // column tiles one row tile touches
+    const int NCT = 15 + CT;                  // column tiles of the block window
+    const int npass = (NCT + CP - 1) / CP;
+    bool ron[16];
+#pragma unroll
+    for (int ri = 0; ri < 16; ++ri) {
+        const int i = i0 + 8 * ri + gq;
+        ron[ri] = i < g.Lq && row_on(g, bh, i);
+    }
+    for (int pass = warp; pass < npass; pass += M::NWARP) {
+        const int c0 = pass * CP;
+        double bf[CP][KS];
+        bool jon[CP][2];
+#pragma unroll
+        for (int u = 0; u < CP; ++u) {
+            const int jr = j0 + 8 * (c0 + u) + gq;  // key row of this lane's B fragment
+            const bool ok = jr >= 0 && jr < g.Lk;
+#pragma unroll
+            for (int s = 0; s < KS; ++s) bf[u][s] = ok ? (double)ldf(Bh + (size_t)jr * D + 4 * s + tq) : 0.0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = j0 + 8 * (c0 + u) + 2 * tq + h;
+                jon[u][h] = j >= 0 && j < g.Lk && col_on(g, bh, j);
+            }
+        }
+        // row tiles touching column tiles [c0, c0 + CP): ri in [c0 - CT + 1, c0 + CP - 1]
+        const int rlo = max(0, c0 - CT + 1), rhi = min(15, c0 + CP - 1);
+        for (int ri = rlo; ri <= rhi; ++ri) {
+            double c[CP][2];
+#pragma unroll
+            for (int u = 0; u < CP; ++u) c[u][0] = c[u][1] = 0.0;
+            const double* ap = sqa + (8 * ri + gq) * P + tq;
+#pragma unroll
+            for (int s = 0; s < KS; ++s) {
+                const double av = ap[4 * s];
+#pragma unroll
+                for (int u = 0; u < CP; ++u) dmma884(c[u][0], c[u][1], av, bf[u][s]);
+            }
+            const int i = i0 + 8 * ri + gq;
+            if (i >= g.Lqp) continue;
+            bool rr = false;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                if (q == ri) rr = ron[q];
+#pragma unroll
+            for (int u = 0; u < CP; ++u)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int j = j0 + 8 * (c0 + u) + 2 * tq + h;
+                    const int k = j - i + g.w;
+                    if (k < 0 || k >= g.Wf) continue;
+                    const bool on = rr && jon[u][h];
+                    float val;
+                    if (kZ) val = on ? (float)c[u][h] : 0.f;
+                    else val = on ? (float)(c[u][h] * (double)g.c2) : -INFINITY;
+                    out[((size_t)bh * g.Lqp + i) * g.Wf + k] = val;
+                }
+        }
     }
 }
 
@@ -174,6 +301,256 @@ __global__ void __launch_bounds__(128) k_stepT(Geo g, const float* __restrict__ 
         }
     }
     out_own[(size_t)bh * g.Lrq + i] = u;
+}
+
+// ---------------------------------------------------------------------------
+// Fused full step over the stored band (fp32 path, no dustbin).  Launch t:
+//   1. combine: v_{t-1}(window) from the column partials of launch t-1 (fixed
+//      order over the <= 3 contributing blocks) and v_{t-2}; the owner block
+//      writes v_{t-1} for its own 128 columns
+//   2. row pass: e_ij = 2^(s2 + v_{t-1,j} + u_{t-1,i}), r_i = sum_j e_ij,
+//      u_t = u_{t-1} - lg2 r_i  (row_half_step, sinkhorn.hpp:15-61)
+//   3. column partials: sum_{i in block} e_ij / r_i, i.e. the column half-step
+//      (col_half_step, sinkhorn.hpp:64-107) reuses the row pass exponentials:
+//      e_ij / r_i = 2^(s2 + u_t,i + v_{t-1,j}) -- one exp per cell per full step.
+// Cold start (t = 1): row max offsets, and log-domain (max, sum) column
+// partials so that no column can underflow.
+// ---------------------------------------------------------------------------
+struct FStep {
+    const float* S2;
+    const float* u_prev;  // [BH][Lrq] u_{t-1} (offsets)
+    float* u_out;         // [BH][Lrq] u_t
+    const float* v_pp;    // [BH][Lrk] v_{t-2} (null when t-2 == 0)
+    float* v_p_out;       // [BH][Lrk] v_{t-1} written by owners (null at t = 1)
+    float* v_p_slot;      // optional extra copy of v_{t-1} (saved slot) or null
+    const float* part_in;   // [BH][NB][Nw] partials of launch t-1
+    const float* partm_in;  // [BH][NB][Nw] partial maxima (launch 1 only) or null
+    float* part_out;
+    float* partm_out;     // written at t = 1
+    int NB, Nw;
+    int* err;
+};
+
+__device__ __forceinline__ float combine_col(const Geo& g, const FStep& f, int bh, int j, bool pairs) {
+    // blocks whose window [128b - w, 128b + 127 + w] contains column j
+    const int a = j - 127 - g.w;
+    const int blo = max(0, a > 0 ? (a + 127) / 128 : 0);  // ceil((j - 127 - w) / 128)
+    const int bhi = min(f.NB - 1, (j + g.w) / 128);
+    const size_t base = (size_t)bh * f.NB * f.Nw;
+    if (!pairs) {
+        float s = 0.f;
+        for (int b = blo; b <= bhi; ++b) s += f.part_in[base + (size_t)b * f.Nw + (j - (128 * b - g.w))];
+        return lg2(s);  // v_{t-1} = v_{t-2} - lg2(s)
+    }
+    float M = -INFINITY;
+    for (int b = blo; b <= bhi; ++b) M = fmaxf(M, f.partm_in[base + (size_t)b * f.Nw + (j - (128 * b - g.w))]);
+    float s = 0.f;
+    for (int b = blo; b <= bhi; ++b) {
+        const size_t k = base + (size_t)b * f.Nw + (j - (128 * b - g.w));
+        const float m = f.partm_in[k];
+        if (m != -INFINITY) s += f.part_in[k] * ex2(m - M);
+    }
+    return M + lg2(s);  // v_1 = -(M + lg2 s)   (v_0 = 0)
+}
+
+// One CTA = one 128-row block, its band tile bulk-copied whole into SMEM; one
+// thread per row in the row pass, one thread per window column in the column
+// pass.  The prologue issues every global load it needs (mask bytes, v_{t-2},
+// the <= 3 block partials per column, u_{t-1}) before consuming any of them,
+// so their latencies overlap one another and the tile copy.
+constexpr int kFsCols = 4;    // window columns per thread (Nw <= 512)
+
+template <bool kFirst, bool kPairsIn>
+__global__ void __launch_bounds__(128) k_fstep(Geo g, FStep f) {
+    extern __shared__ __align__(16) float smf[];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ float inv_r[128];
+    const int bh = blockIdx.y, b = blockIdx.x, i0 = b * 128, tid = threadIdx.x, i = i0 + tid;
+    const int Nw = f.Nw, Wf = g.Wf;
+    float* tile = smf;               // [128][Wf]: scores, then e (or x at cold start)
+    float* vw = smf + 128 * Wf;      // [Nw] window duals v_{t-1}
+    const bool in_rows = i < g.Lq;
+    const uint8_t* rmask = g.row_mask ? g.row_mask + (size_t)(bh / g.H) * g.Lq : nullptr;
+    const uint8_t* cmask = g.col_mask ? g.col_mask + (size_t)(bh / g.H) * g.Lk : nullptr;
+    const bool active = in_rows && (rmask == nullptr || rmask[i] != 0);
+    const float uo = (!kFirst && in_rows) ? f.u_prev[(size_t)bh * g.Lrq + i] : 0.f;
+    const bool any = __syncthreads_or(active);
+    if (any && tid == 0) {
+        sm100::mbar_init(&bar, 1);
+        sm100::fence_mbar_init();
+        const uint32_t bytes = 128u * (uint32_t)Wf * 4u;
+        sm100::mbar_arrive_expect_tx(&bar, bytes);
+        sm100::bulk_g2s(tile, f.S2 + ((size_t)bh * g.Lqp + i0) * Wf, bytes, &bar);
+    }
+    // ---- 1. combine: v_{t-1} on the window; owners write their 128 columns
+    const size_t pb = (size_t)bh * f.NB * Nw;
+#pragma unroll
+    for (int a = 0; a < kFsCols; ++a) {
+        const int c = tid + 128 * a;
+        if (c >= Nw) break;
+        const int j = i0 - g.w + c;
+        const bool inr = j >= 0 && j < g.Lk;
+        const int jc = inr ? j : 0;
+        const bool con = inr && (cmask == nullptr || cmask[jc] != 0);
+        float v = -INFINITY;
+        if (kFirst) {
+            if (con) v = 0.f;
+        } else {
+            // contributing blocks b-2 .. b+2 (w <= 128); window column of j in block b' = c + 128 (b - b')
+            float pv[5], pm[5];
+            bool ok[5];
+#pragma unroll
+            for (int d = 0; d < 5; ++d) {
+                const int bb = b - 2 + d;
+                const int cc = c + 128 * (2 - d);
+                ok[d] = bb >= 0 && bb < f.NB && cc >= 0 && cc < Nw;
+                const size_t k = pb + (size_t)(ok[d] ? bb : 0) * Nw + (ok[d] ? cc : 0);
+                pv[d] = ok[d] ? f.part_in[k] : 0.f;
+                pm[d] = (kPairsIn && ok[d]) ? f.partm_in[k] : -INFINITY;
+            }
+            const float prev = (f.v_pp && inr) ? f.v_pp[(size_t)bh * g.Lrk + jc] : 0.f;
+            if (con) {
+                if (kPairsIn) {
+                    float M = -INFINITY;
+#pragma unroll
+                    for (int d = 0; d < 5; ++d) M = fmaxf(M, pm[d]);
+                    float sum = 0.f;
+#pragma unroll
+                    for (int d = 0; d < 5; ++d)
+                        if (pm[d] != -INFINITY) sum += pv[d] * ex2(pm[d] - M);
+                    v = -(M + lg2(sum));
+                } else {
+                    float sum = 0.f;
+#pragma unroll
+                    for (int d = 0; d < 5; ++d) sum += pv[d];
+                    v = prev - lg2(sum);
+                }
+                if (!isfinite(v)) {
+                    atomicOr(f.err, 32);
+                    v = 0.f;
+                }
+            }
+        }
+        vw[c] = v;
+        if (!kFirst && c >= g.w && c < g.w + 128 && j < g.Lk) {  // owner of column j
+            const float vo = (v == -INFINITY) ? 0.f : v;
+            f.v_p_out[(size_t)bh * g.Lrk + j] = vo;
+            if (f.v_p_slot) f.v_p_slot[(size_t)bh * g.Lrk + j] = vo;
+        }
+    }
+    const size_t pbase = pb + (size_t)b * Nw;
+    if (!any) {  // fully masked block: zero partials, zero duals
+        for (int c = tid; c < Nw; c += 128) {
+            f.part_out[pbase + c] = 0.f;
+            if (kFirst) f.partm_out[pbase + c] = -INFINITY;
+        }
+        if (in_rows) f.u_out[(size_t)bh * g.Lrq + i] = 0.f;
+        return;
+    }
+    __syncthreads();
+    sm100::mbar_wait(&bar, 0);
+    // ---- 2. row pass (thread tid owns row i); tile row becomes e (or x)
+    float* trow = tile + tid * Wf;
+    const float* vr = vw + tid;
+    if (active) {
+        float o;
+        if (kFirst) {
+            float m0 = -INFINITY, m1 = -INFINITY;
+            int k = 0;
+            for (; k + 1 < Wf; k += 2) {
+                m0 = fmaxf(m0, trow[k] + vr[k]);
+                m1 = fmaxf(m1, trow[k + 1] + vr[k + 1]);
+            }
+            if (k < Wf) m0 = fmaxf(m0, trow[k] + vr[k]);
+            o = -fmaxf(m0, m1);
+        } else {
+            o = uo;
+        }
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        int k = 0;
+        for (; k + 3 < Wf; k += 4) {
+            const float x0 = trow[k] + vr[k] + o, x1 = trow[k + 1] + vr[k + 1] + o;
+            const float x2 = trow[k + 2] + vr[k + 2] + o, x3 = trow[k + 3] + vr[k + 3] + o;
+            const float e0 = ex2(x0), e1 = ex2(x1), e2 = ex2(x2), e3 = ex2(x3);
+            trow[k] = kFirst ? x0 : e0;
+            trow[k + 1] = kFirst ? x1 : e1;
+            trow[k + 2] = kFirst ? x2 : e2;
+            trow[k + 3] = kFirst ? x3 : e3;
+            s0 += e0;
+            s1 += e1;
+            s2 += e2;
+            s3 += e3;
+        }
+        for (; k < Wf; ++k) {
+            const float x = trow[k] + vr[k] + o;
+            const float e = ex2(x);
+            trow[k] = kFirst ? x : e;
+            s0 += e;
+        }
+        const float rs = (s0 + s1) + (s2 + s3);
+        const float lr = lg2(rs);
+        float u = o - lr;
+        if (!(rs > 0.f) || !isfinite(u)) {
+            atomicOr(f.err, 64);
+            u = 0.f;
+        }
+        f.u_out[(size_t)bh * g.Lrq + i] = u;
+        inv_r[tid] = kFirst ? lr : 1.f / rs;  // cold start keeps lg2 r_i (log-domain partials)
+    } else {
+        if (in_rows) f.u_out[(size_t)bh * g.Lrq + i] = 0.f;
+        inv_r[tid] = kFirst ? INFINITY : 0.f;
+        const float z = kFirst ? -INFINITY : 0.f;  // no -inf * 0 in the column pass
+        for (int k = 0; k < Wf; ++k) trow[k] = z;
+    }
+    __syncthreads();
+    // ---- 3. column partials: window column c collects rows ii with c - 2w <= ii <= c
+#pragma unroll
+    for (int a = 0; a < kFsCols; ++a) {
+        const int c = tid + 128 * a;
+        if (c >= Nw) break;
+        const int lo = max(0, c - 2 * g.w), hi = min(127, c);
+        const float* tp = tile + lo * Wf + (c - lo);
+        const int step = Wf - 1;
+        if (kFirst) {
+            float M = -INFINITY;
+            for (int ii = lo; ii <= hi; ++ii) M = fmaxf(M, tp[(ii - lo) * step] - inv_r[ii]);
+            float sum = 0.f;
+            if (M != -INFINITY)
+                for (int ii = lo; ii <= hi; ++ii) sum += ex2(tp[(ii - lo) * step] - inv_r[ii] - M);
+            f.part_out[pbase + c] = sum;
+            f.partm_out[pbase + c] = M;
+        } else {
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+            int ii = lo;
+            for (; ii + 3 <= hi; ii += 4, tp += 4 * step) {
+                s0 = fmaf(tp[0], inv_r[ii], s0);
+                s1 = fmaf(tp[step], inv_r[ii + 1], s1);
+                s2 = fmaf(tp[2 * step], inv_r[ii + 2], s2);
+                s3 = fmaf(tp[3 * step], inv_r[ii + 3], s3);
+            }
+            for (; ii <= hi; ++ii, tp += step) s0 = fmaf(tp[0], inv_r[ii], s0);
+            f.part_out[pbase + c] = (s0 + s1) + (s2 + s3);
+        }
+    }
+}
+
+// v_{T+R} from the last partials (the finishing half of the last full step)
+template <bool kPairsIn>
+__global__ void k_ffinal(Geo g, FStep f) {
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long)g.BH * g.Lk) return;
+    const int bh = (int)(t / g.Lk), j = (int)(t % g.Lk);
+    float v = 0.f;
+    if (col_on(g, bh, j)) {
+        const float prev = f.v_pp ? f.v_pp[(size_t)bh * g.Lrk + j] : 0.f;
+        v = kPairsIn ? -combine_col(g, f, bh, j, true) : prev - combine_col(g, f, bh, j, false);
+        if (!isfinite(v)) {
+            atomicOr(f.err, 32);
+            v = 0.f;
+        }
+    }
+    f.v_p_out[(size_t)bh * g.Lrk + j] = v;
+    if (f.v_p_slot) f.v_p_slot[(size_t)bh * g.Lrk + j] = v;
 }
 
 // ---------------------------------------------------------------------------
@@ -277,11 +654,11 @@ __global__ void __launch_bounds__(256) k_col_step(Geo g, const float* __restrict
 template <class TIn>
 __global__ void __launch_bounds__(256) k_output(Geo g, const float* __restrict__ S2, const float* __restrict__ u,
                                                 const float* __restrict__ v, const TIn* __restrict__ V,
-                                                float* __restrict__ O) {
+                                                float* __restrict__ O, int last_only) {
     const int lane = threadIdx.x & 31;
     const long gw = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (gw >= (long)g.BH * g.Lrq) return;
-    const int bh = (int)(gw / g.Lrq), i = (int)(gw % g.Lrq);
+    if (gw >= (long)g.BH * (last_only ? 1 : g.Lrq)) return;
+    const int bh = last_only ? (int)gw : (int)(gw / g.Lrq), i = last_only ? g.Lrq - 1 : (int)(gw % g.Lrq);
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     if (row_on(g, bh, i)) {
         const float ui = u[(size_t)bh * g.Lrq + i];
@@ -603,36 +980,62 @@ long long launch_count(bool reset) {
 }
 static inline unsigned nblocks(long items, int per) { return (unsigned)((items + per - 1) / per); }
 
-cudaError_t launch_scores(const Geo& g, int dtype, const void* Q, const void* K, float* S2, cudaStream_t s) {
-    const size_t smem = (size_t)2 * kScoreRows * (g.d + 1) * sizeof(float);
-    dim3 grid((g.Lq + kScoreRows - 1) / kScoreRows, g.BH);
-    if (dtype == 0) {
-        auto kern = k_scores<float, true, false>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, 256, smem, s>>>(g, (const float*)Q, (const float*)K, S2);
-    } else {
-        auto kern = k_scores<__nv_bfloat16, false, false>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, 256, smem, s>>>(g, (const __nv_bfloat16*)Q, (const __nv_bfloat16*)K, S2);
-    }
+static size_t scores_smem(const Geo& g, size_t elem) {
+    const int ncol = ((kScoreRows + 2 * g.w + 63) / 64) * 64;
+    return (size_t)(kScoreRows + ncol) * (g.d + 1) * elem;
+}
+
+template <class TIn, class TAcc, bool kZ>
+static cudaError_t launch_band_dot(const Geo& g, const void* A, const void* B, float* out, cudaStream_t s) {
+    const size_t smem = scores_smem(g, sizeof(float));
+    auto kern = k_scores<TIn, TAcc, kZ>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<dim3((g.Lq + kScoreRows - 1) / kScoreRows, g.BH), 256, smem, s>>>(g, (const TIn*)A, (const TIn*)B, out);
     ++g_launches;
     return cudaGetLastError();
 }
 
-cudaError_t launch_zband(const Geo& g, int dtype, const void* dO, const void* V, float* Z, cudaStream_t s) {
-    const size_t smem = (size_t)2 * kScoreRows * (g.d + 1) * sizeof(float);
-    dim3 grid((g.Lq + kScoreRows - 1) / kScoreRows, g.BH);
-    if (dtype == 0) {
-        auto kern = k_scores<float, false, true>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, 256, smem, s>>>(g, (const float*)dO, (const float*)V, Z);
-    } else {
-        auto kern = k_scores<__nv_bfloat16, false, true>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, 256, smem, s>>>(g, (const __nv_bfloat16*)dO, (const __nv_bfloat16*)V, Z);
-    }
+template <class TIn, bool kZ, int D>
+static cudaError_t launch_band_mma(const Geo& g, const void* A, const void* B, float* out, cudaStream_t s) {
+    using M = BandMma<D>;
+    const size_t smem = M::smem();
+    auto kern = k_band_mma<TIn, kZ, D>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<dim3((g.Lq + 127) / 128, g.BH), 256, smem, s>>>(g, (const TIn*)A, (const TIn*)B, out);
     ++g_launches;
     return cudaGetLastError();
+}
+
+// FP64-tensor-core band dot when the head dim has a specialisation
+template <bool kZ>
+static bool band_mma(const Geo& g, int dtype, const void* A, const void* B, float* out, cudaStream_t s,
+                     cudaError_t& err) {
+    if (getenv("ST_NO_DMMA")) return false;
+    if (g.d == 32)
+        err = dtype == 0 ? launch_band_mma<float, kZ, 32>(g, A, B, out, s) : launch_band_mma<__nv_bfloat16, kZ, 32>(g, A, B, out, s);
+    else if (g.d == 64)
+        err = dtype == 0 ? launch_band_mma<float, kZ, 64>(g, A, B, out, s) : launch_band_mma<__nv_bfloat16, kZ, 64>(g, A, B, out, s);
+    else if (g.d == 128)
+        err = dtype == 0 ? launch_band_mma<float, kZ, 128>(g, A, B, out, s) : launch_band_mma<__nv_bfloat16, kZ, 128>(g, A, B, out, s);
+    else
+        return false;
+    return true;
+}
+
+cudaError_t launch_scores(const Geo& g, int dtype, const void* Q, const void* K, float* S2, cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    if (band_mma<false>(g, dtype, Q, K, S2, s, e)) return e;
+    return dtype == 0 ? launch_band_dot<float, double, false>(g, Q, K, S2, s)
+                      : launch_band_dot<__nv_bfloat16, float, false>(g, Q, K, S2, s);
+}
+
+cudaError_t launch_zband(const Geo& g, int dtype, const void* dO, const void* V, float* Z, cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    if (band_mma<true>(g, dtype, dO, V, Z, s, e)) return e;
+    return dtype == 0 ? launch_band_dot<float, float, true>(g, dO, V, Z, s)
+                      : launch_band_dot<__nv_bfloat16, float, true>(g, dO, V, Z, s);
 }
 
 cudaError_t launch_row_step(const Geo& g, bool first, const float* S2, const float* v, const float* u_prev,
@@ -669,6 +1072,52 @@ cudaError_t launch_stepT(const Geo& g, bool first, const float* S2, const float*
     return cudaGetLastError();
 }
 
+size_t fstep_smem_bytes(const Geo& g) {
+    if (g.w > 128) return SIZE_MAX;  // <= 3 contributing blocks per column, <= kFsCols columns per thread
+    return (size_t)128 * g.Wf * 4 + (size_t)(128 + 2 * g.w) * 4;
+}
+
+cudaError_t launch_fstep(const Geo& g, int t, const FStepPtrs& p, cudaStream_t s) {
+    FStep f;
+    f.S2 = p.S2;
+    f.u_prev = p.u_prev;
+    f.u_out = p.u_out;
+    f.v_pp = p.v_pp;
+    f.v_p_out = p.v_p_out;
+    f.v_p_slot = p.v_p_slot;
+    f.part_in = p.part_in;
+    f.partm_in = p.partm_in;
+    f.part_out = p.part_out;
+    f.partm_out = p.partm_out;
+    f.NB = (g.Lq + 127) / 128;
+    f.Nw = 128 + 2 * g.w;
+    f.err = p.err;
+    const size_t smem = fstep_smem_bytes(g);
+    auto k = (t == 1) ? k_fstep<true, false> : (t == 2) ? k_fstep<false, true> : k_fstep<false, false>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k<<<dim3(f.NB, g.BH), 128, smem, s>>>(g, f);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ffinal(const Geo& g, int t_last, const FStepPtrs& p, cudaStream_t s) {
+    FStep f{};
+    f.v_pp = p.v_pp;
+    f.v_p_out = p.v_p_out;
+    f.v_p_slot = p.v_p_slot;
+    f.part_in = p.part_in;
+    f.partm_in = p.partm_in;
+    f.NB = (g.Lq + 127) / 128;
+    f.Nw = 128 + 2 * g.w;
+    f.err = p.err;
+    const unsigned nb = nblocks((long)g.BH * g.Lk, 256);
+    if (t_last == 1) k_ffinal<true><<<nb, 256, 0, s>>>(g, f);
+    else k_ffinal<false><<<nb, 256, 0, s>>>(g, f);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_col_step(const Geo& g, bool first, const float* S2, const float* u, const float* v_prev,
                             float* v_out, int* err, cudaStream_t s) {
     const unsigned nb = nblocks((long)g.BH * g.Lrk, 8);
@@ -679,10 +1128,10 @@ cudaError_t launch_col_step(const Geo& g, bool first, const float* S2, const flo
 }
 
 cudaError_t launch_output(const Geo& g, int dtype, const float* S2, const float* u, const float* v, const void* V,
-                          float* O, cudaStream_t s) {
-    const unsigned nb = nblocks((long)g.BH * g.Lrq, 8);
-    if (dtype == 0) k_output<float><<<nb, 256, 0, s>>>(g, S2, u, v, (const float*)V, O);
-    else k_output<__nv_bfloat16><<<nb, 256, 0, s>>>(g, S2, u, v, (const __nv_bfloat16*)V, O);
+                          float* O, cudaStream_t s, int last_only) {
+    const unsigned nb = nblocks((long)g.BH * (last_only ? 1 : g.Lrq), 8);
+    if (dtype == 0) k_output<float><<<nb, 256, 0, s>>>(g, S2, u, v, (const float*)V, O, last_only);
+    else k_output<__nv_bfloat16><<<nb, 256, 0, s>>>(g, S2, u, v, (const __nv_bfloat16*)V, O, last_only);
     ++g_launches;
     return cudaGetLastError();
 }

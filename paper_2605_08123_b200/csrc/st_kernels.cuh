@@ -21,12 +21,31 @@ struct BwdTPtrs {
     float *Zd, *ZdT;
 };
 
+struct FStepPtrs {
+    const float* S2;
+    const float* u_prev;
+    float* u_out;
+    const float* v_pp;
+    float* v_p_out;
+    float* v_p_slot;
+    const float* part_in;
+    const float* partm_in;
+    float* part_out;
+    float* partm_out;
+    int* err;
+};
+size_t fstep_smem_bytes(const Geo& g);
+cudaError_t launch_fstep(const Geo& g, int t, const FStepPtrs& p, cudaStream_t s);
+cudaError_t launch_ffinal(const Geo& g, int t_last, const FStepPtrs& p, cudaStream_t s);
+
 long long launch_count(bool reset);
 void add_launches(long long n);
 size_t bwdT_smem_bytes(const Geo& g);
 bool bwdT_supported(const Geo& g);
 cudaError_t launch_backward_tile(const Geo& g, int dtype, const BwdPtrs& p, const BwdTPtrs& t, bool direct,
                                  cudaStream_t s, long long& launches);
+cudaError_t launch_output_tile(const Geo& g, int dtype, const float* S2, const float* u, const float* v, const void* V,
+                               float* O, cudaStream_t s);
 // the dustbin row / column of one backward stage through the generic sweeps
 cudaError_t launch_backward_dustbin_stage(const Geo& g, int dtype, const BwdPtrs& p, bool direct, int stage,
                                           cudaStream_t s);
@@ -42,7 +61,7 @@ cudaError_t launch_stepT(const Geo& g, bool first, const float* S2, const float*
 cudaError_t launch_col_step(const Geo& g, bool first, const float* S2, const float* u, const float* v_prev,
                             float* v_out, int* err, cudaStream_t s);
 cudaError_t launch_output(const Geo& g, int dtype, const float* S2, const float* u, const float* v, const void* V,
-                          float* O, cudaStream_t s);
+                          float* O, cudaStream_t s, int last_only = 0);
 cudaError_t launch_gauges(const Geo& g, const float* u_slots, int nslots, float* gauge, cudaStream_t s);
 cudaError_t launch_backward(const Geo& g, int dtype, const BwdPtrs& p, bool direct, cudaStream_t s);
 cudaError_t launch_deps_reduce(const Geo& g, const float* part, float* out, cudaStream_t s);
