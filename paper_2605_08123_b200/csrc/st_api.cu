@@ -145,6 +145,7 @@ struct WsLayout {
     size_t S2, S2T, u, v, g_u, u2b, u1b, deps, g_v, v1b, v0b, err;
     size_t qp[3], kp[3], flags, work_q, work_k, cnt;
     size_t vb2, part[2], partm;  // fused-step ping-pong duals and column partials
+    size_t fs_flags, fs_work, fs_cnt, fs_part[2], fs_partm;  // persistent solve: work list, tagged partials
     size_t bytes;
 };
 
@@ -198,6 +199,13 @@ WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
         w.part[0] = take(np);
         w.part[1] = take(np);
         w.partm = take(np);
+        const size_t nb = (size_t)m.BH * ((m.Lq + 127) / 128);
+        w.fs_flags = take(sizeof(int) * nb);
+        w.fs_work = take(sizeof(int) * nb);
+        w.fs_cnt = take(sizeof(int));
+        w.fs_part[0] = take(2 * np);
+        w.fs_part[1] = take(2 * np);
+        w.fs_partm = take(2 * np);
     }
     if (tp.ok) {
         for (int p = 0; p < tp.npl; ++p) {
@@ -390,7 +398,28 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
         ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));  // transport application (generic kernel)
     } else {
         ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));
-        if (fused_ok(desc, m) && T + R >= 1) {
+        if (fused_ok(desc, m) && T + R >= 1 && st::fsolve_supported(g) && !getenv("ST_NO_FSOLVE")) {
+            // one persistent cooperative launch for all T+R steps (band tiles SMEM-resident)
+            st::FSolvePtrs p{};
+            p.S2 = S2;
+            p.ubuf = u_ws;
+            p.vbuf = v_ws;
+            for (int q = 0; q < 3; ++q) {
+                p.u_slot[q] = (sv && q <= R) ? slot_u(q) : nullptr;
+                p.v_slot[q] = (sv && q <= R) ? slot_v(q) : nullptr;
+            }
+            p.part[0] = ws + wl.fs_part[0];
+            p.part[1] = ws + wl.fs_part[1];
+            p.partm = ws + wl.fs_partm;
+            p.vpriv = (float*)(ws + wl.part[0]);
+            p.flags = (int*)(ws + wl.fs_flags);
+            p.work = (int*)(ws + wl.fs_work);
+            p.count = (int*)(ws + wl.fs_cnt);
+            p.err = err;
+            ST_CUDA(st::launch_fsolve(g, (int)T, (int)R, p, st));
+            u_prev = u_ws;
+            v_prev = v_ws;
+        } else if (fused_ok(desc, m) && T + R >= 1) {
             // one launch per full step; the column half-step rides on the row exponentials
             float* vbuf[2] = {v_ws, (float*)(ws + wl.vb2)};
             float* part[2] = {(float*)(ws + wl.part[0]), (float*)(ws + wl.part[1])};

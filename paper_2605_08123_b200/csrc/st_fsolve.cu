@@ -1,0 +1,422 @@
+// st_fsolve.cu -- persistent, band-resident fused Sinkhorn solve (fp32 path).
+//
+// The whole stopped base solve + tail (stopped_base_solve / tail_refine,
+// inc/sinkhorn.hpp:171-221) in ONE cooperative launch:
+//   * each CTA owns one active 128-row block and keeps its score-band tile
+//     (128 x Wf fp32) resident in SMEM for all T+R steps when the compacted
+//     active-block list fits the co-resident grid (config 2: ~390 blocks x
+//     66 KB <= 148 SMs x 3 CTAs); otherwise the same kernel re-streams each
+//     tile every step (bulk copy), several tiles per CTA;
+//   * per step: combine the column partials of the previous step (fixed block
+//     order) into v_{t-1} on the block window, row pass u_t (one exp per
+//     cell), column pass partials sum_i 2^(s2 + u_t + v_{t-1}) (a second exp
+//     per cell -- the tile stays intact), then one grid barrier;
+//   * u_t is kept by the row's thread (ubuf), v_t by the owner block (vbuf),
+//     written every step so the non-resident mode and the saved slots share
+//     one code path.
+// Results are identical to the per-step k_fstep launches up to fp32 rounding
+// of e/r vs 2^(s2+u+v).
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "st_common.cuh"
+#include "st_kernels.cuh"
+#include "st_phase.cuh"
+#include "st_sm100.cuh"
+
+namespace st {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+using u64 = unsigned long long;
+
+struct FSolve {
+    const float* S2;
+    float* ubuf;             // [BH][Lrq] raw base-2 u (final step; every step when non-resident)
+    float* vbuf;             // [BH][Lrk] v_{T+R} (owners)
+    float* u_slot[3];        // saved u at steps T, T+1, T+2 (or null)
+    float* v_slot[3];
+    u64* part[2];            // [BH][NB][Nw] tagged column partials {sum, step}, by step parity
+    u64* partm;              // [BH][NB][Nw] tagged cold-start maxima {max, 1}
+    float* vpriv;            // [n][Nw] window duals of each work item (non-resident mode only)
+    const int* flags;        // [BH][NB] 1 = block is in the work list
+    const int* work;         // compacted active blocks, bh * NB + b
+    const int* nwork;
+    int NB, Nw, T, R;
+    int* err;
+};
+
+__device__ __forceinline__ void st_tagged(u64* p, float v, unsigned tag) {
+    const u64 x = ((u64)tag << 32) | (u64)__float_as_uint(v);
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
+}
+__device__ __forceinline__ u64 ld_tagged(const u64* p) {
+    u64 x;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(p) : "memory");
+    return x;
+}
+__device__ __forceinline__ float tag_value(u64 x) { return __uint_as_float((unsigned)x); }
+
+// The tagged partials of window column c of block b from the (active) blocks
+// b-2 .. b+2 for step `want`, spinning only on entries not yet published.
+__device__ __forceinline__ void gather5(const FSolve& f, const u64* buf, int bh, int b, int c, unsigned want,
+                                       float out[5]) {
+    const u64* p[5];
+    bool ok[5];
+    u64 x[5];
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+        const int bb = b - 2 + d;
+        const int cc = c + 128 * (2 - d);
+        ok[d] = bb >= 0 && bb < f.NB && cc >= 0 && cc < f.Nw && f.flags[bh * f.NB + bb] != 0;
+        p[d] = buf + ((size_t)bh * f.NB + (ok[d] ? bb : 0)) * f.Nw + (ok[d] ? cc : 0);
+        x[d] = ok[d] ? ld_tagged(p[d]) : ((u64)want << 32);
+    }
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+        while ((unsigned)(x[d] >> 32) != want) x[d] = ld_tagged(p[d]);
+        out[d] = ok[d] ? tag_value(x[d]) : 0.f;
+    }
+}
+
+// v_{t-1} of window column c (cold-start pairs at t = 2)
+__device__ __forceinline__ float combine(const FSolve& f, int bh, int b, int c, int t, float prev) {
+    float pv[5];
+    gather5(f, f.part[(t - 1) & 1], bh, b, c, (unsigned)(t - 1), pv);
+    if (t == 2) {
+        float pm[5];
+        gather5(f, f.partm, bh, b, c, 1u, pm);
+        float M = -INFINITY;
+#pragma unroll
+        for (int d = 0; d < 5; ++d)
+            if (pv[d] > 0.f) M = fmaxf(M, pm[d]);
+        float sum = 0.f;
+#pragma unroll
+        for (int d = 0; d < 5; ++d)
+            if (pv[d] > 0.f) sum += pv[d] * ex2(pm[d] - M);
+        return -(M + lg2(sum));
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int d = 0; d < 5; ++d) sum += pv[d];
+    return prev - lg2(sum);
+}
+
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {  // FADD2 (packed fp32, sm_100)
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+__device__ __forceinline__ float2 ex2x2(float2 x) { return make_float2(ex2(x.x), ex2(x.y)); }
+
+// SMEM geometry: tile [128][P] (P = Wf + 1, even: 8-byte aligned rows, half-warp
+// LDS.64 conflict free), the window duals twice (shift 0 / 1, so every row reads
+// aligned pairs), column-pass halves.
+struct FsGeo {
+    int P, P2;
+    __host__ __device__ FsGeo(int Wf, int Nw) : P(Wf + 1), P2(((Nw + 2 + 31) / 32) * 32 + 16) {}
+    __host__ __device__ size_t floats(int Nw) const { return (size_t)128 * P + 2 * (size_t)P2 + 4 * (size_t)Nw; }
+};
+
+__global__ void __launch_bounds__(kThreads) k_fsolve(Geo g, FSolve f) {
+    extern __shared__ __align__(16) float smf[];
+    __shared__ __align__(8) float unew[128];
+    const int Wf = g.Wf, Nw = f.Nw, tid = threadIdx.x;
+    const FsGeo sg(Wf, Nw);
+    const int P = sg.P;
+    const int lane = tid & 31, h = lane >> 4, r = (tid >> 5) * 16 + (lane & 15);
+    const unsigned pmask = (1u << (lane & 15)) | (1u << ((lane & 15) + 16));
+    float* tile = smf;                    // [128][P] s2 (never overwritten), pad column = -inf
+    float* vw0 = smf + 128 * P;           // [P2] v_{t-1}(c)
+    float* vw1 = vw0 + sg.P2;             // [P2] v_{t-1}(c + 1)
+    float* csum = vw1 + sg.P2;            // [2][Nw]
+    float* cmax = csum + 2 * Nw;          // [2][Nw]
+    const int n = *f.nwork;
+    const int G = gridDim.x;
+    const bool resident = n <= G;
+    const int TR = f.T + f.R;
+    for (int x = tid; x < sg.P2; x += kThreads) {
+        if (x >= Nw) vw0[x] = -INFINITY;
+        if (x >= Nw - 1) vw1[x] = -INFINITY;
+    }
+    // step-invariant per-thread state (resident mode keeps it across steps)
+    bool con[2] = {false, false}, act = false;
+    float ureg = 0.f;
+    for (int t = 1; t <= TR + 1; ++t) {
+        const bool fin = t == TR + 1;  // final combine only (v_{T+R})
+        for (int k = blockIdx.x; k < n; k += G) {
+            const int blk = f.work[k];
+            const int bh = blk / f.NB, b = blk % f.NB, i0 = b * 128;
+            const bool need_load = !fin && (!resident || t == 1);
+            if (need_load) {  // re-pitch the band tile Wf -> P (once when resident)
+                const float* src = f.S2 + ((size_t)bh * g.Lqp + i0) * Wf;
+                for (int e = tid; e < 128 * Wf; e += kThreads) {
+                    const int rr = e / Wf;
+                    tile[rr * P + (e - rr * Wf)] = __ldcs(src + e);
+                }
+                for (int rr = tid; rr < 128; rr += kThreads) tile[rr * P + Wf] = -INFINITY;
+            }
+            const int i = i0 + r;
+            if (!resident || t == 1) {
+                const uint8_t* rmask = g.row_mask ? g.row_mask + (size_t)(bh / g.H) * g.Lq : nullptr;
+                const uint8_t* cmask = g.col_mask ? g.col_mask + (size_t)(bh / g.H) * g.Lk : nullptr;
+                act = i < g.Lq && (rmask == nullptr || rmask[i] != 0);
+#pragma unroll
+                for (int a = 0; a < 2; ++a) {
+                    const int j = i0 - g.w + tid + kThreads * a;
+                    con[a] = tid + kThreads * a < Nw && j >= 0 && j < g.Lk && (cmask == nullptr || cmask[j] != 0);
+                }
+                if (!resident && t >= 2 && act) ureg = f.ubuf[(size_t)bh * g.Lrq + i];
+            }
+            // ---- combine: v_{t-1} on the window; owners publish their 128 columns
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+                const int c = tid + kThreads * a;
+                if (c >= Nw) break;
+                const int j = i0 - g.w + c;
+                const bool owner = c >= g.w && c < g.w + 128 && j < g.Lk;
+                if (fin && !owner) continue;
+                float v = -INFINITY;
+                if (t == 1) {
+                    if (con[a]) v = 0.f;
+                } else if (con[a]) {
+                    const float prev = (t < 3) ? 0.f : resident ? vw0[c] : f.vpriv[(size_t)k * Nw + c];
+                    v = combine(f, bh, b, c, t, prev);
+                    if (!isfinite(v)) {
+                        atomicOr(f.err, 32);
+                        v = 0.f;
+                    }
+                }
+                if (!fin) {
+                    vw0[c] = v;
+                    if (c >= 1) vw1[c - 1] = v;
+                }
+                if (!resident) f.vpriv[(size_t)k * Nw + c] = v;
+                if (t >= 2 && owner) {
+                    const float vo = (v == -INFINITY) ? 0.f : v;
+                    const int rv = t - 1 - f.T;
+                    if (rv >= 0 && rv <= 2 && f.v_slot[rv]) f.v_slot[rv][(size_t)bh * g.Lrk + j] = vo;
+                    if (fin) f.vbuf[(size_t)bh * g.Lrk + j] = vo;
+                }
+            }
+            if (fin) continue;
+            __syncthreads();
+            // ---- row pass: threads (r, h) share row i; h takes the 16-cell groups h, h+2, ...
+            const float* trow = tile + r * P;
+            const float* vrow = ((r & 1) ? vw1 : vw0) + (r & ~1);  // vrow[k] = v(r + k), k even aligned
+            if (act) {
+                float o;
+                if (t == 1) {
+                    float m = -INFINITY;
+                    for (int k0 = 16 * h; k0 < P; k0 += 32)
+#pragma unroll
+                        for (int kk = 0; kk < 16; ++kk)
+                            if (k0 + kk < P) m = fmaxf(m, trow[k0 + kk] + vrow[k0 + kk]);
+                    m = fmaxf(m, __shfl_xor_sync(pmask, m, 16));
+                    o = -m;
+                } else {
+                    o = ureg;
+                }
+                const float2 oo = make_float2(o, o);
+                float2 a0 = make_float2(0.f, 0.f), a1 = a0;
+                for (int k0 = 16 * h; k0 < P; k0 += 32) {
+                    if (k0 + 16 <= P) {
+#pragma unroll
+                        for (int kk = 0; kk < 16; kk += 4) {
+                            const float2 sa = *reinterpret_cast<const float2*>(trow + k0 + kk);
+                            const float2 sb = *reinterpret_cast<const float2*>(trow + k0 + kk + 2);
+                            const float2 va = *reinterpret_cast<const float2*>(vrow + k0 + kk);
+                            const float2 vb = *reinterpret_cast<const float2*>(vrow + k0 + kk + 2);
+                            a0 = fadd2(a0, ex2x2(fadd2(fadd2(sa, va), oo)));
+                            a1 = fadd2(a1, ex2x2(fadd2(fadd2(sb, vb), oo)));
+                        }
+                    } else {
+                        for (int kx = k0; kx < P; kx += 2) {
+                            const float2 sa = *reinterpret_cast<const float2*>(trow + kx);
+                            const float2 va = *reinterpret_cast<const float2*>(vrow + kx);
+                            a0 = fadd2(a0, ex2x2(fadd2(fadd2(sa, va), oo)));
+                        }
+                    }
+                }
+                float rs = (a0.x + a0.y) + (a1.x + a1.y);
+                rs += __shfl_xor_sync(pmask, rs, 16);
+                float u = o - lg2(rs);
+                if (!(rs > 0.f) || !isfinite(u)) {
+                    if (h == 0) atomicOr(f.err, 64);
+                    u = 0.f;
+                }
+                ureg = u;
+                if (h == 0) {
+                    unew[r] = u;
+                    if (!resident || t == TR) f.ubuf[(size_t)bh * g.Lrq + i] = u;
+                    const int ru = t - f.T;
+                    if (ru >= 0 && ru <= 2 && f.u_slot[ru]) f.u_slot[ru][(size_t)bh * g.Lrq + i] = u;
+                }
+            } else if (h == 0) {
+                unew[r] = -INFINITY;  // no contribution to any column
+            }
+            __syncthreads();
+            // ---- column pass.  Thread t7 = tid & 127 owns the window columns {t7 + 128 m}:
+            // exactly Wf cells for every t7 (balanced lanes); the thread pair hh = tid >> 7
+            // splits that concatenated cell list at Wf/2 and the halves are combined in
+            // a fixed order through SMEM.  Cell (ii, c) sits at ii * (P - 1) + c.
+            {
+                const int t7 = tid & 127, hh = tid >> 7;
+                const int half = (Wf + 1) >> 1;
+                const int beg = hh ? half : 0, end = hh ? Wf : half;
+                const int step = P - 1;
+                int off = 0;
+                for (int c = t7; c < Nw; c += 128) {
+                    const int lo = max(0, c - 2 * g.w), hi = min(127, c);
+                    const int n_c = hi - lo + 1;
+                    const int a0 = max(beg, off), a1 = min(end, off + n_c);  // my slice of this column
+                    const int ilo = lo + (a0 - off), ihi = lo + (a1 - off) - 1;
+                    off += n_c;
+                    const float vc = vw0[c];
+                    float ps = 0.f, pm = -INFINITY;
+                    if (ilo <= ihi) {
+                        const float* tp = tile + ilo * step + c;
+                        if (t == 1) {
+                            for (int ii = ilo; ii <= ihi; ++ii) pm = fmaxf(pm, tp[(ii - ilo) * step] + unew[ii]);
+                            if (pm != -INFINITY)
+                                for (int ii = ilo; ii <= ihi; ++ii) ps += ex2(tp[(ii - ilo) * step] + unew[ii] - pm);
+                        } else if (vc != -INFINITY) {
+                            const float2 vv = make_float2(vc, vc);
+                            float2 q0 = make_float2(0.f, 0.f), q1 = q0;
+                            int ii = ilo;
+                            if (ii & 1) {  // align the unew pairs
+                                q0.x += ex2(tp[0] + unew[ii] + vc);
+                                ++ii;
+                                tp += step;
+                            }
+                            for (; ii + 3 <= ihi; ii += 4, tp += 4 * step) {
+                                const float2 ua = *reinterpret_cast<const float2*>(unew + ii);
+                                const float2 ub = *reinterpret_cast<const float2*>(unew + ii + 2);
+                                q0 = fadd2(q0, ex2x2(fadd2(make_float2(tp[0], tp[step]), fadd2(ua, vv))));
+                                q1 = fadd2(q1, ex2x2(fadd2(make_float2(tp[2 * step], tp[3 * step]), fadd2(ub, vv))));
+                            }
+                            for (; ii <= ihi; ++ii, tp += step) q1.x += ex2(tp[0] + unew[ii] + vc);
+                            ps = (q0.x + q0.y) + (q1.x + q1.y);
+                        }
+                    }
+                    csum[hh * Nw + c] = ps;
+                    if (t == 1) cmax[hh * Nw + c] = pm;
+                }
+            }
+            __syncthreads();
+            {
+                u64* pout = f.part[t & 1] + ((size_t)bh * f.NB + b) * Nw;
+                for (int c = tid; c < Nw; c += kThreads) {
+                    const float s0 = csum[c], s1 = csum[Nw + c];
+                    if (t == 1) {
+                        const float m0 = cmax[c], m1 = cmax[Nw + c];
+                        const float M = fmaxf(m0, m1);
+                        float sum = 0.f;
+                        if (M != -INFINITY) {
+                            if (m0 != -INFINITY) sum += s0 * ex2(m0 - M);
+                            if (m1 != -INFINITY) sum += s1 * ex2(m1 - M);
+                        }
+                        st_tagged(f.partm + ((size_t)bh * f.NB + b) * Nw + c, M, 1u);
+                        st_tagged(pout + c, sum, 1u);
+                    } else {
+                        st_tagged(pout + c, s0 + s1, (unsigned)t);
+                    }
+                }
+            }
+            __syncthreads();  // tile / unew / vw reuse by the next tile of this CTA
+        }
+    }
+}
+
+// blocks with any active row or any active column (their owner duties)
+__global__ void k_fs_flags(Geo g, int NB, int* __restrict__ flags) {
+    const int bh = blockIdx.y, b = blockIdx.x;
+    const int x = b * 128 + threadIdx.x;
+    int any = 0;
+    if (x < g.Lq && row_on(g, bh, x)) any = 1;
+    if (x < g.Lk && col_on(g, bh, x)) any = 1;
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) flags[bh * NB + b] = any;
+}
+
+}  // namespace
+
+size_t fsolve_smem_bytes(const Geo& g) {
+    const int Nw = 128 + 2 * g.w;
+    return FsGeo(g.Wf, Nw).floats(Nw) * 4;
+}
+
+bool fsolve_supported(const Geo& g) {
+    return !g.dustbin && g.Lq == g.Lk && g.w <= 128 && fsolve_smem_bytes(g) <= 227 * 1024;
+}
+
+cudaError_t launch_fsolve(const Geo& g, int T, int R, const FSolvePtrs& p, cudaStream_t s) {
+    const int NB = (g.Lq + 127) / 128, Nw = 128 + 2 * g.w;
+    const size_t smem = fsolve_smem_bytes(g);
+    cudaError_t e = cudaFuncSetAttribute(k_fsolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0, dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fsolve, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const int G = std::min(per_sm * nsm, g.BH * NB);
+    // work list: active blocks in (head, block) order
+    k_fs_flags<<<dim3(NB, g.BH), 128, 0, s>>>(g, NB, p.flags);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = launch_compact(p.flags, g.BH * NB, p.work, p.count, s)) != cudaSuccess) return e;
+    const size_t nq = sizeof(float) * (size_t)g.BH * g.Lrq, nk = sizeof(float) * (size_t)g.BH * g.Lrk;
+    const size_t np = sizeof(u64) * (size_t)g.BH * NB * Nw;
+    // tags must not survive from a previous call: step tags start at 1
+    cudaMemsetAsync(p.part[0], 0, np, s);
+    cudaMemsetAsync(p.part[1], 0, np, s);
+    cudaMemsetAsync(p.partm, 0, np, s);
+    cudaMemsetAsync(p.ubuf, 0, nq, s);
+    cudaMemsetAsync(p.vbuf, 0, nk, s);
+    for (int q = 0; q < 3; ++q) {
+        if (p.u_slot[q]) cudaMemsetAsync(p.u_slot[q], 0, nq, s);
+        if (p.v_slot[q]) cudaMemsetAsync(p.v_slot[q], 0, nk, s);
+    }
+    FSolve f;
+    f.S2 = p.S2;
+    f.ubuf = p.ubuf;
+    f.vbuf = p.vbuf;
+    for (int q = 0; q < 3; ++q) {
+        f.u_slot[q] = p.u_slot[q];
+        f.v_slot[q] = p.v_slot[q];
+    }
+    f.part[0] = (u64*)p.part[0];
+    f.part[1] = (u64*)p.part[1];
+    f.partm = (u64*)p.partm;
+    f.vpriv = p.vpriv;
+    f.flags = p.flags;
+    f.work = p.work;
+    f.nwork = p.count;
+    f.NB = NB;
+    f.Nw = Nw;
+    f.T = T;
+    f.R = R;
+    f.err = p.err;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // co-residency: CTAs wait on their neighbours' tags
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k_fsolve, g, f);
+    add_launches(3);
+    return e;
+}
+
+}  // namespace st

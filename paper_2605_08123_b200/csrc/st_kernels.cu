@@ -353,19 +353,24 @@ __device__ __forceinline__ float combine_col(const Geo& g, const FStep& f, int b
     return M + lg2(s);  // v_1 = -(M + lg2 s)   (v_0 = 0)
 }
 
-// One CTA = one 128-row block, its band tile bulk-copied whole into SMEM; one
-// thread per row in the row pass, one thread per window column in the column
-// pass.  The prologue issues every global load it needs (mask bytes, v_{t-2},
-// the <= 3 block partials per column, u_{t-1}) before consuming any of them,
-// so their latencies overlap one another and the tile copy.
-constexpr int kFsCols = 4;    // window columns per thread (Nw <= 512)
+// One CTA = one 128-row block, its band tile bulk-copied whole into SMEM.
+// 256 threads: in the row pass two threads share a row (lanes r and r+16 of a
+// warp; thread h takes the 16-cell groups h, h+2, ... -- with the odd pitch Wf
+// the 32 lanes hit 32 distinct banks); in the column pass one thread per
+// window column.  The prologue issues every global load it needs (mask bytes,
+// v_{t-2}, the block partials, u_{t-1}) before consuming any of them, so
+// their latencies overlap one another and the tile copy.
+constexpr int kFsThreads = 256;
+constexpr int kFsCols = 2;    // window columns per thread (Nw <= 512)
 
 template <bool kFirst, bool kPairsIn>
-__global__ void __launch_bounds__(128) k_fstep(Geo g, FStep f) {
+__global__ void __launch_bounds__(kFsThreads) k_fstep(Geo g, FStep f) {
     extern __shared__ __align__(16) float smf[];
     __shared__ __align__(8) uint64_t bar;
     __shared__ float inv_r[128];
-    const int bh = blockIdx.y, b = blockIdx.x, i0 = b * 128, tid = threadIdx.x, i = i0 + tid;
+    const int bh = blockIdx.y, b = blockIdx.x, i0 = b * 128, tid = threadIdx.x;
+    const int lane = tid & 31, h = lane >> 4, r = (tid >> 5) * 16 + (lane & 15), i = i0 + r;
+    const unsigned pmask = (1u << (lane & 15)) | (1u << ((lane & 15) + 16));  // the two lanes of row r
     const int Nw = f.Nw, Wf = g.Wf;
     float* tile = smf;               // [128][Wf]: scores, then e (or x at cold start)
     float* vw = smf + 128 * Wf;      // [Nw] window duals v_{t-1}
@@ -386,7 +391,7 @@ __global__ void __launch_bounds__(128) k_fstep(Geo g, FStep f) {
     const size_t pb = (size_t)bh * f.NB * Nw;
 #pragma unroll
     for (int a = 0; a < kFsCols; ++a) {
-        const int c = tid + 128 * a;
+        const int c = tid + kFsThreads * a;
         if (c >= Nw) break;
         const int j = i0 - g.w + c;
         const bool inr = j >= 0 && j < g.Lk;
@@ -398,15 +403,14 @@ __global__ void __launch_bounds__(128) k_fstep(Geo g, FStep f) {
         } else {
             // contributing blocks b-2 .. b+2 (w <= 128); window column of j in block b' = c + 128 (b - b')
             float pv[5], pm[5];
-            bool ok[5];
 #pragma unroll
             for (int d = 0; d < 5; ++d) {
                 const int bb = b - 2 + d;
                 const int cc = c + 128 * (2 - d);
-                ok[d] = bb >= 0 && bb < f.NB && cc >= 0 && cc < Nw;
-                const size_t k = pb + (size_t)(ok[d] ? bb : 0) * Nw + (ok[d] ? cc : 0);
-                pv[d] = ok[d] ? f.part_in[k] : 0.f;
-                pm[d] = (kPairsIn && ok[d]) ? f.partm_in[k] : -INFINITY;
+                const bool ok = bb >= 0 && bb < f.NB && cc >= 0 && cc < Nw;
+                const size_t k = pb + (size_t)(ok ? bb : 0) * Nw + (ok ? cc : 0);
+                pv[d] = ok ? f.part_in[k] : 0.f;
+                pm[d] = (kPairsIn && ok) ? f.partm_in[k] : -INFINITY;
             }
             const float prev = (f.v_pp && inr) ? f.v_pp[(size_t)bh * g.Lrk + jc] : 0.f;
             if (con) {
@@ -440,73 +444,83 @@ __global__ void __launch_bounds__(128) k_fstep(Geo g, FStep f) {
     }
     const size_t pbase = pb + (size_t)b * Nw;
     if (!any) {  // fully masked block: zero partials, zero duals
-        for (int c = tid; c < Nw; c += 128) {
+        for (int c = tid; c < Nw; c += kFsThreads) {
             f.part_out[pbase + c] = 0.f;
             if (kFirst) f.partm_out[pbase + c] = -INFINITY;
         }
-        if (in_rows) f.u_out[(size_t)bh * g.Lrq + i] = 0.f;
+        if (in_rows && h == 0) f.u_out[(size_t)bh * g.Lrq + i] = 0.f;
         return;
     }
     __syncthreads();
     sm100::mbar_wait(&bar, 0);
-    // ---- 2. row pass (thread tid owns row i); tile row becomes e (or x)
-    float* trow = tile + tid * Wf;
-    const float* vr = vw + tid;
+    // ---- 2. row pass (threads (r, h)); tile row becomes e (or x)
+    float* trow = tile + r * Wf;
+    const float* vr = vw + r;
     if (active) {
         float o;
         if (kFirst) {
-            float m0 = -INFINITY, m1 = -INFINITY;
-            int k = 0;
-            for (; k + 1 < Wf; k += 2) {
-                m0 = fmaxf(m0, trow[k] + vr[k]);
-                m1 = fmaxf(m1, trow[k + 1] + vr[k + 1]);
-            }
-            if (k < Wf) m0 = fmaxf(m0, trow[k] + vr[k]);
-            o = -fmaxf(m0, m1);
+            float m = -INFINITY;
+            for (int k0 = 16 * h; k0 < Wf; k0 += 32)
+#pragma unroll
+                for (int kk = 0; kk < 16; ++kk)
+                    if (k0 + kk < Wf) m = fmaxf(m, trow[k0 + kk] + vr[k0 + kk]);
+            m = fmaxf(m, __shfl_xor_sync(pmask, m, 16));
+            o = -m;
         } else {
             o = uo;
         }
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        int k = 0;
-        for (; k + 3 < Wf; k += 4) {
-            const float x0 = trow[k] + vr[k] + o, x1 = trow[k + 1] + vr[k + 1] + o;
-            const float x2 = trow[k + 2] + vr[k + 2] + o, x3 = trow[k + 3] + vr[k + 3] + o;
-            const float e0 = ex2(x0), e1 = ex2(x1), e2 = ex2(x2), e3 = ex2(x3);
-            trow[k] = kFirst ? x0 : e0;
-            trow[k + 1] = kFirst ? x1 : e1;
-            trow[k + 2] = kFirst ? x2 : e2;
-            trow[k + 3] = kFirst ? x3 : e3;
-            s0 += e0;
-            s1 += e1;
-            s2 += e2;
-            s3 += e3;
+        for (int k0 = 16 * h; k0 < Wf; k0 += 32) {
+            if (k0 + 16 <= Wf) {
+#pragma unroll
+                for (int kk = 0; kk < 16; kk += 4) {
+                    const int k = k0 + kk;
+                    const float x0 = trow[k] + vr[k] + o, x1 = trow[k + 1] + vr[k + 1] + o;
+                    const float x2 = trow[k + 2] + vr[k + 2] + o, x3 = trow[k + 3] + vr[k + 3] + o;
+                    const float e0 = ex2(x0), e1 = ex2(x1), e2 = ex2(x2), e3 = ex2(x3);
+                    trow[k] = kFirst ? x0 : e0;
+                    trow[k + 1] = kFirst ? x1 : e1;
+                    trow[k + 2] = kFirst ? x2 : e2;
+                    trow[k + 3] = kFirst ? x3 : e3;
+                    s0 += e0;
+                    s1 += e1;
+                    s2 += e2;
+                    s3 += e3;
+                }
+            } else {
+                for (int k = k0; k < Wf; ++k) {
+                    const float x = trow[k] + vr[k] + o;
+                    const float e = ex2(x);
+                    trow[k] = kFirst ? x : e;
+                    s0 += e;
+                }
+            }
         }
-        for (; k < Wf; ++k) {
-            const float x = trow[k] + vr[k] + o;
-            const float e = ex2(x);
-            trow[k] = kFirst ? x : e;
-            s0 += e;
-        }
-        const float rs = (s0 + s1) + (s2 + s3);
+        float rs = (s0 + s1) + (s2 + s3);
+        rs += __shfl_xor_sync(pmask, rs, 16);
         const float lr = lg2(rs);
         float u = o - lr;
         if (!(rs > 0.f) || !isfinite(u)) {
-            atomicOr(f.err, 64);
+            if (h == 0) atomicOr(f.err, 64);
             u = 0.f;
         }
-        f.u_out[(size_t)bh * g.Lrq + i] = u;
-        inv_r[tid] = kFirst ? lr : 1.f / rs;  // cold start keeps lg2 r_i (log-domain partials)
+        if (h == 0) {
+            f.u_out[(size_t)bh * g.Lrq + i] = u;
+            inv_r[r] = kFirst ? lr : 1.f / rs;  // cold start keeps lg2 r_i (log-domain partials)
+        }
     } else {
-        if (in_rows) f.u_out[(size_t)bh * g.Lrq + i] = 0.f;
-        inv_r[tid] = kFirst ? INFINITY : 0.f;
+        if (h == 0) {
+            if (in_rows) f.u_out[(size_t)bh * g.Lrq + i] = 0.f;
+            inv_r[r] = kFirst ? INFINITY : 0.f;
+        }
         const float z = kFirst ? -INFINITY : 0.f;  // no -inf * 0 in the column pass
-        for (int k = 0; k < Wf; ++k) trow[k] = z;
+        for (int k = h; k < Wf; k += 2) trow[k] = z;
     }
     __syncthreads();
     // ---- 3. column partials: window column c collects rows ii with c - 2w <= ii <= c
 #pragma unroll
     for (int a = 0; a < kFsCols; ++a) {
-        const int c = tid + 128 * a;
+        const int c = tid + kFsThreads * a;
         if (c >= Nw) break;
         const int lo = max(0, c - 2 * g.w), hi = min(127, c);
         const float* tp = tile + lo * Wf + (c - lo);
@@ -1073,7 +1087,7 @@ cudaError_t launch_stepT(const Geo& g, bool first, const float* S2, const float*
 }
 
 size_t fstep_smem_bytes(const Geo& g) {
-    if (g.w > 128) return SIZE_MAX;  // <= 3 contributing blocks per column, <= kFsCols columns per thread
+    if (g.w > 128) return SIZE_MAX;  // <= 5 contributing blocks per column, <= kFsCols columns per thread
     return (size_t)128 * g.Wf * 4 + (size_t)(128 + 2 * g.w) * 4;
 }
 
@@ -1096,7 +1110,7 @@ cudaError_t launch_fstep(const Geo& g, int t, const FStepPtrs& p, cudaStream_t s
     auto k = (t == 1) ? k_fstep<true, false> : (t == 2) ? k_fstep<false, true> : k_fstep<false, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k<<<dim3(f.NB, g.BH), 128, smem, s>>>(g, f);
+    k<<<dim3(f.NB, g.BH), kFsThreads, smem, s>>>(g, f);
     ++g_launches;
     return cudaGetLastError();
 }

@@ -38,6 +38,25 @@ size_t fstep_smem_bytes(const Geo& g);
 cudaError_t launch_fstep(const Geo& g, int t, const FStepPtrs& p, cudaStream_t s);
 cudaError_t launch_ffinal(const Geo& g, int t_last, const FStepPtrs& p, cudaStream_t s);
 
+// persistent band-resident solve (st_fsolve.cu)
+struct FSolvePtrs {
+    const float* S2;
+    float* ubuf;
+    float* vbuf;
+    float* u_slot[3];
+    float* v_slot[3];
+    void* part[2];    // tagged 64-bit partials [BH][NB][128+2w]
+    void* partm;
+    float* vpriv;     // [BH*NB][128+2w]
+    int* flags;
+    int* work;
+    int* count;
+    int* err;
+};
+size_t fsolve_smem_bytes(const Geo& g);
+bool fsolve_supported(const Geo& g);
+cudaError_t launch_fsolve(const Geo& g, int T, int R, const FSolvePtrs& p, cudaStream_t s);
+
 long long launch_count(bool reset);
 void add_launches(long long n);
 size_t bwdT_smem_bytes(const Geo& g);

@@ -612,6 +612,11 @@ cudaError_t launch_pack(int dtype, const void* X, int BH, int L, int Lr, int Lp,
     return cudaGetLastError();
 }
 
+cudaError_t launch_compact(const int* flags, int n, int* work, int* count, cudaStream_t s) {
+    k_compact<<<1, 1024, 0, s>>>(flags, n, work, count);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_worklist(const uint8_t* mask, int H, int BH, int L, int NB, int* flags, int* work, int* count,
                             cudaStream_t s) {
     k_block_flags<<<BH * NB, 128, 0, s>>>(mask, H, BH, L, NB, flags);

@@ -50,6 +50,7 @@ cudaError_t launch_dustbin(const DustArgs& a, bool first, int BH, cudaStream_t s
 // layout, row r stored at packed row r + shift (other packed rows zero).
 cudaError_t launch_pack(int dtype, const void* X, int BH, int L, int Lr, int Lp, int d, int shift, uint8_t* p0,
                         uint8_t* p1, uint8_t* p2, cudaStream_t s);
+cudaError_t launch_compact(const int* flags, int n, int* work, int* count, cudaStream_t s);
 cudaError_t launch_worklist(const uint8_t* mask, int H, int BH, int L, int NB, int* flags, int* work, int* count,
                             cudaStream_t s);
 

@@ -8,7 +8,7 @@ agg = collections.defaultdict(list)
 for r in data:
     if len(r) <= vi or r[hdr.index('Metric Name')] != 'gpu__time_duration.sum':
         continue
-    v = float(r[vi].replace(',', '')) * {'nsecond': 1e-3, 'usecond': 1, 'msecond': 1e3}.get(r[ui], 1)
+    v = float(r[vi].replace(',', '')) * {'nsecond': 1e-3, 'ns': 1e-3, 'usecond': 1, 'us': 1, 'msecond': 1e3, 'ms': 1e3}.get(r[ui], 1)
     agg[r[ki].split('(')[0][:60]].append(v)
 tot = sum(sum(v) for v in agg.values())
 for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
