@@ -14,6 +14,7 @@
 // The band tile of each CTA is contiguous in memory and arrives with one 1-D
 // bulk async copy per band; window vectors and operand rows are staged beside it.
 // The dustbin row / column (full-length reductions) run in the generic kernels.
+#include <cstdlib>
 #include <type_traits>
 
 #include "st_common.cuh"
@@ -261,6 +262,252 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Vector stages (R6 dQ, C6 dK, C1 dV, RO output) as weights + band GEMM.
+// Phase 1 (two threads per own row): the per-cell weight W (P22 or Sbar) is
+// computed once and written over the S tile in place; scalar partials
+// (g_v, d_eps) are combined over the two halves in a fixed order.
+// Phase 2: out[i][:] = sum_k W[i][k] X[i - w + k][:] as a register-tiled band
+// GEMM: thread = 4 own rows x (D/8) columns, per band step 4 broadcast W loads
+// + D/32 LDS.128 of the operand row feed 4 D/8 FMAs.
+// ---------------------------------------------------------------------------
+template <int kOp, bool kDirect, int D, class TIn>
+__global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
+    extern __shared__ __align__(16) float smf[];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ float sacc[2][128], sdacc[2][128], pd[128];
+    constexpr bool kRow = kOp < 10;
+    constexpr bool kNeedZ = (kOp == R6 || kOp == C1 || kOp == C6);
+    constexpr int CPT = D / 8;  // output columns per thread
+    const int Lo = kRow ? g.Lq : g.Lk, Lx = kRow ? g.Lk : g.Lq;
+    const int Lro = kRow ? g.Lrq : g.Lrk, Lrx = kRow ? g.Lrk : g.Lrq;
+    const int Lpo = kRow ? g.Lqp : g.Lkp;
+    const uint8_t* mo = kRow ? g.row_mask : g.col_mask;
+    const uint8_t* mx = kRow ? g.col_mask : g.row_mask;
+    const int bh = blockIdx.y, i0 = blockIdx.x * 128, tid = threadIdx.x;
+    const size_t bo = (size_t)bh * Lro, bx = (size_t)bh * Lrx;
+    auto on_o = [&](int k) { return k < Lo && (mo == nullptr || mo[(size_t)(bh / g.H) * Lo + k] != 0); };
+    auto on_x = [&](int k) { return k >= 0 && k < Lx && (mx == nullptr || mx[(size_t)(bh / g.H) * Lx + k] != 0); };
+    const int r = tid & 127, hh = tid >> 7, i = i0 + r;
+    const bool active = on_o(i);
+    float* vo = kOp == R6 ? a.dQ : kOp == C1 ? a.dV : kOp == RO ? a.O : a.dK;
+    if (!__syncthreads_or(active)) {
+        if (hh == 0 && i < Lo) {
+            if (kOp == R6) a.deps_part[bo + i] = 0.f;
+            if (kOp == C1) a.g_v[bo + i] = 0.f;
+            for (int x = 0; x < g.d; ++x) vo[(bo + i) * g.d + x] = 0.f;
+        }
+        return;
+    }
+    const int Wf = g.Wf, Nw = 128 + 2 * g.w;
+    float* tS = smf;
+    float* tZ = tS + 128 * Wf;
+    float* wv = tZ + (kNeedZ ? 128 * Wf : 0);  // window vectors [5][Nw]
+    float* ops = wv + ((5 * Nw + 3) & ~3);     // operand rows [Nw][D + 4]
+    if (tid == 0) {
+        sm100::mbar_init(&bar, 1);
+        sm100::fence_mbar_init();
+        const uint32_t tb = 128u * (uint32_t)Wf * 4u;
+        sm100::mbar_arrive_expect_tx(&bar, kNeedZ ? 2 * tb : tb);
+        const size_t off = ((size_t)bh * Lpo + i0) * Wf;
+        sm100::bulk_g2s(tS, (kRow ? a.S2 : a.S2T) + off, tb, &bar);
+        if (kNeedZ) sm100::bulk_g2s(tZ, (kRow ? a.Z : a.ZT) + off, tb, &bar);
+    }
+    // window vectors (other side), c <-> x = i0 - w + c; 0 where invalid (tile carries -inf there)
+    //   R6: v2, beta|v1, delta|v0, v2b(=g_v), v1b     C6: u2, alpha|u1, -, u2b, u1b
+    //   C1: u2                                         RO: v
+    for (int c = tid; c < Nw; c += 256) {
+        const int x = i0 - g.w + c;
+        float w0 = 0.f, w1 = 0.f, w2 = 0.f, w3 = 0.f, w4 = 0.f;
+        if (on_x(x)) {
+            if (kRow) {
+                w0 = a.v2[bx + x];
+                if (kOp == R6) {
+                    const float v1 = a.v1[bx + x], v0 = a.v0[bx + x];
+                    w1 = kDirect ? v1 : ex2(v1 - w0);
+                    w2 = kDirect ? v0 : ex2(v0 - w0);
+                    w3 = a.g_v[bx + x];
+                    w4 = a.v1b[bx + x];
+                }
+            } else {
+                w0 = a.u2[bx + x];
+                if (kOp == C6) {
+                    const float u1 = a.u1[bx + x];
+                    w1 = kDirect ? u1 : ex2(u1 - w0);
+                    w3 = a.u2b[bx + x];
+                    w4 = a.u1b[bx + x];
+                }
+            }
+        }
+        wv[c] = w0;
+        wv[Nw + c] = w1;
+        wv[2 * Nw + c] = w2;
+        wv[3 * Nw + c] = w3;
+        wv[4 * Nw + c] = w4;
+    }
+    {
+        const TIn* src = (kOp == R6) ? a.K : (kOp == C1) ? a.dO : (kOp == RO) ? a.V : a.Q;
+        for (int e = tid; e < Nw * (D / 4); e += 256) {
+            const int c = e / (D / 4), q = (e % (D / 4)) * 4;
+            const int x = i0 - g.w + c;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (x >= 0 && x < Lx) {
+                const TIn* sp = src + (bx + x) * D + q;
+                if constexpr (sizeof(TIn) == 4) {
+                    v = *reinterpret_cast<const float4*>(sp);
+                } else {
+                    v.x = ldf(sp); v.y = ldf(sp + 1); v.z = ldf(sp + 2); v.w = ldf(sp + 3);
+                }
+            }
+            *reinterpret_cast<float4*>(ops + c * (D + 4) + q) = v;
+        }
+    }
+    __syncthreads();
+    sm100::mbar_wait(&bar, 0);
+    // ---- phase 1: weights
+    const int half = (Wf + 1) >> 1;
+    const int kb = hh ? half : 0, ke = hh ? Wf : half;
+    float* ts = tS + r * Wf;
+    const float* tz = tZ + r * Wf;
+    float acc = 0.f, dacc = 0.f;
+    if (active) {
+        float o2, o1 = 0.f, o0 = 0.f, ob2 = 0.f, ob1 = 0.f;
+        if (kRow) {
+            o2 = a.u2[bo + i];
+            o1 = a.u1[bo + i];
+            if (kOp == R6) {
+                ob2 = a.u2b[bo + i];
+                ob1 = a.u1b[bo + i];
+            }
+        } else {
+            o2 = a.v2[bo + i];
+            o1 = a.v1[bo + i];
+            o0 = a.v0[bo + i];
+            if (kOp == C6) {
+                ob2 = a.g_v[bo + i];
+                ob1 = a.v1b[bo + i];
+            }
+        }
+        // one-reference modifiers of the own index: R6 alpha_i; C6 beta_j, delta_j
+        const float ma = ex2(o1 - o2), mb = kRow ? 0.f : ex2(o0 - o2);
+        for (int k = kb; k < ke; ++k) {
+            const int c = r + k;
+            const float s2 = ts[k];
+            float wgt = 0.f;
+            if (s2 != -INFINITY) {
+                const float p = ex2(s2 + o2 + wv[c]);
+                if (kOp == RO) {
+                    wgt = p;
+                } else if (kOp == C1) {
+                    acc += p * tz[k];
+                    wgt = p;
+                } else if (kOp == R6) {
+                    const float z = tz[k];
+                    if (kDirect) {
+                        wgt = sbar_of(true, s2, p, z, o1, o2, wv[2 * Nw + c], wv[Nw + c], wv[c], ob2, ob1,
+                                      wv[3 * Nw + c], wv[4 * Nw + c]);
+                    } else {  // Sbar = P22 (Z - v2b_j - beta_j u2b_i - alpha_i beta_j v1b_j - alpha_i delta_j u1b_i)
+                        const float bj = wv[Nw + c], dj = wv[2 * Nw + c];
+                        wgt = p * (z - wv[3 * Nw + c] - bj * ob2 - ma * bj * wv[4 * Nw + c] - ma * dj * ob1);
+                    }
+                    dacc += wgt * (s2 * kLn2);
+                } else {  // C6: own = column j, window = rows i
+                    const float z = tz[k];
+                    if (kDirect) {
+                        wgt = sbar_of(true, s2, p, z, wv[Nw + c], wv[c], o0, o1, o2, wv[3 * Nw + c], wv[4 * Nw + c],
+                                      ob2, ob1);
+                    } else {  // alpha_i = wv[Nw + c], beta_j = ma, delta_j = mb
+                        const float ai = wv[Nw + c];
+                        wgt = p * (z - ob2 - ma * wv[3 * Nw + c] - ai * ma * ob1 - ai * mb * wv[4 * Nw + c]);
+                    }
+                }
+            }
+            ts[k] = wgt;
+        }
+        if (hh == 0) {
+            float pdv = 0.f;
+            if (g.dustbin) {  // the spoke cell (row i, dustbin column) / (dustbin row, column j)
+                const int xd = Lx;
+                const float s2 = g.sd2;
+                const float x2 = kRow ? a.v2[bx + xd] : a.u2[bx + xd];
+                const float p = ex2(s2 + o2 + x2);
+                if (kOp == RO) {
+                    pdv = p;
+                } else if (kOp == C1) {
+                    acc += p * a.ZdT[(size_t)bh * g.Lkp + i];
+                    pdv = p;
+                } else if (kOp == R6) {
+                    const float x1 = a.v1[bx + xd];
+                    const float sb = sbar_of(kDirect, s2, p, a.Zd[(size_t)bh * g.Lqp + i], o1, o2, a.v0[bx + xd], x1,
+                                             x2, ob2, ob1, a.g_v[bx + xd], a.v1b[bx + xd]);
+                    dacc += sb * (s2 * kLn2);  // constant cost: no dQ contribution
+                }
+            }
+            pd[r] = pdv;
+        }
+    } else {
+        for (int k = kb; k < ke; ++k) ts[k] = 0.f;
+        if (hh == 0) pd[r] = 0.f;
+    }
+    sacc[hh][r] = acc;
+    sdacc[hh][r] = dacc;
+    __syncthreads();
+    if (hh == 0 && i < Lo) {
+        if (kOp == C1) a.g_v[bo + i] = active ? sacc[0][r] + sacc[1][r] : 0.f;
+        if (kOp == R6) a.deps_part[bo + i] = active ? sdacc[0][r] + sdacc[1][r] : 0.f;
+    }
+    // ---- phase 2: band GEMM.  thread = rows 4 rg .. 4 rg + 3, column chunks {4 cg + 32 m}
+    const int rg = tid >> 3, cg = tid & 7;
+    float accv[4][CPT];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < CPT; ++e) accv[q][e] = 0.f;
+    const float* wrow = tS + (4 * rg) * Wf;
+    for (int kk = 0; kk < Wf + 3; ++kk) {
+        float wq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int k = kk - q;
+            wq[q] = (k >= 0 && k < Wf) ? wrow[q * Wf + k] : 0.f;
+        }
+        const float* xr = ops + (4 * rg + kk) * (D + 4) + 4 * cg;
+#pragma unroll
+        for (int m = 0; m < CPT / 4; ++m) {
+            const float4 x4 = *reinterpret_cast<const float4*>(xr + 32 * m);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                accv[q][4 * m + 0] = fmaf(wq[q], x4.x, accv[q][4 * m + 0]);
+                accv[q][4 * m + 1] = fmaf(wq[q], x4.y, accv[q][4 * m + 1]);
+                accv[q][4 * m + 2] = fmaf(wq[q], x4.z, accv[q][4 * m + 2]);
+                accv[q][4 * m + 3] = fmaf(wq[q], x4.w, accv[q][4 * m + 3]);
+            }
+        }
+    }
+    const float sc = (kOp == C1 || kOp == RO) ? 1.f : g.inv_qk;
+    const TIn* dsrc = (kOp == RO) ? a.V : (kOp == C1) ? a.dO : nullptr;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int row = 4 * rg + q, ii = i0 + row;
+        if (ii >= Lo) continue;
+        const float pdq = pd[row];
+#pragma unroll
+        for (int m = 0; m < CPT / 4; ++m) {
+            const int col = 4 * cg + 32 * m;
+            float4 o4 = make_float4(accv[q][4 * m] * sc, accv[q][4 * m + 1] * sc, accv[q][4 * m + 2] * sc,
+                                    accv[q][4 * m + 3] * sc);
+            if (dsrc != nullptr && g.dustbin) {  // + p_dust * (V | dO)_dustbin
+                const TIn* dr = dsrc + (bx + Lx) * D + col;
+                o4.x = fmaf(pdq, ldf(dr), o4.x);
+                o4.y = fmaf(pdq, ldf(dr + 1), o4.y);
+                o4.z = fmaf(pdq, ldf(dr + 2), o4.z);
+                o4.w = fmaf(pdq, ldf(dr + 3), o4.w);
+            }
+            *reinterpret_cast<float4*>(vo + (bo + ii) * D + col) = o4;
+        }
+    }
+}
+
 // Zd_i = dO_i . V_dustbin (rows) and ZdT_j = dO_dustbin . V_j (columns)
 template <class TIn>
 __global__ void k_dust_dots(Geo g, const TIn* __restrict__ dO, const TIn* __restrict__ V, float* Zd, float* ZdT) {
@@ -298,6 +545,20 @@ bool bwdT_supported(const Geo& g) {
 template <int kOp, bool kDirect, int D, class TIn>
 static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
     const bool row = kOp < 10;
+    constexpr bool kVec = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RO);
+    if (kVec && D <= 64 && !getenv("ST_NO_BWDV")) {  // weights + register-tiled band GEMM
+        const size_t smem = bwdT_smem_bytes(g);
+        auto k = k_bwdV<kOp, kDirect, D, TIn>;
+        static size_t cur = 0;
+        if (smem > cur) {
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            cur = smem;
+        }
+        const int n = row ? g.Lq : g.Lk;
+        k<<<dim3((n + 127) / 128, g.BH), 256, smem, s>>>(g, a);
+        return cudaGetLastError();
+    }
     const size_t smem = bwdT_smem_bytes(g);
     auto k = k_bwdT<kOp, kDirect, D, TIn>;
     static size_t cur = 0;
