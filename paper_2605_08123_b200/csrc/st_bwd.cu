@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
     float* tS = smf;
     float* tZ = tS + 128 * Wf;
     float* wv = tZ + (kNeedZ ? 128 * Wf : 0);  // window vectors [nvec][Nw]
-    constexpr int nvec = 5;
+    constexpr int nvec = 5;  // (layout must match bwdT_op_smem)
     float* ops = wv + ((nvec * Nw + 3) & ~3);  // operand rows [Nw][D + 4], 16-byte aligned
     if (threadIdx.x == 0) {
         sm100::mbar_init(&bar, 1);
@@ -542,6 +542,14 @@ bool bwdT_supported(const Geo& g) {
     return (g.d == 32 || g.d == 64 || g.d == 128) && bwdT_smem_bytes(g) <= 227 * 1024;
 }
 
+// SMEM of one k_bwdT stage: S tile, Z tile (R1 / C1 / R6 / C6), window vectors, operand rows (vector stages)
+static size_t bwdT_op_smem(const Geo& g, int op, int D) {
+    const int Nw = 128 + 2 * g.w;
+    const bool z = (op == R1 || op == R6 || op == C1 || op == C6);
+    const bool vec = (op == R6 || op == C1 || op == C6 || op == RO);
+    return (size_t)(z ? 2 : 1) * 128 * g.Wf * 4 + (size_t)((5 * Nw + 3) & ~3) * 4 + (vec ? (size_t)Nw * (D + 4) * 4 : 0) + 64;
+}
+
 template <int kOp, bool kDirect, int D, class TIn>
 static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
     const bool row = kOp < 10;
@@ -559,7 +567,7 @@ static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
         k<<<dim3((n + 127) / 128, g.BH), 256, smem, s>>>(g, a);
         return cudaGetLastError();
     }
-    const size_t smem = bwdT_smem_bytes(g);
+    const size_t smem = bwdT_op_smem(g, kOp, D);
     auto k = k_bwdT<kOp, kDirect, D, TIn>;
     static size_t cur = 0;
     if (smem > cur) {

@@ -11,6 +11,7 @@
 // Every reduction is owned by one warp (one row or one column), so results are
 // deterministic and independent of launch geometry.
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "st_common.cuh"
