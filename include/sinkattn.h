@@ -71,10 +71,17 @@ typedef struct st_desc {
     int32_t dustbin;      /* 0, or 1 = one active dustbin token per side on the spoke support */
     double dustbin_cost;  /* constant cost on every dustbin edge (score = -cost / epsilon) */
     int32_t centered;     /* 1 = reference default: report the centered gauge ledger in saved */
-    int32_t flags;        /* 0 = auto; ST_FLAG_GENERIC forces the generic (non-tensor-core) kernels */
+    int32_t flags;        /* 0 = auto; ST_FLAG_GENERIC forces the generic (non-tensor-core) kernels,
+                             ST_FLAG_REUSE_BAND (backward) reuses the forward's score band */
 } st_desc;
 
 #define ST_FLAG_GENERIC 1
+/* st_backward only: reuse the score band the most recent st_forward left in the
+ * same workspace (the reference's r2_backward consumes run.scaled the same way,
+ * adjoint.hpp:232).  Honoured only when that forward had the same desc, Q and K
+ * pointers (host-side registry); the caller must not have written the workspace
+ * or Q/K in between.  Otherwise the band is recomputed. */
+#define ST_FLAG_REUSE_BAND 2
 
 /* Device bytes of the opaque saved state written by st_forward and read by
  * st_backward: fp32 tail duals u, v at steps T, T+1, T+2 plus the per-head

@@ -27,6 +27,7 @@ ST_NOT_SUPPORTED = 9
 ST_F32 = 0
 ST_BF16 = 1
 ST_FLAG_GENERIC = 1
+ST_FLAG_REUSE_BAND = 2
 ST_ONE_REFERENCE = 0
 ST_DIRECT_FOUR_PLAN = 1
 

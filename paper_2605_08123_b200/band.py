@@ -120,10 +120,12 @@ class Workspace:
 
     def __init__(self) -> None:
         self._buf: Optional[torch.Tensor] = None
+        self.last_forward: Optional[object] = None  # token of the forward whose score band the buffer holds
 
     def get(self, nbytes: int, device) -> torch.Tensor:
         if self._buf is None or self._buf.numel() < nbytes or self._buf.device != torch.device(device):
             self._buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            self.last_forward = None
         return self._buf
 
 
@@ -150,6 +152,7 @@ class SurrogateRun:
     V: torch.Tensor
     row_mask: Optional[torch.Tensor]
     col_mask: Optional[torch.Tensor]
+    workspace: Optional["Workspace"] = None  # holds this forward's score band until reused
 
     def tail_duals(self, row_mask_host=None, col_mask_host=None):
         """(u[3,BH,L'], v[3,BH,L'], gauge[3,BH]) in natural units, centered if spec.centered."""
@@ -209,11 +212,14 @@ def run_surrogate(Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, spec: BandS
         out = torch.empty((spec.batch, spec.heads, spec.rows, spec.head_dim), dtype=torch.float32, device=dev)
     if saved is None:
         saved = torch.empty(spec.saved_bytes(), dtype=torch.uint8, device=dev)
-    ws = (workspace or _default_ws).get(spec.workspace_bytes(), dev)
+    wso = workspace or _default_ws
+    ws = wso.get(spec.workspace_bytes(), dev)
     d = spec.desc()
     _check(lib.st_forward(ctypes.byref(d), _ptr(Q), _ptr(K), _ptr(V), _ptr(row_mask), _ptr(col_mask), _ptr(out),
                           _ptr(saved), _ptr(ws), ws.numel(), torch.cuda.current_stream(dev).cuda_stream))
-    return SurrogateRun(spec, out, saved, Q, K, V, row_mask, col_mask)
+    run = SurrogateRun(spec, out, saved, Q, K, V, row_mask, col_mask, wso)
+    wso.last_forward = run
+    return run
 
 
 def r2_backward(run: SurrogateRun, G: torch.Tensor, mode: str = "one_reference", *,
@@ -234,8 +240,12 @@ def r2_backward(run: SurrogateRun, G: torch.Tensor, mode: str = "one_reference",
     if eta_v is None:
         eta_v = torch.empty((spec.batch, spec.heads, spec.cols), dtype=torch.float32, device=dev)
     m = {"one_reference": _lib.ST_ONE_REFERENCE, "direct_four_plan": _lib.ST_DIRECT_FOUR_PLAN}[mode]
-    ws = (workspace or _default_ws).get(spec.workspace_bytes(), dev)
+    wso = workspace or _default_ws
+    ws = wso.get(spec.workspace_bytes(), dev)
     d = spec.desc()
+    if wso is run.workspace and wso.last_forward is run:
+        # the workspace still holds this forward's score band (reference: r2_backward(run.scaled, ...))
+        d.flags |= _lib.ST_FLAG_REUSE_BAND
     _check(lib.st_backward(ctypes.byref(d), _ptr(run.saved), _ptr(run.Q), _ptr(run.K), _ptr(run.V), _ptr(G),
                            _ptr(run.row_mask), _ptr(run.col_mask), _ptr(dQ), _ptr(dK), _ptr(dV), _ptr(d_eps),
                            _ptr(eta_v), m, _ptr(ws), ws.numel(), torch.cuda.current_stream(dev).cuda_stream))

@@ -11,7 +11,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/sinkattn.h"
@@ -261,6 +263,31 @@ size_t st_workspace_bytes(const st_desc* desc) {
     return ws_layout(m, tc_plan(desc, m)).bytes;
 }
 
+// Which forward last wrote the score band of a workspace (ST_FLAG_REUSE_BAND).
+namespace {
+struct BandKey {
+    const void *Q, *K, *rm, *cm;
+    st_desc d;
+};
+std::mutex g_band_mu;
+std::unordered_map<const void*, BandKey> g_band;
+bool same_desc(const st_desc& a, const st_desc& b) {
+    return a.batch == b.batch && a.heads == b.heads && a.seq_q == b.seq_q && a.seq_k == b.seq_k &&
+           a.head_dim == b.head_dim && a.half_band == b.half_band && a.epsilon == b.epsilon && a.dtype == b.dtype &&
+           a.dustbin == b.dustbin && a.dustbin_cost == b.dustbin_cost;
+}
+void band_record(const void* ws, const void* Q, const void* K, const void* rm, const void* cm, const st_desc* d) {
+    std::lock_guard<std::mutex> lk(g_band_mu);
+    g_band[ws] = BandKey{Q, K, rm, cm, *d};
+}
+bool band_valid(const void* ws, const void* Q, const void* K, const void* rm, const void* cm, const st_desc* d) {
+    std::lock_guard<std::mutex> lk(g_band_mu);
+    auto it = g_band.find(ws);
+    return it != g_band.end() && it->second.Q == Q && it->second.K == K && it->second.rm == rm &&
+           it->second.cm == cm && same_desc(it->second.d, *d);
+}
+}  // namespace
+
 st_status st_forward(const st_desc* desc, const void* Q, const void* K, const void* V, const uint8_t* row_mask,
                      const uint8_t* col_mask, float* O, void* saved, void* workspace, size_t workspace_bytes,
                      void* stream) {
@@ -497,6 +524,7 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
         const int nslots = (int)std::min<long>(R, 2) + 1;
         ST_CUDA(st::launch_gauges(g, su, nslots, (float*)(sv + sl.gauge), st));
     }
+    band_record(workspace, Q, K, row_mask, col_mask, desc);
     return ST_OK;
 }
 
@@ -541,7 +569,9 @@ st_status st_backward(const st_desc* desc, const void* saved, const void* Q, con
     p.dQ = dQ;
     p.dK = dK;
     p.dV = dV;
-    ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, (float*)p.S2, st));
+    const bool reuse = (desc->flags & ST_FLAG_REUSE_BAND) && !(desc->flags & ST_FLAG_GENERIC) &&
+                       band_valid(workspace, Q, K, row_mask, col_mask, desc) && !getenv("ST_NO_REUSE");
+    if (!reuse) ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, (float*)p.S2, st));
     if (st::bwdT_supported(g) && !(desc->flags & ST_FLAG_GENERIC)) {
         // tile backward: score band + transposes, cotangent band Z = dO V^T + transpose
         st::BwdTPtrs t;

@@ -210,3 +210,21 @@ def test_bf16_full_size_properties(cid):
     assert np.abs(colsum - 1.0).max() < 1e-3, np.abs(colsum - 1.0).max()
     g1 = gpu_run(cfg, inp)
     assert np.all(np.isfinite(g1["dQ"])) and np.all(np.isfinite(g1["dK"]))
+
+
+def test_band_reuse_matches_recompute():
+    """ST_FLAG_REUSE_BAND (backward consumes the forward's score band, as r2_backward(run.scaled, ...)
+    does) gives bit-identical gradients to recomputing the band in a fresh workspace."""
+    cfg = configs.CONFIGS[2].replace(B=1)
+    inp = configs.make_inputs(cfg)
+    spec = band.BandSpec(batch=cfg.B, heads=cfg.H, seq_q=cfg.L, seq_k=cfg.L, head_dim=cfg.d, half_band=cfg.w,
+                         base_depth=cfg.T, tail_depth=cfg.R, epsilon=cfg.eps)
+    shp = (cfg.B, cfg.H, cfg.rows, cfg.d)
+    Q, K, V, G = (torch.from_numpy(x).cuda().reshape(shp) for x in (inp.Q, inp.K, inp.V, inp.G))
+    rm = torch.from_numpy(inp.row_mask).cuda()
+    ws = band.Workspace()
+    run = band.run_surrogate(Q, K, V, spec, rm, rm, workspace=ws)
+    a = band.r2_backward(run, G, workspace=ws)           # reuses the band
+    b = band.r2_backward(run, G, workspace=band.Workspace())  # recomputes it
+    for x, y in ((a.grad_q, b.grad_q), (a.grad_k, b.grad_k), (a.grad_v, b.grad_v), (a.d_eps, b.d_eps)):
+        assert torch.equal(x, y)
