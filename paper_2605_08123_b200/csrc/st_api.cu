@@ -268,6 +268,7 @@ namespace {
 struct BandKey {
     const void *Q, *K, *rm, *cm;
     st_desc d;
+    bool hasT;  // the transposed band S2T is valid too
 };
 std::mutex g_band_mu;
 std::unordered_map<const void*, BandKey> g_band;
@@ -276,15 +277,19 @@ bool same_desc(const st_desc& a, const st_desc& b) {
            a.head_dim == b.head_dim && a.half_band == b.half_band && a.epsilon == b.epsilon && a.dtype == b.dtype &&
            a.dustbin == b.dustbin && a.dustbin_cost == b.dustbin_cost;
 }
-void band_record(const void* ws, const void* Q, const void* K, const void* rm, const void* cm, const st_desc* d) {
+void band_record(const void* ws, const void* Q, const void* K, const void* rm, const void* cm, const st_desc* d,
+                 bool hasT) {
     std::lock_guard<std::mutex> lk(g_band_mu);
-    g_band[ws] = BandKey{Q, K, rm, cm, *d};
+    g_band[ws] = BandKey{Q, K, rm, cm, *d, hasT};
 }
-bool band_valid(const void* ws, const void* Q, const void* K, const void* rm, const void* cm, const st_desc* d) {
+// 0: nothing reusable, 1: S2 band, 2: S2 and S2T
+int band_valid(const void* ws, const void* Q, const void* K, const void* rm, const void* cm, const st_desc* d) {
     std::lock_guard<std::mutex> lk(g_band_mu);
     auto it = g_band.find(ws);
-    return it != g_band.end() && it->second.Q == Q && it->second.K == K && it->second.rm == rm &&
-           it->second.cm == cm && same_desc(it->second.d, *d);
+    if (it == g_band.end() || it->second.Q != Q || it->second.K != K || it->second.rm != rm || it->second.cm != cm ||
+        !same_desc(it->second.d, *d))
+        return 0;
+    return it->second.hasT ? 2 : 1;
 }
 }  // namespace
 
@@ -312,6 +317,10 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
     float* su = sv ? (float*)(sv + sl.u) : nullptr;
     float* svv = sv ? (float*)(sv + sl.v) : nullptr;
     if (sv) err = (int*)(sv + sl.status);  // the status word travels with the saved state
+    // with a backward to follow, also write the transposed band (the column stages read it)
+    const bool dualT = sv != nullptr && wl.S2T != 0 && st::bwdT_supported(g) && !(desc->flags & ST_FLAG_GENERIC) &&
+                       st::band_dual_supported(g);
+    float* S2T_ws = (float*)(ws + wl.S2T);
     ST_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
     ST_CUDA(cudaMemsetAsync(u_ws, 0, sizeof(float) * m.BH * m.Lrq, st));
     ST_CUDA(cudaMemsetAsync(v_ws, 0, sizeof(float) * m.BH * m.Lrk, st));
@@ -422,9 +431,11 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
             u_prev = u_out;
             v_prev = v_out;
         }
-        ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));  // transport application (generic kernel)
+        if (dualT) ST_CUDA(st::launch_band_dual(g, desc->dtype, false, Q, K, S2, S2T_ws, st));
+        else ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));  // transport application
     } else {
-        ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));
+        if (dualT) ST_CUDA(st::launch_band_dual(g, desc->dtype, false, Q, K, S2, S2T_ws, st));
+        else ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));
         if (fused_ok(desc, m) && T + R >= 1 && st::fsolve_supported(g) && !getenv("ST_NO_FSOLVE")) {
             // one persistent cooperative launch for all T+R steps (band tiles SMEM-resident)
             st::FSolvePtrs p{};
@@ -524,7 +535,7 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
         const int nslots = (int)std::min<long>(R, 2) + 1;
         ST_CUDA(st::launch_gauges(g, su, nslots, (float*)(sv + sl.gauge), st));
     }
-    band_record(workspace, Q, K, row_mask, col_mask, desc);
+    band_record(workspace, Q, K, row_mask, col_mask, desc, dualT);
     return ST_OK;
 }
 
@@ -569,10 +580,21 @@ st_status st_backward(const st_desc* desc, const void* saved, const void* Q, con
     p.dQ = dQ;
     p.dK = dK;
     p.dV = dV;
-    const bool reuse = (desc->flags & ST_FLAG_REUSE_BAND) && !(desc->flags & ST_FLAG_GENERIC) &&
-                       band_valid(workspace, Q, K, row_mask, col_mask, desc) && !getenv("ST_NO_REUSE");
-    if (!reuse) ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, (float*)p.S2, st));
-    if (st::bwdT_supported(g) && !(desc->flags & ST_FLAG_GENERIC)) {
+    const int reuse = ((desc->flags & ST_FLAG_REUSE_BAND) && !(desc->flags & ST_FLAG_GENERIC) && !getenv("ST_NO_REUSE"))
+                          ? band_valid(workspace, Q, K, row_mask, col_mask, desc)
+                          : 0;
+    const bool tiled = st::bwdT_supported(g) && !(desc->flags & ST_FLAG_GENERIC);
+    const bool dual = tiled && st::band_dual_supported(g);
+    bool haveT = reuse == 2;
+    if (!reuse) {
+        if (dual) {
+            ST_CUDA(st::launch_band_dual(g, desc->dtype, false, Q, K, (float*)p.S2, (float*)(ws + wl.S2T), st));
+            haveT = true;
+        } else {
+            ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, (float*)p.S2, st));
+        }
+    }
+    if (tiled) {
         // tile backward: score band + transposes, cotangent band Z = dO V^T + transpose
         st::BwdTPtrs t;
         float* S2T = (float*)(ws + wl.S2T);
@@ -583,9 +605,13 @@ st_status st_backward(const st_desc* desc, const void* saved, const void* Q, con
         t.ZT = ZT;
         t.Zd = (float*)(ws + wl.Zd);
         t.ZdT = (float*)(ws + wl.ZdT);
-        ST_CUDA(st::launch_transpose_band(g, p.S2, S2T, st, -INFINITY));
-        ST_CUDA(st::launch_zband(g, desc->dtype, dO, V, Z, st));
-        ST_CUDA(st::launch_transpose_band(g, Z, ZT, st, 0.f));
+        if (!haveT) ST_CUDA(st::launch_transpose_band(g, p.S2, S2T, st, -INFINITY));
+        if (dual) {
+            ST_CUDA(st::launch_band_dual(g, desc->dtype, true, dO, V, Z, ZT, st));
+        } else {
+            ST_CUDA(st::launch_zband(g, desc->dtype, dO, V, Z, st));
+            ST_CUDA(st::launch_transpose_band(g, Z, ZT, st, 0.f));
+        }
         long long nl = 0;
         ST_CUDA(st::launch_backward_tile(g, desc->dtype, p, t, mode == ST_DIRECT_FOUR_PLAN, st, nl));
         st::add_launches(nl);

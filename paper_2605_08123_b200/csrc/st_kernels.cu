@@ -10,6 +10,7 @@
 //
 // Every reduction is owned by one warp (one row or one column), so results are
 // deterministic and independent of launch geometry.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -127,7 +128,7 @@ struct BandMma {
 // DMMAs and the inner loop has no conversions.
 template <class TIn, bool kZ, int D>
 __global__ void __launch_bounds__(256) k_band_mma(Geo g, const TIn* __restrict__ A, const TIn* __restrict__ B,
-                                                  float* __restrict__ out) {
+                                                  float* __restrict__ out, float* __restrict__ outT) {
     using M = BandMma<D>;
     constexpr int CP = M::CP, P = M::P, KS = D / 4;
     extern __shared__ __align__(16) double sqa[];  // [128][P] query rows of the block, f64
@@ -157,12 +158,6 @@ __global__ void __launch_bounds__(256) k_band_mma(Geo g, const TIn* __restrict__
     const int CT = (7 + 2 * g.w) / 8 + 1;     // column tiles one row tile touches
     const int NCT = 15 + CT;                  // column tiles of the block window
     const int npass = (NCT + CP - 1) / CP;
-    bool ron[16];
-#pragma unroll
-    for (int ri = 0; ri < 16; ++ri) {
-        const int i = i0 + 8 * ri + gq;
-        ron[ri] = i < g.Lq && row_on(g, bh, i);
-    }
     for (int pass = warp; pass < npass; pass += M::NWARP) {
         const int c0 = pass * CP;
         double bf[CP][KS];
@@ -181,36 +176,48 @@ __global__ void __launch_bounds__(256) k_band_mma(Geo g, const TIn* __restrict__
         }
         // row tiles touching column tiles [c0, c0 + CP): ri in [c0 - CT + 1, c0 + CP - 1]
         const int rlo = max(0, c0 - CT + 1), rhi = min(15, c0 + CP - 1);
-        for (int ri = rlo; ri <= rhi; ++ri) {
-            double c[CP][2];
+        // two row tiles per iteration: 2*CP independent accumulation chains per warp
+        for (int ri = rlo; ri <= rhi; ri += 2) {
+            const bool two = ri + 1 <= rhi;
+            double c[2][CP][2];
 #pragma unroll
-            for (int u = 0; u < CP; ++u) c[u][0] = c[u][1] = 0.0;
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int u = 0; u < CP; ++u) c[q][u][0] = c[q][u][1] = 0.0;
             const double* ap = sqa + (8 * ri + gq) * P + tq;
+            const double* ap2 = ap + (two ? 8 * P : 0);
 #pragma unroll
             for (int s = 0; s < KS; ++s) {
-                const double av = ap[4 * s];
+                const double av = ap[4 * s], av2 = ap2[4 * s];
 #pragma unroll
-                for (int u = 0; u < CP; ++u) dmma884(c[u][0], c[u][1], av, bf[u][s]);
-            }
-            const int i = i0 + 8 * ri + gq;
-            if (i >= g.Lqp) continue;
-            bool rr = false;
-#pragma unroll
-            for (int q = 0; q < 16; ++q)
-                if (q == ri) rr = ron[q];
-#pragma unroll
-            for (int u = 0; u < CP; ++u)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int j = j0 + 8 * (c0 + u) + 2 * tq + h;
-                    const int k = j - i + g.w;
-                    if (k < 0 || k >= g.Wf) continue;
-                    const bool on = rr && jon[u][h];
-                    float val;
-                    if (kZ) val = on ? (float)c[u][h] : 0.f;
-                    else val = on ? (float)(c[u][h] * (double)g.c2) : -INFINITY;
-                    out[((size_t)bh * g.Lqp + i) * g.Wf + k] = val;
+                for (int u = 0; u < CP; ++u) {
+                    dmma884(c[0][u][0], c[0][u][1], av, bf[u][s]);
+                    dmma884(c[1][u][0], c[1][u][1], av2, bf[u][s]);
                 }
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                if (q == 1 && !two) break;
+                const int i = i0 + 8 * (ri + q) + gq;
+                if (i >= g.Lqp) continue;
+                const bool rr = i < g.Lq && row_on(g, bh, i);
+#pragma unroll
+                for (int u = 0; u < CP; ++u)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int j = j0 + 8 * (c0 + u) + 2 * tq + h;
+                        const int k = j - i + g.w;
+                        if (k < 0 || k >= g.Wf) continue;
+                        const bool on = rr && jon[u][h];
+                        float val;
+                        if (kZ) val = on ? (float)c[q][u][h] : 0.f;
+                        else val = on ? (float)(c[q][u][h] * (double)g.c2) : -INFINITY;
+                        out[((size_t)bh * g.Lqp + i) * g.Wf + k] = val;
+                        // the same cell of the transposed band (key side): row j, k' = 2w - k
+                        if (outT != nullptr && j >= 0 && j < g.Lkp)
+                            outT[((size_t)bh * g.Lkp + j) * g.Wf + (2 * g.w - k)] = val;
+                    }
+            }
         }
     }
 }
@@ -1012,28 +1019,29 @@ static cudaError_t launch_band_dot(const Geo& g, const void* A, const void* B, f
 }
 
 template <class TIn, bool kZ, int D>
-static cudaError_t launch_band_mma(const Geo& g, const void* A, const void* B, float* out, cudaStream_t s) {
+static cudaError_t launch_band_mma(const Geo& g, const void* A, const void* B, float* out, float* outT,
+                                   cudaStream_t s) {
     using M = BandMma<D>;
     const size_t smem = M::smem();
     auto kern = k_band_mma<TIn, kZ, D>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<dim3((g.Lq + 127) / 128, g.BH), 256, smem, s>>>(g, (const TIn*)A, (const TIn*)B, out);
+    kern<<<dim3((g.Lq + 127) / 128, g.BH), 256, smem, s>>>(g, (const TIn*)A, (const TIn*)B, out, outT);
     ++g_launches;
     return cudaGetLastError();
 }
 
 // FP64-tensor-core band dot when the head dim has a specialisation
 template <bool kZ>
-static bool band_mma(const Geo& g, int dtype, const void* A, const void* B, float* out, cudaStream_t s,
+static bool band_mma(const Geo& g, int dtype, const void* A, const void* B, float* out, float* outT, cudaStream_t s,
                      cudaError_t& err) {
     if (getenv("ST_NO_DMMA")) return false;
     if (g.d == 32)
-        err = dtype == 0 ? launch_band_mma<float, kZ, 32>(g, A, B, out, s) : launch_band_mma<__nv_bfloat16, kZ, 32>(g, A, B, out, s);
+        err = dtype == 0 ? launch_band_mma<float, kZ, 32>(g, A, B, out, outT, s) : launch_band_mma<__nv_bfloat16, kZ, 32>(g, A, B, out, outT, s);
     else if (g.d == 64)
-        err = dtype == 0 ? launch_band_mma<float, kZ, 64>(g, A, B, out, s) : launch_band_mma<__nv_bfloat16, kZ, 64>(g, A, B, out, s);
+        err = dtype == 0 ? launch_band_mma<float, kZ, 64>(g, A, B, out, outT, s) : launch_band_mma<__nv_bfloat16, kZ, 64>(g, A, B, out, outT, s);
     else if (g.d == 128)
-        err = dtype == 0 ? launch_band_mma<float, kZ, 128>(g, A, B, out, s) : launch_band_mma<__nv_bfloat16, kZ, 128>(g, A, B, out, s);
+        err = dtype == 0 ? launch_band_mma<float, kZ, 128>(g, A, B, out, outT, s) : launch_band_mma<__nv_bfloat16, kZ, 128>(g, A, B, out, outT, s);
     else
         return false;
     return true;
@@ -1041,14 +1049,45 @@ static bool band_mma(const Geo& g, int dtype, const void* A, const void* B, floa
 
 cudaError_t launch_scores(const Geo& g, int dtype, const void* Q, const void* K, float* S2, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
-    if (band_mma<false>(g, dtype, Q, K, S2, s, e)) return e;
+    if (band_mma<false>(g, dtype, Q, K, S2, nullptr, s, e)) return e;
     return dtype == 0 ? launch_band_dot<float, double, false>(g, Q, K, S2, s)
                       : launch_band_dot<__nv_bfloat16, float, false>(g, Q, K, S2, s);
 }
 
+// transposed-band cells whose row i lies outside [0, Lqp): no row block produces them
+__global__ void k_fillT_edges(Geo g, float* __restrict__ outT, float fill) {
+    const int bh = blockIdx.y;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;  // over 2 * min(w, Lkp) rows x Wf
+    const int ne = min(g.w, g.Lkp);
+    if (e >= 2 * ne * g.Wf) return;
+    const int rr = e / g.Wf, kp = e % g.Wf;
+    const int j = rr < ne ? rr : g.Lkp - 2 * ne + rr;
+    const int i = j - g.w + kp;
+    if (i < 0 || i >= g.Lqp) outT[((size_t)bh * g.Lkp + j) * g.Wf + kp] = fill;
+}
+
+bool band_dual_supported(const Geo& g) {
+    return g.Lq == g.Lk && (g.d == 32 || g.d == 64 || g.d == 128) && !getenv("ST_NO_DMMA") && !getenv("ST_NO_DUAL");
+}
+
+// band + its transpose in one pass (band_dual_supported)
+cudaError_t launch_band_dual(const Geo& g, int dtype, bool z, const void* A, const void* B, float* out, float* outT,
+                             cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    const bool ok = z ? band_mma<true>(g, dtype, A, B, out, outT, s, e) : band_mma<false>(g, dtype, A, B, out, outT, s, e);
+    if (!ok) return cudaErrorNotSupported;
+    if (e != cudaSuccess) return e;
+    const int ne = std::min(g.w, g.Lkp);
+    if (ne > 0) {
+        k_fillT_edges<<<dim3((2 * ne * g.Wf + 255) / 256, g.BH), 256, 0, s>>>(g, outT, z ? 0.f : -INFINITY);
+        ++g_launches;
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_zband(const Geo& g, int dtype, const void* dO, const void* V, float* Z, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
-    if (band_mma<true>(g, dtype, dO, V, Z, s, e)) return e;
+    if (band_mma<true>(g, dtype, dO, V, Z, nullptr, s, e)) return e;
     return dtype == 0 ? launch_band_dot<float, float, true>(g, dO, V, Z, s)
                       : launch_band_dot<__nv_bfloat16, float, true>(g, dO, V, Z, s);
 }

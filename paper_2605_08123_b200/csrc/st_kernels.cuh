@@ -73,6 +73,9 @@ cudaError_t launch_scores(const Geo& g, int dtype, const void* Q, const void* K,
 cudaError_t launch_row_step(const Geo& g, bool first, const float* S2, const float* v, const float* u_prev,
                             float* u_out, int* err, cudaStream_t s);
 cudaError_t launch_transpose_band(const Geo& g, const float* S2, float* S2T, cudaStream_t s, float fill);
+bool band_dual_supported(const Geo& g);
+cudaError_t launch_band_dual(const Geo& g, int dtype, bool z, const void* A, const void* B, float* out, float* outT,
+                             cudaStream_t s);
 cudaError_t launch_zband(const Geo& g, int dtype, const void* dO, const void* V, float* Z, cudaStream_t s);
 size_t stepT_smem_bytes(const Geo& g);
 cudaError_t launch_stepT(const Geo& g, bool first, const float* S2, const float* dual_other, const float* off_own,
