@@ -176,7 +176,13 @@ def main():
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    inp = configs.make_inputs(cfg)
+    # weak scaling: the job is world * B examples; rank r owns examples [r*B, (r+1)*B)
+    # (shard.example_partition) -- independent (b, h) problems, no collective on the data path
+    from paper_2605_08123_b200 import shard
+    ex, heads = shard.example_partition(cfg.B, cfg.H, world, rank)
+    inp = configs.make_inputs(cfg.replace(B=cfg.B * world), heads=heads)
+    if inp.row_mask is not None:
+        inp.row_mask, inp.col_mask = inp.row_mask[ex.start:ex.stop], inp.col_mask[ex.start:ex.stop]
     spec = band.BandSpec(batch=cfg.B, heads=cfg.H, seq_q=cfg.L, seq_k=cfg.L, head_dim=cfg.d, half_band=cfg.w,
                          base_depth=cfg.T, tail_depth=cfg.R, epsilon=cfg.eps, dtype=cfg.dtype, dustbin=cfg.dustbin,
                          dustbin_cost=cfg.dustbin_cost)
@@ -354,7 +360,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
             "config": {"workload": workload_str(cfg), "seed": 0, "mode": args.mode,
-                       "parallelism": f"batch x head replicas, {world} GPU(s), no operator collective",
+                       "parallelism": f"batch x head shards: {world} GPU(s) x {cfg.B} examples each, no operator collective",
                        "l2": "flushed between timed steps (256 MiB write)", "cuda_graph": graph is not None,
                        "active_cells_per_step": act, "nominal_cells_per_step": cfg.nominal_cells()},
             "roofline": roofline, "roofline_sfu": roofline_sfu, "cpu_baseline": cpu, "e2e": e2e,
