@@ -33,6 +33,7 @@ inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Dims {
     long BH, Lq, Lk, Lrq, Lrk, d, w, Wf;
+    int esz = 4, dustbin = 0;  // input element bytes, dustbin flag
 };
 
 st_status check_desc(const st_desc* d, Dims& o) {
@@ -53,6 +54,8 @@ st_status check_desc(const st_desc* d, Dims& o) {
     o.d = d->head_dim;
     o.w = std::min<long>(d->half_band, std::max(d->seq_q, d->seq_k));  // wider bands change nothing
     o.Wf = 2 * o.w + 1;
+    o.esz = d->dtype == ST_BF16 ? 2 : 4;
+    o.dustbin = d->dustbin;
     if ((double)o.BH * o.Lq * o.Wf > 4.0e9 || o.Lrq > (1L << 30) || o.Lrk > (1L << 30))
         return fail(ST_SIZE_CAP_EXCEEDED, "problem exceeds the 32-bit index space of the kernels");
     return ST_OK;
@@ -72,6 +75,7 @@ st::Geo make_geo(const st_desc* d, const Dims& m, const uint8_t* rm, const uint8
     g.w = (int)m.w;
     g.Wf = (int)m.Wf;
     g.dustbin = d->dustbin;
+    g.esz = d->dtype == ST_BF16 ? 2 : 4;
     g.eps = (float)d->epsilon;
     g.c2 = (float)(1.4426950408889634 / (std::sqrt((double)m.d) * d->epsilon));
     g.inv_qk = (float)(1.0 / (std::sqrt((double)m.d) * d->epsilon));
@@ -176,6 +180,8 @@ WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
     gg.d = (int)m.d;
     gg.w = (int)m.w;
     gg.Wf = (int)m.Wf;
+    gg.esz = m.esz;
+    gg.dustbin = m.dustbin;
     const bool bt = st::bwdT_supported(gg);
     const size_t band_q = sizeof(float) * (size_t)m.BH * Lqp * m.Wf, band_k = sizeof(float) * (size_t)m.BH * Lkp * m.Wf;
     w.S2T = (!tp.ok || bt) ? take(band_k) : 0;

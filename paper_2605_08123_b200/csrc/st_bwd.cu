@@ -508,6 +508,348 @@ __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Wide-band variants (RB = 64 / 32 rows per CTA, for bands whose 128-row tiles do
+// not fit SMEM: configs 4 and 5).  Same stage math as k_bwdT / k_bwdV; a row is
+// shared by TPR threads that take interleaved groups of GS = 32 / TPR cells (the
+// 32 lanes of a warp hit 32 distinct banks with the odd pitch Wf) and combine
+// with a fixed butterfly.  No dustbin (dustbin configs have narrow bands).
+// ---------------------------------------------------------------------------
+template <int kOp, bool kDirect, int RB, class TIn>
+__global__ void __launch_bounds__(128) k_bwdS(Geo g, BT<TIn> a) {
+    extern __shared__ __align__(16) float smf[];
+    __shared__ __align__(8) uint64_t bar;
+    constexpr int TPR = 128 / RB, GS = 32 / TPR;
+    constexpr bool kRow = kOp < 10;
+    constexpr bool kNeedZ = (kOp == R1);
+    const int Lo = kRow ? g.Lq : g.Lk, Lx = kRow ? g.Lk : g.Lq;
+    const int Lro = kRow ? g.Lrq : g.Lrk, Lrx = kRow ? g.Lrk : g.Lrq;
+    const int Lpo = kRow ? g.Lqp : g.Lkp;
+    const uint8_t* mo = kRow ? g.row_mask : g.col_mask;
+    const uint8_t* mx = kRow ? g.col_mask : g.row_mask;
+    const int bh = blockIdx.y, i0 = blockIdx.x * RB, tid = threadIdx.x, lane = tid & 31;
+    const int part = lane / GS, r = (tid >> 5) * GS + lane % GS, i = i0 + r;
+    const size_t bo = (size_t)bh * Lro, bx = (size_t)bh * Lrx;
+    auto on_o = [&](int k) { return k < Lo && (mo == nullptr || mo[(size_t)(bh / g.H) * Lo + k] != 0); };
+    auto on_x = [&](int k) { return k >= 0 && k < Lx && (mx == nullptr || mx[(size_t)(bh / g.H) * Lx + k] != 0); };
+    const bool active = on_o(i);
+    auto put = [&](float val) {
+        if (kOp == R1) a.g_u[bo + i] = val;
+        if (kOp == R2) a.u2b[bo + i] = val;
+        if (kOp == R4) a.u1b[bo + i] = val;
+        if (kOp == C3) a.v1b[bo + i] = val;
+        if (kOp == C5) a.v0b[bo + i] = val;
+    };
+    if (!__syncthreads_or(active)) {
+        if (part == 0 && i < Lo) put(0.f);
+        return;
+    }
+    const int Wf = g.Wf, Nw = RB + 2 * g.w;
+    float* tS = smf;
+    float* tZ = tS + RB * Wf;
+    float* wv = tZ + (kNeedZ ? RB * Wf : 0);
+    if (tid == 0) {
+        sm100::mbar_init(&bar, 1);
+        sm100::fence_mbar_init();
+        const uint32_t tb = (uint32_t)RB * (uint32_t)Wf * 4u;
+        sm100::mbar_arrive_expect_tx(&bar, kNeedZ ? 2 * tb : tb);
+        const size_t off = ((size_t)bh * Lpo + i0) * Wf;
+        sm100::bulk_g2s(tS, (kRow ? a.S2 : a.S2T) + off, tb, &bar);
+        if (kNeedZ) sm100::bulk_g2s(tZ, a.Z + off, tb, &bar);
+    }
+    for (int c = tid; c < Nw; c += 128) {
+        const int x = i0 - g.w + c;
+        float w0 = 0.f, w1 = 0.f, w3 = 0.f, w4 = 0.f;
+        if (on_x(x)) {
+            if (kRow) {
+                w0 = a.v2[bx + x];
+                w1 = a.v1[bx + x];
+                if (kOp == R2) w3 = a.g_v[bx + x];
+                if (kOp == R4) w4 = a.v1b[bx + x];
+            } else {
+                w0 = a.u2[bx + x];
+                w1 = a.u1[bx + x];
+                if (kOp == C3) w3 = a.u2b[bx + x];
+                if (kOp == C5) w4 = a.u1b[bx + x];
+            }
+        }
+        wv[c] = w0;
+        wv[Nw + c] = w1;
+        wv[3 * Nw + c] = w3;
+        wv[4 * Nw + c] = w4;
+    }
+    __syncthreads();
+    sm100::mbar_wait(&bar, 0);
+    float o2 = 0.f, o1 = 0.f, o0 = 0.f;
+    if (active) {
+        o2 = kRow ? a.u2[bo + i] : a.v2[bo + i];
+        o1 = kRow ? a.u1[bo + i] : a.v1[bo + i];
+        if (!kRow) o0 = a.v0[bo + i];
+    }
+    float acc = 0.f;
+    if (active) {
+        const float* ts = tS + r * Wf;
+        const float* tz = tZ + r * Wf;
+        for (int k0 = part * GS; k0 < Wf; k0 += TPR * GS) {
+#pragma unroll 4
+            for (int kk = 0; kk < GS; ++kk) {
+                const int k = k0 + kk;
+                if (k >= Wf) break;
+                const float s2 = ts[k];
+                if (s2 == -INFINITY) continue;
+                const int c = r + k;
+                const float x2 = wv[c], x1 = wv[Nw + c];
+                const float p = ex2(s2 + o2 + x2);
+                if (kOp == R1) acc += p * tz[k];
+                else if (kOp == R2) acc += p * wv[3 * Nw + c];
+                else if (kOp == R4) acc += kDirect ? ex2(s2 + o1 + x1) * wv[4 * Nw + c] : p * ex2(x1 - x2) * wv[4 * Nw + c];
+                else if (kOp == C3) acc += (kDirect ? ex2(s2 + x2 + o1) : p) * wv[3 * Nw + c];
+                else acc += kDirect ? ex2(s2 + x1 + o0) * wv[4 * Nw + c] : p * ex2(x1 - x2) * wv[4 * Nw + c];
+            }
+        }
+    }
+#pragma unroll
+    for (int off = GS; off < 32; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (part == 0 && i < Lo) {
+        float val = 0.f;
+        if (active) {
+            if (kOp == R1) val = acc;
+            if (kOp == R2) val = a.g_u[bo + i] - acc;
+            if (kOp == R4) val = kDirect ? -acc : -ex2(o1 - o2) * acc;
+            if (kOp == C3) val = kDirect ? -acc : -ex2(o1 - o2) * acc;
+            if (kOp == C5) val = kDirect ? -acc : -ex2(o0 - o2) * acc;
+        }
+        put(val);
+    }
+}
+
+template <class T>
+__device__ __forceinline__ float4 ld4f(const T* p);
+template <>
+__device__ __forceinline__ float4 ld4f<float>(const float* p) {
+    return *reinterpret_cast<const float4*>(p);
+}
+template <>
+__device__ __forceinline__ float4 ld4f<__nv_bfloat16>(const __nv_bfloat16* p) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u), __uint_as_float(u.y << 16),
+                       __uint_as_float(u.y & 0xffff0000u));
+}
+
+template <int RB, int D>
+struct GemmShape {
+    static constexpr int OPT = RB * D / 256;          // outputs per thread
+    static constexpr int RPT = OPT >= 16 ? 4 : 2;     // rows per thread
+    static constexpr int CPT = OPT / RPT;             // columns per thread (multiple of 4)
+    static constexpr int NCG = D / CPT;               // column groups
+    static_assert(CPT % 4 == 0, "column chunks of 4");
+};
+
+template <int kOp, bool kDirect, int D, class TIn, int RB>
+__global__ void __launch_bounds__(256) k_bwdG(Geo g, BT<TIn> a) {
+    extern __shared__ __align__(16) float smf[];
+    __shared__ __align__(8) uint64_t bar;
+    using GS_ = GemmShape<RB, D>;
+    constexpr int TPR = 256 / RB, GS = 32 / TPR;
+    constexpr int OP = D + (sizeof(TIn) == 2 ? 8 : 4);  // operand row pitch (elements), 16-byte rows
+    constexpr bool kRow = kOp < 10;
+    constexpr bool kNeedZ = (kOp == R6 || kOp == C1 || kOp == C6);
+    const int Lo = kRow ? g.Lq : g.Lk, Lx = kRow ? g.Lk : g.Lq;
+    const int Lro = kRow ? g.Lrq : g.Lrk, Lrx = kRow ? g.Lrk : g.Lrq;
+    const int Lpo = kRow ? g.Lqp : g.Lkp;
+    const uint8_t* mo = kRow ? g.row_mask : g.col_mask;
+    const uint8_t* mx = kRow ? g.col_mask : g.row_mask;
+    const int bh = blockIdx.y, i0 = blockIdx.x * RB, tid = threadIdx.x, lane = tid & 31;
+    const int part = lane / GS, r = (tid >> 5) * GS + lane % GS, i = i0 + r;
+    const size_t bo = (size_t)bh * Lro, bx = (size_t)bh * Lrx;
+    auto on_o = [&](int k) { return k < Lo && (mo == nullptr || mo[(size_t)(bh / g.H) * Lo + k] != 0); };
+    auto on_x = [&](int k) { return k >= 0 && k < Lx && (mx == nullptr || mx[(size_t)(bh / g.H) * Lx + k] != 0); };
+    const bool active = on_o(i);
+    float* vo = kOp == R6 ? a.dQ : kOp == C1 ? a.dV : kOp == RO ? a.O : a.dK;
+    if (!__syncthreads_or(active)) {
+        if (part == 0 && i < Lo) {
+            if (kOp == R6) a.deps_part[bo + i] = 0.f;
+            if (kOp == C1) a.g_v[bo + i] = 0.f;
+            for (int x = 0; x < D; ++x) vo[(bo + i) * D + x] = 0.f;
+        }
+        return;
+    }
+    const int Wf = g.Wf, Nw = RB + 2 * g.w;
+    float* tS = smf;
+    float* tZ = tS + RB * Wf;
+    float* wv = tZ + (kNeedZ ? RB * Wf : 0);
+    TIn* ops = reinterpret_cast<TIn*>(wv + ((5 * Nw + 3) & ~3));
+    if (tid == 0) {
+        sm100::mbar_init(&bar, 1);
+        sm100::fence_mbar_init();
+        const uint32_t tb = (uint32_t)RB * (uint32_t)Wf * 4u;
+        sm100::mbar_arrive_expect_tx(&bar, kNeedZ ? 2 * tb : tb);
+        const size_t off = ((size_t)bh * Lpo + i0) * Wf;
+        sm100::bulk_g2s(tS, (kRow ? a.S2 : a.S2T) + off, tb, &bar);
+        if (kNeedZ) sm100::bulk_g2s(tZ, (kRow ? a.Z : a.ZT) + off, tb, &bar);
+    }
+    for (int c = tid; c < Nw; c += 256) {
+        const int x = i0 - g.w + c;
+        float w0 = 0.f, w1 = 0.f, w2 = 0.f, w3 = 0.f, w4 = 0.f;
+        if (on_x(x)) {
+            if (kRow) {
+                w0 = a.v2[bx + x];
+                if (kOp == R6) {
+                    const float v1 = a.v1[bx + x], v0 = a.v0[bx + x];
+                    w1 = kDirect ? v1 : ex2(v1 - w0);
+                    w2 = kDirect ? v0 : ex2(v0 - w0);
+                    w3 = a.g_v[bx + x];
+                    w4 = a.v1b[bx + x];
+                }
+            } else {
+                w0 = a.u2[bx + x];
+                if (kOp == C6) {
+                    const float u1 = a.u1[bx + x];
+                    w1 = kDirect ? u1 : ex2(u1 - w0);
+                    w3 = a.u2b[bx + x];
+                    w4 = a.u1b[bx + x];
+                }
+            }
+        }
+        wv[c] = w0;
+        wv[Nw + c] = w1;
+        wv[2 * Nw + c] = w2;
+        wv[3 * Nw + c] = w3;
+        wv[4 * Nw + c] = w4;
+    }
+    {   // operand window rows, kept in the input dtype (16 bytes at a time)
+        const TIn* src = (kOp == R6) ? a.K : (kOp == C1) ? a.dO : (kOp == RO) ? a.V : a.Q;
+        constexpr int E = 16 / sizeof(TIn);
+        for (int e = tid; e < Nw * (D / E); e += 256) {
+            const int c = e / (D / E), q = (e % (D / E)) * E;
+            const int x = i0 - g.w + c;
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (x >= 0 && x < Lx) v = *reinterpret_cast<const uint4*>(src + (bx + x) * D + q);
+            *reinterpret_cast<uint4*>(ops + c * OP + q) = v;
+        }
+    }
+    __syncthreads();
+    sm100::mbar_wait(&bar, 0);
+    // ---- phase 1: weights over the cell groups of this thread, written in place
+    float acc = 0.f, dacc = 0.f;
+    float* ts = tS + r * Wf;
+    const float* tz = tZ + r * Wf;
+    if (active) {
+        float o2, o1 = 0.f, o0 = 0.f, ob2 = 0.f, ob1 = 0.f;
+        if (kRow) {
+            o2 = a.u2[bo + i];
+            o1 = a.u1[bo + i];
+            if (kOp == R6) {
+                ob2 = a.u2b[bo + i];
+                ob1 = a.u1b[bo + i];
+            }
+        } else {
+            o2 = a.v2[bo + i];
+            o1 = a.v1[bo + i];
+            o0 = a.v0[bo + i];
+            if (kOp == C6) {
+                ob2 = a.g_v[bo + i];
+                ob1 = a.v1b[bo + i];
+            }
+        }
+        const float ma = ex2(o1 - o2), mb = kRow ? 0.f : ex2(o0 - o2);
+        for (int k0 = part * GS; k0 < Wf; k0 += TPR * GS) {
+#pragma unroll 4
+            for (int kk = 0; kk < GS; ++kk) {
+                const int k = k0 + kk;
+                if (k >= Wf) break;
+                const int c = r + k;
+                const float s2 = ts[k];
+                float wgt = 0.f;
+                if (s2 != -INFINITY) {
+                    const float p = ex2(s2 + o2 + wv[c]);
+                    if (kOp == RO) {
+                        wgt = p;
+                    } else if (kOp == C1) {
+                        acc += p * tz[k];
+                        wgt = p;
+                    } else if (kOp == R6) {
+                        const float z = tz[k];
+                        if (kDirect) {
+                            wgt = sbar_of(true, s2, p, z, o1, o2, wv[2 * Nw + c], wv[Nw + c], wv[c], ob2, ob1,
+                                          wv[3 * Nw + c], wv[4 * Nw + c]);
+                        } else {
+                            const float bj = wv[Nw + c], dj = wv[2 * Nw + c];
+                            wgt = p * (z - wv[3 * Nw + c] - bj * ob2 - ma * bj * wv[4 * Nw + c] - ma * dj * ob1);
+                        }
+                        dacc += wgt * (s2 * kLn2);
+                    } else {
+                        const float z = tz[k];
+                        if (kDirect) {
+                            wgt = sbar_of(true, s2, p, z, wv[Nw + c], wv[c], o0, o1, o2, wv[3 * Nw + c],
+                                          wv[4 * Nw + c], ob2, ob1);
+                        } else {
+                            const float ai = wv[Nw + c];
+                            wgt = p * (z - ob2 - ma * wv[3 * Nw + c] - ai * ma * ob1 - ai * mb * wv[4 * Nw + c]);
+                        }
+                    }
+                }
+                ts[k] = wgt;
+            }
+        }
+    } else {
+        for (int k0 = part * GS; k0 < Wf; k0 += TPR * GS)
+            for (int kk = 0; kk < GS && k0 + kk < Wf; ++kk) ts[k0 + kk] = 0.f;
+    }
+#pragma unroll
+    for (int off = GS; off < 32; off <<= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        dacc += __shfl_xor_sync(0xffffffffu, dacc, off);
+    }
+    if (part == 0 && i < Lo) {
+        if (kOp == C1) a.g_v[bo + i] = active ? acc : 0.f;
+        if (kOp == R6) a.deps_part[bo + i] = active ? dacc : 0.f;
+    }
+    __syncthreads();
+    // ---- phase 2: band GEMM, thread = RPT own rows x CPT columns (chunks of 4, stride 4 NCG)
+    constexpr int RPT = GS_::RPT, CPT = GS_::CPT, NCG = GS_::NCG;
+    const int rg = tid / NCG, cg = tid % NCG;
+    float accv[RPT][CPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q)
+#pragma unroll
+        for (int e = 0; e < CPT; ++e) accv[q][e] = 0.f;
+    const float* wrow = tS + (RPT * rg) * Wf;
+    for (int kk = 0; kk < Wf + RPT - 1; ++kk) {
+        float wq[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+            const int k = kk - q;
+            wq[q] = (k >= 0 && k < Wf) ? wrow[q * Wf + k] : 0.f;
+        }
+        const TIn* xr = ops + (RPT * rg + kk) * OP + 4 * cg;
+#pragma unroll
+        for (int m = 0; m < CPT / 4; ++m) {
+            const float4 x4 = ld4f<TIn>(xr + 4 * NCG * m);
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                accv[q][4 * m + 0] = fmaf(wq[q], x4.x, accv[q][4 * m + 0]);
+                accv[q][4 * m + 1] = fmaf(wq[q], x4.y, accv[q][4 * m + 1]);
+                accv[q][4 * m + 2] = fmaf(wq[q], x4.z, accv[q][4 * m + 2]);
+                accv[q][4 * m + 3] = fmaf(wq[q], x4.w, accv[q][4 * m + 3]);
+            }
+        }
+    }
+    const float sc = (kOp == C1 || kOp == RO) ? 1.f : g.inv_qk;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+        const int ii = i0 + RPT * rg + q;
+        if (ii >= Lo) continue;
+#pragma unroll
+        for (int m = 0; m < CPT / 4; ++m) {
+            const int col = 4 * cg + 4 * NCG * m;
+            *reinterpret_cast<float4*>(vo + (bo + ii) * D + col) =
+                make_float4(accv[q][4 * m] * sc, accv[q][4 * m + 1] * sc, accv[q][4 * m + 2] * sc,
+                            accv[q][4 * m + 3] * sc);
+        }
+    }
+}
+
 // Zd_i = dO_i . V_dustbin (rows) and ZdT_j = dO_dustbin . V_j (columns)
 template <class TIn>
 __global__ void k_dust_dots(Geo g, const TIn* __restrict__ dO, const TIn* __restrict__ V, float* Zd, float* ZdT) {
@@ -538,10 +880,6 @@ size_t bwdT_smem_bytes(const Geo& g) {
     return (size_t)2 * 128 * g.Wf * 4 + (size_t)((5 * Nw + 3) & ~3) * 4 + (size_t)Nw * (D + 4) * 4 + 64;
 }
 
-bool bwdT_supported(const Geo& g) {
-    return (g.d == 32 || g.d == 64 || g.d == 128) && bwdT_smem_bytes(g) <= 227 * 1024;
-}
-
 // SMEM of one k_bwdT stage: S tile, Z tile (R1 / C1 / R6 / C6), window vectors, operand rows (vector stages)
 static size_t bwdT_op_smem(const Geo& g, int op, int D) {
     const int Nw = 128 + 2 * g.w;
@@ -550,11 +888,71 @@ static size_t bwdT_op_smem(const Geo& g, int op, int D) {
     return (size_t)(z ? 2 : 1) * 128 * g.Wf * 4 + (size_t)((5 * Nw + 3) & ~3) * 4 + (vec ? (size_t)Nw * (D + 4) * 4 : 0) + 64;
 }
 
+// SMEM of the wide-band kernels (k_bwdS scalar stages, k_bwdG vector stages) at RB rows per CTA
+static size_t wide_smem(const Geo& g, int op, int D, int esz, int RB) {
+    const int Nw = RB + 2 * g.w;
+    const bool vec = (op == R6 || op == C1 || op == C6 || op == RO);
+    const bool z = vec ? (op != RO) : (op == R1);
+    const int OP = D + (esz == 2 ? 8 : 4);
+    return (size_t)(z ? 2 : 1) * RB * g.Wf * 4 + (size_t)((5 * Nw + 3) & ~3) * 4 + (vec ? (size_t)Nw * OP * esz : 0) + 64;
+}
+
+// rows per CTA for a stage: 128 (the k_bwdT / k_bwdV tiles or k_bwdG<128>), else 64 / 32; 0 = none fits
+static int pick_rb(const Geo& g, int op, int D, int esz) {
+    constexpr size_t kMax = 227 * 1024;
+    const bool vec = (op == R6 || op == C1 || op == C6 || op == RO);
+    if (!vec && bwdT_op_smem(g, op, D) <= kMax) return 128;
+    for (int RB : {128, 64, 32}) {
+        if (vec && D == 32 && RB == 32) continue;
+        if (g.dustbin && RB < 128) continue;  // the spoke cells live in the 128-row kernels
+        if (!vec && RB == 128) continue;      // covered above
+        if (wide_smem(g, op, D, esz, RB) <= kMax) return RB;
+    }
+    return 0;
+}
+
+bool bwdT_supported(const Geo& g) {
+    if (!(g.d == 32 || g.d == 64 || g.d == 128)) return false;
+    const int esz = g.esz ? g.esz : 4;
+    const bool narrow = g.d <= 64 && bwdT_smem_bytes(g) <= 227 * 1024;  // k_bwdV path for the vector stages
+    for (int op : {R1, R2, R4, C3, C5})
+        if (!pick_rb(g, op, g.d, esz)) return false;
+    if (!narrow)
+        for (int op : {R6, C6, C1, RO})
+            if (!pick_rb(g, op, g.d, esz)) return false;
+    return true;
+}
+
+template <int kOp, bool kDirect, int D, class TIn, int RB>
+static cudaError_t run_wide(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
+    constexpr bool kVec = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RO);
+    const bool row = kOp < 10;
+    const int n = row ? g.Lq : g.Lk;
+    const size_t smem = wide_smem(g, kOp, D, (int)sizeof(TIn), RB);
+    if constexpr (kVec) {
+        if constexpr (D == 32 && RB == 32) {
+            return cudaErrorNotSupported;
+        } else {
+            auto k = k_bwdG<kOp, kDirect, D, TIn, RB>;
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            k<<<dim3((n + RB - 1) / RB, g.BH), 256, smem, s>>>(g, a);
+        }
+    } else {
+        auto k = k_bwdS<kOp, kDirect, RB, TIn>;
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k<<<dim3((n + RB - 1) / RB, g.BH), 128, smem, s>>>(g, a);
+    }
+    return cudaGetLastError();
+}
+
 template <int kOp, bool kDirect, int D, class TIn>
 static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
     const bool row = kOp < 10;
     constexpr bool kVec = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RO);
-    if (kVec && D <= 64 && !getenv("ST_NO_BWDV")) {  // weights + register-tiled band GEMM
+    if (kVec && D <= 64 && bwdT_smem_bytes(g) <= 227 * 1024 && !getenv("ST_NO_BWDV")) {
+        // 128-row weights + register-tiled band GEMM (operands as f32)
         const size_t smem = bwdT_smem_bytes(g);
         auto k = k_bwdV<kOp, kDirect, D, TIn>;
         static size_t cur = 0;
@@ -566,6 +964,13 @@ static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
         const int n = row ? g.Lq : g.Lk;
         k<<<dim3((n + 127) / 128, g.BH), 256, smem, s>>>(g, a);
         return cudaGetLastError();
+    }
+    const int rb = pick_rb(g, kOp, D, (int)sizeof(TIn));
+    if (rb == 0) return cudaErrorNotSupported;
+    if (kVec || rb != 128) {
+        if (rb == 128) return run_wide<kOp, kDirect, D, TIn, 128>(g, a, s);
+        if (rb == 64) return run_wide<kOp, kDirect, D, TIn, 64>(g, a, s);
+        return run_wide<kOp, kDirect, D, TIn, 32>(g, a, s);
     }
     const size_t smem = bwdT_op_smem(g, kOp, D);
     auto k = k_bwdT<kOp, kDirect, D, TIn>;
