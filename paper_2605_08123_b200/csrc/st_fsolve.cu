@@ -334,6 +334,289 @@ __global__ void __launch_bounds__(kThreads) k_fsolve(Geo g, FSolve f) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// TMEM-resident variant (bands up to Wf = 129): the score cells k < 128 of the
+// 128-row tile live in Tensor Memory (128 columns per CTA, row = TMEM lane,
+// three CTAs per SM use 384 of the 512 columns; the cell k = 128 of a w = 64
+// band stays in SMEM), so SMEM is free to hold the row-pass exponentials and
+// the column pass reuses them: ONE exp per cell per full step
+// (sum_i e_ij / r_i = sum_i 2^(s2 + u_t,i + v_{t-1},j)).
+// Warp w reads its TMEM lane quarter: row r = 32 (w & 3) + lane, and warps w,
+// w + 4 split the row's columns [0, 64) / [64, 128) (+ the SMEM cell).
+// ---------------------------------------------------------------------------
+constexpr int kTmCols = 128;
+constexpr int kTmGroups = 3;  // tiles (warp groups) per CTA: 3 x 128 TMEM columns
+
+struct TmGeo {
+    int P, P2;
+    // pitch 130 for every Wf <= 129: the row pass writes all 128 TMEM cells (+1), 8-byte aligned rows
+    __host__ __device__ TmGeo(int Wf, int Nw) : P(kTmCols + 2), P2(((Nw + 2 + 31) / 32) * 32 + 16) { (void)Wf; }
+    // e tile [128][P] | extra cells [128] | vw0 [P2] | vw1 [P2] | csum [2][Nw] | cmax [2][Nw]
+    __host__ __device__ size_t floats(int Nw) const { return (size_t)128 * P + 128 + 2 * (size_t)P2 + 4 * (size_t)Nw; }
+};
+
+__global__ void __launch_bounds__(kTmGroups * kThreads, 1) k_fsolve_tm(Geo g, FSolve f) {
+    extern __shared__ __align__(16) float smf[];
+    __shared__ __align__(8) float inv_r_all[kTmGroups][128];  // 1 / r_i (t >= 2) or lg2 r_i (cold start)
+    __shared__ float rpart_all[kTmGroups][2][128];            // per-half row sums / maxima
+    __shared__ uint32_t tmem_base;
+    // one CTA per SM, kTmGroups independent warp groups of 256 threads, one band tile each
+    const int grp = threadIdx.x / kThreads, tid = threadIdx.x % kThreads;
+    float* inv_r = inv_r_all[grp];
+    float(*rpart)[128] = rpart_all[grp];
+    auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(kThreads) : "memory"); };
+    const int Wf = g.Wf, Nw = f.Nw;
+    const TmGeo sg(Wf, Nw);
+    const int P = sg.P;
+    const int wq = (tid >> 5) & 3, hh = tid >> 7, lane = tid & 31;
+    const int r = 32 * wq + lane;
+    float* et = smf + (size_t)grp * sg.floats(Nw);  // [128][P]: s2 staging, then e (or x at the cold start)
+    float* extra = et + 128 * P;           // [128] cell k = 128 (Wf = 129)
+    float* vw0 = extra + 128;              // [P2] v_{t-1}(c)
+    float* vw1 = vw0 + sg.P2;              // [P2] v_{t-1}(c + 1)
+    float* csum = vw1 + sg.P2;             // [2][Nw]
+    float* cmax = csum + 2 * Nw;           // [2][Nw]
+    const int n = *f.nwork;
+    const int G = gridDim.x * kTmGroups;  // tile slots
+    const int slot = blockIdx.x * kTmGroups + grp;
+    const bool resident = n <= G;
+    const int TR = f.T + f.R;
+    const int kt = Wf < kTmCols ? Wf : kTmCols;  // cells held in TMEM
+    if (threadIdx.x < 32) {
+        sm100::tc_alloc(&tmem_base, 512);
+        sm100::tc_relinquish();
+    }
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t trow = tmem_base + ((uint32_t)(32 * wq) << 16) + (uint32_t)(kTmCols * grp);  // lane quarter
+    for (int x = tid; x < sg.P2; x += kThreads) {
+        if (x >= Nw) vw0[x] = -INFINITY;
+        if (x >= Nw - 1) vw1[x] = -INFINITY;
+    }
+    bool con[2] = {false, false}, act = false;
+    float ureg = 0.f;
+    for (int t = 1; t <= TR + 1; ++t) {
+        const bool fin = t == TR + 1;
+        for (int k = slot; k < n; k += G) {
+            const int blk = f.work[k];
+            const int bh = blk / f.NB, b = blk % f.NB, i0 = b * 128;
+            const bool need_load = !fin && (!resident || t == 1);
+            if (need_load) {  // stage the band tile in SMEM, then move cells k < 128 into TMEM
+                const float* src = f.S2 + ((size_t)bh * g.Lqp + i0) * Wf;
+                for (int e = tid; e < 128 * Wf; e += kThreads) {
+                    const int rr = e / Wf;
+                    et[rr * P + (e - rr * Wf)] = __ldcs(src + e);
+                }
+                gsync();
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int c0 = 64 * hh + 32 * q;
+                    float vv[32];
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) vv[x] = (c0 + x < kt) ? et[r * P + c0 + x] : -INFINITY;
+                    sm100::tc_st32(trow + (uint32_t)c0, vv);
+                }
+                if (hh == 0) extra[r] = (Wf > kTmCols) ? et[r * P + kTmCols] : -INFINITY;
+                sm100::tc_wait_st();
+            }
+            const int i = i0 + r;
+            if (!resident || t == 1) {
+                const uint8_t* rmask = g.row_mask ? g.row_mask + (size_t)(bh / g.H) * g.Lq : nullptr;
+                const uint8_t* cmask = g.col_mask ? g.col_mask + (size_t)(bh / g.H) * g.Lk : nullptr;
+                act = i < g.Lq && (rmask == nullptr || rmask[i] != 0);
+#pragma unroll
+                for (int a = 0; a < 2; ++a) {
+                    const int j = i0 - g.w + tid + kThreads * a;
+                    con[a] = tid + kThreads * a < Nw && j >= 0 && j < g.Lk && (cmask == nullptr || cmask[j] != 0);
+                }
+                if (!resident && t >= 2 && act) ureg = f.ubuf[(size_t)bh * g.Lrq + i];
+            }
+            // ---- combine: v_{t-1} on the window; owners publish their 128 columns
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+                const int c = tid + kThreads * a;
+                if (c >= Nw) break;
+                const int j = i0 - g.w + c;
+                const bool owner = c >= g.w && c < g.w + 128 && j < g.Lk;
+                if (fin && !owner) continue;
+                float v = -INFINITY;
+                if (t == 1) {
+                    if (con[a]) v = 0.f;
+                } else if (con[a]) {
+                    const float prev = (t < 3) ? 0.f : resident ? vw0[c] : f.vpriv[(size_t)k * Nw + c];
+                    v = combine(f, bh, b, c, t, prev);
+                    if (!isfinite(v)) {
+                        atomicOr(f.err, 32);
+                        v = 0.f;
+                    }
+                }
+                if (!fin) {
+                    vw0[c] = v;
+                    if (c >= 1) vw1[c - 1] = v;
+                }
+                if (!resident) f.vpriv[(size_t)k * Nw + c] = v;
+                if (t >= 2 && owner) {
+                    const float vo = (v == -INFINITY) ? 0.f : v;
+                    const int rv = t - 1 - f.T;
+                    if (rv >= 0 && rv <= 2 && f.v_slot[rv]) f.v_slot[rv][(size_t)bh * g.Lrk + j] = vo;
+                    if (fin) f.vbuf[(size_t)bh * g.Lrk + j] = vo;
+                }
+            }
+            if (fin) continue;
+            gsync();
+            // ---- row pass: half hh of row r -- TMEM cells [64 hh, 64 hh + 64) (+ the SMEM cell for hh = 1)
+            const float* vrow = ((r & 1) ? vw1 : vw0) + (r & ~1);  // vrow[k] = v(r + k), k even aligned
+            float* erow = et + r * P;
+            float o = 0.f;
+            // tcgen05.ld is warp-collective (.sync.aligned): every lane loads (one 32-column chunk
+            // at a time), inactive rows only mask the math
+            if (t == 1) {  // cold start: row max of s2 + v over both halves
+                float m = -INFINITY;
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    float sv[32];
+                    sm100::tc_ld32(trow + (uint32_t)(64 * hh + 32 * q), sv);
+                    sm100::tc_wait_ld();
+                    if (act) {
+#pragma unroll
+                        for (int x = 0; x < 32; ++x) m = fmaxf(m, sv[x] + vrow[64 * hh + 32 * q + x]);
+                    }
+                }
+                if (act && hh == 1) m = fmaxf(m, extra[r] + vrow[kTmCols]);
+                rpart[hh][r] = m;
+                gsync();
+                o = -fmaxf(rpart[0][r], rpart[1][r]);
+                gsync();
+            } else {
+                o = ureg;
+            }
+            float2 a0 = make_float2(0.f, 0.f), a1 = a0;
+            const float2 oo = make_float2(o, o);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int c0 = 64 * hh + 32 * q;
+                float sv[32];
+                sm100::tc_ld32(trow + (uint32_t)c0, sv);
+                sm100::tc_wait_ld();
+                if (act) {
+#pragma unroll
+                    for (int x = 0; x < 32; x += 4) {
+                        const float2 va = *reinterpret_cast<const float2*>(vrow + c0 + x);
+                        const float2 vb = *reinterpret_cast<const float2*>(vrow + c0 + x + 2);
+                        const float2 xa = fadd2(fadd2(make_float2(sv[x], sv[x + 1]), va), oo);
+                        const float2 xb = fadd2(fadd2(make_float2(sv[x + 2], sv[x + 3]), vb), oo);
+                        const float2 ea = ex2x2(xa), eb = ex2x2(xb);
+                        a0 = fadd2(a0, ea);
+                        a1 = fadd2(a1, eb);
+                        *reinterpret_cast<float2*>(erow + c0 + x) = (t == 1) ? xa : ea;
+                        *reinterpret_cast<float2*>(erow + c0 + x + 2) = (t == 1) ? xb : eb;
+                    }
+                } else {  // inactive row: contributes nothing to any column
+                    const float z = (t == 1) ? -INFINITY : 0.f;
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) erow[c0 + x] = z;
+                }
+            }
+            if (hh == 1) {
+                if (act && Wf > kTmCols) {
+                    const float x = extra[r] + vrow[kTmCols] + o;
+                    const float e = ex2(x);
+                    a0.x += e;
+                    erow[kTmCols] = (t == 1) ? x : e;
+                } else if (!act) {
+                    erow[kTmCols] = (t == 1) ? -INFINITY : 0.f;
+                }
+            }
+            rpart[hh][r] = (a0.x + a0.y) + (a1.x + a1.y);
+            gsync();
+            if (hh == 0) {
+                if (act) {
+                    const float rs = rpart[0][r] + rpart[1][r];
+                    const float lr = lg2(rs);
+                    float u = o - lr;
+                    if (!(rs > 0.f) || !isfinite(u)) {
+                        atomicOr(f.err, 64);
+                        u = 0.f;
+                    }
+                    inv_r[r] = (t == 1) ? lr : 1.f / rs;
+                    if (!resident || t == TR) f.ubuf[(size_t)bh * g.Lrq + i] = u;
+                    const int ru = t - f.T;
+                    if (ru >= 0 && ru <= 2 && f.u_slot[ru]) f.u_slot[ru][(size_t)bh * g.Lrq + i] = u;
+                    rpart[0][r] = u;  // hand the new dual to the other half
+                } else {
+                    inv_r[r] = (t == 1) ? INFINITY : 0.f;
+                }
+            }
+            gsync();
+            if (act) ureg = rpart[0][r];
+            // ---- column pass over the stored exponentials.  Thread t7 = tid & 127 owns the
+            // window columns {t7 + 128 m} (Wf cells for every t7); the thread pair hh splits
+            // that list at Wf/2, halves combined in a fixed order.  Cell (ii, c) at ii (P-1) + c.
+            {
+                const int t7 = tid & 127;
+                const int half = (Wf + 1) >> 1;
+                const int beg = hh ? half : 0, end = hh ? Wf : half;
+                const int step = P - 1;
+                int off = 0;
+                for (int c = t7; c < Nw; c += 128) {
+                    const int lo = max(0, c - 2 * g.w), hi = min(127, c);
+                    const int n_c = hi - lo + 1;
+                    const int x0 = max(beg, off), x1 = min(end, off + n_c);
+                    const int ilo = lo + (x0 - off), ihi = lo + (x1 - off) - 1;
+                    off += n_c;
+                    float ps = 0.f, pm = -INFINITY;
+                    if (ilo <= ihi) {
+                        const float* tp = et + ilo * step + c;
+                        if (t == 1) {
+                            for (int ii = ilo; ii <= ihi; ++ii) pm = fmaxf(pm, tp[(ii - ilo) * step] - inv_r[ii]);
+                            if (pm != -INFINITY)
+                                for (int ii = ilo; ii <= ihi; ++ii) ps += ex2(tp[(ii - ilo) * step] - inv_r[ii] - pm);
+                        } else {
+                            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+                            int ii = ilo;
+                            for (; ii + 3 <= ihi; ii += 4, tp += 4 * step) {
+                                s0 = fmaf(tp[0], inv_r[ii], s0);
+                                s1 = fmaf(tp[step], inv_r[ii + 1], s1);
+                                s2 = fmaf(tp[2 * step], inv_r[ii + 2], s2);
+                                s3 = fmaf(tp[3 * step], inv_r[ii + 3], s3);
+                            }
+                            for (; ii <= ihi; ++ii, tp += step) s0 = fmaf(tp[0], inv_r[ii], s0);
+                            ps = (s0 + s1) + (s2 + s3);
+                        }
+                    }
+                    csum[hh * Nw + c] = ps;
+                    if (t == 1) cmax[hh * Nw + c] = pm;
+                }
+            }
+            gsync();
+            {
+                u64* pout = f.part[t & 1] + ((size_t)bh * f.NB + b) * Nw;
+                for (int c = tid; c < Nw; c += kThreads) {
+                    const float s0 = csum[c], s1 = csum[Nw + c];
+                    if (t == 1) {
+                        const float m0 = cmax[c], m1 = cmax[Nw + c];
+                        const float M = fmaxf(m0, m1);
+                        float sum = 0.f;
+                        if (M != -INFINITY) {
+                            if (m0 != -INFINITY) sum += s0 * ex2(m0 - M);
+                            if (m1 != -INFINITY) sum += s1 * ex2(m1 - M);
+                        }
+                        st_tagged(f.partm + ((size_t)bh * f.NB + b) * Nw + c, M, 1u);
+                        st_tagged(pout + c, sum, 1u);
+                    } else {
+                        st_tagged(pout + c, s0 + s1, (unsigned)t);
+                    }
+                }
+            }
+            gsync();
+        }
+    }
+    sm100::tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) sm100::tc_dealloc(tmem_base, 512);
+}
+
 // blocks with any active row or any active column (their owner duties)
 __global__ void k_fs_flags(Geo g, int NB, int* __restrict__ flags) {
     const int bh = blockIdx.y, b = blockIdx.x;
@@ -347,9 +630,14 @@ __global__ void k_fs_flags(Geo g, int NB, int* __restrict__ flags) {
 
 }  // namespace
 
+static bool use_tmem(const Geo& g) {
+    const int Nw = 128 + 2 * g.w;
+    return g.Wf <= kTmCols + 1 && kTmGroups * TmGeo(g.Wf, Nw).floats(Nw) * 4 <= 220 * 1024 && !getenv("ST_NO_TMEM");
+}
+
 size_t fsolve_smem_bytes(const Geo& g) {
     const int Nw = 128 + 2 * g.w;
-    return FsGeo(g.Wf, Nw).floats(Nw) * 4;
+    return FsGeo(g.Wf, Nw).floats(Nw) * 4;  // the SMEM-only variant (eligibility check)
 }
 
 bool fsolve_supported(const Geo& g) {
@@ -358,16 +646,19 @@ bool fsolve_supported(const Geo& g) {
 
 cudaError_t launch_fsolve(const Geo& g, int T, int R, const FSolvePtrs& p, cudaStream_t s) {
     const int NB = (g.Lq + 127) / 128, Nw = 128 + 2 * g.w;
-    const size_t smem = fsolve_smem_bytes(g);
-    cudaError_t e = cudaFuncSetAttribute(k_fsolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const bool tm = use_tmem(g);
+    const size_t smem = tm ? kTmGroups * TmGeo(g.Wf, Nw).floats(Nw) * 4 : fsolve_smem_bytes(g);
+    auto kern = tm ? k_fsolve_tm : k_fsolve;
+    const int threads = tm ? kTmGroups * kThreads : kThreads;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0, dev = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fsolve, kThreads, smem);
-    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    const int G = std::min(per_sm * nsm, g.BH * NB);
+    const int G = tm ? std::min(per_sm * nsm, (g.BH * NB + kTmGroups - 1) / kTmGroups)
+                     : std::min(per_sm * nsm, g.BH * NB);
     // work list: active blocks in (head, block) order
     k_fs_flags<<<dim3(NB, g.BH), 128, 0, s>>>(g, NB, p.flags);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -406,7 +697,7 @@ cudaError_t launch_fsolve(const Geo& g, int T, int R, const FSolvePtrs& p, cudaS
     f.err = p.err;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(G);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -414,7 +705,18 @@ cudaError_t launch_fsolve(const Geo& g, int T, int R, const FSolvePtrs& p, cudaS
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, k_fsolve, g, f);
+    e = cudaLaunchKernelEx(&cfg, kern, g, f);
+    if (tm && e != cudaSuccess) {  // co-residency refused: the SMEM-only variant
+        cudaGetLastError();
+        const size_t smem2 = FsGeo(g.Wf, Nw).floats(Nw) * 4;
+        if ((e = cudaFuncSetAttribute(k_fsolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2)) != cudaSuccess)
+            return e;
+        int ps2 = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps2, k_fsolve, kThreads, smem2);
+        cfg.gridDim = dim3(std::min(std::max(ps2, 1) * nsm, g.BH * NB));
+        cfg.dynamicSmemBytes = smem2;
+        e = cudaLaunchKernelEx(&cfg, k_fsolve, g, f);
+    }
     add_launches(3);
     return e;
 }
