@@ -76,6 +76,7 @@ st::Geo make_geo(const st_desc* d, const Dims& m, const uint8_t* rm, const uint8
     g.Wf = (int)m.Wf;
     g.dustbin = d->dustbin;
     g.esz = d->dtype == ST_BF16 ? 2 : 4;
+    g.dbg = getenv("ST_BWD_DBG") ? atoi(getenv("ST_BWD_DBG")) : 0;
     g.eps = (float)d->epsilon;
     g.c2 = (float)(1.4426950408889634 / (std::sqrt((double)m.d) * d->epsilon));
     g.inv_qk = (float)(1.0 / (std::sqrt((double)m.d) * d->epsilon));

@@ -34,6 +34,7 @@ struct BT {
     const TIn *Q, *K, *V, *dO;
     float *dQ, *dK, *dV, *deps_part;
     float* O;  // transport output (RO)
+    int fuse_c5;  // C6 also produces v0b (the C5 sweep) -- no dustbin
 };
 
 enum { R1 = 0, R2 = 1, R4 = 2, R6 = 3, RO = 4, C1 = 10, C3 = 11, C5 = 12, C6 = 13 };
@@ -295,6 +296,7 @@ __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
         if (hh == 0 && i < Lo) {
             if (kOp == R6) a.deps_part[bo + i] = 0.f;
             if (kOp == C1) a.g_v[bo + i] = 0.f;
+            if (kOp == C6 && a.fuse_c5) a.v0b[bo + i] = 0.f;
             for (int x = 0; x < g.d; ++x) vo[(bo + i) * g.d + x] = 0.f;
         }
         return;
@@ -303,15 +305,21 @@ __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
     float* tS = smf;
     float* tZ = tS + 128 * Wf;
     float* wv = tZ + (kNeedZ ? 128 * Wf : 0);  // window vectors [5][Nw]
-    float* ops = wv + ((5 * Nw + 3) & ~3);     // operand rows [Nw][D + 4]
+    float* ops = wv + ((5 * Nw + 3) & ~3);     // operand rows [Nw][D] (window row c <-> x = i0 - w + c)
+    const TIn* osrc = (kOp == R6) ? a.K : (kOp == C1) ? a.dO : (kOp == RO) ? a.V : a.Q;
+    // f32 operands: the valid window rows are one contiguous run in global memory -> one bulk copy
+    const int xlo = max(0, i0 - g.w), xhi = min(Lx, i0 - g.w + Nw);
+    const int clo = xlo - (i0 - g.w), chi = clo + max(0, xhi - xlo);
+    const uint32_t obytes = (sizeof(TIn) == 4 && chi > clo) ? (uint32_t)(chi - clo) * D * 4u : 0u;
     if (tid == 0) {
         sm100::mbar_init(&bar, 1);
         sm100::fence_mbar_init();
         const uint32_t tb = 128u * (uint32_t)Wf * 4u;
-        sm100::mbar_arrive_expect_tx(&bar, kNeedZ ? 2 * tb : tb);
+        sm100::mbar_arrive_expect_tx(&bar, (kNeedZ ? 2 * tb : tb) + obytes);
         const size_t off = ((size_t)bh * Lpo + i0) * Wf;
         sm100::bulk_g2s(tS, (kRow ? a.S2 : a.S2T) + off, tb, &bar);
         if (kNeedZ) sm100::bulk_g2s(tZ, (kRow ? a.Z : a.ZT) + off, tb, &bar);
+        if (obytes) sm100::bulk_g2s(ops + clo * D, osrc + (bx + xlo) * D, obytes, &bar);
     }
     // window vectors (other side), c <-> x = i0 - w + c; 0 where invalid (tile carries -inf there)
     //   R6: v2, beta|v1, delta|v0, v2b(=g_v), v1b     C6: u2, alpha|u1, -, u2b, u1b
@@ -345,21 +353,19 @@ __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
         wv[3 * Nw + c] = w3;
         wv[4 * Nw + c] = w4;
     }
-    {
-        const TIn* src = (kOp == R6) ? a.K : (kOp == C1) ? a.dO : (kOp == RO) ? a.V : a.Q;
+    if constexpr (sizeof(TIn) == 4) {  // zero the rows outside the sequence (the bulk copy fills the rest)
+        for (int e = tid; e < clo * D; e += 256) ops[e] = 0.f;
+        for (int e = chi * D + tid; e < Nw * D; e += 256) ops[e] = 0.f;
+    } else {  // bf16 operands, converted to f32
         for (int e = tid; e < Nw * (D / 4); e += 256) {
             const int c = e / (D / 4), q = (e % (D / 4)) * 4;
             const int x = i0 - g.w + c;
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (x >= 0 && x < Lx) {
-                const TIn* sp = src + (bx + x) * D + q;
-                if constexpr (sizeof(TIn) == 4) {
-                    v = *reinterpret_cast<const float4*>(sp);
-                } else {
-                    v.x = ldf(sp); v.y = ldf(sp + 1); v.z = ldf(sp + 2); v.w = ldf(sp + 3);
-                }
+                const TIn* sp = osrc + (bx + x) * D + q;
+                v.x = ldf(sp); v.y = ldf(sp + 1); v.z = ldf(sp + 2); v.w = ldf(sp + 3);
             }
-            *reinterpret_cast<float4*>(ops + c * (D + 4) + q) = v;
+            *reinterpret_cast<float4*>(ops + c * D + q) = v;
         }
     }
     __syncthreads();
@@ -416,9 +422,11 @@ __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
                     if (kDirect) {
                         wgt = sbar_of(true, s2, p, z, wv[Nw + c], wv[c], o0, o1, o2, wv[3 * Nw + c], wv[4 * Nw + c],
                                       ob2, ob1);
+                        if (a.fuse_c5) acc += ex2(s2 + wv[Nw + c] + o0) * wv[4 * Nw + c];  // C5: P10 u1b
                     } else {  // alpha_i = wv[Nw + c], beta_j = ma, delta_j = mb
                         const float ai = wv[Nw + c];
                         wgt = p * (z - ob2 - ma * wv[3 * Nw + c] - ai * ma * ob1 - ai * mb * wv[4 * Nw + c]);
+                        acc += p * ai * wv[4 * Nw + c];  // C5: P22 alpha_i u1b_i (used when fuse_c5)
                     }
                 }
             }
@@ -455,8 +463,13 @@ __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
     if (hh == 0 && i < Lo) {
         if (kOp == C1) a.g_v[bo + i] = active ? sacc[0][r] + sacc[1][r] : 0.f;
         if (kOp == R6) a.deps_part[bo + i] = active ? sdacc[0][r] + sdacc[1][r] : 0.f;
+        if (kOp == C6 && a.fuse_c5) {  // v0b_j = -delta_j sum_i P22 alpha_i u1b_i  (direct: -sum P10 u1b)
+            const float s5 = sacc[0][r] + sacc[1][r];
+            a.v0b[bo + i] = !active ? 0.f : kDirect ? -s5 : -ex2(a.v0[bo + i] - a.v2[bo + i]) * s5;
+        }
     }
     // ---- phase 2: band GEMM.  thread = rows 4 rg .. 4 rg + 3, column chunks {4 cg + 32 m}
+    if (g.dbg & 1) return;  // timing studies only (ST_BWD_DBG)
     const int rg = tid >> 3, cg = tid & 7;
     float accv[4][CPT];
 #pragma unroll
@@ -471,7 +484,7 @@ __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
             const int k = kk - q;
             wq[q] = (k >= 0 && k < Wf) ? wrow[q * Wf + k] : 0.f;
         }
-        const float* xr = ops + (4 * rg + kk) * (D + 4) + 4 * cg;
+        const float* xr = ops + (4 * rg + kk) * D + 4 * cg;
 #pragma unroll
         for (int m = 0; m < CPT / 4; ++m) {
             const float4 x4 = *reinterpret_cast<const float4*>(xr + 32 * m);
@@ -651,7 +664,7 @@ __global__ void __launch_bounds__(256) k_bwdG(Geo g, BT<TIn> a) {
     __shared__ __align__(8) uint64_t bar;
     using GS_ = GemmShape<RB, D>;
     constexpr int TPR = 256 / RB, GS = 32 / TPR;
-    constexpr int OP = D + (sizeof(TIn) == 2 ? 8 : 4);  // operand row pitch (elements), 16-byte rows
+    constexpr int OP = D;  // operand row pitch (elements): contiguous window rows, one bulk copy
     constexpr bool kRow = kOp < 10;
     constexpr bool kNeedZ = (kOp == R6 || kOp == C1 || kOp == C6);
     const int Lo = kRow ? g.Lq : g.Lk, Lx = kRow ? g.Lk : g.Lq;
@@ -670,6 +683,7 @@ __global__ void __launch_bounds__(256) k_bwdG(Geo g, BT<TIn> a) {
         if (part == 0 && i < Lo) {
             if (kOp == R6) a.deps_part[bo + i] = 0.f;
             if (kOp == C1) a.g_v[bo + i] = 0.f;
+            if (kOp == C6 && a.fuse_c5) a.v0b[bo + i] = 0.f;
             for (int x = 0; x < D; ++x) vo[(bo + i) * D + x] = 0.f;
         }
         return;
@@ -679,14 +693,19 @@ __global__ void __launch_bounds__(256) k_bwdG(Geo g, BT<TIn> a) {
     float* tZ = tS + RB * Wf;
     float* wv = tZ + (kNeedZ ? RB * Wf : 0);
     TIn* ops = reinterpret_cast<TIn*>(wv + ((5 * Nw + 3) & ~3));
+    const TIn* osrc = (kOp == R6) ? a.K : (kOp == C1) ? a.dO : (kOp == RO) ? a.V : a.Q;
+    const int xlo = max(0, i0 - g.w), xhi = min(Lx, i0 - g.w + Nw);
+    const int clo = xlo - (i0 - g.w), chi = clo + max(0, xhi - xlo);
+    const uint32_t obytes = chi > clo ? (uint32_t)(chi - clo) * D * (uint32_t)sizeof(TIn) : 0u;
     if (tid == 0) {
         sm100::mbar_init(&bar, 1);
         sm100::fence_mbar_init();
         const uint32_t tb = (uint32_t)RB * (uint32_t)Wf * 4u;
-        sm100::mbar_arrive_expect_tx(&bar, kNeedZ ? 2 * tb : tb);
+        sm100::mbar_arrive_expect_tx(&bar, (kNeedZ ? 2 * tb : tb) + obytes);
         const size_t off = ((size_t)bh * Lpo + i0) * Wf;
         sm100::bulk_g2s(tS, (kRow ? a.S2 : a.S2T) + off, tb, &bar);
         if (kNeedZ) sm100::bulk_g2s(tZ, (kRow ? a.Z : a.ZT) + off, tb, &bar);
+        if (obytes) sm100::bulk_g2s(ops + clo * D, osrc + (bx + xlo) * D, obytes, &bar);
     }
     for (int c = tid; c < Nw; c += 256) {
         const int x = i0 - g.w + c;
@@ -717,16 +736,10 @@ __global__ void __launch_bounds__(256) k_bwdG(Geo g, BT<TIn> a) {
         wv[3 * Nw + c] = w3;
         wv[4 * Nw + c] = w4;
     }
-    {   // operand window rows, kept in the input dtype (16 bytes at a time)
-        const TIn* src = (kOp == R6) ? a.K : (kOp == C1) ? a.dO : (kOp == RO) ? a.V : a.Q;
-        constexpr int E = 16 / sizeof(TIn);
-        for (int e = tid; e < Nw * (D / E); e += 256) {
-            const int c = e / (D / E), q = (e % (D / E)) * E;
-            const int x = i0 - g.w + c;
-            uint4 v = make_uint4(0u, 0u, 0u, 0u);
-            if (x >= 0 && x < Lx) v = *reinterpret_cast<const uint4*>(src + (bx + x) * D + q);
-            *reinterpret_cast<uint4*>(ops + c * OP + q) = v;
-        }
+    {   // operand window rows (input dtype): the bulk copy brings the valid run, zero the rest
+        const TIn z{};
+        for (int e = tid; e < clo * D; e += 256) ops[e] = z;
+        for (int e = chi * D + tid; e < Nw * D; e += 256) ops[e] = z;
     }
     __syncthreads();
     sm100::mbar_wait(&bar, 0);
@@ -783,9 +796,11 @@ __global__ void __launch_bounds__(256) k_bwdG(Geo g, BT<TIn> a) {
                         if (kDirect) {
                             wgt = sbar_of(true, s2, p, z, wv[Nw + c], wv[c], o0, o1, o2, wv[3 * Nw + c],
                                           wv[4 * Nw + c], ob2, ob1);
+                            if (a.fuse_c5) acc += ex2(s2 + wv[Nw + c] + o0) * wv[4 * Nw + c];
                         } else {
                             const float ai = wv[Nw + c];
                             wgt = p * (z - ob2 - ma * wv[3 * Nw + c] - ai * ma * ob1 - ai * mb * wv[4 * Nw + c]);
+                            acc += p * ai * wv[4 * Nw + c];
                         }
                     }
                 }
@@ -804,6 +819,8 @@ __global__ void __launch_bounds__(256) k_bwdG(Geo g, BT<TIn> a) {
     if (part == 0 && i < Lo) {
         if (kOp == C1) a.g_v[bo + i] = active ? acc : 0.f;
         if (kOp == R6) a.deps_part[bo + i] = active ? dacc : 0.f;
+        if (kOp == C6 && a.fuse_c5)
+            a.v0b[bo + i] = !active ? 0.f : kDirect ? -acc : -ex2(a.v0[bo + i] - a.v2[bo + i]) * acc;
     }
     __syncthreads();
     // ---- phase 2: band GEMM, thread = RPT own rows x CPT columns (chunks of 4, stride 4 NCG)
@@ -877,7 +894,7 @@ __global__ void k_dust_dots(Geo g, const TIn* __restrict__ dO, const TIn* __rest
 size_t bwdT_smem_bytes(const Geo& g) {
     const int Nw = 128 + 2 * g.w;
     const int D = g.d <= 32 ? 32 : g.d <= 64 ? 64 : 128;
-    return (size_t)2 * 128 * g.Wf * 4 + (size_t)((5 * Nw + 3) & ~3) * 4 + (size_t)Nw * (D + 4) * 4 + 64;
+    return (size_t)2 * 128 * g.Wf * 4 + (size_t)((5 * Nw + 3) & ~3) * 4 + (size_t)Nw * D * 4 + 64;
 }
 
 // SMEM of one k_bwdT stage: S tile, Z tile (R1 / C1 / R6 / C6), window vectors, operand rows (vector stages)
@@ -893,8 +910,7 @@ static size_t wide_smem(const Geo& g, int op, int D, int esz, int RB) {
     const int Nw = RB + 2 * g.w;
     const bool vec = (op == R6 || op == C1 || op == C6 || op == RO);
     const bool z = vec ? (op != RO) : (op == R1);
-    const int OP = D + (esz == 2 ? 8 : 4);
-    return (size_t)(z ? 2 : 1) * RB * g.Wf * 4 + (size_t)((5 * Nw + 3) & ~3) * 4 + (vec ? (size_t)Nw * OP * esz : 0) + 64;
+    return (size_t)(z ? 2 : 1) * RB * g.Wf * 4 + (size_t)((5 * Nw + 3) & ~3) * 4 + (vec ? (size_t)Nw * D * esz : 0) + 64;
 }
 
 // rows per CTA for a stage: 128 (the k_bwdT / k_bwdV tiles or k_bwdG<128>), else 64 / 32; 0 = none fits
@@ -1014,6 +1030,7 @@ static cudaError_t run_all(const Geo& g, const BwdPtrs& p, const BwdTPtrs& t, in
     a.dK = p.dK;
     a.dV = p.dV;
     a.deps_part = p.deps_part;
+    a.fuse_c5 = 0;
     cudaError_t e;
 #define ST_RUN(op)                                                     \
     do {                                                               \
@@ -1035,8 +1052,11 @@ static cudaError_t run_all(const Geo& g, const BwdPtrs& p, const BwdTPtrs& t, in
     ST_DUST(2);
     ST_RUN(R4);
     ST_DUST(3);
-    ST_RUN(C5);
-    ST_DUST(4);
+    a.fuse_c5 = g.dustbin ? 0 : 1;  // the C5 sweep rides in C6 (same tiles and window vectors)
+    if (!a.fuse_c5) {
+        ST_RUN(C5);
+        ST_DUST(4);
+    }
     ST_RUN(R6);
     ST_RUN(C6);
     ST_DUST(5);

@@ -27,6 +27,7 @@ struct Geo {
     int d, w, Wf;    // head dim, half band, full band 2w+1
     int dustbin;     // 0 / 1
     int esz;         // input element bytes (4 f32, 2 bf16)
+    int dbg;         // timing studies only (ST_BWD_DBG)
     float sd2;       // base-2 dustbin score: -cost * log2(e) / eps
     float c2;        // log2(e) / (sqrt(d) * eps)
     float inv_qk;    // 1 / (sqrt(d) * eps)

@@ -114,6 +114,14 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {  // FADD2 (packed 
     return d;
 }
 __device__ __forceinline__ float2 ex2x2(float2 x) { return make_float2(ex2(x.x), ex2(x.y)); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {  // FFMA2 (packed fp32, sm_100)
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "mov.b64 rc, {%6, %7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
 
 // SMEM geometry: tile [128][P] (P = Wf + 1, even: 8-byte aligned rows, half-warp
 // LDS.64 conflict free), the window duals twice (shift 0 / 1, so every row reads
@@ -572,17 +580,22 @@ __global__ void __launch_bounds__(kTmGroups * kThreads, 1) k_fsolve_tm(Geo g, FS
                             for (int ii = ilo; ii <= ihi; ++ii) pm = fmaxf(pm, tp[(ii - ilo) * step] - inv_r[ii]);
                             if (pm != -INFINITY)
                                 for (int ii = ilo; ii <= ihi; ++ii) ps += ex2(tp[(ii - ilo) * step] - inv_r[ii] - pm);
-                        } else {
-                            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+                        } else {  // row pairs: FFMA2 with an aligned LDS.64 of inv_r
+                            float2 q0 = make_float2(0.f, 0.f), q1 = q0;
                             int ii = ilo;
-                            for (; ii + 3 <= ihi; ii += 4, tp += 4 * step) {
-                                s0 = fmaf(tp[0], inv_r[ii], s0);
-                                s1 = fmaf(tp[step], inv_r[ii + 1], s1);
-                                s2 = fmaf(tp[2 * step], inv_r[ii + 2], s2);
-                                s3 = fmaf(tp[3 * step], inv_r[ii + 3], s3);
+                            if (ii & 1) {
+                                q0.x = fmaf(tp[0], inv_r[ii], q0.x);
+                                ++ii;
+                                tp += step;
                             }
-                            for (; ii <= ihi; ++ii, tp += step) s0 = fmaf(tp[0], inv_r[ii], s0);
-                            ps = (s0 + s1) + (s2 + s3);
+                            for (; ii + 3 <= ihi; ii += 4, tp += 4 * step) {
+                                const float2 ia = *reinterpret_cast<const float2*>(inv_r + ii);
+                                const float2 ib = *reinterpret_cast<const float2*>(inv_r + ii + 2);
+                                q0 = ffma2(make_float2(tp[0], tp[step]), ia, q0);
+                                q1 = ffma2(make_float2(tp[2 * step], tp[3 * step]), ib, q1);
+                            }
+                            for (; ii <= ihi; ++ii, tp += step) q1.x = fmaf(tp[0], inv_r[ii], q1.x);
+                            ps = (q0.x + q0.y) + (q1.x + q1.y);
                         }
                     }
                     csum[hh * Nw + c] = ps;
@@ -609,7 +622,7 @@ __global__ void __launch_bounds__(kTmGroups * kThreads, 1) k_fsolve_tm(Geo g, FS
                     }
                 }
             }
-            gsync();
+            if (!resident) gsync();  // the next tile of this group restages the SMEM tile
         }
     }
     sm100::tc_fence_before();

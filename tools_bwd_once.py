@@ -1,0 +1,20 @@
+"""Dev helper: forward + backward of one config (for ncu launch timing)."""
+import sys
+import numpy as np, torch
+sys.path.insert(0, '.')
+from paper_2605_08123_b200 import band, configs
+cid = int(sys.argv[1])
+cfg = configs.CONFIGS[cid]
+inp = configs.make_inputs(cfg)
+spec = band.BandSpec(batch=cfg.B, heads=cfg.H, seq_q=cfg.L, seq_k=cfg.L, head_dim=cfg.d, half_band=cfg.w,
+                     base_depth=cfg.T, tail_depth=cfg.R, epsilon=cfg.eps, dtype=cfg.dtype, dustbin=cfg.dustbin)
+shp = (cfg.B, cfg.H, cfg.rows, cfg.d)
+b = inp.bits or {}
+dev = lambda x, k: (torch.from_numpy(b[k].astype(np.int16)).view(torch.bfloat16) if k in b else torch.from_numpy(x)).cuda().reshape(shp)
+Q, K, V, G = dev(inp.Q, 'Q'), dev(inp.K, 'K'), dev(inp.V, 'V'), dev(inp.G, 'G')
+rm = None if inp.row_mask is None else torch.from_numpy(inp.row_mask).cuda()
+for _ in range(2):
+    run = band.run_surrogate(Q, K, V, spec, rm, rm, validate=False)
+    band.r2_backward(run, G)
+torch.cuda.synchronize()
+print("done")
