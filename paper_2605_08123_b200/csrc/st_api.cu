@@ -538,10 +538,8 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
     } else {
         ST_CUDA(st::launch_output(g, desc->dtype, S2, u_prev, v_prev, V, O, st));
     }
-    if (sv) {
-        const int nslots = (int)std::min<long>(R, 2) + 1;
-        ST_CUDA(st::launch_gauges(g, su, nslots, (float*)(sv + sl.gauge), st));
-    }
+    // the gauge ledger (mean of the valid raw u, center() in sinkhorn.hpp:109-140) is only needed by
+    // st_saved_duals, which reads the saved duals to the host anyway and computes it there in f64
     band_record(workspace, Q, K, row_mask, col_mask, desc, dualT);
     return ST_OK;
 }
@@ -641,15 +639,23 @@ st_status st_saved_duals(const st_desc* desc, const void* saved, const uint8_t* 
     ST_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
     const float* hu = (const float*)(h.data() + sl.u);
     const float* hv = (const float*)(h.data() + sl.v);
-    const float* hg = (const float*)(h.data() + sl.gauge);
     const int status = *(const int*)(h.data() + sl.status);
     const double ln2 = 0.6931471805599453;
     const long H = desc->heads;
     for (int r = 0; r < 3; ++r)
         for (long bh = 0; bh < m.BH; ++bh) {
             const long b = bh / H;
-            const double C = desc->centered ? (double)hg[r * m.BH + bh] * ln2 : 0.0;
-            if (gauge) gauge[r * m.BH + bh] = (double)hg[r * m.BH + bh] * ln2;
+            // ledger gauge: mean of the raw u over the valid rows (the dustbin row counts as valid)
+            double su = 0.0;
+            long cnt = 0;
+            for (long i = 0; i < m.Lrq; ++i)
+                if (i >= m.Lq || !row_mask_host || row_mask_host[b * m.Lq + i]) {
+                    su += (double)hu[((size_t)r * m.BH + bh) * m.Lrq + i];
+                    ++cnt;
+                }
+            const double gr = cnt ? su / (double)cnt : 0.0;
+            const double C = desc->centered ? gr * ln2 : 0.0;
+            if (gauge) gauge[r * m.BH + bh] = gr * ln2;
             for (long i = 0; i < m.Lrq; ++i) {
                 const bool on = i >= m.Lq || !row_mask_host || row_mask_host[b * m.Lq + i];
                 const size_t k = ((size_t)r * m.BH + bh) * m.Lrq + i;

@@ -37,7 +37,8 @@ struct BT {
     int fuse_c5;  // C6 also produces v0b (the C5 sweep) -- no dustbin
 };
 
-enum { R1 = 0, R2 = 1, R4 = 2, R6 = 3, RO = 4, C1 = 10, C3 = 11, C5 = 12, C6 = 13 };
+enum { R1 = 0, R2 = 1, R4 = 2, R6 = 3, RO = 4, R12 = 5, C1 = 10, C3 = 11, C5 = 12, C6 = 13 };
+// R12 = R1 and R2 in one sweep (g_u_i = sum P22 Z, u2b_i = g_u_i - sum P22 g_v_j): needs C1 first
 
 __device__ __forceinline__ float sbar_of(bool direct, float s2, float p22, float z, float u1i, float u2i,
                                          float v0j, float v1j, float v2j, float u2bi, float u1bi, float v2bj,
@@ -59,7 +60,7 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
     extern __shared__ __align__(16) float smf[];
     __shared__ __align__(8) uint64_t bar;
     constexpr bool kRow = kOp < 10;
-    constexpr bool kNeedZ = (kOp == R1 || kOp == R6 || kOp == C1 || kOp == C6);
+    constexpr bool kNeedZ = (kOp == R1 || kOp == R12 || kOp == R6 || kOp == C1 || kOp == C6);
     constexpr bool kVec = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RO);
     // own = rows (row stages) or columns (column stages)
     const int Lo = kRow ? g.Lq : g.Lk, Lx = kRow ? g.Lk : g.Lq;
@@ -75,8 +76,8 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
 
     if (!__syncthreads_or(active)) {
         if (i < Lo) {
-            if (kOp == R1) a.g_u[bo + i] = 0.f;
-            if (kOp == R2) a.u2b[bo + i] = 0.f;
+            if (kOp == R1 || kOp == R12) a.g_u[bo + i] = 0.f;
+            if (kOp == R2 || kOp == R12) a.u2b[bo + i] = 0.f;
             if (kOp == R4) a.u1b[bo + i] = 0.f;
             if (kOp == R6) a.deps_part[bo + i] = 0.f;
             if (kOp == C1) a.g_v[bo + i] = 0.f;
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
                 w0 = a.v2[bx + x];
                 w1 = a.v1[bx + x];
                 w2 = a.v0[bx + x];
-                if (kOp == R2 || kOp == R6) w3 = a.g_v[bx + x];
+                if (kOp == R2 || kOp == R12 || kOp == R6) w3 = a.g_v[bx + x];
                 if (kOp == R4 || kOp == R6) w4 = a.v1b[bx + x];
             } else {  // rows: u2, u1, u2b, u1b
                 w0 = a.u2[bx + x];
@@ -141,8 +142,8 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
     sm100::mbar_wait(&bar, 0);
     if (i >= Lo) return;
     if (!active) {
-        if (kOp == R1) a.g_u[bo + i] = 0.f;
-        if (kOp == R2) a.u2b[bo + i] = 0.f;
+        if (kOp == R1 || kOp == R12) a.g_u[bo + i] = 0.f;
+        if (kOp == R2 || kOp == R12) a.u2b[bo + i] = 0.f;
         if (kOp == R4) a.u1b[bo + i] = 0.f;
         if (kOp == R6) a.deps_part[bo + i] = 0.f;
         if (kOp == C1) a.g_v[bo + i] = 0.f;
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
     }
     const float* ts = tS + r * Wf;
     const float* tz = tZ + r * Wf;
-    float acc = 0.f, dacc = 0.f;
+    float acc = 0.f, dacc = 0.f, acc2 = 0.f;
     float vacc[kVec ? D : 1];
 #pragma unroll
     for (int e = 0; e < (kVec ? D : 1); ++e) vacc[e] = 0.f;
@@ -187,6 +188,9 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
         if (kOp == R1 || kOp == C1) {
             acc += p * tz[k];
             wgt = p;
+        } else if (kOp == R12) {
+            acc += p * tz[k];
+            acc2 += p * wv[3 * Nw + c];
         } else if (kOp == RO) {
             wgt = p;
         } else if (kOp == R2) {
@@ -227,6 +231,9 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
         if (kOp == RO) {  // O_i += p * V_dustbin
 #pragma unroll
             for (int e = 0; e < (kVec ? D : 1); ++e) vacc[e] = fmaf(p, ldf(a.V + (bx + xd) * g.d + e), vacc[e]);
+        } else if (kOp == R12) {
+            acc += p * z;
+            acc2 += p * a.g_v[bx + xd];
         } else if (kOp == R1 || kOp == C1) {
             acc += p * z;
             if (kOp == C1) {  // dV_j += p * dO_dustbin
@@ -249,6 +256,10 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
         // C6: no dK contribution from constant-cost cells
     }
     if (kOp == R1) a.g_u[bo + i] = acc;
+    if (kOp == R12) {
+        a.g_u[bo + i] = acc;
+        a.u2b[bo + i] = acc - acc2;
+    }
     if (kOp == C1) a.g_v[bo + i] = acc;
     if (kOp == R2) a.u2b[bo + i] = a.g_u[bo + i] - acc;
     if (kOp == R4) a.u1b[bo + i] = kDirect ? -acc : -ex2(o1 - o2) * acc;
@@ -534,7 +545,7 @@ __global__ void __launch_bounds__(128) k_bwdS(Geo g, BT<TIn> a) {
     __shared__ __align__(8) uint64_t bar;
     constexpr int TPR = 128 / RB, GS = 32 / TPR;
     constexpr bool kRow = kOp < 10;
-    constexpr bool kNeedZ = (kOp == R1);
+    constexpr bool kNeedZ = (kOp == R1 || kOp == R12);
     const int Lo = kRow ? g.Lq : g.Lk, Lx = kRow ? g.Lk : g.Lq;
     const int Lro = kRow ? g.Lrq : g.Lrk, Lrx = kRow ? g.Lrk : g.Lrq;
     const int Lpo = kRow ? g.Lqp : g.Lkp;
@@ -547,7 +558,7 @@ __global__ void __launch_bounds__(128) k_bwdS(Geo g, BT<TIn> a) {
     auto on_x = [&](int k) { return k >= 0 && k < Lx && (mx == nullptr || mx[(size_t)(bh / g.H) * Lx + k] != 0); };
     const bool active = on_o(i);
     auto put = [&](float val) {
-        if (kOp == R1) a.g_u[bo + i] = val;
+        if (kOp == R1 || kOp == R12) a.g_u[bo + i] = val;
         if (kOp == R2) a.u2b[bo + i] = val;
         if (kOp == R4) a.u1b[bo + i] = val;
         if (kOp == C3) a.v1b[bo + i] = val;
@@ -577,7 +588,7 @@ __global__ void __launch_bounds__(128) k_bwdS(Geo g, BT<TIn> a) {
             if (kRow) {
                 w0 = a.v2[bx + x];
                 w1 = a.v1[bx + x];
-                if (kOp == R2) w3 = a.g_v[bx + x];
+                if (kOp == R2 || kOp == R12) w3 = a.g_v[bx + x];
                 if (kOp == R4) w4 = a.v1b[bx + x];
             } else {
                 w0 = a.u2[bx + x];
@@ -599,7 +610,7 @@ __global__ void __launch_bounds__(128) k_bwdS(Geo g, BT<TIn> a) {
         o1 = kRow ? a.u1[bo + i] : a.v1[bo + i];
         if (!kRow) o0 = a.v0[bo + i];
     }
-    float acc = 0.f;
+    float acc = 0.f, acc2 = 0.f;
     if (active) {
         const float* ts = tS + r * Wf;
         const float* tz = tZ + r * Wf;
@@ -614,7 +625,10 @@ __global__ void __launch_bounds__(128) k_bwdS(Geo g, BT<TIn> a) {
                 const float x2 = wv[c], x1 = wv[Nw + c];
                 const float p = ex2(s2 + o2 + x2);
                 if (kOp == R1) acc += p * tz[k];
-                else if (kOp == R2) acc += p * wv[3 * Nw + c];
+                else if (kOp == R12) {
+                    acc += p * tz[k];
+                    acc2 += p * wv[3 * Nw + c];
+                } else if (kOp == R2) acc += p * wv[3 * Nw + c];
                 else if (kOp == R4) acc += kDirect ? ex2(s2 + o1 + x1) * wv[4 * Nw + c] : p * ex2(x1 - x2) * wv[4 * Nw + c];
                 else if (kOp == C3) acc += (kDirect ? ex2(s2 + x2 + o1) : p) * wv[3 * Nw + c];
                 else acc += kDirect ? ex2(s2 + x1 + o0) * wv[4 * Nw + c] : p * ex2(x1 - x2) * wv[4 * Nw + c];
@@ -622,11 +636,15 @@ __global__ void __launch_bounds__(128) k_bwdS(Geo g, BT<TIn> a) {
         }
     }
 #pragma unroll
-    for (int off = GS; off < 32; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    for (int off = GS; off < 32; off <<= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (kOp == R12) acc2 += __shfl_xor_sync(0xffffffffu, acc2, off);
+    }
+    if (kOp == R12 && part == 0 && i < Lo) a.u2b[bo + i] = active ? acc - acc2 : 0.f;
     if (part == 0 && i < Lo) {
         float val = 0.f;
         if (active) {
-            if (kOp == R1) val = acc;
+            if (kOp == R1 || kOp == R12) val = acc;
             if (kOp == R2) val = a.g_u[bo + i] - acc;
             if (kOp == R4) val = kDirect ? -acc : -ex2(o1 - o2) * acc;
             if (kOp == C3) val = kDirect ? -acc : -ex2(o1 - o2) * acc;
@@ -900,7 +918,7 @@ size_t bwdT_smem_bytes(const Geo& g) {
 // SMEM of one k_bwdT stage: S tile, Z tile (R1 / C1 / R6 / C6), window vectors, operand rows (vector stages)
 static size_t bwdT_op_smem(const Geo& g, int op, int D) {
     const int Nw = 128 + 2 * g.w;
-    const bool z = (op == R1 || op == R6 || op == C1 || op == C6);
+    const bool z = (op == R1 || op == R12 || op == R6 || op == C1 || op == C6);
     const bool vec = (op == R6 || op == C1 || op == C6 || op == RO);
     return (size_t)(z ? 2 : 1) * 128 * g.Wf * 4 + (size_t)((5 * Nw + 3) & ~3) * 4 + (vec ? (size_t)Nw * (D + 4) * 4 : 0) + 64;
 }
@@ -909,7 +927,7 @@ static size_t bwdT_op_smem(const Geo& g, int op, int D) {
 static size_t wide_smem(const Geo& g, int op, int D, int esz, int RB) {
     const int Nw = RB + 2 * g.w;
     const bool vec = (op == R6 || op == C1 || op == C6 || op == RO);
-    const bool z = vec ? (op != RO) : (op == R1);
+    const bool z = vec ? (op != RO) : (op == R1 || op == R12);
     return (size_t)(z ? 2 : 1) * RB * g.Wf * 4 + (size_t)((5 * Nw + 3) & ~3) * 4 + (vec ? (size_t)Nw * D * esz : 0) + 64;
 }
 
@@ -931,7 +949,7 @@ bool bwdT_supported(const Geo& g) {
     if (!(g.d == 32 || g.d == 64 || g.d == 128)) return false;
     const int esz = g.esz ? g.esz : 4;
     const bool narrow = g.d <= 64 && bwdT_smem_bytes(g) <= 227 * 1024;  // k_bwdV path for the vector stages
-    for (int op : {R1, R2, R4, C3, C5})
+    for (int op : {R12, R4, C3, C5})
         if (!pick_rb(g, op, g.d, esz)) return false;
     if (!narrow)
         for (int op : {R6, C6, C1, RO})
@@ -1043,11 +1061,16 @@ static cudaError_t run_all(const Geo& g, const BwdPtrs& p, const BwdTPtrs& t, in
             if ((e = launch_backward_dustbin_stage(g, dtype, p, kDirect, stage, s)) != cudaSuccess) return e; \
         }                                                                                        \
     } while (0)
-    ST_RUN(R1);
-    ST_RUN(C1);
-    ST_DUST(0);
-    ST_RUN(R2);
-    ST_DUST(1);
+    if (g.dustbin) {  // the dustbin row/column stages interleave with R1 / R2
+        ST_RUN(R1);
+        ST_RUN(C1);
+        ST_DUST(0);
+        ST_RUN(R2);
+        ST_DUST(1);
+    } else {  // C1 first, then R1 + R2 in one sweep
+        ST_RUN(C1);
+        ST_RUN(R12);
+    }
     ST_RUN(C3);
     ST_DUST(2);
     ST_RUN(R4);

@@ -220,6 +220,20 @@ __global__ void __launch_bounds__(256) k_band_mma(Geo g, const TIn* __restrict__
             }
         }
     }
+    // transposed-band cells whose row i falls outside [0, Lqp) (no row block produces them):
+    // the head's edge cells are split evenly over its row-block CTAs
+    if (outT != nullptr) {
+        const float fill = kZ ? 0.f : -INFINITY;
+        const int ne = min(g.w, g.Lkp), tot = 2 * ne * g.Wf;
+        const int per = (tot + gridDim.x - 1) / gridDim.x;
+        const int e0 = blockIdx.x * per, e1 = min(tot, e0 + per);
+        for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+            const int rr = e / g.Wf, kp = e % g.Wf;
+            const int j = rr < ne ? rr : g.Lkp - 2 * ne + rr;
+            const int i = j - g.w + kp;
+            if (i < 0 || i >= g.Lqp) outT[((size_t)bh * g.Lkp + j) * g.Wf + kp] = fill;
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1077,12 +1091,7 @@ cudaError_t launch_band_dual(const Geo& g, int dtype, bool z, const void* A, con
     const bool ok = z ? band_mma<true>(g, dtype, A, B, out, outT, s, e) : band_mma<false>(g, dtype, A, B, out, outT, s, e);
     if (!ok) return cudaErrorNotSupported;
     if (e != cudaSuccess) return e;
-    const int ne = std::min(g.w, g.Lkp);
-    if (ne > 0) {
-        k_fillT_edges<<<dim3((2 * ne * g.Wf + 255) / 256, g.BH), 256, 0, s>>>(g, outT, z ? 0.f : -INFINITY);
-        ++g_launches;
-    }
-    return cudaGetLastError();
+    return cudaGetLastError();  // edge cells of the transposed band: filled by k_band_mma's end blocks
 }
 
 cudaError_t launch_zband(const Geo& g, int dtype, const void* dO, const void* V, float* Z, cudaStream_t s) {
