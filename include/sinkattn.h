@@ -73,7 +73,17 @@ typedef struct st_desc {
     int32_t centered;     /* 1 = reference default: report the centered gauge ledger in saved */
     int32_t flags;        /* 0 = auto; ST_FLAG_GENERIC forces the generic (non-tensor-core) kernels,
                              ST_FLAG_REUSE_BAND (backward) reuses the forward's score band */
+    /* epsilon-continuation schedule of the base solve (EpsSchedule, trace.hpp:12-50): stage q runs
+     * stage_iters[q] full steps at temperature stage_eps[q]; temperatures non-increasing, iterations
+     * summing to base_depth, the last stage at `epsilon` (the tail temperature, as
+     * EpsSchedule::final_epsilon).  n_stages = 0: one stage of base_depth steps at `epsilon`.
+     * Host pointers, read during the call only; at most ST_MAX_STAGES stages. */
+    int32_t n_stages;
+    const double* stage_eps;
+    const int64_t* stage_iters;
 } st_desc;
+
+#define ST_MAX_STAGES 8
 
 #define ST_FLAG_GENERIC 1
 /* st_backward only: reuse the score band the most recent st_forward left in the

@@ -43,6 +43,10 @@ struct BatchArgs {
     const std::uint8_t *row_mask, *col_mask;
     int precision, mode, tile_block, centered;
     double *O, *dQ, *dK, *dV, *d_eps, *eta_v, *duals, *gauges;
+    // EpsSchedule stages (trace.hpp:12-50); n_stages == 0 -> one stage at eps
+    int n_stages = 0;
+    const double* stage_eps = nullptr;
+    const std::int64_t* stage_iters = nullptr;
 };
 
 template <class T>
@@ -81,6 +85,11 @@ void run_head(const BatchArgs& a, std::int64_t bh) {
     }
     auto sched = TileSchedule::build(sup, a.tile_block);
     EpsSchedule<T> es = EpsSchedule<T>::single(static_cast<T>(a.eps), a.T);
+    if (a.n_stages > 0) {
+        es.stages.clear();
+        for (int q = 0; q < a.n_stages; ++q) es.stages.push_back({static_cast<T>(a.stage_eps[q]), a.stage_iters[q]});
+        es.validate(a.T);
+    }
     SurrogateRun<T> run = run_surrogate<T>(Q, K, V, sched, a.T, a.R, es, a.centered != 0, pc);
     for (size_t k = 0; k < run.output.a.size(); ++k) a.O[off + k] = static_cast<double>(run.output.a[k]);
     if (a.duals) {
@@ -135,15 +144,19 @@ std::int64_t stoc_banded_entry_count(std::int64_t L, std::int64_t w) { return st
 
 // Batched reference path.  Tensors are [B, H, Lr, d] doubles (Lr = L + dustbin),
 // masks [B, L] uint8 or NULL.  dQ == NULL runs the forward only.
-int stoc_run_batch(std::int64_t B, std::int64_t H, std::int64_t L, std::int64_t d, std::int64_t half_band,
-                   std::int64_t T, std::int64_t R, double eps, int dustbin, double dustbin_cost, const double* Q,
-                   const double* K, const double* V, const double* G, const std::uint8_t* row_mask,
-                   const std::uint8_t* col_mask, int precision, int mode, int tile_block, int centered,
-                   int nthreads, std::int64_t head_begin, std::int64_t head_end, double* O, double* dQ, double* dK,
-                   double* dV, double* d_eps, double* eta_v, double* duals, double* gauges) {
+int stoc_run_batch_sched(std::int64_t B, std::int64_t H, std::int64_t L, std::int64_t d, std::int64_t half_band,
+                         std::int64_t T, std::int64_t R, double eps, int dustbin, double dustbin_cost,
+                         const double* Q, const double* K, const double* V, const double* G,
+                         const std::uint8_t* row_mask, const std::uint8_t* col_mask, int precision, int mode,
+                         int tile_block, int centered, int nthreads, std::int64_t head_begin, std::int64_t head_end,
+                         double* O, double* dQ, double* dK, double* dV, double* d_eps, double* eta_v, double* duals,
+                         double* gauges, int n_stages, const double* stage_eps, const std::int64_t* stage_iters) {
     BatchArgs a{B,      H,        L,    d,       half_band, T,          R,        eps,  dustbin, dustbin_cost,
                 Q,      K,        V,    G,       row_mask,  col_mask,   precision, mode, tile_block, centered,
                 O,      dQ,       dK,   dV,      d_eps,     eta_v,      duals,    gauges};
+    a.n_stages = n_stages;
+    a.stage_eps = stage_eps;
+    a.stage_iters = stage_iters;
     if (head_end < 0 || head_end > B * H) head_end = B * H;
     if (head_begin < 0) head_begin = 0;
     if (nthreads < 1) nthreads = 1;
@@ -176,6 +189,17 @@ int stoc_run_batch(std::int64_t B, std::int64_t H, std::int64_t L, std::int64_t 
     for (auto& th : pool) th.join();
     if (status.load() != STOC_OK) g_err = first_err;
     return status.load();
+}
+
+int stoc_run_batch(std::int64_t B, std::int64_t H, std::int64_t L, std::int64_t d, std::int64_t half_band,
+                   std::int64_t T, std::int64_t R, double eps, int dustbin, double dustbin_cost, const double* Q,
+                   const double* K, const double* V, const double* G, const std::uint8_t* row_mask,
+                   const std::uint8_t* col_mask, int precision, int mode, int tile_block, int centered,
+                   int nthreads, std::int64_t head_begin, std::int64_t head_end, double* O, double* dQ, double* dK,
+                   double* dV, double* d_eps, double* eta_v, double* duals, double* gauges) {
+    return stoc_run_batch_sched(B, H, L, d, half_band, T, R, eps, dustbin, dustbin_cost, Q, K, V, G, row_mask,
+                                col_mask, precision, mode, tile_block, centered, nthreads, head_begin, head_end, O, dQ,
+                                dK, dV, d_eps, eta_v, duals, gauges, 0, nullptr, nullptr);
 }
 
 }  // extern "C"

@@ -28,6 +28,7 @@ ST_F32 = 0
 ST_BF16 = 1
 ST_FLAG_GENERIC = 1
 ST_FLAG_REUSE_BAND = 2
+ST_MAX_STAGES = 8
 ST_ONE_REFERENCE = 0
 ST_DIRECT_FOUR_PLAN = 1
 
@@ -45,6 +46,8 @@ class StDesc(ctypes.Structure):
         ("base_depth", ctypes.c_int64), ("tail_depth", ctypes.c_int64), ("epsilon", ctypes.c_double),
         ("dtype", ctypes.c_int32), ("dustbin", ctypes.c_int32), ("dustbin_cost", ctypes.c_double),
         ("centered", ctypes.c_int32), ("flags", ctypes.c_int32),
+        ("n_stages", ctypes.c_int32), ("stage_eps", ctypes.POINTER(ctypes.c_double)),
+        ("stage_iters", ctypes.POINTER(ctypes.c_int64)),
     ]
 
 

@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import dataclasses
-from typing import Optional
+from typing import Optional, Sequence, Tuple
 
 import numpy as np
 import torch
@@ -90,13 +90,24 @@ class BandSpec:
     dustbin_cost: float = 1.0
     centered: bool = True
     generic: bool = False       # force the generic (non-tensor-core) kernels (testing / ablation)
+    # EpsSchedule of the base solve (trace.hpp:12-50): ((epsilon, iterations), ...), non-increasing
+    # temperatures, iterations summing to base_depth, the last stage at `epsilon`.  None: one stage.
+    eps_schedule: Optional[Sequence[Tuple[float, int]]] = None
 
     def desc(self) -> _lib.StDesc:
-        return _lib.StDesc(self.batch, self.heads, self.seq_q, self.seq_k, self.head_dim, self.half_band,
-                           self.base_depth, self.tail_depth, float(self.epsilon),
-                           _lib.ST_BF16 if self.dtype == "bf16" else _lib.ST_F32, int(self.dustbin),
-                           float(self.dustbin_cost), int(bool(self.centered)),
-                           _lib.ST_FLAG_GENERIC if self.generic else 0)
+        d = _lib.StDesc(self.batch, self.heads, self.seq_q, self.seq_k, self.head_dim, self.half_band,
+                        self.base_depth, self.tail_depth, float(self.epsilon),
+                        _lib.ST_BF16 if self.dtype == "bf16" else _lib.ST_F32, int(self.dustbin),
+                        float(self.dustbin_cost), int(bool(self.centered)),
+                        _lib.ST_FLAG_GENERIC if self.generic else 0)
+        if self.eps_schedule:
+            n = len(self.eps_schedule)
+            d._eps = (ctypes.c_double * n)(*[float(e) for e, _ in self.eps_schedule])  # kept alive by d
+            d._its = (ctypes.c_int64 * n)(*[int(k) for _, k in self.eps_schedule])
+            d.n_stages = n
+            d.stage_eps = ctypes.cast(d._eps, ctypes.POINTER(ctypes.c_double))
+            d.stage_iters = ctypes.cast(d._its, ctypes.POINTER(ctypes.c_int64))
+        return d
 
     @property
     def rows(self) -> int:

@@ -45,6 +45,22 @@ st_status check_desc(const st_desc* d, Dims& o) {
     if (d->base_depth < 0 || d->tail_depth < 0) return fail(ST_INVALID_ARGUMENT, "depths must be >= 0");
     if (d->dtype != ST_F32 && d->dtype != ST_BF16) return fail(ST_INVALID_ARGUMENT, "dtype must be ST_F32 or ST_BF16");
     if (d->dustbin != 0 && d->dustbin != 1) return fail(ST_INVALID_ARGUMENT, "dustbin must be 0 or 1");
+    if (d->n_stages < 0 || d->n_stages > ST_MAX_STAGES) return fail(ST_NOT_SUPPORTED, "at most ST_MAX_STAGES epsilon stages");
+    if (d->n_stages > 0) {  // EpsSchedule::validate (trace.hpp:37-49)
+        if (!d->stage_eps || !d->stage_iters) return fail(ST_INVALID_ARGUMENT, "null epsilon schedule");
+        int64_t tot = 0;
+        for (int q = 0; q < d->n_stages; ++q) {
+            if (!(d->stage_eps[q] > 0.0) || !std::isfinite(d->stage_eps[q]))
+                return fail(ST_INVALID_TEMPERATURE, "stage epsilon must be > 0");
+            if (q > 0 && d->stage_eps[q] > d->stage_eps[q - 1])
+                return fail(ST_INVALID_TEMPERATURE, "stage epsilons must be non-increasing");
+            if (d->stage_iters[q] < 0) return fail(ST_INVALID_ARGUMENT, "stage iterations must be >= 0");
+            tot += d->stage_iters[q];
+        }
+        if (tot != d->base_depth) return fail(ST_INVALID_ARGUMENT, "epsilon schedule iterations do not sum to T");
+        if (d->stage_eps[d->n_stages - 1] != d->epsilon)
+            return fail(ST_INVALID_ARGUMENT, "the last stage epsilon must equal desc->epsilon (final temperature)");
+    }
     if (d->head_dim > 128) return fail(ST_NOT_SUPPORTED, "head_dim > 128 is not implemented");
     o.BH = d->batch * d->heads;
     o.Lq = d->seq_q;
@@ -270,6 +286,19 @@ size_t st_workspace_bytes(const st_desc* desc) {
     return ws_layout(m, tc_plan(desc, m)).bytes;
 }
 
+// Score scale of full step t (1-based) relative to the final temperature: the band is stored at
+// desc->epsilon, a base step of stage q runs at stage_eps[q] (scale_to_temperature per stage,
+// sinkhorn.hpp:186-195), the tail at the final temperature.
+float step_scale(const st_desc* d, long t) {
+    if (d->n_stages <= 0 || t > d->base_depth) return 1.f;
+    long end = 0;
+    for (int q = 0; q < d->n_stages; ++q) {
+        end += d->stage_iters[q];
+        if (t <= end) return (float)(d->epsilon / d->stage_eps[q]);
+    }
+    return 1.f;
+}
+
 // Which forward last wrote the score band of a workspace (ST_FLAG_REUSE_BAND).
 namespace {
 struct BandKey {
@@ -392,39 +421,17 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
         dr.L_own = g.Lq; dr.L_other = g.Lk; dr.Lr_own = g.Lrq; dr.Lr_other = g.Lrk; dr.mask_other = col_mask;
         dc.L_own = g.Lk; dc.L_other = g.Lq; dc.Lr_own = g.Lrk; dc.Lr_other = g.Lrq; dc.mask_other = row_mask;
         const int grid = std::min(num_sms(), (int)(m.BH * std::max(tp.NBq, tp.NBk)));
-        // ST_TRACE_PHASE=t: dump the device timeline of the row phase of step t (debug only)
-        static const long trace_step = getenv("ST_TRACE_PHASE") ? atol(getenv("ST_TRACE_PHASE")) : -1;
-        unsigned long long* trace = nullptr;
-        if (trace_step >= 1) {
-            cudaMalloc(&trace, 16 * 64 * sizeof(unsigned long long));
-            cudaMemsetAsync(trace, 0, 16 * 64 * sizeof(unsigned long long), st);
-        }
         for (long t = 1; t <= T + R; ++t) {
             const long r = t - T;
             float* u_out = (sv && r >= 0 && r <= 2) ? slot_u(r) : u_ws;
             float* v_out = (sv && r >= 0 && r <= 2) ? slot_v(r) : v_ws;
+            // epsilon stage of this step: the scores are recomputed here, so only their scale changes
+            const float lam = step_scale(desc, t);
+            pr.c2 = pc.c2 = g.c2 * lam;
+            pr.sd2 = pc.sd2 = dr.sd2 = dc.sd2 = g.sd2 * lam;
             pr.dual_other = v_prev; pr.off_own = u_prev; pr.out_own = u_out;
-            pr.trace = (t == trace_step) ? trace : nullptr;
+            pr.trace = nullptr;
             ST_CUDA(st::launch_phase(pr, t == 1, grid, st));
-            if (t == trace_step) {
-                unsigned long long h[16 * 64];
-                cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st);
-                cudaStreamSynchronize(st);
-                for (int c = 0; c < 16; ++c) {
-                    const unsigned long long t0 = h[c * 64];
-                    fprintf(stderr, "cta %2d nblk %llu:", c, h[c * 64 + 42]);
-                    auto pr_ = [&](const char* nm, int base, int n) {
-                        fprintf(stderr, " %s", nm);
-                        for (int k = 0; k < n; ++k)
-                            if (h[c * 64 + base + k]) fprintf(stderr, " %.2f", (h[c * 64 + base + k] - t0) * 1e-3);
-                    };
-                    pr_("prodA", 1, 8); pr_("| mmaA", 9, 8); pr_("| mmaEnd", 17, 8); pr_("| epiS", 25, 8);
-                    pr_("| epiE", 33, 8); pr_("| end", 41, 1); pr_("\n      kfull/tempty b0", 43, 10); pr_("b1", 53, 10);
-                    fprintf(stderr, "\n");
-                }
-                cudaFree(trace);
-                trace = nullptr;
-            }
             if (g.dustbin) {
                 dr.dual_other = v_prev; dr.off_own = u_prev; dr.out_own = u_out;
                 ST_CUDA(st::launch_dustbin(dr, t == 1, g.BH, st));
@@ -461,11 +468,21 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
             p.work = (int*)(ws + wl.fs_work);
             p.count = (int*)(ws + wl.fs_cnt);
             p.err = err;
+            p.nst = 0;
+            for (long t = 1; t <= T; ++t) {  // per-stage score scale (run-length over the base steps)
+                const float lam = step_scale(desc, t);
+                if (p.nst == 0 || p.st_scale[p.nst - 1] != lam) {
+                    if (p.nst == ST_MAX_STAGES) return fail(ST_NOT_SUPPORTED, "too many epsilon stages");
+                    p.st_scale[p.nst++] = lam;
+                }
+                p.st_end[p.nst - 1] = (int)t;
+            }
             ST_CUDA(st::launch_fsolve(g, (int)T, (int)R, p, st));
             u_prev = u_ws;
             v_prev = v_ws;
         } else if (fused_ok(desc, m) && T + R >= 1) {
             // one launch per full step; the column half-step rides on the row exponentials
+            float band_lam = 1.f;  // temperature scale of the stored band
             float* vbuf[2] = {v_ws, (float*)(ws + wl.vb2)};
             float* part[2] = {(float*)(ws + wl.part[0]), (float*)(ws + wl.part[1])};
             float* partm = (float*)(ws + wl.partm);
@@ -474,6 +491,13 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
             p.err = err;
             for (long t = 1; t <= T + R; ++t) {
                 const long r = t - T;
+                const float lam = step_scale(desc, t);
+                if (lam != band_lam) {  // epsilon stage change: scores at this stage's temperature
+                    st::Geo gs = g;
+                    gs.c2 = g.c2 * lam;
+                    ST_CUDA(st::launch_scores(gs, desc->dtype, Q, K, S2, st));
+                    band_lam = lam;
+                }
                 float* u_out = (sv && r >= 0 && r <= 2) ? slot_u(r) : u_ws;
                 p.u_prev = u_prev;
                 p.u_out = u_out;
@@ -500,32 +524,43 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
         const bool tile = st::stepT_smem_bytes(g) <= 227 * 1024;
         float* S2T = (float*)(ws + wl.S2T);
         if (tile) ST_CUDA(st::launch_transpose_band(g, S2, S2T, st, -INFINITY));
-        const st::Geo gt = st::transposed(g);
         st::DustArgs dr{}, dc{};
         dr.H = dc.H = g.H;
         dr.sd2 = dc.sd2 = g.sd2;
         dr.err = dc.err = err;
         dr.L_own = g.Lq; dr.L_other = g.Lk; dr.Lr_own = g.Lrq; dr.Lr_other = g.Lrk; dr.mask_other = col_mask;
         dc.L_own = g.Lk; dc.L_other = g.Lq; dc.Lr_own = g.Lrk; dc.Lr_other = g.Lrq; dc.mask_other = row_mask;
+        float band_lam = 1.f;  // temperature scale of the stored band (and its transpose)
         for (long t = 1; t <= T + R; ++t) {
             const long r = t - T;
             float* u_out = (sv && r >= 0 && r <= 2) ? slot_u(r) : u_ws;
             float* v_out = (sv && r >= 0 && r <= 2) ? slot_v(r) : v_ws;
+            const float lam = step_scale(desc, t);
+            st::Geo gs = g;  // this step's temperature: scores (band) and the dustbin score
+            gs.c2 = g.c2 * lam;
+            gs.sd2 = g.sd2 * lam;
+            if (lam != band_lam) {  // epsilon stage change: recompute the band at the stage temperature
+                ST_CUDA(st::launch_scores(gs, desc->dtype, Q, K, S2, st));
+                if (tile) ST_CUDA(st::launch_transpose_band(g, S2, S2T, st, -INFINITY));
+                band_lam = lam;
+            }
+            const st::Geo gts = st::transposed(gs);
+            dr.sd2 = dc.sd2 = gs.sd2;
             if (tile) {
                 // fp32 path: bulk-copied band tiles, in-thread reductions; columns via the transposed band
-                ST_CUDA(st::launch_stepT(g, t == 1, S2, v_prev, u_prev, u_out, err, st));
+                ST_CUDA(st::launch_stepT(gs, t == 1, S2, v_prev, u_prev, u_out, err, st));
                 if (g.dustbin) {
                     dr.dual_other = v_prev; dr.off_own = u_prev; dr.out_own = u_out;
                     ST_CUDA(st::launch_dustbin(dr, t == 1, g.BH, st));
                 }
-                ST_CUDA(st::launch_stepT(gt, t == 1, S2T, u_out, v_prev, v_out, err, st));
+                ST_CUDA(st::launch_stepT(gts, t == 1, S2T, u_out, v_prev, v_out, err, st));
                 if (g.dustbin) {
                     dc.dual_other = u_out; dc.off_own = v_prev; dc.out_own = v_out;
                     ST_CUDA(st::launch_dustbin(dc, t == 1, g.BH, st));
                 }
             } else {
-                ST_CUDA(st::launch_row_step(g, t == 1, S2, v_prev, u_prev, u_out, err, st));
-                ST_CUDA(st::launch_col_step(g, t == 1, S2, u_out, v_prev, v_out, err, st));
+                ST_CUDA(st::launch_row_step(gs, t == 1, S2, v_prev, u_prev, u_out, err, st));
+                ST_CUDA(st::launch_col_step(gs, t == 1, S2, u_out, v_prev, v_out, err, st));
             }
             u_prev = u_out;
             v_prev = v_out;

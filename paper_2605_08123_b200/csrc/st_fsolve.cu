@@ -46,6 +46,9 @@ struct FSolve {
     const int* work;         // compacted active blocks, bh * NB + b
     const int* nwork;
     int NB, Nw, T, R;
+    int nst;                 // epsilon stages (run-length over the base steps): step t <= st_end[q] -> st_scale[q]
+    int st_end[8];
+    float st_scale[8];
     int* err;
 };
 
@@ -114,6 +117,17 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {  // FADD2 (packed 
     return d;
 }
 __device__ __forceinline__ float2 ex2x2(float2 x) { return make_float2(ex2(x.x), ex2(x.y)); }
+
+// score scale of full step t: the band is stored at the final temperature; base step t of an
+// EpsSchedule stage runs at that stage's (scale_to_temperature, sinkhorn.hpp:186-195); tail: 1
+template <class F>
+__device__ __forceinline__ float stage_scale(const F& f, int t) {
+    if (t > f.T) return 1.f;
+    float lam = 1.f;
+    for (int q = f.nst - 1; q >= 0; --q)
+        if (t <= f.st_end[q]) lam = f.st_scale[q];
+    return lam;
+}
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {  // FFMA2 (packed fp32, sm_100)
     float2 d;
     asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
@@ -215,6 +229,8 @@ __global__ void __launch_bounds__(kThreads) k_fsolve(Geo g, FSolve f) {
             }
             if (fin) continue;
             __syncthreads();
+            const float lam = stage_scale(f, t);
+            const float2 ll = make_float2(lam, lam);
             // ---- row pass: threads (r, h) share row i; h takes the 16-cell groups h, h+2, ...
             const float* trow = tile + r * P;
             const float* vrow = ((r & 1) ? vw1 : vw0) + (r & ~1);  // vrow[k] = v(r + k), k even aligned
@@ -225,7 +241,7 @@ __global__ void __launch_bounds__(kThreads) k_fsolve(Geo g, FSolve f) {
                     for (int k0 = 16 * h; k0 < P; k0 += 32)
 #pragma unroll
                         for (int kk = 0; kk < 16; ++kk)
-                            if (k0 + kk < P) m = fmaxf(m, trow[k0 + kk] + vrow[k0 + kk]);
+                            if (k0 + kk < P) m = fmaxf(m, fmaf(trow[k0 + kk], lam, vrow[k0 + kk]));
                     m = fmaxf(m, __shfl_xor_sync(pmask, m, 16));
                     o = -m;
                 } else {
@@ -241,14 +257,14 @@ __global__ void __launch_bounds__(kThreads) k_fsolve(Geo g, FSolve f) {
                             const float2 sb = *reinterpret_cast<const float2*>(trow + k0 + kk + 2);
                             const float2 va = *reinterpret_cast<const float2*>(vrow + k0 + kk);
                             const float2 vb = *reinterpret_cast<const float2*>(vrow + k0 + kk + 2);
-                            a0 = fadd2(a0, ex2x2(fadd2(fadd2(sa, va), oo)));
-                            a1 = fadd2(a1, ex2x2(fadd2(fadd2(sb, vb), oo)));
+                            a0 = fadd2(a0, ex2x2(fadd2(ffma2(sa, ll, va), oo)));
+                            a1 = fadd2(a1, ex2x2(fadd2(ffma2(sb, ll, vb), oo)));
                         }
                     } else {
                         for (int kx = k0; kx < P; kx += 2) {
                             const float2 sa = *reinterpret_cast<const float2*>(trow + kx);
                             const float2 va = *reinterpret_cast<const float2*>(vrow + kx);
-                            a0 = fadd2(a0, ex2x2(fadd2(fadd2(sa, va), oo)));
+                            a0 = fadd2(a0, ex2x2(fadd2(ffma2(sa, ll, va), oo)));
                         }
                     }
                 }
@@ -291,25 +307,25 @@ __global__ void __launch_bounds__(kThreads) k_fsolve(Geo g, FSolve f) {
                     if (ilo <= ihi) {
                         const float* tp = tile + ilo * step + c;
                         if (t == 1) {
-                            for (int ii = ilo; ii <= ihi; ++ii) pm = fmaxf(pm, tp[(ii - ilo) * step] + unew[ii]);
+                            for (int ii = ilo; ii <= ihi; ++ii) pm = fmaxf(pm, fmaf(tp[(ii - ilo) * step], lam, unew[ii]));
                             if (pm != -INFINITY)
-                                for (int ii = ilo; ii <= ihi; ++ii) ps += ex2(tp[(ii - ilo) * step] + unew[ii] - pm);
+                                for (int ii = ilo; ii <= ihi; ++ii) ps += ex2(fmaf(tp[(ii - ilo) * step], lam, unew[ii]) - pm);
                         } else if (vc != -INFINITY) {
                             const float2 vv = make_float2(vc, vc);
                             float2 q0 = make_float2(0.f, 0.f), q1 = q0;
                             int ii = ilo;
                             if (ii & 1) {  // align the unew pairs
-                                q0.x += ex2(tp[0] + unew[ii] + vc);
+                                q0.x += ex2(fmaf(tp[0], lam, unew[ii]) + vc);
                                 ++ii;
                                 tp += step;
                             }
                             for (; ii + 3 <= ihi; ii += 4, tp += 4 * step) {
                                 const float2 ua = *reinterpret_cast<const float2*>(unew + ii);
                                 const float2 ub = *reinterpret_cast<const float2*>(unew + ii + 2);
-                                q0 = fadd2(q0, ex2x2(fadd2(make_float2(tp[0], tp[step]), fadd2(ua, vv))));
-                                q1 = fadd2(q1, ex2x2(fadd2(make_float2(tp[2 * step], tp[3 * step]), fadd2(ub, vv))));
+                                q0 = fadd2(q0, ex2x2(ffma2(make_float2(tp[0], tp[step]), ll, fadd2(ua, vv))));
+                                q1 = fadd2(q1, ex2x2(ffma2(make_float2(tp[2 * step], tp[3 * step]), ll, fadd2(ub, vv))));
                             }
-                            for (; ii <= ihi; ++ii, tp += step) q1.x += ex2(tp[0] + unew[ii] + vc);
+                            for (; ii <= ihi; ++ii, tp += step) q1.x += ex2(fmaf(tp[0], lam, unew[ii]) + vc);
                             ps = (q0.x + q0.y) + (q1.x + q1.y);
                         }
                     }
@@ -477,6 +493,8 @@ __global__ void __launch_bounds__(kTmGroups * kThreads, 1) k_fsolve_tm(Geo g, FS
             const float* vrow = ((r & 1) ? vw1 : vw0) + (r & ~1);  // vrow[k] = v(r + k), k even aligned
             float* erow = et + r * P;
             float o = 0.f;
+            const float lam = stage_scale(f, t);
+            const float2 ll = make_float2(lam, lam);
             // tcgen05.ld is warp-collective (.sync.aligned): every lane loads (one 32-column chunk
             // at a time), inactive rows only mask the math
             if (t == 1) {  // cold start: row max of s2 + v over both halves
@@ -488,10 +506,10 @@ __global__ void __launch_bounds__(kTmGroups * kThreads, 1) k_fsolve_tm(Geo g, FS
                     sm100::tc_wait_ld();
                     if (act) {
 #pragma unroll
-                        for (int x = 0; x < 32; ++x) m = fmaxf(m, sv[x] + vrow[64 * hh + 32 * q + x]);
+                        for (int x = 0; x < 32; ++x) m = fmaxf(m, fmaf(sv[x], lam, vrow[64 * hh + 32 * q + x]));
                     }
                 }
-                if (act && hh == 1) m = fmaxf(m, extra[r] + vrow[kTmCols]);
+                if (act && hh == 1) m = fmaxf(m, fmaf(extra[r], lam, vrow[kTmCols]));
                 rpart[hh][r] = m;
                 gsync();
                 o = -fmaxf(rpart[0][r], rpart[1][r]);
@@ -512,8 +530,8 @@ __global__ void __launch_bounds__(kTmGroups * kThreads, 1) k_fsolve_tm(Geo g, FS
                     for (int x = 0; x < 32; x += 4) {
                         const float2 va = *reinterpret_cast<const float2*>(vrow + c0 + x);
                         const float2 vb = *reinterpret_cast<const float2*>(vrow + c0 + x + 2);
-                        const float2 xa = fadd2(fadd2(make_float2(sv[x], sv[x + 1]), va), oo);
-                        const float2 xb = fadd2(fadd2(make_float2(sv[x + 2], sv[x + 3]), vb), oo);
+                        const float2 xa = fadd2(ffma2(make_float2(sv[x], sv[x + 1]), ll, va), oo);
+                        const float2 xb = fadd2(ffma2(make_float2(sv[x + 2], sv[x + 3]), ll, vb), oo);
                         const float2 ea = ex2x2(xa), eb = ex2x2(xb);
                         a0 = fadd2(a0, ea);
                         a1 = fadd2(a1, eb);
@@ -528,7 +546,7 @@ __global__ void __launch_bounds__(kTmGroups * kThreads, 1) k_fsolve_tm(Geo g, FS
             }
             if (hh == 1) {
                 if (act && Wf > kTmCols) {
-                    const float x = extra[r] + vrow[kTmCols] + o;
+                    const float x = fmaf(extra[r], lam, vrow[kTmCols]) + o;
                     const float e = ex2(x);
                     a0.x += e;
                     erow[kTmCols] = (t == 1) ? x : e;
@@ -708,6 +726,11 @@ cudaError_t launch_fsolve(const Geo& g, int T, int R, const FSolvePtrs& p, cudaS
     f.T = T;
     f.R = R;
     f.err = p.err;
+    f.nst = p.nst;
+    for (int q = 0; q < 8; ++q) {
+        f.st_end[q] = p.st_end[q];
+        f.st_scale[q] = p.st_scale[q];
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(G);
     cfg.blockDim = dim3(threads);

@@ -52,6 +52,9 @@ struct FSolvePtrs {
     int* work;
     int* count;
     int* err;
+    int nst;            // epsilon stages of the base solve (run-length): steps <= st_end[q] scale by st_scale[q]
+    int st_end[8];
+    float st_scale[8];
 };
 size_t fsolve_smem_bytes(const Geo& g);
 bool fsolve_supported(const Geo& g);

@@ -37,6 +37,8 @@ def lib():
                                      ctypes.c_double, D, D, D, D, U8, U8, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_int, I64, I64, D, D, D, D, D, D, D, D]
         L.stoc_run_batch.restype = ctypes.c_int
+        L.stoc_run_batch_sched.argtypes = L.stoc_run_batch.argtypes + [ctypes.c_int, D, ctypes.POINTER(I64)]
+        L.stoc_run_batch_sched.restype = ctypes.c_int
         L.stoc_normal_fill.argtypes = [ctypes.c_uint64, ctypes.c_char_p, ctypes.c_uint64, I64, ctypes.c_double, D]
         L.stoc_normal_fill.restype = None
         L.stoc_last_error.restype = ctypes.c_char_p
@@ -59,7 +61,7 @@ class OracleError(RuntimeError):
 
 
 def run(cfg, Q, K, V, G, row_mask=None, col_mask=None, *, heads=None, precision=64, mode=0, backward=True,
-        threads=None, tile_block=128, centered=True):
+        threads=None, tile_block=128, centered=True, eps_schedule=None):
     """Reference path per head: run_surrogate + r2_backward (inc/validation.hpp:102-114).
 
     Q, K, V, G: [nh, L', d] arrays of the heads `heads` (global b*H+h indices,
@@ -86,12 +88,16 @@ def run(cfg, Q, K, V, G, row_mask=None, col_mask=None, *, heads=None, precision=
     p = lambda a: a.ctypes.data_as(P)
     rm = None if row_mask is None else np.ascontiguousarray(row_mask, dtype=np.uint8)
     cm = None if col_mask is None else np.ascontiguousarray(col_mask, dtype=np.uint8)
-    code = lib().stoc_run_batch(
+    # eps_schedule: [(epsilon, iterations), ...] base-solve stages (EpsSchedule, trace.hpp:12-50)
+    se = None if not eps_schedule else np.array([e for e, _ in eps_schedule], dtype=np.float64)
+    si = None if not eps_schedule else np.array([n for _, n in eps_schedule], dtype=np.int64)
+    code = lib().stoc_run_batch_sched(
         Bb, Hh, Lreal, d, cfg.w, cfg.T, cfg.R, cfg.eps, cfg.dustbin, cfg.dustbin_cost,
         p(Q), p(K), p(V), p(G), None if rm is None else rm.ctypes.data, None if cm is None else cm.ctypes.data,
         precision, mode, tile_block, 1 if centered else 0, threads or os.cpu_count() or 1, 0, nh,
         p(out["O"]), p(out["dQ"]) if backward else None, p(out["dK"]), p(out["dV"]), p(out["d_eps"]),
-        p(out["eta_v"]), p(out["duals"]), p(out["gauges"]))
+        p(out["eta_v"]), p(out["duals"]), p(out["gauges"]), 0 if se is None else len(se),
+        None if se is None else p(se), None if si is None else si.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
     if code != 0:
         raise OracleError(code, lib().stoc_last_error().decode())
     return out

@@ -117,3 +117,17 @@ def test_bf16_rounding_is_rne():
     assert back[0] == 1.0 and back[1] == 1.0  # tie to even
     assert back[2] == 1.0078125
     assert abs(back[4] - 3.140625) < 1e-7
+
+
+def test_eps_schedule_validation():
+    """EpsSchedule::validate (trace.hpp:37-49) through the C-ABI, before any device work."""
+    def desc(stages):
+        return band.BandSpec(batch=1, heads=1, seq_q=8, seq_k=8, head_dim=4, half_band=1, base_depth=4,
+                             epsilon=0.5, eps_schedule=stages).desc()
+    def fwd(d):
+        return _lib.lib.st_forward(ctypes.byref(d), None, None, None, None, None, None, None, None, 0, None)
+    assert fwd(desc([(1.0, 2), (2.0, 2)])) == _lib.ST_INVALID_TEMPERATURE       # increasing temperature
+    assert fwd(desc([(1.0, 2), (-0.5, 2)])) == _lib.ST_INVALID_TEMPERATURE      # non-positive
+    assert fwd(desc([(1.0, 2), (0.5, 1)])) == _lib.ST_INVALID_ARGUMENT          # iterations != T
+    assert fwd(desc([(1.0, 2), (0.25, 2)])) == _lib.ST_INVALID_ARGUMENT         # last stage != epsilon
+    assert fwd(desc([(1.0, 2), (0.5, 2)])) == _lib.ST_INVALID_ARGUMENT          # valid schedule, null tensors

