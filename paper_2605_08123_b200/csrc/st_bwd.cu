@@ -488,12 +488,14 @@ __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
 #pragma unroll
         for (int e = 0; e < CPT; ++e) accv[q][e] = 0.f;
     const float* wrow = tS + (4 * rg) * Wf;
-    for (int kk = 0; kk < Wf + 3; ++kk) {
+    // band step kk feeds rows q with cell k = kk - q; only the first / last 3 steps need the
+    // k in [0, Wf) guard, the interior runs check-free
+    auto step = [&](int kk, bool guard) {
         float wq[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int k = kk - q;
-            wq[q] = (k >= 0 && k < Wf) ? wrow[q * Wf + k] : 0.f;
+            wq[q] = (!guard || (k >= 0 && k < Wf)) ? wrow[q * Wf + k] : 0.f;
         }
         const float* xr = ops + (4 * rg + kk) * D + 4 * cg;
 #pragma unroll
@@ -507,7 +509,12 @@ __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
                 accv[q][4 * m + 3] = fmaf(wq[q], x4.w, accv[q][4 * m + 3]);
             }
         }
-    }
+    };
+    const int kin = min(3, Wf + 3);
+    for (int kk = 0; kk < kin; ++kk) step(kk, true);
+#pragma unroll 2
+    for (int kk = 3; kk < Wf; ++kk) step(kk, false);
+    for (int kk = max(Wf, kin); kk < Wf + 3; ++kk) step(kk, true);
     const float sc = (kOp == C1 || kOp == RO) ? 1.f : g.inv_qk;
     const TIn* dsrc = (kOp == RO) ? a.V : (kOp == C1) ? a.dO : nullptr;
 #pragma unroll
@@ -850,12 +857,12 @@ __global__ void __launch_bounds__(256) k_bwdG(Geo g, BT<TIn> a) {
 #pragma unroll
         for (int e = 0; e < CPT; ++e) accv[q][e] = 0.f;
     const float* wrow = tS + (RPT * rg) * Wf;
-    for (int kk = 0; kk < Wf + RPT - 1; ++kk) {
+    auto step = [&](int kk, bool guard) {
         float wq[RPT];
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
             const int k = kk - q;
-            wq[q] = (k >= 0 && k < Wf) ? wrow[q * Wf + k] : 0.f;
+            wq[q] = (!guard || (k >= 0 && k < Wf)) ? wrow[q * Wf + k] : 0.f;
         }
         const TIn* xr = ops + (RPT * rg + kk) * OP + 4 * cg;
 #pragma unroll
@@ -869,7 +876,12 @@ __global__ void __launch_bounds__(256) k_bwdG(Geo g, BT<TIn> a) {
                 accv[q][4 * m + 3] = fmaf(wq[q], x4.w, accv[q][4 * m + 3]);
             }
         }
-    }
+    };
+    const int kin = min(RPT - 1, Wf + RPT - 1);
+    for (int kk = 0; kk < kin; ++kk) step(kk, true);
+#pragma unroll 2
+    for (int kk = RPT - 1; kk < Wf; ++kk) step(kk, false);
+    for (int kk = max(Wf, kin); kk < Wf + RPT - 1; ++kk) step(kk, true);
     const float sc = (kOp == C1 || kOp == RO) ? 1.f : g.inv_qk;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
