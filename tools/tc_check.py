@@ -1,7 +1,7 @@
 """Dev check: tensor-core forward vs generic forward on the same inputs (+ timing)."""
-import sys, time
+import os, sys, time
 import numpy as np, torch
-sys.path.insert(0, '.')
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), '..'))
 from paper_2605_08123_b200 import band, configs
 
 def run(cfg, generic, iters=3):

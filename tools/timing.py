@@ -1,7 +1,7 @@
 """Quick per-config timing of the CUDA path (development helper, not the bench)."""
-import sys, time
+import os, sys, time
 import numpy as np, torch
-sys.path.insert(0, '.')
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), '..'))
 from paper_2605_08123_b200 import band, configs
 
 def bench(cid, iters=3, L=None):
