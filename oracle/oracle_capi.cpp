@@ -47,6 +47,7 @@ struct BatchArgs {
     int n_stages = 0;
     const double* stage_eps = nullptr;
     const std::int64_t* stage_iters = nullptr;
+    std::int64_t Lk = -1;  // key count (rectangular problems, no dustbin); -1: Lk = L
 };
 
 template <class T>
@@ -54,24 +55,25 @@ void run_head(const BatchArgs& a, std::int64_t bh) {
     using namespace stoc;
     const std::int64_t b = bh / a.H;
     const std::int64_t L = a.L, Lr = a.L + (a.dustbin ? 1 : 0), d = a.d;
-    const size_t off = static_cast<size_t>(bh * Lr * d);
-    auto load = [&](const double* src) {
-        Mat<T> m(Lr, d);
-        for (size_t k = 0; k < m.a.size(); ++k) m.a[k] = static_cast<T>(src[off + k]);
+    const std::int64_t Lk = a.Lk < 0 ? L : a.Lk, Lrk = Lk + (a.dustbin ? 1 : 0);
+    const size_t off = static_cast<size_t>(bh * Lr * d), offk = static_cast<size_t>(bh * Lrk * d);
+    auto load = [&](const double* src, std::int64_t rows, size_t o) {
+        Mat<T> m(rows, d);
+        for (size_t k = 0; k < m.a.size(); ++k) m.a[k] = static_cast<T>(src[o + k]);
         return m;
     };
-    Mat<T> Q = load(a.Q), K = load(a.K), V = load(a.V), G = load(a.G);
+    Mat<T> Q = load(a.Q, Lr, off), K = load(a.K, Lrk, offk), V = load(a.V, Lrk, offk), G = load(a.G, Lr, off);
     std::vector<bool> rm, cm;
     if (a.row_mask) {
         rm.resize(static_cast<size_t>(L));
         for (std::int64_t i = 0; i < L; ++i) rm[static_cast<size_t>(i)] = a.row_mask[b * L + i] != 0;
     }
     if (a.col_mask) {
-        cm.resize(static_cast<size_t>(L));
-        for (std::int64_t j = 0; j < L; ++j) cm[static_cast<size_t>(j)] = a.col_mask[b * L + j] != 0;
+        cm.resize(static_cast<size_t>(Lk));
+        for (std::int64_t j = 0; j < Lk; ++j) cm[static_cast<size_t>(j)] = a.col_mask[b * Lk + j] != 0;
     }
     SupportMask sup = a.dustbin ? spoke_dustbin_support(L, a.half_band, rm, cm)
-                                : build_band_support(L, L, a.half_band, rm, cm);
+                                : build_band_support(L, Lk, a.half_band, rm, cm);
     // linear loss: G zeroed on inactive rows (inc/loss.hpp:78-82)
     for (std::int64_t i = 0; i < Lr; ++i)
         if (!sup.row_active(i)) for (std::int64_t x = 0; x < d; ++x) G(i, x) = T(0);
@@ -92,7 +94,7 @@ void run_head(const BatchArgs& a, std::int64_t bh) {
     }
     SurrogateRun<T> run = run_surrogate<T>(Q, K, V, sched, a.T, a.R, es, a.centered != 0, pc);
     for (size_t k = 0; k < run.output.a.size(); ++k) a.O[off + k] = static_cast<double>(run.output.a[k]);
-    if (a.duals) {
+    if (a.duals && Lk == L) {
         double* dp = a.duals + static_cast<size_t>(bh) * 6 * Lr;
         for (std::int64_t r = 0; r <= 2 && r <= a.R; ++r) {
             const auto& u = run.trace.tail_u(r);
@@ -106,14 +108,15 @@ void run_head(const BatchArgs& a, std::int64_t bh) {
     CotangentSet<T> c =
         r2_backward<T>(run.scaled, run.trace, G, Q, K, V,
                        a.mode == 1 ? BackwardMode::DirectFourPlan : BackwardMode::OneReference, pc);
-    for (size_t k = 0; k < c.grad_q.a.size(); ++k) {
-        a.dQ[off + k] = static_cast<double>(c.grad_q.a[k]);
-        a.dK[off + k] = static_cast<double>(c.grad_k.a[k]);
-        a.dV[off + k] = static_cast<double>(c.grad_v.a[k]);
+    for (size_t k = 0; k < c.grad_q.a.size(); ++k) a.dQ[off + k] = static_cast<double>(c.grad_q.a[k]);
+    for (size_t k = 0; k < c.grad_k.a.size(); ++k) {
+        a.dK[offk + k] = static_cast<double>(c.grad_k.a[k]);
+        a.dV[offk + k] = static_cast<double>(c.grad_v.a[k]);
     }
     if (a.d_eps) a.d_eps[bh] = static_cast<double>(c.d_eps);
     if (a.eta_v)
-        for (std::int64_t j = 0; j < Lr; ++j) a.eta_v[bh * Lr + j] = static_cast<double>(c.base_v[static_cast<size_t>(j)]);
+        for (std::int64_t j = 0; j < Lrk; ++j)
+            a.eta_v[bh * Lrk + j] = static_cast<double>(c.base_v[static_cast<size_t>(j)]);
 }
 
 int classify(const std::exception& e) {
@@ -188,6 +191,38 @@ int stoc_run_batch_sched(std::int64_t B, std::int64_t H, std::int64_t L, std::in
     worker();
     for (auto& th : pool) th.join();
     if (status.load() != STOC_OK) g_err = first_err;
+    return status.load();
+}
+
+// rectangular problems (L_q != L_k, no dustbin): Q, G [B*H][Lq][d]; K, V, dK, dV [B*H][Lk][d]
+int stoc_run_batch_rect(std::int64_t B, std::int64_t H, std::int64_t Lq, std::int64_t Lk, std::int64_t d,
+                        std::int64_t half_band, std::int64_t T, std::int64_t R, double eps, const double* Q,
+                        const double* K, const double* V, const double* G, const std::uint8_t* row_mask,
+                        const std::uint8_t* col_mask, int precision, int mode, int nthreads, double* O, double* dQ,
+                        double* dK, double* dV, double* d_eps, double* eta_v) {
+    BatchArgs a{B,    H,  Lq, d,  half_band, T,        R,        eps,  0,   0.0,     Q,       K,      V,      G,
+                row_mask, col_mask, precision, mode, 128, 1, O, dQ, dK, dV, d_eps, eta_v, nullptr, nullptr};
+    a.Lk = Lk;
+    if (nthreads < 1) nthreads = 1;
+    std::atomic<std::int64_t> next{0};
+    std::atomic<int> status{STOC_OK};
+    auto worker = [&]() {
+        for (;;) {
+            const std::int64_t bh = next.fetch_add(1);
+            if (bh >= B * H || status.load() != STOC_OK) return;
+            try {
+                if (precision == 32) run_head<float>(a, bh);
+                else run_head<double>(a, bh);
+            } catch (const std::exception& e) {
+                status.store(classify(e));
+                return;
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < std::min<std::int64_t>(nthreads, B * H); ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
     return status.load();
 }
 

@@ -101,3 +101,32 @@ def run(cfg, Q, K, V, G, row_mask=None, col_mask=None, *, heads=None, precision=
     if code != 0:
         raise OracleError(code, lib().stoc_last_error().decode())
     return out
+
+
+def run_rect(Lq, Lk, d, w, eps, T, R, Q, K, V, G, row_mask=None, col_mask=None, precision=64, mode=0):
+    """Rectangular problems (L_q != L_k, no dustbin; build_band_support(Lq, Lk, ...), support.cpp:111):
+    Q, G [nh, Lq, d]; K, V [nh, Lk, d]; masks [nh, L] (one pseudo-example per head)."""
+    L_ = lib()
+    if not hasattr(L_, "_rect"):
+        D = ctypes.POINTER(ctypes.c_double)
+        I64 = ctypes.c_int64
+        L_.stoc_run_batch_rect.argtypes = [I64, I64, I64, I64, I64, I64, I64, I64, ctypes.c_double, D, D, D, D,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_int, D, D, D, D, D, D]
+        L_.stoc_run_batch_rect.restype = ctypes.c_int
+        L_._rect = True
+    Q, K, V, G = (np.ascontiguousarray(x, dtype=np.float64) for x in (Q, K, V, G))
+    nh = Q.shape[0]
+    out = {"O": np.zeros_like(Q), "dQ": np.zeros_like(Q), "dK": np.zeros_like(K), "dV": np.zeros_like(K),
+           "d_eps": np.zeros(nh), "eta_v": np.zeros((nh, Lk))}
+    P = ctypes.POINTER(ctypes.c_double)
+    p = lambda a: a.ctypes.data_as(P)
+    rm = None if row_mask is None else np.ascontiguousarray(row_mask, dtype=np.uint8)
+    cm = None if col_mask is None else np.ascontiguousarray(col_mask, dtype=np.uint8)
+    code = L_.stoc_run_batch_rect(nh, 1, Lq, Lk, d, w, T, R, eps, p(Q), p(K), p(V), p(G),
+                                  None if rm is None else rm.ctypes.data, None if cm is None else cm.ctypes.data,
+                                  precision, mode, os.cpu_count() or 1, p(out["O"]), p(out["dQ"]), p(out["dK"]),
+                                  p(out["dV"]), p(out["d_eps"]), p(out["eta_v"]))
+    if code != 0:
+        raise OracleError(code, lib().stoc_last_error().decode())
+    return out

@@ -253,3 +253,34 @@ def test_eps_schedule_parity(cid, L, nh, sched):
 def test_eps_schedule_generic_kernels():
     cfg = configs.Config(0, B=1, H=2, L=64, d=8, w=5, eps=0.5, T=6, R=2, dtype="f32")
     check_against_oracle(cfg, configs.make_inputs(cfg), 2e-5, 5e-5, eps_schedule=[(1.0, 3), (0.5, 3)])
+
+
+@pytest.mark.parametrize("Lq,Lk,d,w,masked", [(160, 150, 32, 20, False), (96, 120, 64, 33, True),
+                                               (130, 126, 8, 5, False)])
+def test_rectangular_parity(Lq, Lk, d, w, masked):
+    """L_q != L_k supports (build_band_support(Lq, Lk, w, ...), support.cpp:111; the reference's
+    rectangular adjoint test, test_adjoint.cpp:378-409) on the per-step and generic kernels."""
+    rng = np.random.default_rng(7)
+    nh, eps, T, R = 2, 0.3, 6, 2
+    Q, G = (rng.standard_normal((nh, Lq, d)).astype(np.float32) for _ in range(2))
+    K, V = (rng.standard_normal((nh, Lk, d)).astype(np.float32) for _ in range(2))
+    rm = cm = None
+    if masked:
+        rm = (np.arange(Lq)[None, :] < np.array([[Lq - 10], [Lq]])).astype(np.uint8)
+        cm = (np.arange(Lk)[None, :] < np.array([[Lk - 40], [Lk - 3]])).astype(np.uint8)
+    spec = band.BandSpec(batch=nh, heads=1, seq_q=Lq, seq_k=Lk, head_dim=d, half_band=w, base_depth=T,
+                         tail_depth=R, epsilon=eps)
+    dev = lambda x, L: torch.from_numpy(x).cuda().reshape(nh, 1, L, d)
+    run = band.run_surrogate(dev(Q, Lq), dev(K, Lk), dev(V, Lk), spec,
+                             None if rm is None else torch.from_numpy(rm).cuda(),
+                             None if cm is None else torch.from_numpy(cm).cuda())
+    cot = band.r2_backward(run, dev(G, Lq))
+    torch.cuda.synchronize()
+    g = {"O": run.output, "dQ": cot.grad_q, "dK": cot.grad_k, "dV": cot.grad_v, "d_eps": cot.d_eps}
+    g = {k: x.cpu().numpy().astype(np.float64).reshape(nh, -1) for k, x in g.items()}
+    r = oracle_ref.run_rect(Lq, Lk, d, w, eps, T, R, Q, K, V, G, rm, cm)
+    r32 = oracle_ref.run_rect(Lq, Lk, d, w, eps, T, R, Q, K, V, G, rm, cm, precision=32)
+    for k in ("O", "dQ", "dK", "dV", "d_eps"):
+        e, fl = rel(g[k], r[k].reshape(nh, -1)), rel(r32[k].reshape(nh, -1), r[k].reshape(nh, -1))
+        tol = DEPS_TOL if k == "d_eps" else FP32_TOL
+        assert e <= max(tol, (3.0 if k == "d_eps" else 1.5) * fl), (k, e, fl)
