@@ -117,6 +117,28 @@ st_status st_backward(const st_desc* desc, const void* saved, const void* Q, con
                       float* eta_v, int32_t mode, void* workspace, size_t workspace_bytes,
                       void* stream);
 
+/* Sequence sharding (config 5): the problem a rank passes is its own rows plus a halo of up to
+ * half_band rows on each side.  The library calls `hook` right after it has ENQUEUED (on `stream`)
+ * each kernel that produces a vector the next kernel reads across the shard edge -- kind 0: a row
+ * vector u / u-bar ([B*H][L'_q] f32), kind 1: a column vector v / v-bar ([B*H][L'_k]).  The hook
+ * must enqueue, on `stream`, the replacement of the vector's halo entries by the neighbours' values
+ * (e.g. NCCL point-to-point of the w boundary entries); every own row's and own column's reduction
+ * lies inside the local window, so the result for the own rows equals the unsharded one.  Outputs
+ * of halo rows are unspecified; d_eps sums the rows [own_begin, own_end) only.  Dustbin problems
+ * are not supported on this path. */
+typedef void (*st_halo_fn)(void* user, int32_t kind, float* vec, int64_t len, void* stream);
+
+st_status st_forward_halo(const st_desc* desc, const void* Q, const void* K, const void* V,
+                          const uint8_t* row_mask, const uint8_t* col_mask, float* O, void* saved,
+                          void* workspace, size_t workspace_bytes, void* stream, st_halo_fn hook, void* user);
+
+st_status st_backward_halo(const st_desc* desc, const void* saved, const void* Q, const void* K,
+                           const void* V, const void* dO, const uint8_t* row_mask,
+                           const uint8_t* col_mask, float* dQ, float* dK, float* dV, float* d_eps,
+                           float* eta_v, int32_t mode, void* workspace, size_t workspace_bytes,
+                           void* stream, st_halo_fn hook, void* user, int64_t own_begin,
+                           int64_t own_end);
+
 /* Host-side copy of the saved tail duals in the reference's natural-log units:
  * u[3][B*H][L'_q], v[3][B*H][L'_k] (steps T, T+1, T+2; centered when
  * desc->centered, inactive entries 0) and gauge[3][B*H] (the cumulative ledger

@@ -36,6 +36,7 @@ ST_DIRECT_FOUR_PLAN = 1
 EXPORTED = (
     "st_saved_bytes", "st_workspace_bytes", "st_forward", "st_backward", "st_saved_duals",
     "st_validate_support", "st_normal_fill", "st_uniform_fill", "st_last_error", "st_launch_count",
+    "st_forward_halo", "st_backward_halo",
 )
 
 
@@ -49,6 +50,10 @@ class StDesc(ctypes.Structure):
         ("n_stages", ctypes.c_int32), ("stage_eps", ctypes.POINTER(ctypes.c_double)),
         ("stage_iters", ctypes.POINTER(ctypes.c_int64)),
     ]
+
+
+# void (*st_halo_fn)(void* user, int32_t kind, float* vec, int64_t len, void* stream)
+HALO_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
 
 
 def _load() -> ctypes.CDLL:
@@ -67,6 +72,11 @@ def _load() -> ctypes.CDLL:
     lib.st_forward.restype = ctypes.c_int
     lib.st_backward.argtypes = [P, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, I32, VP, ctypes.c_size_t, VP]
     lib.st_backward.restype = ctypes.c_int
+    lib.st_forward_halo.argtypes = [P, VP, VP, VP, VP, VP, VP, VP, VP, ctypes.c_size_t, VP, HALO_FN, VP]
+    lib.st_forward_halo.restype = ctypes.c_int
+    lib.st_backward_halo.argtypes = [P, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, I32, VP, ctypes.c_size_t,
+                                     VP, HALO_FN, VP, I64, I64]
+    lib.st_backward_halo.restype = ctypes.c_int
     lib.st_saved_duals.argtypes = [P, VP, VP, VP, D, D, D, VP]
     lib.st_saved_duals.restype = ctypes.c_int
     lib.st_validate_support.argtypes = [P, VP, VP]

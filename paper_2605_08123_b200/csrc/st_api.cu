@@ -329,13 +329,18 @@ int band_valid(const void* ws, const void* Q, const void* K, const void* rm, con
 }
 }  // namespace
 
-st_status st_forward(const st_desc* desc, const void* Q, const void* K, const void* V, const uint8_t* row_mask,
-                     const uint8_t* col_mask, float* O, void* saved, void* workspace, size_t workspace_bytes,
-                     void* stream) {
+static st_status forward_impl(const st_desc* desc, const void* Q, const void* K, const void* V,
+                              const uint8_t* row_mask, const uint8_t* col_mask, float* O, void* saved,
+                              void* workspace, size_t workspace_bytes, void* stream, st_halo_fn hook, void* user) {
     Dims m;
     st_status s = check_desc(desc, m);
     if (s != ST_OK) return s;
     if (!Q || !K || !V || !O) return fail(ST_INVALID_ARGUMENT, "null tensor pointer");
+    if (hook && desc->dustbin) return fail(ST_NOT_SUPPORTED, "sequence sharding of dustbin problems");
+    // sequence sharding: hand each just-enqueued dual to the caller's halo exchange
+    auto halo = [&](int kind, float* vec) {
+        if (hook) hook(user, kind, vec, kind == 0 ? m.BH * m.Lrq : m.BH * m.Lrk, stream);
+    };
     const TcPlan tp = tc_plan(desc, m);
     const WsLayout wl = ws_layout(m, tp);
     if (workspace == nullptr || workspace_bytes < wl.bytes)
@@ -436,12 +441,14 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
                 dr.dual_other = v_prev; dr.off_own = u_prev; dr.out_own = u_out;
                 ST_CUDA(st::launch_dustbin(dr, t == 1, g.BH, st));
             }
+            halo(0, u_out);
             pc.dual_other = u_out; pc.off_own = v_prev; pc.out_own = v_out;
             ST_CUDA(st::launch_phase(pc, t == 1, grid, st));
             if (g.dustbin) {
                 dc.dual_other = u_out; dc.off_own = v_prev; dc.out_own = v_out;
                 ST_CUDA(st::launch_dustbin(dc, t == 1, g.BH, st));
             }
+            halo(1, v_out);
             u_prev = u_out;
             v_prev = v_out;
         }
@@ -450,7 +457,7 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
     } else {
         if (dualT) ST_CUDA(st::launch_band_dual(g, desc->dtype, false, Q, K, S2, S2T_ws, st));
         else ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));
-        if (fused_ok(desc, m) && T + R >= 1 && st::fsolve_supported(g) && !getenv("ST_NO_FSOLVE")) {
+        if (!hook && fused_ok(desc, m) && T + R >= 1 && st::fsolve_supported(g) && !getenv("ST_NO_FSOLVE")) {
             // one persistent cooperative launch for all T+R steps (band tiles SMEM-resident)
             st::FSolvePtrs p{};
             p.S2 = S2;
@@ -480,7 +487,7 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
             ST_CUDA(st::launch_fsolve(g, (int)T, (int)R, p, st));
             u_prev = u_ws;
             v_prev = v_ws;
-        } else if (fused_ok(desc, m) && T + R >= 1) {
+        } else if (!hook && fused_ok(desc, m) && T + R >= 1) {
             // one launch per full step; the column half-step rides on the row exponentials
             float band_lam = 1.f;  // temperature scale of the stored band
             float* vbuf[2] = {v_ws, (float*)(ws + wl.vb2)};
@@ -553,14 +560,18 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
                     dr.dual_other = v_prev; dr.off_own = u_prev; dr.out_own = u_out;
                     ST_CUDA(st::launch_dustbin(dr, t == 1, g.BH, st));
                 }
+                halo(0, u_out);
                 ST_CUDA(st::launch_stepT(gts, t == 1, S2T, u_out, v_prev, v_out, err, st));
                 if (g.dustbin) {
                     dc.dual_other = u_out; dc.off_own = v_prev; dc.out_own = v_out;
                     ST_CUDA(st::launch_dustbin(dc, t == 1, g.BH, st));
                 }
+                halo(1, v_out);
             } else {
                 ST_CUDA(st::launch_row_step(gs, t == 1, S2, v_prev, u_prev, u_out, err, st));
+                halo(0, u_out);
                 ST_CUDA(st::launch_col_step(gs, t == 1, S2, u_out, v_prev, v_out, err, st));
+                halo(1, v_out);
             }
             u_prev = u_out;
             v_prev = v_out;
@@ -579,13 +590,15 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
     return ST_OK;
 }
 
-st_status st_backward(const st_desc* desc, const void* saved, const void* Q, const void* K, const void* V,
-                      const void* dO, const uint8_t* row_mask, const uint8_t* col_mask, float* dQ, float* dK,
-                      float* dV, float* d_eps, float* eta_v, int32_t mode, void* workspace, size_t workspace_bytes,
-                      void* stream) {
+static st_status backward_impl(const st_desc* desc, const void* saved, const void* Q, const void* K,
+                               const void* V, const void* dO, const uint8_t* row_mask, const uint8_t* col_mask,
+                               float* dQ, float* dK, float* dV, float* d_eps, float* eta_v, int32_t mode,
+                               void* workspace, size_t workspace_bytes, void* stream, st_halo_fn hook, void* user,
+                               int64_t own_begin, int64_t own_end) {
     Dims m;
     st_status s = check_desc(desc, m);
     if (s != ST_OK) return s;
+    if (hook && desc->dustbin) return fail(ST_NOT_SUPPORTED, "sequence sharding of dustbin problems");
     if (desc->tail_depth != 2) return fail(ST_UNSUPPORTED_DEPTH, "r2_backward requires a tail of depth 2");
     if (saved == nullptr) return fail(ST_MISSING_BASE_TRACE, "backward needs the forward's saved state");
     if (!Q || !K || !V || !dO || !dQ || !dK || !dV) return fail(ST_INVALID_ARGUMENT, "null tensor pointer");
@@ -620,10 +633,11 @@ st_status st_backward(const st_desc* desc, const void* saved, const void* Q, con
     p.dQ = dQ;
     p.dK = dK;
     p.dV = dV;
-    const int reuse = ((desc->flags & ST_FLAG_REUSE_BAND) && !(desc->flags & ST_FLAG_GENERIC) && !getenv("ST_NO_REUSE"))
+    const int reuse = (!hook && (desc->flags & ST_FLAG_REUSE_BAND) && !(desc->flags & ST_FLAG_GENERIC) && !getenv("ST_NO_REUSE"))
                           ? band_valid(workspace, Q, K, row_mask, col_mask, desc)
                           : 0;
     const bool tiled = st::bwdT_supported(g) && !(desc->flags & ST_FLAG_GENERIC);
+    if (hook && !tiled) return fail(ST_NOT_SUPPORTED, "sequence sharding needs the tiled backward (d in {32,64,128})");
     const bool dual = tiled && st::band_dual_supported(g);
     bool haveT = reuse == 2;
     if (!reuse) {
@@ -653,13 +667,49 @@ st_status st_backward(const st_desc* desc, const void* saved, const void* Q, con
             ST_CUDA(st::launch_transpose_band(g, Z, ZT, st, 0.f));
         }
         long long nl = 0;
-        ST_CUDA(st::launch_backward_tile(g, desc->dtype, p, t, mode == ST_DIRECT_FOUR_PLAN, st, nl));
+        st::BwdHook bh{hook, user, (int64_t)(m.BH * m.Lrq), (int64_t)(m.BH * m.Lrk)};
+        ST_CUDA(st::launch_backward_tile(g, desc->dtype, p, t, mode == ST_DIRECT_FOUR_PLAN, st, nl,
+                                         hook ? &bh : nullptr));
         st::add_launches(nl);
     } else {
         ST_CUDA(st::launch_backward(g, desc->dtype, p, mode == ST_DIRECT_FOUR_PLAN, st));
     }
-    if (d_eps) ST_CUDA(st::launch_deps_reduce(g, p.deps_part, d_eps, st));
+    if (d_eps) {
+        const int ib = (int)std::max<int64_t>(0, own_begin);
+        const int ie = (own_end < 0) ? (int)m.Lrq : (int)std::min<int64_t>(own_end, m.Lrq);
+        ST_CUDA(st::launch_deps_reduce(g, p.deps_part, d_eps, st, ib, ie));
+    }
     return ST_OK;
+}
+
+st_status st_forward(const st_desc* desc, const void* Q, const void* K, const void* V, const uint8_t* row_mask,
+                     const uint8_t* col_mask, float* O, void* saved, void* workspace, size_t workspace_bytes,
+                     void* stream) {
+    return forward_impl(desc, Q, K, V, row_mask, col_mask, O, saved, workspace, workspace_bytes, stream, nullptr,
+                        nullptr);
+}
+
+st_status st_forward_halo(const st_desc* desc, const void* Q, const void* K, const void* V, const uint8_t* row_mask,
+                          const uint8_t* col_mask, float* O, void* saved, void* workspace, size_t workspace_bytes,
+                          void* stream, st_halo_fn hook, void* user) {
+    return forward_impl(desc, Q, K, V, row_mask, col_mask, O, saved, workspace, workspace_bytes, stream, hook, user);
+}
+
+st_status st_backward(const st_desc* desc, const void* saved, const void* Q, const void* K, const void* V,
+                      const void* dO, const uint8_t* row_mask, const uint8_t* col_mask, float* dQ, float* dK,
+                      float* dV, float* d_eps, float* eta_v, int32_t mode, void* workspace, size_t workspace_bytes,
+                      void* stream) {
+    return backward_impl(desc, saved, Q, K, V, dO, row_mask, col_mask, dQ, dK, dV, d_eps, eta_v, mode, workspace,
+                         workspace_bytes, stream, nullptr, nullptr, 0, -1);
+}
+
+st_status st_backward_halo(const st_desc* desc, const void* saved, const void* Q, const void* K, const void* V,
+                           const void* dO, const uint8_t* row_mask, const uint8_t* col_mask, float* dQ, float* dK,
+                           float* dV, float* d_eps, float* eta_v, int32_t mode, void* workspace,
+                           size_t workspace_bytes, void* stream, st_halo_fn hook, void* user, int64_t own_begin,
+                           int64_t own_end) {
+    return backward_impl(desc, saved, Q, K, V, dO, row_mask, col_mask, dQ, dK, dV, d_eps, eta_v, mode, workspace,
+                         workspace_bytes, stream, hook, user, own_begin, own_end);
 }
 
 st_status st_saved_duals(const st_desc* desc, const void* saved, const uint8_t* row_mask_host,

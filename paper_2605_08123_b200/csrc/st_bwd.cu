@@ -1033,7 +1033,10 @@ static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
 
 template <bool kDirect, int D, class TIn>
 static cudaError_t run_all(const Geo& g, const BwdPtrs& p, const BwdTPtrs& t, int dtype, cudaStream_t s,
-                           long long& launches) {
+                           long long& launches, const BwdHook* hook) {
+    auto halo = [&](int kind, float* vec) {  // let the caller complete the vector's halo (sequence sharding)
+        if (hook && hook->fn) hook->fn(hook->user, kind, vec, kind == 0 ? hook->nq : hook->nk, (void*)s);
+    };
     BT<TIn> a;
     a.S2 = p.S2;
     a.S2T = t.S2T;
@@ -1081,12 +1084,16 @@ static cudaError_t run_all(const Geo& g, const BwdPtrs& p, const BwdTPtrs& t, in
         ST_DUST(1);
     } else {  // C1 first, then R1 + R2 in one sweep
         ST_RUN(C1);
+        halo(1, a.g_v);
         ST_RUN(R12);
+        halo(0, a.u2b);
     }
     ST_RUN(C3);
     ST_DUST(2);
+    halo(1, a.v1b);
     ST_RUN(R4);
     ST_DUST(3);
+    halo(0, a.u1b);
     a.fuse_c5 = g.dustbin ? 0 : 1;  // the C5 sweep rides in C6 (same tiles and window vectors)
     if (!a.fuse_c5) {
         ST_RUN(C5);
@@ -1126,7 +1133,7 @@ cudaError_t launch_output_tile(const Geo& g, int dtype, const float* S2, const f
 }
 
 cudaError_t launch_backward_tile(const Geo& g, int dtype, const BwdPtrs& p, const BwdTPtrs& t, bool direct,
-                                 cudaStream_t s, long long& launches) {
+                                 cudaStream_t s, long long& launches, const BwdHook* hook) {
     if (g.dustbin) {
         const long n = (long)g.BH * (g.Lq + g.Lk);
         if (dtype == 0) k_dust_dots<float><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, (const float*)p.dO, (const float*)p.V, t.Zd, t.ZdT);
@@ -1134,10 +1141,10 @@ cudaError_t launch_backward_tile(const Geo& g, int dtype, const BwdPtrs& p, cons
         ++launches;
     }
 #define ST_DISPATCH(D)                                                                                 \
-    if (dtype == 0) return direct ? run_all<true, D, float>(g, p, t, dtype, s, launches)               \
-                                  : run_all<false, D, float>(g, p, t, dtype, s, launches);            \
-    return direct ? run_all<true, D, __nv_bfloat16>(g, p, t, dtype, s, launches)                      \
-                  : run_all<false, D, __nv_bfloat16>(g, p, t, dtype, s, launches);
+    if (dtype == 0) return direct ? run_all<true, D, float>(g, p, t, dtype, s, launches, hook)         \
+                                  : run_all<false, D, float>(g, p, t, dtype, s, launches, hook);      \
+    return direct ? run_all<true, D, __nv_bfloat16>(g, p, t, dtype, s, launches, hook)                \
+                  : run_all<false, D, __nv_bfloat16>(g, p, t, dtype, s, launches, hook);
     if (g.d == 32) { ST_DISPATCH(32) }
     if (g.d == 64) { ST_DISPATCH(64) }
     ST_DISPATCH(128)

@@ -984,10 +984,11 @@ __global__ void __launch_bounds__(256) k_bwd_col(Geo g, BwdArgs<TIn> a, int last
 }
 
 // d_eps[bh] = -(1/eps) * sum_i deps_part[bh][i]  (fixed-order reduction)
-__global__ void __launch_bounds__(256) k_deps_reduce(Geo g, const float* __restrict__ part, float* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_deps_reduce(Geo g, const float* __restrict__ part, float* __restrict__ out,
+                                                     int i_begin, int i_end) {
     const int bh = blockIdx.x;
     double s = 0.0;
-    for (int i = threadIdx.x; i < g.Lrq; i += blockDim.x) s += (double)part[(size_t)bh * g.Lrq + i];
+    for (int i = i_begin + threadIdx.x; i < i_end; i += blockDim.x) s += (double)part[(size_t)bh * g.Lrq + i];
     __shared__ double ss[256];
     ss[threadIdx.x] = s;
     __syncthreads();
@@ -1327,8 +1328,9 @@ cudaError_t launch_backward(const Geo& g, int dtype, const BwdPtrs& p, bool dire
     return dtype == 0 ? run_backward_t<float>(g, p, direct, s) : run_backward_t<__nv_bfloat16>(g, p, direct, s);
 }
 
-cudaError_t launch_deps_reduce(const Geo& g, const float* part, float* out, cudaStream_t s) {
-    k_deps_reduce<<<g.BH, 256, 0, s>>>(g, part, out);
+cudaError_t launch_deps_reduce(const Geo& g, const float* part, float* out, cudaStream_t s, int i_begin, int i_end) {
+    if (i_end < 0) i_end = g.Lrq;
+    k_deps_reduce<<<g.BH, 256, 0, s>>>(g, part, out, i_begin, i_end);
     ++g_launches;
     return cudaGetLastError();
 }

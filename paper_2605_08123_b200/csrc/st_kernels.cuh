@@ -64,8 +64,15 @@ long long launch_count(bool reset);
 void add_launches(long long n);
 size_t bwdT_smem_bytes(const Geo& g);
 bool bwdT_supported(const Geo& g);
+// host hook after each adjoint sweep that produces a vector the neighbours' sweeps read
+// (sequence sharding, st_backward_halo): kind 0 = row vector [BH][Lrq], 1 = column vector [BH][Lrk]
+struct BwdHook {
+    void (*fn)(void* user, int32_t kind, float* vec, int64_t len, void* stream);
+    void* user;
+    int64_t nq, nk;  // vector lengths
+};
 cudaError_t launch_backward_tile(const Geo& g, int dtype, const BwdPtrs& p, const BwdTPtrs& t, bool direct,
-                                 cudaStream_t s, long long& launches);
+                                 cudaStream_t s, long long& launches, const BwdHook* hook = nullptr);
 cudaError_t launch_output_tile(const Geo& g, int dtype, const float* S2, const float* u, const float* v, const void* V,
                                float* O, cudaStream_t s);
 // the dustbin row / column of one backward stage through the generic sweeps
@@ -89,7 +96,8 @@ cudaError_t launch_output(const Geo& g, int dtype, const float* S2, const float*
                           float* O, cudaStream_t s, int last_only = 0);
 cudaError_t launch_gauges(const Geo& g, const float* u_slots, int nslots, float* gauge, cudaStream_t s);
 cudaError_t launch_backward(const Geo& g, int dtype, const BwdPtrs& p, bool direct, cudaStream_t s);
-cudaError_t launch_deps_reduce(const Geo& g, const float* part, float* out, cudaStream_t s);
+cudaError_t launch_deps_reduce(const Geo& g, const float* part, float* out, cudaStream_t s, int i_begin = 0,
+                               int i_end = -1);
 cudaError_t launch_scale(const float* src, float* dst, long n, float sc, cudaStream_t s);
 
 }  // namespace st

@@ -145,3 +145,129 @@ def exchange(plan: SeqShard, to_left: Optional[torch.Tensor], to_right: Optional
         for req in dist.batch_isend_irecv(ops):
             req.wait()
     return got_l, got_r
+
+
+# --------------------------------------------------------------------------- device path
+# A rank runs the band operator on its local problem = own rows plus a w-wide halo each side
+# (SeqShard.window), through st_forward_halo / st_backward_halo.  The library calls back right
+# after it has enqueued each kernel whose output vector the next kernel reads across the shard
+# edge; the callback completes that vector's halo entries on the same stream.
+
+def _halo_slices(plan: SeqShard):
+    """(left halo width, right halo width, own [lo, hi) in local indices)."""
+    hl = plan.rows.start - plan.window.start
+    hr = plan.window.stop - plan.rows.stop
+    return hl, hr, hl, hl + len(plan.rows)
+
+
+def nccl_halo(plan: SeqShard, group=None):
+    """Halo completion over torch.distributed point-to-point (NCCL over NVLink for CUDA tensors).
+    The ops are stream-ordered after the producing kernel; nothing synchronises the host."""
+    hl, hr, lo, hi = _halo_slices(plan)
+    left, right = plan.neighbour(-1), plan.neighbour(+1)
+
+    def ex(v: torch.Tensor) -> None:  # v: [BH, L'] view of the produced vector
+        to_l = v[:, lo: lo + (left.window.stop - left.rows.stop)].contiguous() if left else None
+        to_r = v[:, hi - (right.rows.start - right.window.start): hi].contiguous() if right else None
+        like_l = v.new_empty((v.shape[0], hl)) if left else None
+        like_r = v.new_empty((v.shape[0], hr)) if right else None
+        got_l, got_r = exchange(plan, to_l, to_r, like_l, like_r, group)
+        if left:
+            v[:, :hl].copy_(got_l)
+        if right:
+            v[:, hi: hi + hr].copy_(got_r)
+    return ex
+
+
+class Lockstep:
+    """Single-GPU emulation of the sequence-sharded run: one host thread per shard, each on its own
+    CUDA stream; at every hook the shards meet at a barrier and copy each other's boundary entries
+    (stream-ordered by events -- no kernel ever waits on another).  Test harness for the protocol
+    nccl_halo runs across GPUs."""
+
+    def __init__(self, plans, streams):
+        import threading
+        self.plans, self.streams = plans, streams
+        self.barrier = threading.Barrier(len(plans))
+        self.views = [None] * len(plans)
+        self.ready = [torch.cuda.Event() for _ in plans]
+        self.copied = [torch.cuda.Event() for _ in plans]
+
+    def exchange_for(self, r: int):
+        plan = self.plans[r]
+        hl, hr, lo, hi = _halo_slices(plan)
+
+        def ex(v: torch.Tensor) -> None:
+            s = self.streams[r]
+            self.views[r] = v
+            self.ready[r].record(s)
+            self.barrier.wait()
+            nbs = [q for q in (r - 1, r + 1) if 0 <= q < len(self.plans)]
+            with torch.cuda.stream(s):
+                for q in nbs:
+                    s.wait_event(self.ready[q])
+                    o = self.plans[q]
+                    vo = self.views[q]
+                    _, ohr, olo, ohi = _halo_slices(o)
+                    if q < r:  # its last hl own entries -> my left halo
+                        v[:, :hl].copy_(vo[:, ohi - hl: ohi])
+                    else:      # its first hr own entries -> my right halo
+                        v[:, hi: hi + hr].copy_(vo[:, olo: olo + hr])
+                self.copied[r].record(s)
+            self.barrier.wait()
+            for q in nbs:  # the neighbour read my vector: its copy precedes my next write of it
+                s.wait_event(self.copied[q])
+            self.barrier.wait()
+        return ex
+
+
+class _Hook:
+    """ctypes st_halo_fn that maps the library's vector back to a [BH, L'] float view."""
+
+    def __init__(self, bh: int, buffers, ex):
+        self.bh, self.buffers, self.ex = bh, buffers, ex
+        self.error = None
+        from . import _lib
+        self.cfn = _lib.HALO_FN(self)
+
+    def __call__(self, user, kind, vec, n, stream):
+        try:
+            for t in self.buffers:
+                base, nbytes = t.data_ptr(), t.numel() * t.element_size()
+                if base <= vec < base + nbytes:
+                    off = (vec - base) // 4
+                    flat = t.view(-1).view(torch.uint8)[: (nbytes // 4) * 4].view(torch.float32)
+                    self.ex(flat[off: off + n].view(self.bh, -1))
+                    return
+            raise RuntimeError("halo vector outside the registered buffers")
+        except Exception as e:  # never raise through C
+            self.error = e
+
+
+def sharded_forward_backward(spec, Q, K, V, G, row_mask, col_mask, ex, own_rows: range, mode="one_reference"):
+    """One rank's sequence-sharded fwd + bwd on its local problem (own rows + halos).
+    Returns (O, dQ, dK, dV, d_eps) of the local problem; rows outside `own_rows` are unspecified
+    and d_eps covers the own rows only (sum it over ranks)."""
+    import ctypes
+    from . import _lib
+    from .band import _check, _ptr
+    lib = _lib.lib
+    dev = Q.device
+    ws = torch.empty(max(spec.workspace_bytes(), 256), dtype=torch.uint8, device=dev)
+    saved = torch.empty(spec.saved_bytes(), dtype=torch.uint8, device=dev)
+    O = torch.empty((spec.batch, spec.heads, spec.rows, spec.head_dim), dtype=torch.float32, device=dev)
+    dQ, dK, dV = (torch.empty_like(O) for _ in range(3))
+    d_eps = torch.empty(spec.batch * spec.heads, dtype=torch.float32, device=dev)
+    eta = torch.empty((spec.batch, spec.heads, spec.cols), dtype=torch.float32, device=dev)
+    hook = _Hook(spec.batch * spec.heads, [ws, saved], ex)
+    d = spec.desc()
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    _check(lib.st_forward_halo(ctypes.byref(d), _ptr(Q), _ptr(K), _ptr(V), _ptr(row_mask), _ptr(col_mask), _ptr(O),
+                               _ptr(saved), _ptr(ws), ws.numel(), stream, hook.cfn, None))
+    m = {"one_reference": _lib.ST_ONE_REFERENCE, "direct_four_plan": _lib.ST_DIRECT_FOUR_PLAN}[mode]
+    _check(lib.st_backward_halo(ctypes.byref(d), _ptr(saved), _ptr(Q), _ptr(K), _ptr(V), _ptr(G), _ptr(row_mask),
+                                _ptr(col_mask), _ptr(dQ), _ptr(dK), _ptr(dV), _ptr(d_eps), _ptr(eta), m, _ptr(ws),
+                                ws.numel(), stream, hook.cfn, None, own_rows.start, own_rows.stop))
+    if hook.error is not None:
+        raise hook.error
+    return O, dQ, dK, dV, d_eps

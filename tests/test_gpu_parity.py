@@ -284,3 +284,65 @@ def test_rectangular_parity(Lq, Lk, d, w, masked):
         e, fl = rel(g[k], r[k].reshape(nh, -1)), rel(r32[k].reshape(nh, -1), r[k].reshape(nh, -1))
         tol = DEPS_TOL if k == "d_eps" else FP32_TOL
         assert e <= max(tol, (3.0 if k == "d_eps" else 1.5) * fl), (k, e, fl)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_sequence_sharded_lockstep_matches_unsharded(dtype):
+    """Config-5 style sequence sharding on one GPU: two shards (own rows + w-wide halos) run the
+    per-step kernels in lockstep host threads with the halo hook completing every dual / adjoint
+    vector (shard.Lockstep, the protocol nccl_halo runs across GPUs); own rows / columns and the
+    summed d_eps equal the unsharded run on the same kernels."""
+    import threading
+    from paper_2605_08123_b200 import shard
+    B, H, L, d, w, eps, T, R = 1, 2, 1024, 64, 64, 0.1, 8, 2
+    rng = np.random.default_rng(11)
+    mk = lambda: rng.standard_normal((B, H, L, d)).astype(np.float32) / np.sqrt(d)
+    Qh, Kh, Vh, Gh = mk(), mk(), mk(), mk()
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    to = lambda x: torch.from_numpy(x).cuda().to(tdt).contiguous()
+    spec = lambda n: band.BandSpec(batch=B, heads=H, seq_q=n, seq_k=n, head_dim=d, half_band=w, base_depth=T,
+                                   tail_depth=R, epsilon=eps, dtype=dtype)
+    # unsharded, same per-step kernels (a no-op hook selects them)
+    ref = shard.sharded_forward_backward(spec(L), to(Qh), to(Kh), to(Vh), to(Gh), None, None,
+                                         lambda v: None, range(0, L))
+    plans = [shard.SeqShard(L=L, w=w, world=2, rank=r) for r in range(2)]
+    streams = [torch.cuda.Stream() for _ in plans]
+    ls = shard.Lockstep(plans, streams)
+    outs, errs = [None, None], []
+
+    def run(r):
+        try:
+            p = plans[r]
+            win = slice(p.window.start, p.window.stop)
+            hl = p.rows.start - p.window.start
+            with torch.cuda.stream(streams[r]):
+                args = [to(x[:, :, win]) for x in (Qh, Kh, Vh, Gh)]
+                outs[r] = shard.sharded_forward_backward(spec(len(p.window)), *args, None, None, ls.exchange_for(r),
+                                                         range(hl, hl + len(p.rows)))
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+            ls.barrier.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(300)
+    assert not errs, errs
+    torch.cuda.synchronize()
+    for k in range(4):  # O, dQ (own rows), dK, dV (own columns)
+        got = torch.empty_like(ref[k])
+        for r, p in enumerate(plans):
+            hl = p.rows.start - p.window.start
+            got[:, :, p.rows.start:p.rows.stop] = outs[r][k][:, :, hl:hl + len(p.rows)]
+        assert rel(got.cpu().numpy(), ref[k].cpu().numpy()) < 1e-6, k
+    deps = sum(o[4] for o in outs)
+    assert rel(deps.cpu().numpy(), ref[4].cpu().numpy()) < 1e-5
+    # negative control: without the halo exchange the shards' edge rows are wrong
+    p = plans[0]
+    hl = p.rows.start - p.window.start
+    alone = shard.sharded_forward_backward(spec(len(p.window)), *[to(x[:, :, p.window.start:p.window.stop])
+                                                                for x in (Qh, Kh, Vh, Gh)],
+                                           None, None, lambda v: None, range(hl, hl + len(p.rows)))
+    edge = slice(p.rows.stop - w, p.rows.stop)
+    assert rel(alone[0][:, :, edge].cpu().numpy(), ref[0][:, :, edge].cpu().numpy()) > 1e-4
