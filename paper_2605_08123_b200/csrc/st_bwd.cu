@@ -1099,9 +1099,29 @@ static cudaError_t run_all(const Geo& g, const BwdPtrs& p, const BwdTPtrs& t, in
         ST_RUN(C5);
         ST_DUST(4);
     }
-    ST_RUN(R6);
-    ST_RUN(C6);
-    ST_DUST(5);
+    if (!g.dustbin && !getenv("ST_NO_FORK")) {
+        // R6 (dQ, d_eps) and C6 (dK, v0b) read the same finished vectors and write disjoint outputs:
+        // run them on two streams so each fills the other's partial last wave (event fork / join,
+        // captured as graph dependencies)
+        static thread_local cudaStream_t side = nullptr;
+        static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+        if (!side) {
+            cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+            cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
+        }
+        if ((e = cudaEventRecord(ev_fork, s)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(side, ev_fork, 0)) != cudaSuccess) return e;
+        if ((e = run_op<C6, kDirect, D, TIn>(g, a, side)) != cudaSuccess) return e;
+        ++launches;
+        ST_RUN(R6);
+        if ((e = cudaEventRecord(ev_join, side)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(s, ev_join, 0)) != cudaSuccess) return e;
+    } else {
+        ST_RUN(R6);
+        ST_RUN(C6);
+        ST_DUST(5);
+    }
 #undef ST_RUN
 #undef ST_DUST
     return cudaSuccess;
