@@ -24,6 +24,7 @@
 // Offsets: cold start uses an online running max; every later step uses the
 // previous dual of the same row (terms <= 1, sums in [1/W, W]).
 #include <cstdio>
+#include <cstdlib>
 
 #include "st_common.cuh"
 #include "st_phase.cuh"
@@ -39,7 +40,7 @@ struct Smem {
     uint8_t* A;       // [NA][npl][128 * row_bytes]
     uint8_t* K;       // [NSK][npl][CR * row_bytes]
     float* vwin;      // [2][maxwin]
-    float* part;      // [256] partial (sum, max) of the second column half
+    float* part;      // [3][256] partial (sum, max) of the column parts 1..3
     uint64_t* a_full;
     uint64_t* a_empty;
     uint64_t* k_full;
@@ -56,7 +57,7 @@ __device__ __forceinline__ Smem carve(uint8_t* base, const PhaseArgs& a, int nst
     s.K = s.A + (size_t)a.NA * a.npl * blk;
     s.vwin = (float*)(s.K + (size_t)a.NSK * a.npl * chk);
     s.part = s.vwin + 2 * a.maxwin;
-    uint64_t* bars = (uint64_t*)(s.part + 256);
+    uint64_t* bars = (uint64_t*)(s.part + 768);
     s.a_full = bars;
     s.a_empty = bars + 2;
     s.k_full = bars + 4;
@@ -104,8 +105,10 @@ __device__ __forceinline__ float window_dual(const PhaseArgs& a, int bh, int j) 
 
 }  // namespace
 
-template <int kNPL, int kCR, bool kFirst>
-__global__ void __launch_bounds__(320, 1) k_phase(PhaseArgs a) {
+template <int kNPL, int kCR, bool kFirst, int kEW>
+__global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
+    constexpr int kParts = kEW / 4;         // epilogue warps per TMEM lane quadrant (column parts)
+    constexpr int NE = 32 * kEW;            // epilogue threads
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     constexpr int NST = 512 / kCR;  // TMEM accumulator slots
     const Smem s = carve(smem_raw, a, NST);
@@ -123,7 +126,7 @@ __global__ void __launch_bounds__(320, 1) k_phase(PhaseArgs a) {
         }
         for (int k = 0; k < NST; ++k) {
             mbar_init(&s.t_full[k], 1);
-            mbar_init(&s.t_empty[k], 8);
+            mbar_init(&s.t_empty[k], kEW);
         }
         fence_mbar_init();
     }
@@ -265,27 +268,28 @@ __global__ void __launch_bounds__(320, 1) k_phase(PhaseArgs a) {
             rel_seq = max(rel_seq, keep_from);
         }
     } else {
-        // ------------------------------------------------------------ epilogue (warps 2..9)
-        constexpr int HC = kCR / 2;               // columns per warp per chunk
-        const int ew = warp - 2;                  // 0..7
+        // ------------------------------------------------------------ epilogue (warps 2 .. 2 + kEW)
+        constexpr int HC = kCR / kParts;          // columns per warp per chunk
+        static_assert(HC % 32 == 0, "32-column TMEM loads");
+        const int ew = warp - 2;                  // 0 .. kEW-1
         const int qd = warp & 3;                  // TMEM lane quadrant (warp_id % 4)
-        const int half = ew >> 2;
+        const int half = ew >> 2;                 // column part 0 .. kParts-1
         const int r = qd * 32 + lane;             // row inside the 128-row block
-        const int et = threadIdx.x - 64;          // 0..255
+        const int et = threadIdx.x - 64;          // 0 .. NE-1
         uint32_t tseq = 0;
         if (g_begin < g_end) {  // window duals of the first block (later ones are prefetched)
             const Blk b = block_of(a, a.work[g_begin]);
             const int wbase = b.q0 * kCR - a.shift, nwin = (b.q1 - b.q0 + 1) * kCR;
-            for (int c = et; c < nwin; c += 256) s.vwin[c] = window_dual(a, b.bh, wbase + c);
+            for (int c = et; c < nwin; c += NE) s.vwin[c] = window_dual(a, b.bh, wbase + c);
         }
         for (int gi = g_begin; gi < g_end; ++gi) {
             const Blk b = block_of(a, a.work[gi]);
             const float* vw = s.vwin + ((gi - g_begin) & 1) * a.maxwin;
             const int wbase = b.q0 * kCR - a.shift;   // original column of window column 0
-            named_bar(1, 256);  // vw complete; previous block fully consumed
+            named_bar(1, NE);  // vw complete; previous block fully consumed
             if (et == 0) ST_TRACE(25 + min(gi - g_begin, 7));
             // prefetch the next block's window duals into registers (parked in SMEM after this block)
-            constexpr int kPre = 4;
+            constexpr int kPre = 1024 / NE;
             float pre[kPre];
             Blk nb{};
             const bool has_next = gi + 1 < g_end;
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(320, 1) k_phase(PhaseArgs a) {
                 nwin_next = (nb.q1 - nb.q0 + 1) * kCR;
 #pragma unroll
                 for (int k = 0; k < kPre; ++k) {
-                    const int c = et + 256 * k;
+                    const int c = et + NE * k;
                     pre[k] = (c < nwin_next) ? window_dual(a, nb.bh, nb.q0 * kCR - a.shift + c) : -INFINITY;
                 }
             }
@@ -368,27 +372,31 @@ __global__ void __launch_bounds__(320, 1) k_phase(PhaseArgs a) {
                 float* nvw = s.vwin + ((gi + 1 - g_begin) & 1) * a.maxwin;
 #pragma unroll
                 for (int k = 0; k < kPre; ++k)
-                    if (et + 256 * k < nwin_next) nvw[et + 256 * k] = pre[k];
-                for (int c = et + 256 * kPre; c < nwin_next; c += 256)
+                    if (et + NE * k < nwin_next) nvw[et + NE * k] = pre[k];
+                for (int c = et + NE * kPre; c < nwin_next; c += NE)
                     nvw[c] = window_dual(a, nb.bh, nb.q0 * kCR - a.shift + c);
             }
             if (et == 0) ST_TRACE(33 + min(gi - g_begin, 7));
-            // combine the two column halves of every row
-            if (half == 1) {
-                s.part[r] = acc_s;
-                s.part[128 + r] = M;
+            // combine the column parts of every row (fixed order 0, 1, .., kParts-1)
+            if (half > 0) {
+                s.part[(half - 1) * 256 + r] = acc_s;
+                s.part[(half - 1) * 256 + 128 + r] = M;
             }
-            named_bar(2, 256);
+            named_bar(2, NE);
             if (half == 0 && i < a.L_own) {
-                const float s1 = s.part[r];
                 float u = 0.f;
-                if (kFirst) {
-                    const float M1 = s.part[128 + r];
-                    const float Mx = fmaxf(M, M1);
-                    acc_s = (M == -INFINITY ? 0.f : acc_s * ex2(M - Mx)) + (M1 == -INFINITY ? 0.f : s1 * ex2(M1 - Mx));
-                    M = Mx;
-                } else {
-                    acc_s += s1;
+#pragma unroll
+                for (int pp = 1; pp < kParts; ++pp) {
+                    const float s1 = s.part[(pp - 1) * 256 + r];
+                    if (kFirst) {
+                        const float M1 = s.part[(pp - 1) * 256 + 128 + r];
+                        const float Mx = fmaxf(M, M1);
+                        acc_s = (M == -INFINITY ? 0.f : acc_s * ex2(M - Mx)) +
+                                (M1 == -INFINITY ? 0.f : s1 * ex2(M1 - Mx));
+                        M = Mx;
+                    } else {
+                        acc_s += s1;
+                    }
                 }
                 if (active) {
                     if (a.dustbin) {  // the spoke cell (i, dustbin) with constant score sd2
@@ -576,23 +584,30 @@ long long phase_launch_count(bool reset) {
 size_t phase_smem_bytes(const PhaseArgs& a) {
     const int nst = 512 / a.CR;
     return (size_t)a.NA * a.npl * 128 * a.row_bytes + (size_t)a.NSK * a.npl * a.CR * a.row_bytes +
-           (size_t)(2 * a.maxwin + 256) * 4 + (size_t)(4 + 2 * a.NSK + 2 * nst) * 8 + 16;
+           (size_t)(2 * a.maxwin + 768) * 4 + (size_t)(4 + 2 * a.NSK + 2 * nst) * 8 + 16;
 }
 
-template <int kNPL, int kCR>
+template <int kNPL, int kCR, int kEW>
 static cudaError_t launch_phase_t(const PhaseArgs& a, bool first, int grid, cudaStream_t s) {
     const size_t smem = phase_smem_bytes(a);
-    auto k = first ? k_phase<kNPL, kCR, true> : k_phase<kNPL, kCR, false>;
+    auto k = first ? k_phase<kNPL, kCR, true, kEW> : k_phase<kNPL, kCR, false, kEW>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k<<<grid, 320, smem, s>>>(a);
+    k<<<grid, 64 + 32 * kEW, smem, s>>>(a);
     ++g_phase_launches;
     return cudaGetLastError();
 }
 
 cudaError_t launch_phase(const PhaseArgs& a, bool first, int grid, cudaStream_t s) {
-    if (a.npl == 1) return a.CR == 128 ? launch_phase_t<1, 128>(a, first, grid, s) : launch_phase_t<1, 64>(a, first, grid, s);
-    return a.CR == 128 ? launch_phase_t<3, 128>(a, first, grid, s) : launch_phase_t<3, 64>(a, first, grid, s);
+    // 128-column chunks: 16 epilogue warps (4 per TMEM lane quadrant, 32 columns each) hide the
+    // tcgen05.ld -> MUFU latency; 64-column chunks keep 8 (2 per quadrant)
+    static const int ew = getenv("ST_PHASE_EW") ? atoi(getenv("ST_PHASE_EW")) : 16;
+    if (a.npl == 1) {
+        if (a.CR == 128) return ew == 8 ? launch_phase_t<1, 128, 8>(a, first, grid, s) : launch_phase_t<1, 128, 16>(a, first, grid, s);
+        return launch_phase_t<1, 64, 8>(a, first, grid, s);
+    }
+    if (a.CR == 128) return ew == 8 ? launch_phase_t<3, 128, 8>(a, first, grid, s) : launch_phase_t<3, 128, 16>(a, first, grid, s);
+    return launch_phase_t<3, 64, 8>(a, first, grid, s);
 }
 
 cudaError_t launch_dustbin(const DustArgs& a, bool first, int BH, cudaStream_t s) {
