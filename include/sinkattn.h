@@ -54,7 +54,9 @@ typedef enum st_dtype { ST_F32 = 0, ST_BF16 = 1 } st_dtype;
 
 typedef enum st_backward_mode {
     ST_ONE_REFERENCE = 0,    /* BackwardMode::OneReference (adjoint.hpp:255-310) */
-    ST_DIRECT_FOUR_PLAN = 1  /* BackwardMode::DirectFourPlan (adjoint.hpp:311-368), ablation */
+    ST_DIRECT_FOUR_PLAN = 1, /* BackwardMode::DirectFourPlan (adjoint.hpp:311-368), ablation */
+    ST_GENERIC_TAIL = 2      /* tail_adjoint_generic (adjoint.hpp:132-200): any tail depth R <= 8,
+                                materialised score cotangent; no dustbin, d in {32, 64, 128} */
 } st_backward_mode;
 
 typedef struct st_desc {
@@ -65,7 +67,7 @@ typedef struct st_desc {
     int64_t head_dim;     /* d */
     int64_t half_band;    /* reference W: (i, j) active iff |i - j| <= half_band (support.hpp:20-23) */
     int64_t base_depth;   /* T: stopped base steps from the cold start u = v = 0 */
-    int64_t tail_depth;   /* R: differentiable tail steps (backward requires 2) */
+    int64_t tail_depth;   /* R: differentiable tail steps (r2_backward modes require 2) */
     double epsilon;       /* entropic temperature, > 0 */
     int32_t dtype;        /* st_dtype of Q, K, V, dO (outputs and gradients are always f32) */
     int32_t dustbin;      /* 0, or 1 = one active dustbin token per side on the spoke support */
@@ -108,7 +110,8 @@ st_status st_forward(const st_desc* desc, const void* Q, const void* K, const vo
                      const uint8_t* row_mask, const uint8_t* col_mask, float* O, void* saved,
                      void* workspace, size_t workspace_bytes, void* stream);
 
-/* Backward = r2_backward: dQ, dK, dV (f32, [B, H, L', d]), d_eps ([B*H] f32,
+/* Backward = r2_backward (modes ST_ONE_REFERENCE / ST_DIRECT_FOUR_PLAN, tail_depth 2) or
+ * tail_adjoint_generic (mode ST_GENERIC_TAIL, any tail_depth <= 8): dQ, dK, dV (f32, [B, H, L', d]), d_eps ([B*H] f32,
  * dL/d(epsilon) per head, may be NULL) and eta_v (the base cotangent v-bar^(0),
  * [B, H, L'_k] f32, may be NULL).  dO is the output cotangent G in desc->dtype. */
 st_status st_backward(const st_desc* desc, const void* saved, const void* Q, const void* K,

@@ -105,9 +105,12 @@ void run_head(const BatchArgs& a, std::int64_t bh) {
         }
     }
     if (a.dQ == nullptr) return;  // forward only
-    CotangentSet<T> c =
-        r2_backward<T>(run.scaled, run.trace, G, Q, K, V,
-                       a.mode == 1 ? BackwardMode::DirectFourPlan : BackwardMode::OneReference, pc);
+    // mode 0 / 1: r2_backward (OneReference / DirectFourPlan); mode 2: tail_adjoint_generic (any R)
+    CotangentSet<T> c = (a.mode == 2)
+                            ? tail_adjoint_generic<T>(run.scaled, run.trace, G, Q, K, V, pc)
+                            : r2_backward<T>(run.scaled, run.trace, G, Q, K, V,
+                                             a.mode == 1 ? BackwardMode::DirectFourPlan : BackwardMode::OneReference,
+                                             pc);
     for (size_t k = 0; k < c.grad_q.a.size(); ++k) a.dQ[off + k] = static_cast<double>(c.grad_q.a[k]);
     for (size_t k = 0; k < c.grad_k.a.size(); ++k) {
         a.dK[offk + k] = static_cast<double>(c.grad_k.a[k]);

@@ -31,6 +31,7 @@ ST_FLAG_REUSE_BAND = 2
 ST_MAX_STAGES = 8
 ST_ONE_REFERENCE = 0
 ST_DIRECT_FOUR_PLAN = 1
+ST_GENERIC_TAIL = 2
 
 # every symbol include/sinkattn.h declares
 EXPORTED = (

@@ -237,9 +237,25 @@ def r2_backward(run: SurrogateRun, G: torch.Tensor, mode: str = "one_reference",
                 grads: Optional[tuple] = None, d_eps: Optional[torch.Tensor] = None,
                 eta_v: Optional[torch.Tensor] = None, workspace: Optional[Workspace] = None) -> CotangentSet:
     """Exact R=2 adjoint (adjoint.hpp:232-373); mode "one_reference" or "direct_four_plan"."""
-    spec = run.spec
-    if spec.tail_depth != 2:
+    if run.spec.tail_depth != 2:
         raise UnsupportedDepth("r2_backward requires a tail of depth 2")
+    m = {"one_reference": _lib.ST_ONE_REFERENCE, "direct_four_plan": _lib.ST_DIRECT_FOUR_PLAN}[mode]
+    return _backward(run, G, m, grads, d_eps, eta_v, workspace)
+
+
+def tail_adjoint(run: SurrogateRun, G: torch.Tensor, *, grads: Optional[tuple] = None,
+                 d_eps: Optional[torch.Tensor] = None, eta_v: Optional[torch.Tensor] = None,
+                 workspace: Optional[Workspace] = None) -> CotangentSet:
+    """Exact reverse pass of the tail for any depth R <= 8 (tail_adjoint_generic, adjoint.hpp:132-200):
+    the score cotangent is materialised as a band, then contracted to dQ / dK / d_eps.
+    eta_v = v-bar^(0) (the base-trace cotangent; dO-weighted column sums when R = 0)."""
+    if not 0 <= run.spec.tail_depth <= 8:
+        raise UnsupportedDepth("the generic tail adjoint supports tail depths 0..8")
+    return _backward(run, G, _lib.ST_GENERIC_TAIL, grads, d_eps, eta_v, workspace)
+
+
+def _backward(run, G, m, grads, d_eps, eta_v, workspace) -> CotangentSet:
+    spec = run.spec
     _check_tensor("G", G, spec, spec.rows)
     dev = G.device
     if grads is None:
@@ -250,7 +266,6 @@ def r2_backward(run: SurrogateRun, G: torch.Tensor, mode: str = "one_reference",
         d_eps = torch.empty(spec.batch * spec.heads, dtype=torch.float32, device=dev)
     if eta_v is None:
         eta_v = torch.empty((spec.batch, spec.heads, spec.cols), dtype=torch.float32, device=dev)
-    m = {"one_reference": _lib.ST_ONE_REFERENCE, "direct_four_plan": _lib.ST_DIRECT_FOUR_PLAN}[mode]
     wso = workspace or _default_ws
     ws = wso.get(spec.workspace_bytes(), dev)
     d = spec.desc()

@@ -34,6 +34,7 @@ inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 struct Dims {
     long BH, Lq, Lk, Lrq, Lrk, d, w, Wf;
     int esz = 4, dustbin = 0;  // input element bytes, dustbin flag
+    long R = 2;                // tail depth
 };
 
 st_status check_desc(const st_desc* d, Dims& o) {
@@ -72,6 +73,7 @@ st_status check_desc(const st_desc* d, Dims& o) {
     o.Wf = 2 * o.w + 1;
     o.esz = d->dtype == ST_BF16 ? 2 : 4;
     o.dustbin = d->dustbin;
+    o.R = d->tail_depth;
     if ((double)o.BH * o.Lq * o.Wf > 4.0e9 || o.Lrq > (1L << 30) || o.Lrk > (1L << 30))
         return fail(ST_SIZE_CAP_EXCEEDED, "problem exceeds the 32-bit index space of the kernels");
     return ST_OK;
@@ -102,15 +104,19 @@ st::Geo make_geo(const st_desc* d, const Dims& m, const uint8_t* rm, const uint8
     return g;
 }
 
-// saved-state layout (fp32, base-2 raw duals): u[3][BH][Lrq] | v[3][BH][Lrk] | gauge[3][BH] | status int
+// saved-state layout (fp32, base-2 raw duals): u[NS][BH][Lrq] | v[NS][BH][Lrk] | gauge[3][BH] | status int
+// with NS = max(3, R + 1) tail slots (steps T .. T+R; the generic-R adjoint reads all of them)
+constexpr long kMaxTail = 8;
 struct SavedLayout {
     size_t u, v, gauge, status, bytes;
+    long ns;
 };
 SavedLayout saved_layout(const Dims& m) {
     SavedLayout s;
+    s.ns = std::max<long>(3, m.R + 1);
     s.u = 0;
-    s.v = align_up(s.u + sizeof(float) * 3 * m.BH * m.Lrq);
-    s.gauge = align_up(s.v + sizeof(float) * 3 * m.BH * m.Lrk);
+    s.v = align_up(s.u + sizeof(float) * s.ns * m.BH * m.Lrq);
+    s.gauge = align_up(s.v + sizeof(float) * s.ns * m.BH * m.Lrk);
     s.status = align_up(s.gauge + sizeof(float) * 3 * m.BH);
     s.bytes = align_up(s.status + sizeof(int));
     return s;
@@ -169,6 +175,7 @@ struct WsLayout {
     size_t qp[3], kp[3], flags, work_q, work_k, cnt;
     size_t vb2, part[2], partm;  // fused-step ping-pong duals and column partials
     size_t fs_flags, fs_work, fs_cnt, fs_part[2], fs_partm;  // persistent solve: work list, tagged partials
+    size_t tail_u, tail_v;  // generic-R adjoint: (R+1) row / column cotangent vectors
     size_t bytes;
 };
 
@@ -216,6 +223,8 @@ WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
     w.v1b = take(rk);
     w.v0b = take(rk);
     w.err = take(sizeof(int));
+    w.tail_u = take(rq * (size_t)(m.R + 1));
+    w.tail_v = take(rk * (size_t)(m.R + 1));
     for (int p = 0; p < 3; ++p) w.qp[p] = w.kp[p] = 0;
     w.flags = w.work_q = w.work_k = w.cnt = 0;
     w.vb2 = take(rk);
@@ -337,6 +346,7 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
     if (s != ST_OK) return s;
     if (!Q || !K || !V || !O) return fail(ST_INVALID_ARGUMENT, "null tensor pointer");
     if (hook && desc->dustbin) return fail(ST_NOT_SUPPORTED, "sequence sharding of dustbin problems");
+    if (saved && desc->tail_depth > kMaxTail) return fail(ST_NOT_SUPPORTED, "saved state holds at most 8 tail steps");
     // sequence sharding: hand each just-enqueued dual to the caller's halo exchange
     auto halo = [&](int kind, float* vec) {
         if (hook) hook(user, kind, vec, kind == 0 ? m.BH * m.Lrq : m.BH * m.Lrk, stream);
@@ -428,8 +438,8 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
         const int grid = std::min(num_sms(), (int)(m.BH * std::max(tp.NBq, tp.NBk)));
         for (long t = 1; t <= T + R; ++t) {
             const long r = t - T;
-            float* u_out = (sv && r >= 0 && r <= 2) ? slot_u(r) : u_ws;
-            float* v_out = (sv && r >= 0 && r <= 2) ? slot_v(r) : v_ws;
+            float* u_out = (sv && r >= 0 && r < sl.ns) ? slot_u(r) : u_ws;
+            float* v_out = (sv && r >= 0 && r < sl.ns) ? slot_v(r) : v_ws;
             // epsilon stage of this step: the scores are recomputed here, so only their scale changes
             const float lam = step_scale(desc, t);
             pr.c2 = pc.c2 = g.c2 * lam;
@@ -463,9 +473,9 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
             p.S2 = S2;
             p.ubuf = u_ws;
             p.vbuf = v_ws;
-            for (int q = 0; q < 3; ++q) {
-                p.u_slot[q] = (sv && q <= R) ? slot_u(q) : nullptr;
-                p.v_slot[q] = (sv && q <= R) ? slot_v(q) : nullptr;
+            for (int q = 0; q < (int)kMaxTail + 1; ++q) {
+                p.u_slot[q] = (sv && q <= R && q < sl.ns) ? slot_u(q) : nullptr;
+                p.v_slot[q] = (sv && q <= R && q < sl.ns) ? slot_v(q) : nullptr;
             }
             p.part[0] = ws + wl.fs_part[0];
             p.part[1] = ws + wl.fs_part[1];
@@ -505,13 +515,13 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
                     ST_CUDA(st::launch_scores(gs, desc->dtype, Q, K, S2, st));
                     band_lam = lam;
                 }
-                float* u_out = (sv && r >= 0 && r <= 2) ? slot_u(r) : u_ws;
+                float* u_out = (sv && r >= 0 && r < sl.ns) ? slot_u(r) : u_ws;
                 p.u_prev = u_prev;
                 p.u_out = u_out;
                 p.v_pp = (t >= 3) ? vbuf[(t - 2) & 1] : nullptr;
                 p.v_p_out = (t >= 2) ? vbuf[(t - 1) & 1] : nullptr;
                 const long rv = t - 1 - T;
-                p.v_p_slot = (t >= 2 && sv && rv >= 0 && rv <= 2) ? slot_v(rv) : nullptr;
+                p.v_p_slot = (t >= 2 && sv && rv >= 0 && rv < sl.ns) ? slot_v(rv) : nullptr;
                 p.part_in = (t >= 2) ? part[(t - 1) & 1] : nullptr;
                 p.partm_in = partm;
                 p.part_out = part[t & 1];
@@ -522,7 +532,7 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
             const long tl = T + R;
             p.v_pp = (tl >= 2) ? vbuf[(tl - 1) & 1] : nullptr;
             p.v_p_out = vbuf[tl & 1];
-            p.v_p_slot = (sv && R <= 2) ? slot_v(R) : nullptr;
+            p.v_p_slot = (sv && R < sl.ns) ? slot_v(R) : nullptr;
             p.part_in = part[tl & 1];
             p.partm_in = partm;
             ST_CUDA(st::launch_ffinal(g, (int)tl, p, st));
@@ -540,8 +550,8 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
         float band_lam = 1.f;  // temperature scale of the stored band (and its transpose)
         for (long t = 1; t <= T + R; ++t) {
             const long r = t - T;
-            float* u_out = (sv && r >= 0 && r <= 2) ? slot_u(r) : u_ws;
-            float* v_out = (sv && r >= 0 && r <= 2) ? slot_v(r) : v_ws;
+            float* u_out = (sv && r >= 0 && r < sl.ns) ? slot_u(r) : u_ws;
+            float* v_out = (sv && r >= 0 && r < sl.ns) ? slot_v(r) : v_ws;
             const float lam = step_scale(desc, t);
             st::Geo gs = g;  // this step's temperature: scores (band) and the dustbin score
             gs.c2 = g.c2 * lam;
@@ -599,10 +609,17 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
     st_status s = check_desc(desc, m);
     if (s != ST_OK) return s;
     if (hook && desc->dustbin) return fail(ST_NOT_SUPPORTED, "sequence sharding of dustbin problems");
-    if (desc->tail_depth != 2) return fail(ST_UNSUPPORTED_DEPTH, "r2_backward requires a tail of depth 2");
+    if (mode != ST_ONE_REFERENCE && mode != ST_DIRECT_FOUR_PLAN && mode != ST_GENERIC_TAIL)
+        return fail(ST_INVALID_ARGUMENT, "unknown mode");
+    const bool generic_tail = mode == ST_GENERIC_TAIL;
+    if (!generic_tail && desc->tail_depth != 2)
+        return fail(ST_UNSUPPORTED_DEPTH, "r2_backward requires a tail of depth 2");
+    if (generic_tail && desc->tail_depth > kMaxTail)
+        return fail(ST_UNSUPPORTED_DEPTH, "the generic tail adjoint supports at most 8 tail steps");
+    if (generic_tail && (hook || desc->dustbin))
+        return fail(ST_NOT_SUPPORTED, "the generic tail adjoint has no dustbin / sequence-sharded variant");
     if (saved == nullptr) return fail(ST_MISSING_BASE_TRACE, "backward needs the forward's saved state");
     if (!Q || !K || !V || !dO || !dQ || !dK || !dV) return fail(ST_INVALID_ARGUMENT, "null tensor pointer");
-    if (mode != ST_ONE_REFERENCE && mode != ST_DIRECT_FOUR_PLAN) return fail(ST_INVALID_ARGUMENT, "unknown mode");
     const WsLayout wl = ws_layout(m, tc_plan(desc, m));
     if (workspace == nullptr || workspace_bytes < wl.bytes)
         return fail(ST_WORKSPACE_TOO_SMALL, "workspace smaller than st_workspace_bytes()");
@@ -638,6 +655,7 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
                           : 0;
     const bool tiled = st::bwdT_supported(g) && !(desc->flags & ST_FLAG_GENERIC);
     if (hook && !tiled) return fail(ST_NOT_SUPPORTED, "sequence sharding needs the tiled backward (d in {32,64,128})");
+    if (generic_tail && !tiled) return fail(ST_NOT_SUPPORTED, "the generic tail adjoint needs d in {32, 64, 128}");
     const bool dual = tiled && st::band_dual_supported(g);
     bool haveT = reuse == 2;
     if (!reuse) {
@@ -667,9 +685,24 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
             ST_CUDA(st::launch_transpose_band(g, Z, ZT, st, 0.f));
         }
         long long nl = 0;
-        st::BwdHook bh{hook, user, (int64_t)(m.BH * m.Lrq), (int64_t)(m.BH * m.Lrk)};
-        ST_CUDA(st::launch_backward_tile(g, desc->dtype, p, t, mode == ST_DIRECT_FOUR_PLAN, st, nl,
-                                         hook ? &bh : nullptr));
+        if (generic_tail) {
+            st::TailPtrs tp{};
+            tp.R = (int)m.R;
+            for (int q = 0; q <= tp.R; ++q) {
+                tp.u[q] = su + (size_t)q * m.BH * m.Lrq;
+                tp.v[q] = svv + (size_t)q * m.BH * m.Lrk;
+                tp.ub[q] = (float*)(ws + wl.tail_u) + (size_t)q * m.BH * m.Lrq;
+                tp.vb[q] = (float*)(ws + wl.tail_v) + (size_t)q * m.BH * m.Lrk;
+            }
+            if (eta_v) tp.vb[0] = eta_v;  // eta = vb_0
+            tp.g_u = p.g_u;
+            ST_CUDA(st::launch_tail_adjoint(g, desc->dtype, tp, p.S2, S2T, Z, ZT, Q, K, V, dO, dQ, dK, dV,
+                                            p.deps_part, st, nl));
+        } else {
+            st::BwdHook bh{hook, user, (int64_t)(m.BH * m.Lrq), (int64_t)(m.BH * m.Lrk)};
+            ST_CUDA(st::launch_backward_tile(g, desc->dtype, p, t, mode == ST_DIRECT_FOUR_PLAN, st, nl,
+                                             hook ? &bh : nullptr));
+        }
         st::add_launches(nl);
     } else {
         ST_CUDA(st::launch_backward(g, desc->dtype, p, mode == ST_DIRECT_FOUR_PLAN, st));

@@ -37,7 +37,8 @@ struct BT {
     int fuse_c5;  // C6 also produces v0b (the C5 sweep) -- no dustbin
 };
 
-enum { R1 = 0, R2 = 1, R4 = 2, R6 = 3, RO = 4, R12 = 5, C1 = 10, C3 = 11, C5 = 12, C6 = 13 };
+enum { R1 = 0, R2 = 1, R4 = 2, R6 = 3, RO = 4, R12 = 5, RW = 6, C1 = 10, C3 = 11, C5 = 12, C6 = 13, CW = 14 };
+// RW / CW: dQ (+ d_eps) / dK from a materialised score-cotangent band (generic-R tail adjoint)
 // R12 = R1 and R2 in one sweep (g_u_i = sum P22 Z, u2b_i = g_u_i - sum P22 g_v_j): needs C1 first
 
 __device__ __forceinline__ float sbar_of(bool direct, float s2, float p22, float z, float u1i, float u2i,
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
     __shared__ __align__(8) uint64_t bar;
     constexpr bool kRow = kOp < 10;
     constexpr bool kNeedZ = (kOp == R1 || kOp == R12 || kOp == R6 || kOp == C1 || kOp == C6);
-    constexpr bool kVec = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RO);
+    constexpr bool kVec = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RO || kOp == RW || kOp == CW);
     // own = rows (row stages) or columns (column stages)
     const int Lo = kRow ? g.Lq : g.Lk, Lx = kRow ? g.Lk : g.Lq;
     const int Lro = kRow ? g.Lrq : g.Lrk, Lrx = kRow ? g.Lrk : g.Lrq;
@@ -289,7 +290,7 @@ __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
     __shared__ __align__(8) uint64_t bar;
     __shared__ float sacc[2][128], sdacc[2][128], pd[128];
     constexpr bool kRow = kOp < 10;
-    constexpr bool kNeedZ = (kOp == R6 || kOp == C1 || kOp == C6);
+    constexpr bool kNeedZ = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RW || kOp == CW);
     constexpr int CPT = D / 8;  // output columns per thread
     const int Lo = kRow ? g.Lq : g.Lk, Lx = kRow ? g.Lk : g.Lq;
     const int Lro = kRow ? g.Lrq : g.Lrk, Lrx = kRow ? g.Lrk : g.Lrq;
@@ -302,10 +303,10 @@ __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
     auto on_x = [&](int k) { return k >= 0 && k < Lx && (mx == nullptr || mx[(size_t)(bh / g.H) * Lx + k] != 0); };
     const int r = tid & 127, hh = tid >> 7, i = i0 + r;
     const bool active = on_o(i);
-    float* vo = kOp == R6 ? a.dQ : kOp == C1 ? a.dV : kOp == RO ? a.O : a.dK;
+    float* vo = (kOp == R6 || kOp == RW) ? a.dQ : kOp == C1 ? a.dV : kOp == RO ? a.O : a.dK;
     if (!__syncthreads_or(active)) {
         if (hh == 0 && i < Lo) {
-            if (kOp == R6) a.deps_part[bo + i] = 0.f;
+            if (kOp == R6 || kOp == RW) a.deps_part[bo + i] = 0.f;
             if (kOp == C1) a.g_v[bo + i] = 0.f;
             if (kOp == C6 && a.fuse_c5) a.v0b[bo + i] = 0.f;
             for (int x = 0; x < g.d; ++x) vo[(bo + i) * g.d + x] = 0.f;
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
     float* tZ = tS + 128 * Wf;
     float* wv = tZ + (kNeedZ ? 128 * Wf : 0);  // window vectors [5][Nw]
     float* ops = wv + ((5 * Nw + 3) & ~3);     // operand rows [Nw][D] (window row c <-> x = i0 - w + c)
-    const TIn* osrc = (kOp == R6) ? a.K : (kOp == C1) ? a.dO : (kOp == RO) ? a.V : a.Q;
+    const TIn* osrc = (kOp == R6 || kOp == RW) ? a.K : (kOp == C1) ? a.dO : (kOp == RO) ? a.V : a.Q;
     // f32 operands: the valid window rows are one contiguous run in global memory -> one bulk copy
     const int xlo = max(0, i0 - g.w), xhi = min(Lx, i0 - g.w + Nw);
     const int clo = xlo - (i0 - g.w), chi = clo + max(0, xhi - xlo);
@@ -412,8 +413,11 @@ __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
             const float s2 = ts[k];
             float wgt = 0.f;
             if (s2 != -INFINITY) {
-                const float p = ex2(s2 + o2 + wv[c]);
-                if (kOp == RO) {
+                const float p = (kOp == RW || kOp == CW) ? 0.f : ex2(s2 + o2 + wv[c]);
+                if (kOp == RW || kOp == CW) {  // the band already holds Sbar
+                    wgt = tz[k];
+                    if (kOp == RW) dacc += wgt * (s2 * kLn2);
+                } else if (kOp == RO) {
                     wgt = p;
                 } else if (kOp == C1) {
                     acc += p * tz[k];
@@ -473,7 +477,7 @@ __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
     __syncthreads();
     if (hh == 0 && i < Lo) {
         if (kOp == C1) a.g_v[bo + i] = active ? sacc[0][r] + sacc[1][r] : 0.f;
-        if (kOp == R6) a.deps_part[bo + i] = active ? sdacc[0][r] + sdacc[1][r] : 0.f;
+        if (kOp == R6 || kOp == RW) a.deps_part[bo + i] = active ? sdacc[0][r] + sdacc[1][r] : 0.f;
         if (kOp == C6 && a.fuse_c5) {  // v0b_j = -delta_j sum_i P22 alpha_i u1b_i  (direct: -sum P10 u1b)
             const float s5 = sacc[0][r] + sacc[1][r];
             a.v0b[bo + i] = !active ? 0.f : kDirect ? -s5 : -ex2(a.v0[bo + i] - a.v2[bo + i]) * s5;
@@ -691,7 +695,7 @@ __global__ void __launch_bounds__(256) k_bwdG(Geo g, BT<TIn> a) {
     constexpr int TPR = 256 / RB, GS = 32 / TPR;
     constexpr int OP = D;  // operand row pitch (elements): contiguous window rows, one bulk copy
     constexpr bool kRow = kOp < 10;
-    constexpr bool kNeedZ = (kOp == R6 || kOp == C1 || kOp == C6);
+    constexpr bool kNeedZ = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RW || kOp == CW);
     const int Lo = kRow ? g.Lq : g.Lk, Lx = kRow ? g.Lk : g.Lq;
     const int Lro = kRow ? g.Lrq : g.Lrk, Lrx = kRow ? g.Lrk : g.Lrq;
     const int Lpo = kRow ? g.Lqp : g.Lkp;
@@ -703,10 +707,10 @@ __global__ void __launch_bounds__(256) k_bwdG(Geo g, BT<TIn> a) {
     auto on_o = [&](int k) { return k < Lo && (mo == nullptr || mo[(size_t)(bh / g.H) * Lo + k] != 0); };
     auto on_x = [&](int k) { return k >= 0 && k < Lx && (mx == nullptr || mx[(size_t)(bh / g.H) * Lx + k] != 0); };
     const bool active = on_o(i);
-    float* vo = kOp == R6 ? a.dQ : kOp == C1 ? a.dV : kOp == RO ? a.O : a.dK;
+    float* vo = (kOp == R6 || kOp == RW) ? a.dQ : kOp == C1 ? a.dV : kOp == RO ? a.O : a.dK;
     if (!__syncthreads_or(active)) {
         if (part == 0 && i < Lo) {
-            if (kOp == R6) a.deps_part[bo + i] = 0.f;
+            if (kOp == R6 || kOp == RW) a.deps_part[bo + i] = 0.f;
             if (kOp == C1) a.g_v[bo + i] = 0.f;
             if (kOp == C6 && a.fuse_c5) a.v0b[bo + i] = 0.f;
             for (int x = 0; x < D; ++x) vo[(bo + i) * D + x] = 0.f;
@@ -718,7 +722,7 @@ __global__ void __launch_bounds__(256) k_bwdG(Geo g, BT<TIn> a) {
     float* tZ = tS + RB * Wf;
     float* wv = tZ + (kNeedZ ? RB * Wf : 0);
     TIn* ops = reinterpret_cast<TIn*>(wv + ((5 * Nw + 3) & ~3));
-    const TIn* osrc = (kOp == R6) ? a.K : (kOp == C1) ? a.dO : (kOp == RO) ? a.V : a.Q;
+    const TIn* osrc = (kOp == R6 || kOp == RW) ? a.K : (kOp == C1) ? a.dO : (kOp == RO) ? a.V : a.Q;
     const int xlo = max(0, i0 - g.w), xhi = min(Lx, i0 - g.w + Nw);
     const int clo = xlo - (i0 - g.w), chi = clo + max(0, xhi - xlo);
     const uint32_t obytes = chi > clo ? (uint32_t)(chi - clo) * D * (uint32_t)sizeof(TIn) : 0u;
@@ -800,8 +804,11 @@ __global__ void __launch_bounds__(256) k_bwdG(Geo g, BT<TIn> a) {
                 const float s2 = ts[k];
                 float wgt = 0.f;
                 if (s2 != -INFINITY) {
-                    const float p = ex2(s2 + o2 + wv[c]);
-                    if (kOp == RO) {
+                    const float p = (kOp == RW || kOp == CW) ? 0.f : ex2(s2 + o2 + wv[c]);
+                    if (kOp == RW || kOp == CW) {  // the band already holds Sbar
+                        wgt = tz[k];
+                        if (kOp == RW) dacc += wgt * (s2 * kLn2);
+                    } else if (kOp == RO) {
                         wgt = p;
                     } else if (kOp == C1) {
                         acc += p * tz[k];
@@ -843,7 +850,7 @@ __global__ void __launch_bounds__(256) k_bwdG(Geo g, BT<TIn> a) {
     }
     if (part == 0 && i < Lo) {
         if (kOp == C1) a.g_v[bo + i] = active ? acc : 0.f;
-        if (kOp == R6) a.deps_part[bo + i] = active ? dacc : 0.f;
+        if (kOp == R6 || kOp == RW) a.deps_part[bo + i] = active ? dacc : 0.f;
         if (kOp == C6 && a.fuse_c5)
             a.v0b[bo + i] = !active ? 0.f : kDirect ? -acc : -ex2(a.v0[bo + i] - a.v2[bo + i]) * acc;
     }
@@ -938,7 +945,7 @@ static size_t bwdT_op_smem(const Geo& g, int op, int D) {
 // SMEM of the wide-band kernels (k_bwdS scalar stages, k_bwdG vector stages) at RB rows per CTA
 static size_t wide_smem(const Geo& g, int op, int D, int esz, int RB) {
     const int Nw = RB + 2 * g.w;
-    const bool vec = (op == R6 || op == C1 || op == C6 || op == RO);
+    const bool vec = (op == R6 || op == C1 || op == C6 || op == RO || op == RW || op == CW);
     const bool z = vec ? (op != RO) : (op == R1 || op == R12);
     return (size_t)(z ? 2 : 1) * RB * g.Wf * 4 + (size_t)((5 * Nw + 3) & ~3) * 4 + (vec ? (size_t)Nw * D * esz : 0) + 64;
 }
@@ -946,7 +953,7 @@ static size_t wide_smem(const Geo& g, int op, int D, int esz, int RB) {
 // rows per CTA for a stage: 128 (the k_bwdT / k_bwdV tiles or k_bwdG<128>), else 64 / 32; 0 = none fits
 static int pick_rb(const Geo& g, int op, int D, int esz) {
     constexpr size_t kMax = 227 * 1024;
-    const bool vec = (op == R6 || op == C1 || op == C6 || op == RO);
+    const bool vec = (op == R6 || op == C1 || op == C6 || op == RO || op == RW || op == CW);
     if (!vec && bwdT_op_smem(g, op, D) <= kMax) return 128;
     for (int RB : {128, 64, 32}) {
         if (vec && D == 32 && RB == 32) continue;
@@ -971,7 +978,7 @@ bool bwdT_supported(const Geo& g) {
 
 template <int kOp, bool kDirect, int D, class TIn, int RB>
 static cudaError_t run_wide(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
-    constexpr bool kVec = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RO);
+    constexpr bool kVec = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RO || kOp == RW || kOp == CW);
     const bool row = kOp < 10;
     const int n = row ? g.Lq : g.Lk;
     const size_t smem = wide_smem(g, kOp, D, (int)sizeof(TIn), RB);
@@ -996,7 +1003,7 @@ static cudaError_t run_wide(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
 template <int kOp, bool kDirect, int D, class TIn>
 static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
     const bool row = kOp < 10;
-    constexpr bool kVec = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RO);
+    constexpr bool kVec = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RO || kOp == RW || kOp == CW);
     if (kVec && D <= 64 && bwdT_smem_bytes(g) <= 227 * 1024 && !getenv("ST_NO_BWDV")) {
         // 128-row weights + register-tiled band GEMM (operands as f32)
         const size_t smem = bwdT_smem_bytes(g);
@@ -1125,6 +1132,110 @@ static cudaError_t run_all(const Geo& g, const BwdPtrs& p, const BwdTPtrs& t, in
 #undef ST_RUN
 #undef ST_DUST
     return cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------
+// Generic-R tail adjoint (adjoint.hpp:132-200).  The R=2 path never materialises the score
+// cotangent; for any other depth it is built once in place over the Z band:
+//   Sbar = P^(RR) (.) Z - sum_{t=1..R} [ P^(h,h) (.) vb_t,j + P^(h,h-1) (.) ub_t,i ],  h = T+t,
+// then transposed and contracted by the RW (dQ, d_eps) / CW (dK) band GEMMs.  2R+1 exps per cell.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_sbar_band(Geo g, TailPtrs tp, const float* __restrict__ S2,
+                                                   float* __restrict__ Z) {
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long total = (long)g.BH * g.Lqp * g.Wf;
+    if (t >= total) return;
+    const int k = (int)(t % g.Wf);
+    const long ri = t / g.Wf;
+    const int i = (int)(ri % g.Lqp), bh = (int)(ri / g.Lqp);
+    const int j = i - g.w + k;
+    const float s2 = S2[t];
+    float out = 0.f;
+    if (i < g.Lq && j >= 0 && j < g.Lk && s2 != -INFINITY) {
+        const size_t oi = (size_t)bh * g.Lrq + i, oj = (size_t)bh * g.Lrk + j;
+        const int R = tp.R;
+        const float uR = tp.u[R][oi];
+        float acc = ex2(s2 + uR + tp.v[R][oj]) * Z[t];
+        for (int q = R; q >= 1; --q) {
+            const float uq = tp.u[q][oi];
+            acc -= ex2(s2 + uq + tp.v[q][oj]) * tp.vb[q][oj];
+            acc -= ex2(s2 + uq + tp.v[q - 1][oj]) * tp.ub[q][oi];
+        }
+        out = acc;
+    }
+    Z[t] = out;
+}
+
+template <int D, class TIn>
+static cudaError_t run_tail(const Geo& g, const TailPtrs& tp, const float* S2, const float* S2T, float* Z, float* ZT,
+                            const void* Q, const void* K, const void* V, const void* dO, float* dQ, float* dK,
+                            float* dV, float* deps_part, cudaStream_t s, long long& launches) {
+    const int R = tp.R;
+    BT<TIn> a{};
+    a.S2 = S2;
+    a.S2T = S2T;
+    a.Z = Z;
+    a.ZT = ZT;
+    a.Q = (const TIn*)Q;
+    a.K = (const TIn*)K;
+    a.V = (const TIn*)V;
+    a.dO = (const TIn*)dO;
+    a.dQ = dQ;
+    a.dK = dK;
+    a.dV = dV;
+    a.deps_part = deps_part;
+    a.fuse_c5 = 0;
+    // a stage that reads one plan P^(hu,hv) binds every dual slot of its side to that step, so the
+    // one-reference ratios alpha / beta / delta are exactly 1
+    auto bind = [&](int hu, int hv) {
+        a.u1 = a.u2 = tp.u[hu];
+        a.v0 = a.v1 = a.v2 = tp.v[hv];
+    };
+    cudaError_t e;
+#define ST_RUN(op)                                                                           do {                                                                                         if ((e = run_op<op, false, D, TIn>(g, a, s)) != cudaSuccess) return e;                   ++launches;                                                                          } while (0)
+    // C1: vb_R = g_v = colsum(P^(RR) (.) Z), dV = P^(RR)^T dO
+    bind(R, R);
+    a.g_v = tp.vb[R];
+    ST_RUN(C1);
+    if (R >= 1) {  // ub_R = g_u - P^(RR) vb_R
+        a.g_u = tp.g_u;
+        a.u2b = tp.ub[R];
+        ST_RUN(R12);
+        for (int q = R; q >= 1; --q) {
+            bind(q, q - 1);  // vb_{q-1} = -P^(h,h-1)^T ub_q
+            a.u2b = tp.ub[q];
+            a.v1b = tp.vb[q - 1];
+            ST_RUN(C3);
+            if (q >= 2) {  // ub_{q-1} = -P^(h-1,h-1) vb_{q-1}
+                bind(q - 1, q - 1);
+                a.v1b = tp.vb[q - 1];
+                a.u1b = tp.ub[q - 1];
+                ST_RUN(R4);
+            }
+        }
+    }
+    const long total = (long)g.BH * g.Lqp * g.Wf;
+    k_sbar_band<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(g, tp, S2, Z);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++launches;
+    if ((e = launch_transpose_band(g, Z, ZT, s, 0.f)) != cudaSuccess) return e;
+    bind(R, R);
+    ST_RUN(RW);
+    ST_RUN(CW);
+#undef ST_RUN
+    return cudaSuccess;
+}
+
+cudaError_t launch_tail_adjoint(const Geo& g, int dtype, const TailPtrs& tp, const float* S2, const float* S2T,
+                                float* Z, float* ZT, const void* Q, const void* K, const void* V, const void* dO,
+                                float* dQ, float* dK, float* dV, float* deps_part, cudaStream_t s,
+                                long long& launches) {
+    if (tp.R < 0 || tp.R > kMaxTailSteps || g.dustbin) return cudaErrorNotSupported;
+#define ST_TAIL(D)                                                                                              return dtype == 0 ? run_tail<D, float>(g, tp, S2, S2T, Z, ZT, Q, K, V, dO, dQ, dK, dV, deps_part, s, launches)                       : run_tail<D, __nv_bfloat16>(g, tp, S2, S2T, Z, ZT, Q, K, V, dO, dQ, dK, dV, deps_part, s, launches);
+    if (g.d == 32) { ST_TAIL(32) }
+    if (g.d == 64) { ST_TAIL(64) }
+    ST_TAIL(128)
+#undef ST_TAIL
 }
 
 // O = P^(T+R,T+R) V on the stored band (apply_transport, sinkhorn.hpp:262-277): the RO row stage

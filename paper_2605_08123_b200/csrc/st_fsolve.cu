@@ -37,8 +37,8 @@ struct FSolve {
     const float* S2;
     float* ubuf;             // [BH][Lrq] raw base-2 u (final step; every step when non-resident)
     float* vbuf;             // [BH][Lrk] v_{T+R} (owners)
-    float* u_slot[3];        // saved u at steps T, T+1, T+2 (or null)
-    float* v_slot[3];
+    float* u_slot[9];        // saved u at tail steps T .. T+8 (or null)
+    float* v_slot[9];
     u64* part[2];            // [BH][NB][Nw] tagged column partials {sum, step}, by step parity
     u64* partm;              // [BH][NB][Nw] tagged cold-start maxima {max, 1}
     float* vpriv;            // [n][Nw] window duals of each work item (non-resident mode only)
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kThreads) k_fsolve(Geo g, FSolve f) {
                 if (t >= 2 && owner) {
                     const float vo = (v == -INFINITY) ? 0.f : v;
                     const int rv = t - 1 - f.T;
-                    if (rv >= 0 && rv <= 2 && f.v_slot[rv]) f.v_slot[rv][(size_t)bh * g.Lrk + j] = vo;
+                    if (rv >= 0 && rv <= 8 && f.v_slot[rv]) f.v_slot[rv][(size_t)bh * g.Lrk + j] = vo;
                     if (fin) f.vbuf[(size_t)bh * g.Lrk + j] = vo;
                 }
             }
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(kThreads) k_fsolve(Geo g, FSolve f) {
                     unew[r] = u;
                     if (!resident || t == TR) f.ubuf[(size_t)bh * g.Lrq + i] = u;
                     const int ru = t - f.T;
-                    if (ru >= 0 && ru <= 2 && f.u_slot[ru]) f.u_slot[ru][(size_t)bh * g.Lrq + i] = u;
+                    if (ru >= 0 && ru <= 8 && f.u_slot[ru]) f.u_slot[ru][(size_t)bh * g.Lrq + i] = u;
                 }
             } else if (h == 0) {
                 unew[r] = -INFINITY;  // no contribution to any column
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(kTmGroups * kThreads, 1) k_fsolve_tm(Geo g, FS
                 if (t >= 2 && owner) {
                     const float vo = (v == -INFINITY) ? 0.f : v;
                     const int rv = t - 1 - f.T;
-                    if (rv >= 0 && rv <= 2 && f.v_slot[rv]) f.v_slot[rv][(size_t)bh * g.Lrk + j] = vo;
+                    if (rv >= 0 && rv <= 8 && f.v_slot[rv]) f.v_slot[rv][(size_t)bh * g.Lrk + j] = vo;
                     if (fin) f.vbuf[(size_t)bh * g.Lrk + j] = vo;
                 }
             }
@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(kTmGroups * kThreads, 1) k_fsolve_tm(Geo g, FS
                     inv_r[r] = (t == 1) ? lr : 1.f / rs;
                     if (!resident || t == TR) f.ubuf[(size_t)bh * g.Lrq + i] = u;
                     const int ru = t - f.T;
-                    if (ru >= 0 && ru <= 2 && f.u_slot[ru]) f.u_slot[ru][(size_t)bh * g.Lrq + i] = u;
+                    if (ru >= 0 && ru <= 8 && f.u_slot[ru]) f.u_slot[ru][(size_t)bh * g.Lrq + i] = u;
                     rpart[0][r] = u;  // hand the new dual to the other half
                 } else {
                     inv_r[r] = (t == 1) ? INFINITY : 0.f;
@@ -702,7 +702,7 @@ cudaError_t launch_fsolve(const Geo& g, int T, int R, const FSolvePtrs& p, cudaS
     cudaMemsetAsync(p.partm, 0, np, s);
     cudaMemsetAsync(p.ubuf, 0, nq, s);
     cudaMemsetAsync(p.vbuf, 0, nk, s);
-    for (int q = 0; q < 3; ++q) {
+    for (int q = 0; q < 9; ++q) {
         if (p.u_slot[q]) cudaMemsetAsync(p.u_slot[q], 0, nq, s);
         if (p.v_slot[q]) cudaMemsetAsync(p.v_slot[q], 0, nk, s);
     }
@@ -710,7 +710,7 @@ cudaError_t launch_fsolve(const Geo& g, int T, int R, const FSolvePtrs& p, cudaS
     f.S2 = p.S2;
     f.ubuf = p.ubuf;
     f.vbuf = p.vbuf;
-    for (int q = 0; q < 3; ++q) {
+    for (int q = 0; q < 9; ++q) {
         f.u_slot[q] = p.u_slot[q];
         f.v_slot[q] = p.v_slot[q];
     }

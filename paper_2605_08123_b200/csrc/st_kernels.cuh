@@ -43,8 +43,8 @@ struct FSolvePtrs {
     const float* S2;
     float* ubuf;
     float* vbuf;
-    float* u_slot[3];
-    float* v_slot[3];
+    float* u_slot[9];   // saved u / v at tail steps T .. T+8 (or null)
+    float* v_slot[9];
     void* part[2];    // tagged 64-bit partials [BH][NB][128+2w]
     void* partm;
     float* vpriv;     // [BH*NB][128+2w]
@@ -73,6 +73,21 @@ struct BwdHook {
 };
 cudaError_t launch_backward_tile(const Geo& g, int dtype, const BwdPtrs& p, const BwdTPtrs& t, bool direct,
                                  cudaStream_t s, long long& launches, const BwdHook* hook = nullptr);
+// generic-R tail adjoint (adjoint.hpp:132-200): u[t] / v[t] = raw duals of step T+t (base 2),
+// ub[t] / vb[t] = their cotangents (written), t = 0..R
+constexpr int kMaxTailSteps = 8;
+struct TailPtrs {
+    int R;
+    const float* u[kMaxTailSteps + 1];
+    const float* v[kMaxTailSteps + 1];
+    float* ub[kMaxTailSteps + 1];
+    float* vb[kMaxTailSteps + 1];
+    float* g_u;  // scratch [BH][Lrq]
+};
+cudaError_t launch_tail_adjoint(const Geo& g, int dtype, const TailPtrs& tp, const float* S2, const float* S2T,
+                                float* Z, float* ZT, const void* Q, const void* K, const void* V, const void* dO,
+                                float* dQ, float* dK, float* dV, float* deps_part, cudaStream_t s,
+                                long long& launches);
 cudaError_t launch_output_tile(const Geo& g, int dtype, const float* S2, const float* u, const float* v, const void* V,
                                float* O, cudaStream_t s);
 // the dustbin row / column of one backward stage through the generic sweeps

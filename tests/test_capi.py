@@ -79,7 +79,17 @@ def test_error_contract_without_gpu():
     d = _spec(tail_depth=1).desc()
     assert lib.st_backward(ctypes.byref(d), 1, 1, 1, 1, 1, None, None, 1, 1, 1, None, None, 0, None, 0,
                            None) == _lib.ST_UNSUPPORTED_DEPTH
+    # the generic tail adjoint (mode 2) takes any depth up to 8, no dustbin
+    for R, want in ((1, _lib.ST_MISSING_BASE_TRACE), (9, _lib.ST_UNSUPPORTED_DEPTH)):
+        d = _spec(tail_depth=R).desc()
+        assert lib.st_backward(ctypes.byref(d), None, 1, 1, 1, 1, None, None, 1, 1, 1, None, None,
+                               _lib.ST_GENERIC_TAIL, None, 0, None) == want, R
+    d = _spec(dustbin=1).desc()
+    assert lib.st_backward(ctypes.byref(d), 1, 1, 1, 1, 1, None, None, 1, 1, 1, None, None,
+                           _lib.ST_GENERIC_TAIL, None, 0, None) == _lib.ST_NOT_SUPPORTED
     d = _spec().desc()
+    assert lib.st_backward(ctypes.byref(d), 1, 1, 1, 1, 1, None, None, 1, 1, 1, None, None, 7, None, 0,
+                           None) == _lib.ST_INVALID_ARGUMENT
     assert lib.st_backward(ctypes.byref(d), None, 1, 1, 1, 1, None, None, 1, 1, 1, None, None, 0, None, 0,
                            None) == _lib.ST_MISSING_BASE_TRACE
     assert lib.st_forward(ctypes.byref(d), 1, 1, 1, None, None, 1, None, None, 0, None) == _lib.ST_WORKSPACE_TOO_SMALL
