@@ -120,6 +120,25 @@ st_status st_backward(const st_desc* desc, const void* saved, const void* Q, con
                       float* eta_v, int32_t mode, void* workspace, size_t workspace_bytes,
                       void* stream);
 
+/* tail_adjoint_generic (adjoint.hpp:132-200) with its full base cotangent: as st_backward in mode
+ * ST_GENERIC_TAIL, plus eta_u ([B*H, L'_q] f32, may be NULL) = u-bar^(0), which is nonzero only for
+ * tail_depth 0 (then eta = (g_u, g_v), the row / column sums of P^(T,T) (.) dO V^T). */
+st_status st_tail_adjoint(const st_desc* desc, const void* saved, const void* Q, const void* K,
+                          const void* V, const void* dO, const uint8_t* row_mask, const uint8_t* col_mask,
+                          float* dQ, float* dK, float* dV, float* d_eps, float* eta_u, float* eta_v,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
+/* base_solve_vjp (certificates.hpp:25-70): pull a base-state cotangent (eta_u [B*H, L'_q] or NULL
+ * = 0, eta_v [B*H, L'_k]: the v-bar^(0) that st_backward returns) back through the T stopped base
+ * steps to dQ, dK ([B, H, L', d] f32) -- the omitted-gradient certificate c_R of the tail depth
+ * (bias_certificate, certificates.hpp:112-140).  Recomputes the base solve keeping every step's
+ * duals (T+1 dual pairs in the workspace), then runs the reverse recurrences at each step's stage
+ * temperature.  No dustbin; d in {32, 64, 128}.  base_depth = 0 gives zeros. */
+size_t st_base_vjp_workspace_bytes(const st_desc* desc);
+st_status st_base_solve_vjp(const st_desc* desc, const void* Q, const void* K, const uint8_t* row_mask,
+                            const uint8_t* col_mask, const float* eta_u, const float* eta_v, float* dQ,
+                            float* dK, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Sequence sharding (config 5): the problem a rank passes is its own rows plus a halo of up to
  * half_band rows on each side.  The library calls `hook` right after it has ENQUEUED (on `stream`)
  * each kernel that produces a vector the next kernel reads across the shard edge -- kind 0: a row

@@ -1195,6 +1195,86 @@ TEST("ext: spoke dustbin constant cost == reference-semantics embedding (SURVEY 
     CHECK(std::abs(fde - one.d_eps) < 1e-7 * std::max(1.0, std::abs(fde)));
 }
 
+// ---- certificates (test_certificates.cpp) -------------------------------------------------------
+CertificateProblem cert_problem(Index n, Index w, Index t, std::uint64_t seed, double loss_scale = 1.0) {
+    auto inst = make_inst(n, w, t, 2, seed, 64);
+    CertificateProblem p;
+    p.Q = inst.Q;
+    p.K = inst.K;
+    p.V = inst.V;
+    p.schedule = inst.schedule;
+    p.base_depth = t;
+    p.eps = inst.eps;
+    p.loss = random_linear_loss(inst, loss_scale);
+    return p;
+}
+double mat_max_abs(const Mat<double>& m) {
+    double x = 0.0;
+    for (double v : m.a) x = std::max(x, std::abs(v));
+    return x;
+}
+TEST("certificates: base-solve VJP edge cases (test_certificates.cpp:38-54)") {
+    auto p = cert_problem(16, 5, 4, 50);
+    auto run = run_surrogate<double>(p.Q, p.K, p.V, p.schedule, p.base_depth, 2, p.eps);
+    Vec<double> z(16, 0.0), one(16, 1.0);
+    auto c0 = base_solve_vjp(run.raw, run.trace, z, z, p.Q, p.K);
+    CHECK(mat_max_abs(c0.grad_q) == 0.0);
+    CHECK(mat_max_abs(c0.grad_k) == 0.0);
+    auto cold = run_surrogate<double>(p.Q, p.K, p.V, p.schedule, 0, 2, EpsSchedule<double>::single(1.0, 0));
+    auto cz = base_solve_vjp(cold.raw, cold.trace, one, one, p.Q, p.K);
+    CHECK(mat_max_abs(cz.grad_q) == 0.0);
+    CHECK(mat_max_abs(cz.grad_k) == 0.0);
+}
+TEST("certificates: remainder identity full - stopped = c_R (test_certificates.cpp:56-65)") {
+    for (std::uint64_t seed : {0, 1}) {
+        auto p = cert_problem(48, 16, 8, seed);
+        for (Index r : {0, 1, 2}) {
+            auto cert = bias_certificate(p, r);
+            CHECK(cert.residual_computed);
+            CHECK(cert.residual < 1e-12);
+        }
+    }
+}
+TEST("certificates: output-independent loss zeroes every field (test_certificates.cpp:67-74)") {
+    auto p = cert_problem(16, 5, 4, 51, 0.0);
+    auto cert = bias_certificate(p, 2);
+    CHECK(cert.eta_norm == 0.0);
+    CHECK(cert.c_inf == 0.0);
+    CHECK(cert.max_gap == 0.0);
+    CHECK(cert.residual == 0.0);
+}
+TEST("certificates: eta decays strictly with the tail depth (test_certificates.cpp:76-86)") {
+    for (std::uint64_t seed = 0; seed < 20; ++seed) {
+        auto p = cert_problem(32, 32, 10, 100 + seed);
+        double prev = std::numeric_limits<double>::infinity();
+        for (Index r = 0; r <= 3; ++r) {
+            const double e = bias_certificate(p, r, false).eta_norm;
+            CHECK(e < prev);
+            prev = e;
+        }
+    }
+}
+TEST("certificates: selector returns the first feasible depth (test_certificates.cpp:106-133)") {
+    auto p = cert_problem(32, 32, 10, 8);
+    CHECK(select_tail_depth(p, 1e3, 4).selected == 0);
+    auto s1 = select_tail_depth(p, 1e-30, 3);
+    CHECK(s1.selected == -1);
+    CHECK(s1.trail.size() == 4);
+    const double tau = bias_certificate(p, 2, false).c_inf * 1.5;
+    Index expected = -1;
+    for (Index r = 0; r <= 5; ++r)
+        if (bias_certificate(p, r, false).c_inf <= tau) { expected = r; break; }
+    CHECK(select_tail_depth(p, tau, 5).selected == expected);
+    CHECK_THROWS_AS(select_tail_depth(p, -1.0, 3), std::invalid_argument);
+    CHECK_THROWS_AS(select_tail_depth(p, 1.0, 3, [](Index r) { return -static_cast<double>(r); }),
+                    std::invalid_argument);
+    const double bound = 1.0;
+    const double tau1 = bound * bias_certificate(p, 1, false).eta_norm * 1.01;
+    auto s = select_tail_depth(p, tau1, 4, [](Index r) { return static_cast<double>(r); }, &bound);
+    CHECK(s.used_sufficient_bound);
+    CHECK(s.selected == 1);
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {

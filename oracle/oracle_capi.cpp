@@ -48,6 +48,8 @@ struct BatchArgs {
     const double* stage_eps = nullptr;
     const std::int64_t* stage_iters = nullptr;
     std::int64_t Lk = -1;  // key count (rectangular problems, no dustbin); -1: Lk = L
+    double* eta_u = nullptr;              // base cotangent u part (u-bar^(0))
+    double *cQ = nullptr, *cK = nullptr;  // base_solve_vjp of the adjoint's base cotangent (certificates)
 };
 
 template <class T>
@@ -120,6 +122,13 @@ void run_head(const BatchArgs& a, std::int64_t bh) {
     if (a.eta_v)
         for (std::int64_t j = 0; j < Lrk; ++j)
             a.eta_v[bh * Lrk + j] = static_cast<double>(c.base_v[static_cast<size_t>(j)]);
+    if (a.eta_u)
+        for (std::int64_t i = 0; i < Lr; ++i) a.eta_u[bh * Lr + i] = static_cast<double>(c.base_u[static_cast<size_t>(i)]);
+    if (a.cQ) {  // certificates.hpp:112-118: c_R = base_solve_vjp(raw, trace, base_cotangent)
+        BaseVjpResult<T> bv = base_solve_vjp<T>(run.raw, run.trace, c.base_u, c.base_v, Q, K);
+        for (size_t k = 0; k < bv.grad_q.a.size(); ++k) a.cQ[off + k] = static_cast<double>(bv.grad_q.a[k]);
+        for (size_t k = 0; k < bv.grad_k.a.size(); ++k) a.cK[offk + k] = static_cast<double>(bv.grad_k.a[k]);
+    }
 }
 
 int classify(const std::exception& e) {
@@ -206,6 +215,44 @@ int stoc_run_batch_rect(std::int64_t B, std::int64_t H, std::int64_t Lq, std::in
     BatchArgs a{B,    H,  Lq, d,  half_band, T,        R,        eps,  0,   0.0,     Q,       K,      V,      G,
                 row_mask, col_mask, precision, mode, 128, 1, O, dQ, dK, dV, d_eps, eta_v, nullptr, nullptr};
     a.Lk = Lk;
+    if (nthreads < 1) nthreads = 1;
+    std::atomic<std::int64_t> next{0};
+    std::atomic<int> status{STOC_OK};
+    auto worker = [&]() {
+        for (;;) {
+            const std::int64_t bh = next.fetch_add(1);
+            if (bh >= B * H || status.load() != STOC_OK) return;
+            try {
+                if (precision == 32) run_head<float>(a, bh);
+                else run_head<double>(a, bh);
+            } catch (const std::exception& e) {
+                status.store(classify(e));
+                return;
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < std::min<std::int64_t>(nthreads, B * H); ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
+    return status.load();
+}
+
+// generic tail adjoint + base-solve VJP per head (the bias certificate's c_R, certificates.hpp:112-118)
+int stoc_run_batch_cert(std::int64_t B, std::int64_t H, std::int64_t L, std::int64_t d, std::int64_t half_band,
+                        std::int64_t T, std::int64_t R, double eps, const double* Q, const double* K,
+                        const double* V, const double* G, const std::uint8_t* row_mask, const std::uint8_t* col_mask,
+                        int precision, int nthreads, int n_stages, const double* stage_eps,
+                        const std::int64_t* stage_iters, double* O, double* dQ, double* dK, double* dV,
+                        double* d_eps, double* eta_u, double* eta_v, double* cQ, double* cK) {
+    BatchArgs a{B,    H,  L, d,  half_band, T,        R,        eps,  0,   0.0,     Q,       K,      V,      G,
+                row_mask, col_mask, precision, 2, 128, 1, O, dQ, dK, dV, d_eps, eta_v, nullptr, nullptr};
+    a.n_stages = n_stages;
+    a.stage_eps = stage_eps;
+    a.stage_iters = stage_iters;
+    a.cQ = cQ;
+    a.cK = cK;
+    a.eta_u = eta_u;
     if (nthreads < 1) nthreads = 1;
     std::atomic<std::int64_t> next{0};
     std::atomic<int> status{STOC_OK};

@@ -34,6 +34,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <limits>
 #include <memory>
 #include <optional>
@@ -61,6 +62,9 @@ struct UnsupportedDepth : std::runtime_error {
 };
 struct SizeCapExceeded : std::runtime_error {
     explicit SizeCapExceeded(const std::string& w) : std::runtime_error(w) {}
+};
+struct MissingBaseTrace : std::runtime_error {
+    explicit MissingBaseTrace(const std::string& w) : std::runtime_error(w) {}
 };
 
 // ---------------------------------------------------------------------------
@@ -1059,6 +1063,52 @@ CotangentSet<T> tail_adjoint_generic(const ScoreField<T>& S, const DualTrace<T>&
     return out;
 }
 
+// certificates.hpp:25-70 -- pull a base-state cotangent (u-bar, v-bar at step T) back through the
+// stopped base solve to (Q, K): the tail recurrences extended over h = T..1, each step's plans at its
+// stage temperature, the raw-score cotangent weighted by 1/eps_h.
+template <class T>
+struct BaseVjpResult {
+    Mat<T> grad_q, grad_k;
+};
+
+template <class T>
+BaseVjpResult<T> base_solve_vjp(const ScoreField<T>& raw, const DualTrace<T>& tr, const Vec<T>& eta_u,
+                                const Vec<T>& eta_v, const Mat<T>& Q, const Mat<T>& K) {
+    if (!raw.raw) throw std::invalid_argument("base_solve_vjp expects raw (unscaled) scores");
+    if (static_cast<Index>(tr.u_hist.size()) <= tr.split) throw MissingBaseTrace("trace does not retain all base duals");
+    const SupportMask& m = raw.support();
+    const size_t nr = static_cast<size_t>(m.n_rows()), nc = static_cast<size_t>(m.n_cols());
+    if (eta_u.size() != nr || eta_v.size() != nc)
+        throw std::invalid_argument("base-state cotangent sized to the wrong support");
+    BaseVjpResult<T> out;
+    out.grad_q = Mat<T>(Q.rows(), Q.cols());
+    out.grad_k = Mat<T>(K.rows(), K.cols());
+    if (tr.split == 0) return out;  // the cold start does not depend on the parameters
+    BlockField<T> raw_bar(raw.values.schedule);
+    Vec<T> ub = eta_u, vb = eta_v;
+    int stage = tr.stage_at(tr.split);
+    ScoreField<T> S = scale_to_temperature(raw, tr.eps_at(tr.split));
+    for (Index h = tr.split; h >= 1; --h) {
+        if (tr.stage_at(h) != stage) {
+            stage = tr.stage_at(h);
+            S = scale_to_temperature(raw, tr.eps_at(h));
+        }
+        const T inv_eps = T(1) / tr.eps_at(h);
+        Vec<T> pv(nr, T(0));
+        plan_apply(S, tr, h, h, vb, pv);
+        Vec<T> ab(nr);
+        for (size_t i = 0; i < nr; ++i) ab[i] = ub[i] - pv[i];
+        subtract_plan_outer<T>(S, tr, h, h, nullptr, &vb, raw_bar, inv_eps);
+        Vec<T> vprev(nc, T(0));
+        plan_apply_transpose(S, tr, h, h - 1, ab, vprev);
+        subtract_plan_outer<T>(S, tr, h, h - 1, &ab, nullptr, raw_bar, inv_eps);
+        for (size_t j = 0; j < nc; ++j) vb[j] = -vprev[j];
+        std::fill(ub.begin(), ub.end(), T(0));
+    }
+    backprop_scores_to_qkv(raw_bar, Q, K, T(1), out.grad_q, out.grad_k);
+    return out;
+}
+
 // adjoint.hpp:202-226 -- one-reference-tile score cotangent
 //   Sbar_ij = P22_ij (Z_ij - v2b_j - g21 b_j u2b_i - a_i b_j v1b_j - g10 a_i d_j u1b_i)
 template <class T>
@@ -1723,4 +1773,110 @@ inline DenseProblem make_dense_problem(const Instance<double>& inst, LossSpec<do
 }
 
 }  // namespace dense
+
+// certificates.hpp:72-150 -- the omitted-gradient certificate of a tail depth: eta_R from the generic
+// tail adjoint, pulled back through the base solve (c_R); with the dense oracle in reach, the exact
+// remainder identity (full BPTT - stopped) = c_R is checked
+struct BiasCertificate {
+    Index tail_depth = 0;
+    double eta_norm = 0.0, c_inf = 0.0, c_l2 = 0.0;
+    Mat<double> c_q, c_k;
+    double max_gap = std::numeric_limits<double>::quiet_NaN();
+    double residual = std::numeric_limits<double>::quiet_NaN();
+    bool residual_computed = false;
+};
+
+struct CertificateProblem {
+    Mat<double> Q, K, V;
+    std::shared_ptr<const TileSchedule> schedule;
+    Index base_depth = 0;
+    EpsSchedule<double> eps;
+    LossSpec<double> loss;
+};
+
+inline dense::DenseProblem to_dense_problem(const CertificateProblem& p, Index tail_depth) {
+    dense::DenseProblem d;
+    d.Q = p.Q;
+    d.K = p.K;
+    d.V = p.V;
+    d.support = dense::dense_support_of(p.schedule->support());
+    d.epsilon = p.eps.final_epsilon();
+    d.base_depth = p.base_depth;
+    d.tail_depth = tail_depth;
+    d.schedule = p.eps;
+    d.loss = p.loss;
+    return d;
+}
+
+inline BiasCertificate bias_certificate(const CertificateProblem& p, Index tail_depth, bool want_residual = true) {
+    SurrogateRun<double> run = run_surrogate<double>(p.Q, p.K, p.V, p.schedule, p.base_depth, tail_depth, p.eps);
+    const auto rv = p.schedule->support().row_mask();
+    const Mat<double> G = p.loss.output_cotangent(run.output, p.V, rv);
+    const CotangentSet<double> adj = tail_adjoint_generic(run.scaled, run.trace, G, p.Q, p.K, p.V);
+    const BaseVjpResult<double> c = base_solve_vjp(run.raw, run.trace, adj.base_u, adj.base_v, p.Q, p.K);
+    BiasCertificate cert;
+    cert.tail_depth = tail_depth;
+    cert.eta_norm = adj.base_l2();
+    cert.c_q = c.grad_q;
+    cert.c_k = c.grad_k;
+    double l2 = 0.0;
+    for (double x : c.grad_q.a) { cert.c_inf = std::max(cert.c_inf, std::abs(x)); l2 += x * x; }
+    for (double x : c.grad_k.a) { cert.c_inf = std::max(cert.c_inf, std::abs(x)); l2 += x * x; }
+    cert.c_l2 = std::sqrt(l2);
+    const SupportMask& m = p.schedule->support();
+    if (want_residual && m.n_rows() <= dense::kBpttCap && m.n_cols() <= dense::kBpttCap) {
+        const dense::DenseGradients full = dense::full_bptt_grad(to_dense_problem(p, tail_depth));
+        double gap = 0.0, res = 0.0;
+        for (size_t k = 0; k < full.grad_q.a.size(); ++k) {
+            const double g = full.grad_q.a[k] - adj.grad_q.a[k];
+            gap = std::max(gap, std::abs(g));
+            res = std::max(res, std::abs(g - c.grad_q.a[k]));
+        }
+        for (size_t k = 0; k < full.grad_k.a.size(); ++k) {
+            const double g = full.grad_k.a[k] - adj.grad_k.a[k];
+            gap = std::max(gap, std::abs(g));
+            res = std::max(res, std::abs(g - c.grad_k.a[k]));
+        }
+        cert.max_gap = gap;
+        cert.residual = res;
+        cert.residual_computed = true;
+    }
+    return cert;
+}
+
+// certificates.hpp:152-179 -- smallest R <= r_max whose certified omitted gradient is <= tau
+// (cost nondecreasing, so the first feasible depth is the min-cost one); with an operator-norm
+// bound the sufficient test bound * ||eta_R|| <= tau replaces c_inf
+struct TailDepthSelection {
+    Index selected = -1;
+    bool used_sufficient_bound = false;
+    std::vector<BiasCertificate> trail;
+};
+
+inline TailDepthSelection select_tail_depth(const CertificateProblem& p, double tau, Index r_max,
+                                            const std::function<double(Index)>& cost =
+                                                [](Index r) { return static_cast<double>(r); },
+                                            const double* operator_norm_bound = nullptr) {
+    if (!(tau > 0)) throw std::invalid_argument("tolerance must be > 0");
+    if (r_max < 0) throw std::invalid_argument("R_max must be >= 0");
+    double prev = -std::numeric_limits<double>::infinity();
+    for (Index r = 0; r <= r_max; ++r) {
+        const double c = cost(r);
+        if (c < prev) throw std::invalid_argument("cost function must be nondecreasing");
+        prev = c;
+    }
+    TailDepthSelection sel;
+    sel.used_sufficient_bound = operator_norm_bound != nullptr;
+    for (Index r = 0; r <= r_max; ++r) {
+        BiasCertificate cert = bias_certificate(p, r, false);
+        const bool ok = operator_norm_bound ? (*operator_norm_bound * cert.eta_norm <= tau) : (cert.c_inf <= tau);
+        sel.trail.push_back(std::move(cert));
+        if (ok) {
+            sel.selected = r;
+            break;
+        }
+    }
+    return sel;
+}
+
 }  // namespace stoc

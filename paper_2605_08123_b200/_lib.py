@@ -37,7 +37,8 @@ ST_GENERIC_TAIL = 2
 EXPORTED = (
     "st_saved_bytes", "st_workspace_bytes", "st_forward", "st_backward", "st_saved_duals",
     "st_validate_support", "st_normal_fill", "st_uniform_fill", "st_last_error", "st_launch_count",
-    "st_forward_halo", "st_backward_halo",
+    "st_forward_halo", "st_backward_halo", "st_base_vjp_workspace_bytes", "st_base_solve_vjp",
+    "st_tail_adjoint",
 )
 
 
@@ -78,6 +79,12 @@ def _load() -> ctypes.CDLL:
     lib.st_backward_halo.argtypes = [P, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, I32, VP, ctypes.c_size_t,
                                      VP, HALO_FN, VP, I64, I64]
     lib.st_backward_halo.restype = ctypes.c_int
+    lib.st_tail_adjoint.argtypes = [P, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP, ctypes.c_size_t, VP]
+    lib.st_tail_adjoint.restype = ctypes.c_int
+    lib.st_base_vjp_workspace_bytes.argtypes = [P]
+    lib.st_base_vjp_workspace_bytes.restype = ctypes.c_size_t
+    lib.st_base_solve_vjp.argtypes = [P, VP, VP, VP, VP, VP, VP, VP, VP, VP, ctypes.c_size_t, VP]
+    lib.st_base_solve_vjp.restype = ctypes.c_int
     lib.st_saved_duals.argtypes = [P, VP, VP, VP, D, D, D, VP]
     lib.st_saved_duals.restype = ctypes.c_int
     lib.st_validate_support.argtypes = [P, VP, VP]

@@ -191,6 +191,7 @@ class CotangentSet:
     grad_v: torch.Tensor
     d_eps: torch.Tensor   # [B*H]
     eta_v: torch.Tensor   # base cotangent v-bar^(0), [B, H, L'_k]
+    eta_u: Optional[torch.Tensor] = None  # u-bar^(0), [B, H, L'_q] (tail_adjoint; nonzero only at R = 0)
 
 
 def _check_tensor(name: str, t: torch.Tensor, spec: BandSpec, rows: int) -> None:
@@ -251,10 +252,33 @@ def tail_adjoint(run: SurrogateRun, G: torch.Tensor, *, grads: Optional[tuple] =
     eta_v = v-bar^(0) (the base-trace cotangent; dO-weighted column sums when R = 0)."""
     if not 0 <= run.spec.tail_depth <= 8:
         raise UnsupportedDepth("the generic tail adjoint supports tail depths 0..8")
-    return _backward(run, G, _lib.ST_GENERIC_TAIL, grads, d_eps, eta_v, workspace)
+    return _backward(run, G, _lib.ST_GENERIC_TAIL, grads, d_eps, eta_v, workspace, want_eta_u=True)
 
 
-def _backward(run, G, m, grads, d_eps, eta_v, workspace) -> CotangentSet:
+def base_solve_vjp(run: SurrogateRun, eta_v: torch.Tensor, eta_u: Optional[torch.Tensor] = None, *,
+                   workspace: Optional[Workspace] = None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Pull a base-state cotangent (eta_u, eta_v) back through the T stopped base steps to (dQ, dK)
+    (base_solve_vjp, certificates.hpp:25-70).  With eta = the tail adjoint's v-bar^(0) this is the
+    omitted gradient c_R of the stopped surrogate (bias_certificate, certificates.hpp:112-118)."""
+    spec = run.spec
+    dev = run.Q.device
+    for name, t, n in (("eta_v", eta_v, spec.cols), ("eta_u", eta_u, spec.rows)):
+        if t is not None and (t.dtype != torch.float32 or not t.is_contiguous() or t.numel() != spec.batch * spec.heads * n
+                              or t.device != dev):
+            raise ValueError(f"{name} must be a contiguous f32 [B, H, {n}] tensor on {dev}")
+    gq = torch.empty((spec.batch, spec.heads, spec.rows, spec.head_dim), dtype=torch.float32, device=dev)
+    gk = torch.empty((spec.batch, spec.heads, spec.cols, spec.head_dim), dtype=torch.float32, device=dev)
+    d = spec.desc()
+    wso = workspace or _default_ws
+    ws = wso.get(int(lib.st_base_vjp_workspace_bytes(ctypes.byref(d))), dev)
+    wso.last_forward = None  # the score band in the workspace is overwritten
+    _check(lib.st_base_solve_vjp(ctypes.byref(d), _ptr(run.Q), _ptr(run.K), _ptr(run.row_mask), _ptr(run.col_mask),
+                                 _ptr(eta_u), _ptr(eta_v), _ptr(gq), _ptr(gk), _ptr(ws), ws.numel(),
+                                 torch.cuda.current_stream(dev).cuda_stream))
+    return gq, gk
+
+
+def _backward(run, G, m, grads, d_eps, eta_v, workspace, want_eta_u=False) -> CotangentSet:
     spec = run.spec
     _check_tensor("G", G, spec, spec.rows)
     dev = G.device
@@ -272,9 +296,16 @@ def _backward(run, G, m, grads, d_eps, eta_v, workspace) -> CotangentSet:
     if wso is run.workspace and wso.last_forward is run:
         # the workspace still holds this forward's score band (reference: r2_backward(run.scaled, ...))
         d.flags |= _lib.ST_FLAG_REUSE_BAND
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    if want_eta_u:  # tail_adjoint_generic: the whole base cotangent
+        eta_u = torch.empty((spec.batch, spec.heads, spec.rows), dtype=torch.float32, device=dev)
+        _check(lib.st_tail_adjoint(ctypes.byref(d), _ptr(run.saved), _ptr(run.Q), _ptr(run.K), _ptr(run.V), _ptr(G),
+                                   _ptr(run.row_mask), _ptr(run.col_mask), _ptr(dQ), _ptr(dK), _ptr(dV),
+                                   _ptr(d_eps), _ptr(eta_u), _ptr(eta_v), _ptr(ws), ws.numel(), stream))
+        return CotangentSet(dQ, dK, dV, d_eps, eta_v, eta_u)
     _check(lib.st_backward(ctypes.byref(d), _ptr(run.saved), _ptr(run.Q), _ptr(run.K), _ptr(run.V), _ptr(G),
                            _ptr(run.row_mask), _ptr(run.col_mask), _ptr(dQ), _ptr(dK), _ptr(dV), _ptr(d_eps),
-                           _ptr(eta_v), m, _ptr(ws), ws.numel(), torch.cuda.current_stream(dev).cuda_stream))
+                           _ptr(eta_v), m, _ptr(ws), ws.numel(), stream))
     return CotangentSet(dQ, dK, dV, d_eps, eta_v)
 
 

@@ -35,6 +35,7 @@ struct Dims {
     long BH, Lq, Lk, Lrq, Lrk, d, w, Wf;
     int esz = 4, dustbin = 0;  // input element bytes, dustbin flag
     long R = 2;                // tail depth
+    long T = 0;                // base depth
 };
 
 st_status check_desc(const st_desc* d, Dims& o) {
@@ -74,6 +75,7 @@ st_status check_desc(const st_desc* d, Dims& o) {
     o.esz = d->dtype == ST_BF16 ? 2 : 4;
     o.dustbin = d->dustbin;
     o.R = d->tail_depth;
+    o.T = d->base_depth;
     if ((double)o.BH * o.Lq * o.Wf > 4.0e9 || o.Lrq > (1L << 30) || o.Lrk > (1L << 30))
         return fail(ST_SIZE_CAP_EXCEEDED, "problem exceeds the 32-bit index space of the kernels");
     return ST_OK;
@@ -328,6 +330,11 @@ void band_record(const void* ws, const void* Q, const void* K, const void* rm, c
     g_band[ws] = BandKey{Q, K, rm, cm, *d, hasT};
 }
 // 0: nothing reusable, 1: S2 band, 2: S2 and S2T
+void band_forget(const void* ws) {
+    std::lock_guard<std::mutex> lk(g_band_mu);
+    g_band.erase(ws);
+}
+
 int band_valid(const void* ws, const void* Q, const void* K, const void* rm, const void* cm, const st_desc* d) {
     std::lock_guard<std::mutex> lk(g_band_mu);
     auto it = g_band.find(ws);
@@ -604,7 +611,7 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
                                const void* V, const void* dO, const uint8_t* row_mask, const uint8_t* col_mask,
                                float* dQ, float* dK, float* dV, float* d_eps, float* eta_v, int32_t mode,
                                void* workspace, size_t workspace_bytes, void* stream, st_halo_fn hook, void* user,
-                               int64_t own_begin, int64_t own_end) {
+                               int64_t own_begin, int64_t own_end, float* eta_u = nullptr) {
     Dims m;
     st_status s = check_desc(desc, m);
     if (s != ST_OK) return s;
@@ -696,6 +703,8 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
             }
             if (eta_v) tp.vb[0] = eta_v;  // eta = vb_0
             tp.g_u = p.g_u;
+            tp.eta_u = eta_u;
+            if (eta_u && m.R >= 1) ST_CUDA(cudaMemsetAsync(eta_u, 0, sizeof(float) * m.BH * m.Lrq, st));  // ub_0 = 0
             ST_CUDA(st::launch_tail_adjoint(g, desc->dtype, tp, p.S2, S2T, Z, ZT, Q, K, V, dO, dQ, dK, dV,
                                             p.deps_part, st, nl));
         } else {
@@ -743,6 +752,128 @@ st_status st_backward_halo(const st_desc* desc, const void* saved, const void* Q
                            int64_t own_end) {
     return backward_impl(desc, saved, Q, K, V, dO, row_mask, col_mask, dQ, dK, dV, d_eps, eta_v, mode, workspace,
                          workspace_bytes, stream, hook, user, own_begin, own_end);
+}
+
+// ---- base_solve_vjp (certificates.hpp:25-70) --------------------------------------------------------
+struct BaseVjpLayout {
+    size_t hu, hv, ab, vb0, vb1, zero, bytes;
+};
+static BaseVjpLayout base_vjp_layout(const Dims& m, size_t base) {
+    BaseVjpLayout b;
+    size_t o = align_up(base);
+    auto take = [&](size_t n) {
+        const size_t at = o;
+        o = align_up(o + n);
+        return at;
+    };
+    const size_t rq = sizeof(float) * m.BH * m.Lrq, rk = sizeof(float) * m.BH * m.Lrk;
+    const size_t T1 = (size_t)std::max<long>(m.T, 0) + 1;
+    b.hu = take(rq * T1);
+    b.hv = take(rk * T1);
+    b.ab = take(rq);
+    b.vb0 = take(rk);
+    b.vb1 = take(rk);
+    b.zero = take(rq);
+    b.bytes = o;
+    return b;
+}
+
+size_t st_base_vjp_workspace_bytes(const st_desc* desc) {
+    Dims m;
+    if (check_desc(desc, m) != ST_OK) return 0;
+    return base_vjp_layout(m, ws_layout(m, tc_plan(desc, m)).bytes).bytes;
+}
+
+st_status st_base_solve_vjp(const st_desc* desc, const void* Q, const void* K, const uint8_t* row_mask,
+                            const uint8_t* col_mask, const float* eta_u, const float* eta_v, float* dQ, float* dK,
+                            void* workspace, size_t workspace_bytes, void* stream) {
+    Dims m;
+    st_status s = check_desc(desc, m);
+    if (s != ST_OK) return s;
+    if (!Q || !K || !eta_v || !dQ || !dK) return fail(ST_INVALID_ARGUMENT, "null tensor pointer");
+    if (desc->dustbin) return fail(ST_NOT_SUPPORTED, "base_solve_vjp has no dustbin variant");
+    const WsLayout wl = ws_layout(m, tc_plan(desc, m));
+    const BaseVjpLayout bl = base_vjp_layout(m, wl.bytes);
+    if (workspace == nullptr || workspace_bytes < bl.bytes)
+        return fail(ST_WORKSPACE_TOO_SMALL, "workspace smaller than st_base_vjp_workspace_bytes()");
+    cudaStream_t st = (cudaStream_t)stream;
+    char* ws = (char*)workspace;
+    const st::Geo g = make_geo(desc, m, row_mask, col_mask);
+    if (!st::bwdT_supported(g) || st::stepT_smem_bytes(g) > 227 * 1024)
+        return fail(ST_NOT_SUPPORTED, "base_solve_vjp needs d in {32, 64, 128} and a band tile that fits SMEM");
+    const long T = desc->base_depth;
+    const size_t nq = (size_t)m.BH * m.Lrq, nk = (size_t)m.BH * m.Lrk;
+    if (T == 0) {  // the cold start does not depend on the parameters
+        ST_CUDA(cudaMemsetAsync(dQ, 0, sizeof(float) * nq * m.d, st));
+        ST_CUDA(cudaMemsetAsync(dK, 0, sizeof(float) * nk * m.d, st));
+        return ST_OK;
+    }
+    float* S2 = (float*)(ws + wl.S2);
+    float* S2T = (float*)(ws + wl.S2T);
+    float* hu = (float*)(ws + bl.hu);
+    float* hv = (float*)(ws + bl.hv);
+    int* err = (int*)(ws + wl.err);
+    ST_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+    ST_CUDA(cudaMemsetAsync(hu, 0, sizeof(float) * nq, st));  // cold start u_0 = v_0 = 0
+    ST_CUDA(cudaMemsetAsync(hv, 0, sizeof(float) * nk, st));
+    ST_CUDA(cudaMemsetAsync(ws + bl.zero, 0, sizeof(float) * nq, st));
+    band_forget(workspace);  // the score band below is overwritten
+    // the base solve again, keeping every step's duals (the reference's DualTrace history)
+    std::vector<float> lam((size_t)T + 1, 1.f);
+    float band_lam = 0.f;
+    long long nl = 0;
+    for (long t = 1; t <= T; ++t) {
+        lam[(size_t)t] = step_scale(desc, t);
+        st::Geo gs = g;
+        gs.c2 = g.c2 * lam[(size_t)t];
+        if (lam[(size_t)t] != band_lam) {
+            if (st::band_dual_supported(g)) {
+                ST_CUDA(st::launch_band_dual(gs, desc->dtype, false, Q, K, S2, S2T, st));
+            } else {
+                ST_CUDA(st::launch_scores(gs, desc->dtype, Q, K, S2, st));
+                ST_CUDA(st::launch_transpose_band(g, S2, S2T, st, -INFINITY));
+            }
+            band_lam = lam[(size_t)t];
+        }
+        float* u_out = hu + (size_t)t * nq;
+        float* v_out = hv + (size_t)t * nk;
+        const float* u_prev = hu + (size_t)(t - 1) * nq;
+        const float* v_prev = hv + (size_t)(t - 1) * nk;
+        ST_CUDA(st::launch_stepT(gs, t == 1, S2, v_prev, u_prev, u_out, err, st));
+        ST_CUDA(st::launch_stepT(st::transposed(gs), t == 1, S2T, u_out, v_prev, v_out, err, st));
+        nl += 2;
+    }
+    st::BaseVjpPtrs p{};
+    p.T = (int)T;
+    p.hu = hu;
+    p.hv = hv;
+    p.lam = lam.data();
+    p.Q = Q;
+    p.K = K;
+    p.S2 = S2;
+    p.S2T = S2T;
+    p.A = (float*)(ws + wl.Z);
+    p.AT = (float*)(ws + wl.ZT);
+    p.eta_u = eta_u;
+    p.eta_v = eta_v;
+    p.ab = (float*)(ws + bl.ab);
+    p.vb[0] = (float*)(ws + bl.vb0);
+    p.vb[1] = (float*)(ws + bl.vb1);
+    p.zero_u = (float*)(ws + bl.zero);
+    p.dQ = dQ;
+    p.dK = dK;
+    p.deps_part = (float*)(ws + wl.deps);
+    ST_CUDA(st::launch_base_vjp(g, desc->dtype, p, st, nl));
+    st::add_launches(nl);
+    return ST_OK;
+}
+
+st_status st_tail_adjoint(const st_desc* desc, const void* saved, const void* Q, const void* K, const void* V,
+                          const void* dO, const uint8_t* row_mask, const uint8_t* col_mask, float* dQ, float* dK,
+                          float* dV, float* d_eps, float* eta_u, float* eta_v, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+    return backward_impl(desc, saved, Q, K, V, dO, row_mask, col_mask, dQ, dK, dV, d_eps, eta_v, ST_GENERIC_TAIL,
+                         workspace, workspace_bytes, stream, nullptr, nullptr, 0, -1, eta_u);
 }
 
 st_status st_saved_duals(const st_desc* desc, const void* saved, const uint8_t* row_mask_host,

@@ -1197,6 +1197,10 @@ static cudaError_t run_tail(const Geo& g, const TailPtrs& tp, const float* S2, c
     bind(R, R);
     a.g_v = tp.vb[R];
     ST_RUN(C1);
+    if (R == 0 && tp.eta_u) {  // base cotangent u part: g_u = rowsum(P^(TT) (.) Z)
+        a.g_u = tp.eta_u;
+        ST_RUN(R1);
+    }
     if (R >= 1) {  // ub_R = g_u - P^(RR) vb_R
         a.g_u = tp.g_u;
         a.u2b = tp.ub[R];
@@ -1236,6 +1240,111 @@ cudaError_t launch_tail_adjoint(const Geo& g, int dtype, const TailPtrs& tp, con
     if (g.d == 64) { ST_TAIL(64) }
     ST_TAIL(128)
 #undef ST_TAIL
+}
+
+// ---------------------------------------------------------------------------
+// base_solve_vjp (certificates.hpp:25-70): the reverse recurrences through the T base steps.  Step h
+// (band at eps_h): abar = ubar - P^(h,h) vbar (row stage), vbar <- -P^(h,h-1)^T abar (column stage),
+// and the raw-score cotangent band gains -(eps/eps_h) [P^(h,h) (.) vbar_j + P^(h,h-1) (.) abar_i]
+// (k_base_acc; stored times eps so the RW / CW contraction's 1/(sqrt(d) eps) gives grad = raw_bar K/sqrt(d)).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_base_acc(Geo g, const float* __restrict__ S2, float* __restrict__ A,
+                                                  const float* __restrict__ uh, const float* __restrict__ vh,
+                                                  const float* __restrict__ vhm1, const float* __restrict__ vb,
+                                                  const float* __restrict__ ab, float coef, int init) {
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long total = (long)g.BH * g.Lqp * g.Wf;
+    if (t >= total) return;
+    const int k = (int)(t % g.Wf);
+    const long ri = t / g.Wf;
+    const int i = (int)(ri % g.Lqp), bh = (int)(ri / g.Lqp);
+    const int j = i - g.w + k;
+    const float s2 = S2[t];
+    float acc = init ? 0.f : A[t];
+    if (i < g.Lq && j >= 0 && j < g.Lk && s2 != -INFINITY) {
+        const size_t oi = (size_t)bh * g.Lrq + i, oj = (size_t)bh * g.Lrk + j;
+        const float u = uh[oi];
+        acc -= coef * (ex2(s2 + u + vh[oj]) * vb[oj] + ex2(s2 + u + vhm1[oj]) * ab[oi]);
+    }
+    A[t] = acc;
+}
+
+template <int D, class TIn>
+static cudaError_t run_base_vjp(const Geo& g, int dtype, const BaseVjpPtrs& p, cudaStream_t s, long long& launches) {
+    const size_t nq = (size_t)g.BH * g.Lrq, nk = (size_t)g.BH * g.Lrk;
+    auto hu = [&](int h) { return p.hu + (size_t)h * nq; };
+    auto hv = [&](int h) { return p.hv + (size_t)h * nk; };
+    BT<TIn> a{};
+    a.Q = (const TIn*)p.Q;
+    a.K = (const TIn*)p.K;
+    a.dQ = p.dQ;
+    a.dK = p.dK;
+    a.deps_part = p.deps_part;
+    a.fuse_c5 = 0;
+    cudaError_t e;
+#define ST_RUN(op)                                                              \
+    do {                                                                        \
+        if ((e = run_op<op, false, D, TIn>(g, a, s)) != cudaSuccess) return e; \
+        ++launches;                                                             \
+    } while (0)
+    float band_lam = 0.f;
+    const float* vcur = p.eta_v;
+    const long total = (long)g.BH * g.Lqp * g.Wf;
+    for (int h = p.T; h >= 1; --h) {
+        const float lam = p.lam[h];
+        Geo gs = g;
+        gs.c2 = g.c2 * lam;
+        if (lam != band_lam) {  // scores at this step's stage temperature
+            if (band_dual_supported(g)) {
+                if ((e = launch_band_dual(gs, dtype, false, p.Q, p.K, p.S2, p.S2T, s)) != cudaSuccess) return e;
+            } else {
+                if ((e = launch_scores(gs, dtype, p.Q, p.K, p.S2, s)) != cudaSuccess) return e;
+                if ((e = launch_transpose_band(g, p.S2, p.S2T, s, -INFINITY)) != cudaSuccess) return e;
+            }
+            band_lam = lam;
+        }
+        a.S2 = p.S2;
+        a.S2T = p.S2T;
+        // abar = ubar - P^(h,h) vbar: R2 with g_u = ubar (step T: eta_u) ...
+        a.u1 = a.u2 = hu(h);
+        a.v0 = a.v1 = a.v2 = hv(h);
+        a.g_v = const_cast<float*>(vcur);
+        a.g_u = (h == p.T && p.eta_u) ? const_cast<float*>(p.eta_u) : p.zero_u;
+        a.u2b = p.ab;
+        ST_RUN(R2);
+        float* vnext = p.vb[h & 1];
+        k_base_acc<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(gs, p.S2, p.A, hu(h), hv(h), hv(h - 1), vcur, p.ab,
+                                                                   lam, h == p.T);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        ++launches;
+        // ... vbar <- -P^(h,h-1)^T abar: C3 on the plan (u_h, v_{h-1})
+        a.v0 = a.v1 = a.v2 = hv(h - 1);
+        a.u2b = p.ab;
+        a.v1b = vnext;
+        ST_RUN(C3);
+        vcur = vnext;
+    }
+    if ((e = launch_transpose_band(g, p.A, p.AT, s, 0.f)) != cudaSuccess) return e;
+    a.S2 = p.S2;
+    a.S2T = p.S2T;
+    a.Z = p.A;
+    a.ZT = p.AT;
+    a.u1 = a.u2 = hu(p.T);
+    a.v0 = a.v1 = a.v2 = hv(p.T);
+    ST_RUN(RW);
+    ST_RUN(CW);
+#undef ST_RUN
+    return cudaSuccess;
+}
+
+cudaError_t launch_base_vjp(const Geo& g, int dtype, const BaseVjpPtrs& p, cudaStream_t s, long long& launches) {
+    if (g.dustbin || p.T < 1) return cudaErrorNotSupported;
+#define ST_BV(D) \
+    return dtype == 0 ? run_base_vjp<D, float>(g, dtype, p, s, launches) : run_base_vjp<D, __nv_bfloat16>(g, dtype, p, s, launches);
+    if (g.d == 32) { ST_BV(32) }
+    if (g.d == 64) { ST_BV(64) }
+    ST_BV(128)
+#undef ST_BV
 }
 
 // O = P^(T+R,T+R) V on the stored band (apply_transport, sinkhorn.hpp:262-277): the RO row stage

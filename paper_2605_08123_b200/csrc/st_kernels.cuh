@@ -82,12 +82,26 @@ struct TailPtrs {
     const float* v[kMaxTailSteps + 1];
     float* ub[kMaxTailSteps + 1];
     float* vb[kMaxTailSteps + 1];
-    float* g_u;  // scratch [BH][Lrq]
+    float* g_u;    // scratch [BH][Lrq]
+    float* eta_u;  // R = 0: the base cotangent's u part g_u (may be null)
 };
 cudaError_t launch_tail_adjoint(const Geo& g, int dtype, const TailPtrs& tp, const float* S2, const float* S2T,
                                 float* Z, float* ZT, const void* Q, const void* K, const void* V, const void* dO,
                                 float* dQ, float* dK, float* dV, float* deps_part, cudaStream_t s,
                                 long long& launches);
+// base_solve_vjp (certificates.hpp:25-70): hu / hv = the base duals u_h, v_h of steps h = 0..T
+// ([T+1][BH][Lr], base 2); lam[h] = eps / eps_h (host, h = 1..T)
+struct BaseVjpPtrs {
+    int T;
+    const float *hu, *hv;
+    const float* lam;
+    const void *Q, *K;
+    float *S2, *S2T, *A, *AT;  // score band (+T) at the running stage; raw-score cotangent band (+T)
+    const float *eta_u, *eta_v;
+    float *ab, *vb[2], *zero_u;
+    float *dQ, *dK, *deps_part;
+};
+cudaError_t launch_base_vjp(const Geo& g, int dtype, const BaseVjpPtrs& p, cudaStream_t s, long long& launches);
 cudaError_t launch_output_tile(const Geo& g, int dtype, const float* S2, const float* u, const float* v, const void* V,
                                float* O, cudaStream_t s);
 // the dustbin row / column of one backward stage through the generic sweeps

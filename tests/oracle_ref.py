@@ -130,3 +130,40 @@ def run_rect(Lq, Lk, d, w, eps, T, R, Q, K, V, G, row_mask=None, col_mask=None, 
     if code != 0:
         raise OracleError(code, lib().stoc_last_error().decode())
     return out
+
+
+def run_cert(cfg, Q, K, V, G, row_mask=None, col_mask=None, *, heads=None, precision=64, eps_schedule=None):
+    """Generic tail adjoint + base_solve_vjp of its base cotangent per head (the bias certificate's
+    c_R = (cQ, cK), certificates.hpp:112-118).  Q, K, V, G: [nh, L, d] (no dustbin); masks [B, L]."""
+    L_ = lib()
+    if not hasattr(L_, "_cert"):
+        D = ctypes.POINTER(ctypes.c_double)
+        I64 = ctypes.c_int64
+        L_.stoc_run_batch_cert.argtypes = [I64, I64, I64, I64, I64, I64, I64, ctypes.c_double, D, D, D, D,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, D, D, D, D, D, D, D, D, D]
+        L_.stoc_run_batch_cert.restype = ctypes.c_int
+        L_._cert = True
+    Q, K, V, G = (np.ascontiguousarray(x, dtype=np.float64) for x in (Q, K, V, G))
+    nh, Lr, d = Q.shape
+    heads = range(nh) if heads is None else heads
+    sel = np.array([h // cfg.H for h in heads], dtype=np.int64)
+    rm = None if row_mask is None else np.ascontiguousarray(np.asarray(row_mask)[sel], dtype=np.uint8)
+    cm = None if col_mask is None else np.ascontiguousarray(np.asarray(col_mask)[sel], dtype=np.uint8)
+    out = {k: np.zeros_like(Q) for k in ("O", "dQ", "dK", "dV", "cQ", "cK")}
+    out["d_eps"] = np.zeros(nh)
+    out["eta_v"] = np.zeros((nh, Lr))
+    out["eta_u"] = np.zeros((nh, Lr))
+    se = None if not eps_schedule else np.array([e for e, _ in eps_schedule], dtype=np.float64)
+    si = None if not eps_schedule else np.array([n for _, n in eps_schedule], dtype=np.int64)
+    P = ctypes.POINTER(ctypes.c_double)
+    p = lambda a: a.ctypes.data_as(P)
+    code = L_.stoc_run_batch_cert(nh, 1, cfg.L, d, cfg.w, cfg.T, cfg.R, cfg.eps, p(Q), p(K), p(V), p(G),
+                                  None if rm is None else rm.ctypes.data, None if cm is None else cm.ctypes.data,
+                                  precision, os.cpu_count() or 1, 0 if se is None else len(se),
+                                  None if se is None else se.ctypes.data, None if si is None else si.ctypes.data,
+                                  p(out["O"]), p(out["dQ"]), p(out["dK"]), p(out["dV"]), p(out["d_eps"]),
+                                  p(out["eta_u"]), p(out["eta_v"]), p(out["cQ"]), p(out["cK"]))
+    if code != 0:
+        raise OracleError(code, lib().stoc_last_error().decode())
+    return out

@@ -378,3 +378,62 @@ def test_generic_tail_matches_r2_path():
     b = gpu_run(cfg, inp, mode="one_reference", duals=False)
     for k in KEYS:
         assert rel(a[k], b[k]) <= (DEPS_TOL if k == "d_eps" else 2e-5), (k, rel(a[k], b[k]))
+
+
+def _cert_inputs(cfg, inp):
+    nh = len(inp.heads)
+    shp = (cfg.B, cfg.H, cfg.rows, cfg.d)
+    b = inp.bits or {}
+    dev = {k: _dev(getattr(inp, k), b.get(k)).reshape(shp) for k in ("Q", "K", "V", "G")}
+    rm = None if inp.row_mask is None else torch.from_numpy(inp.row_mask).cuda()
+    cm = None if inp.col_mask is None else torch.from_numpy(inp.col_mask).cuda()
+    return dev, rm, cm, nh
+
+
+@pytest.mark.parametrize("R,d,dtype,mask,sched", [(2, 64, "f32", "uniform_len", None), (0, 32, "f32", "none", None),
+                                                  (1, 64, "f32", "none", [(0.6, 4), (0.3, 6)]),
+                                                  (3, 128, "bf16", "uniform_len", None)])
+def test_base_solve_vjp_parity(R, d, dtype, mask, sched):
+    """base_solve_vjp of the tail adjoint's base cotangent (the bias certificate's c_R,
+    certificates.hpp:25-70 / :112-118) against the oracle, including an epsilon schedule."""
+    from paper_2605_08123_b200 import certificates
+    cfg = configs.Config(0, B=2, H=2, L=260, d=d, w=20, eps=0.3, T=10, R=R, dtype=dtype, mask=mask)
+    inp = configs.make_inputs(cfg)
+    t, rm, cm, nh = _cert_inputs(cfg, inp)
+    spec = band.BandSpec(batch=cfg.B, heads=cfg.H, seq_q=cfg.L, seq_k=cfg.L, head_dim=d, half_band=cfg.w,
+                         base_depth=cfg.T, tail_depth=R, epsilon=cfg.eps, dtype=dtype, eps_schedule=sched)
+    cert = certificates.bias_certificate(t["Q"], t["K"], t["V"], t["G"], spec, R, rm, cm)
+    torch.cuda.synchronize()
+    r = oracle_ref.run_cert(cfg, inp.Q, inp.K, inp.V, inp.G, inp.row_mask, inp.col_mask, eps_schedule=sched)
+    r32 = oracle_ref.run_cert(cfg, inp.Q, inp.K, inp.V, inp.G, inp.row_mask, inp.col_mask, precision=32,
+                              eps_schedule=sched)
+    tol = BF16_TOL if dtype == "bf16" else FP32_TOL
+    for k, g in (("cQ", cert.c_q), ("cK", cert.c_k)):
+        g = g.cpu().numpy().astype(np.float64).reshape(nh, cfg.rows, d)
+        e, fl = rel(g, r[k]), rel(r32[k], r[k])
+        print(f"base vjp R={R} {k}: rel-L2 gpu {e:.2e} ref-f32 {fl:.2e}")
+        assert e <= max(tol, 1.5 * fl), (k, e, fl)
+    eta = np.sqrt(np.sum(r["eta_v"] ** 2, axis=1) + np.sum(r["eta_u"] ** 2, axis=1))
+    assert np.allclose(cert.eta_norm.cpu().numpy(), eta, rtol=max(tol, 1e-4) * 10)
+
+
+def test_certificate_eta_decays_and_selector_is_first_feasible():
+    """test_certificates.cpp:76-86 / :106-133 on the device path: ||eta_R|| strictly decreases with
+    R, and the selector returns the first depth an exhaustive scan finds feasible."""
+    from paper_2605_08123_b200 import certificates
+    cfg = configs.Config(0, B=1, H=2, L=200, d=32, w=16, eps=0.5, T=10, R=2, dtype="f32")
+    inp = configs.make_inputs(cfg)
+    t, rm, cm, _ = _cert_inputs(cfg, inp)
+    spec = band.BandSpec(batch=1, heads=2, seq_q=cfg.L, seq_k=cfg.L, head_dim=cfg.d, half_band=cfg.w,
+                         base_depth=cfg.T, tail_depth=2, epsilon=cfg.eps)
+    certs = [certificates.bias_certificate(t["Q"], t["K"], t["V"], t["G"], spec, r) for r in range(5)]
+    eta = np.array([c.eta_norm.cpu().numpy() for c in certs])
+    assert np.all(np.diff(eta, axis=0) < 0), eta
+    c_inf = [float(c.c_inf.max()) for c in certs]
+    for tau in (1e3, c_inf[2] * 1.5, c_inf[4] * 0.5):
+        s = certificates.select_tail_depth(t["Q"], t["K"], t["V"], t["G"], spec, tau, 4)
+        want = next((r for r in range(5) if c_inf[r] <= tau), -1)
+        assert s.selected == want, (tau, s.selected, want, c_inf)
+    s = certificates.select_tail_depth(t["Q"], t["K"], t["V"], t["G"], spec, float(eta[1].max()) * 1.01, 4,
+                                       operator_norm_bound=1.0)
+    assert s.used_sufficient_bound and s.selected == 1
