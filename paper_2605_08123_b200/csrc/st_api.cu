@@ -174,7 +174,7 @@ TcPlan tc_plan(const st_desc* d, const Dims& m) {
 struct WsLayout {
     size_t Z, ZT, Zd, ZdT;  // tile backward bands
     size_t S2, S2T, u, v, g_u, u2b, u1b, deps, g_v, v1b, v0b, err;
-    size_t qp[3], kp[3], flags, work_q, work_k, cnt;
+    size_t qp[3], kp[3], flags, work_q, work_k, cnt, pad_u, pad_v;
     size_t vb2, part[2], partm;  // fused-step ping-pong duals and column partials
     size_t fs_flags, fs_work, fs_cnt, fs_part[2], fs_partm;  // persistent solve: work list, tagged partials
     size_t tail_u, tail_v;  // generic-R adjoint: (R+1) row / column cotangent vectors
@@ -228,7 +228,7 @@ WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
     w.tail_u = take(rq * (size_t)(m.R + 1));
     w.tail_v = take(rk * (size_t)(m.R + 1));
     for (int p = 0; p < 3; ++p) w.qp[p] = w.kp[p] = 0;
-    w.flags = w.work_q = w.work_k = w.cnt = 0;
+    w.flags = w.work_q = w.work_k = w.cnt = w.pad_u = w.pad_v = 0;
     w.vb2 = take(rk);
     {
         const size_t np = sizeof(float) * (size_t)m.BH * ((m.Lq + 127) / 128) * (128 + 2 * m.w);
@@ -253,6 +253,8 @@ WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
         w.work_q = take(sizeof(int) * (size_t)m.BH * tp.NBq);
         w.work_k = take(sizeof(int) * (size_t)m.BH * tp.NBk);
         w.cnt = take(sizeof(int) * 2);
+        w.pad_u = take(sizeof(float) * (size_t)m.BH * (tp.CR + tp.Lpq));
+        w.pad_v = take(sizeof(float) * (size_t)m.BH * (tp.CR + tp.Lpk));
     }
     w.bytes = o;
     return w;
@@ -407,8 +409,15 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
         ST_CUDA(st::launch_pack(desc->dtype, K, g.BH, g.Lk, g.Lrk, tp.Lpk, g.d, tp.shift, kp[0], kp[1], kp[2], st));
         ST_CUDA(st::launch_worklist(row_mask, g.H, g.BH, g.Lq, tp.NBq, flags, work_q, cnt, st));
         ST_CUDA(st::launch_worklist(col_mask, g.H, g.BH, g.Lk, tp.NBk, flags, work_k, cnt + 1, st));
+        // masked padded dual buffers (the producer bulk-copies dual windows from them): cold start
+        float* pad_u = (float*)(ws + wl.pad_u);
+        float* pad_v = (float*)(ws + wl.pad_v);
+        const int pad_ld_q = tp.CR + tp.Lpq, pad_ld_k = tp.CR + tp.Lpk;
+        ST_CUDA(st::launch_pad_fill(pad_u, nullptr, g.BH, g.H, g.Lq, g.Lrq, pad_ld_q, tp.CR, row_mask, st));
+        ST_CUDA(st::launch_pad_fill(pad_v, nullptr, g.BH, g.H, g.Lk, g.Lrk, pad_ld_k, tp.CR, col_mask, st));
         st::PhaseArgs pr{};
         pr.npl = tp.npl;
+        pr.pad_off = tp.CR;
         pr.CR = tp.CR;
         pr.shift = tp.shift;
         pr.NA = tp.NA;
@@ -427,6 +436,7 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
         pr.L_own = g.Lq; pr.L_other = g.Lk; pr.Lr_own = g.Lrq; pr.Lr_other = g.Lrk;
         pr.Lp_own = tp.Lpq; pr.Lp_other = tp.Lpk;
         pr.mask_own = row_mask; pr.mask_other = col_mask;
+        pr.pad_own = pad_u; pr.pad_other = pad_v; pr.pad_ld_own = pad_ld_q; pr.pad_ld_other = pad_ld_k;
         for (int p = 0; p < 3; ++p) { pr.A_pack[p] = qp[p]; pr.B_pack[p] = kp[p]; }
         pr.work = work_q; pr.nwork = cnt;
         // column phase: own = keys (A = K block), other = queries (B = Q window)
@@ -434,6 +444,7 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
         pc.L_own = g.Lk; pc.L_other = g.Lq; pc.Lr_own = g.Lrk; pc.Lr_other = g.Lrq;
         pc.Lp_own = tp.Lpk; pc.Lp_other = tp.Lpq;
         pc.mask_own = col_mask; pc.mask_other = row_mask;
+        pc.pad_own = pad_v; pc.pad_other = pad_u; pc.pad_ld_own = pad_ld_k; pc.pad_ld_other = pad_ld_q;
         for (int p = 0; p < 3; ++p) { pc.A_pack[p] = kp[p]; pc.B_pack[p] = qp[p]; }
         pc.work = work_k; pc.nwork = cnt + 1;
         st::DustArgs dr{}, dc{};
@@ -458,14 +469,20 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
                 dr.dual_other = v_prev; dr.off_own = u_prev; dr.out_own = u_out;
                 ST_CUDA(st::launch_dustbin(dr, t == 1, g.BH, st));
             }
-            halo(0, u_out);
+            if (hook) {  // the halo exchange completed u_out's boundary entries: refresh the padded copy
+                halo(0, u_out);
+                ST_CUDA(st::launch_pad_fill(pad_u, u_out, g.BH, g.H, g.Lq, g.Lrq, pad_ld_q, tp.CR, row_mask, st));
+            }
             pc.dual_other = u_out; pc.off_own = v_prev; pc.out_own = v_out;
             ST_CUDA(st::launch_phase(pc, t == 1, grid, st));
             if (g.dustbin) {
                 dc.dual_other = u_out; dc.off_own = v_prev; dc.out_own = v_out;
                 ST_CUDA(st::launch_dustbin(dc, t == 1, g.BH, st));
             }
-            halo(1, v_out);
+            if (hook) {
+                halo(1, v_out);
+                ST_CUDA(st::launch_pad_fill(pad_v, v_out, g.BH, g.H, g.Lk, g.Lrk, pad_ld_k, tp.CR, col_mask, st));
+            }
             u_prev = u_out;
             v_prev = v_out;
         }

@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kThreads) k_fsolve(Geo g, FSolve f) {
                 const float* src = f.S2 + ((size_t)bh * g.Lqp + i0) * Wf;
                 for (int e = tid; e < 128 * Wf; e += kThreads) {
                     const int rr = e / Wf;
-                    tile[rr * P + (e - rr * Wf)] = __ldcs(src + e);
+                    tile[rr * P + (e - rr * Wf)] = (i0 + rr < g.Lq) ? __ldcs(src + e) : -INFINITY;  // pad rows unwritten
                 }
                 for (int rr = tid; rr < 128; rr += kThreads) tile[rr * P + Wf] = -INFINITY;
             }
@@ -373,8 +373,11 @@ constexpr int kTmGroups = 3;  // tiles (warp groups) per CTA: 3 x 128 TMEM colum
 
 struct TmGeo {
     int P, P2;
-    // pitch 130 for every Wf <= 129: the row pass writes all 128 TMEM cells (+1), 8-byte aligned rows
-    __host__ __device__ TmGeo(int Wf, int Nw) : P(kTmCols + 2), P2(((Nw + 2 + 31) / 32) * 32 + 16) { (void)Wf; }
+    // pitch 130 for every Wf <= 129: the row pass writes all 128 TMEM cells (+1), 8-byte aligned rows.
+    // The row pass reads the window duals of all 128 TMEM cells of its row (vw[r + k], k < 128) even
+    // when the band is narrower, so the -inf-filled window vectors span at least 2 * 128 entries.
+    __host__ __device__ TmGeo(int Wf, int Nw)
+        : P(kTmCols + 2), P2(max(((Nw + 2 + 31) / 32) * 32, 2 * kTmCols + 2) + 16) { (void)Wf; }
     // e tile [128][P] | extra cells [128] | vw0 [P2] | vw1 [P2] | csum [2][Nw] | cmax [2][Nw]
     __host__ __device__ size_t floats(int Nw) const { return (size_t)128 * P + 128 + 2 * (size_t)P2 + 4 * (size_t)Nw; }
 };
@@ -430,7 +433,7 @@ __global__ void __launch_bounds__(kTmGroups * kThreads, 1) k_fsolve_tm(Geo g, FS
                 const float* src = f.S2 + ((size_t)bh * g.Lqp + i0) * Wf;
                 for (int e = tid; e < 128 * Wf; e += kThreads) {
                     const int rr = e / Wf;
-                    et[rr * P + (e - rr * Wf)] = __ldcs(src + e);
+                    et[rr * P + (e - rr * Wf)] = (i0 + rr < g.Lq) ? __ldcs(src + e) : -INFINITY;  // pad rows unwritten
                 }
                 gsync();
 #pragma unroll

@@ -23,6 +23,7 @@
 //               block ahead into a double-buffered SMEM slot
 // Offsets: cold start uses an online running max; every later step uses the
 // previous dual of the same row (terms <= 1, sums in [1/W, W]).
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -36,11 +37,15 @@ using namespace sm100;
 
 namespace {
 
+constexpr int kNV = 3;  // dual-window ring slots
+
 struct Smem {
     uint8_t* A;       // [NA][npl][128 * row_bytes]
     uint8_t* K;       // [NSK][npl][CR * row_bytes]
-    float* vwin;      // [2][maxwin]
-    float* part;      // [3][256] partial (sum, max) of the column parts 1..3
+    float* vwin;      // [kNV][maxwin + 128]: the block's window duals, then its 128 own previous duals
+    float* part;      // [2][3][256] partial (sum, max) of the column parts 1..3, by block parity
+    uint64_t* v_full;
+    uint64_t* v_empty;
     uint64_t* a_full;
     uint64_t* a_empty;
     uint64_t* k_full;
@@ -56,8 +61,11 @@ __device__ __forceinline__ Smem carve(uint8_t* base, const PhaseArgs& a, int nst
     s.A = base;
     s.K = s.A + (size_t)a.NA * a.npl * blk;
     s.vwin = (float*)(s.K + (size_t)a.NSK * a.npl * chk);
-    s.part = s.vwin + 2 * a.maxwin;
-    uint64_t* bars = (uint64_t*)(s.part + 768);
+    s.part = s.vwin + kNV * (a.maxwin + 128);
+    uint64_t* bars = (uint64_t*)(s.part + 1536);
+    s.v_full = bars;
+    s.v_empty = bars + kNV;
+    bars += 2 * kNV;
     s.a_full = bars;
     s.a_empty = bars + 2;
     s.k_full = bars + 4;
@@ -98,10 +106,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
         if (a.trace && blockIdx.x < 16 && (slot) < 64) a.trace[blockIdx.x * 64 + (slot)] = gtimer(); \
     } while (0)
 
-__device__ __forceinline__ float window_dual(const PhaseArgs& a, int bh, int j) {
-    if (j < 0 || j >= a.L_other || !on_mask(a.mask_other, a.H, a.L_other, bh, j)) return -INFINITY;
-    return a.dual_other[(size_t)bh * a.Lr_other + j];
-}
 
 }  // namespace
 
@@ -128,6 +132,10 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
             mbar_init(&s.t_full[k], 1);
             mbar_init(&s.t_empty[k], kEW);
         }
+        for (int k = 0; k < kNV; ++k) {
+            mbar_init(&s.v_full[k], 1);
+            mbar_init(&s.v_empty[k], kEW);
+        }
         fence_mbar_init();
     }
     if (warp == 1) {
@@ -150,6 +158,21 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
         uint32_t kseq = 0;
         for (int gi = g_begin; gi < g_end; ++gi) {
             const Blk b = block_of(a, a.work[gi]);
+            {   // masked window duals of the other side + previous own duals (padded buffers, -inf guards)
+                const int vs = (gi - g_begin) % kNV;
+                const uint32_t vn = (gi - g_begin) / kNV;
+                mbar_wait(&s.v_empty[vs], (vn & 1) ^ 1);
+                if (elect_one()) {
+                    const int wbase = b.q0 * a.CR - a.shift, nwin = (b.q1 - b.q0 + 1) * a.CR;
+                    float* dst = s.vwin + (size_t)vs * (a.maxwin + 128);
+                    mbar_arrive_expect_tx(&s.v_full[vs], (uint32_t)(nwin + 128) * 4u);
+                    bulk_g2s(dst, a.pad_other + (size_t)b.bh * a.pad_ld_other + a.pad_off + wbase, (uint32_t)nwin * 4u,
+                             &s.v_full[vs]);
+                    bulk_g2s(dst + a.maxwin, a.pad_own + (size_t)b.bh * a.pad_ld_own + a.pad_off + b.i0, 512u,
+                             &s.v_full[vs]);
+                }
+                __syncwarp();
+            }
             const int ab = (gi - g_begin) % a.NA;
             const uint32_t an = (gi - g_begin) / a.NA;
             mbar_wait(&s.a_empty[ab], (an & 1) ^ 1);
@@ -277,36 +300,18 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
         const int r = qd * 32 + lane;             // row inside the 128-row block
         const int et = threadIdx.x - 64;          // 0 .. NE-1
         uint32_t tseq = 0;
-        if (g_begin < g_end) {  // window duals of the first block (later ones are prefetched)
-            const Blk b = block_of(a, a.work[g_begin]);
-            const int wbase = b.q0 * kCR - a.shift, nwin = (b.q1 - b.q0 + 1) * kCR;
-            for (int c = et; c < nwin; c += NE) s.vwin[c] = window_dual(a, b.bh, wbase + c);
-        }
         for (int gi = g_begin; gi < g_end; ++gi) {
             const Blk b = block_of(a, a.work[gi]);
-            const float* vw = s.vwin + ((gi - g_begin) & 1) * a.maxwin;
+            const int vs = (gi - g_begin) % kNV;
+            mbar_wait(&s.v_full[vs], ((gi - g_begin) / kNV) & 1);
+            const float* vw = s.vwin + (size_t)vs * (a.maxwin + 128);
             const int wbase = b.q0 * kCR - a.shift;   // original column of window column 0
-            named_bar(1, NE);  // vw complete; previous block fully consumed
             if (et == 0) ST_TRACE(25 + min(gi - g_begin, 7));
-            // prefetch the next block's window duals into registers (parked in SMEM after this block)
-            constexpr int kPre = 1024 / NE;
-            float pre[kPre];
-            Blk nb{};
-            const bool has_next = gi + 1 < g_end;
-            int nwin_next = 0;
-            if (has_next) {
-                nb = block_of(a, a.work[gi + 1]);
-                nwin_next = (nb.q1 - nb.q0 + 1) * kCR;
-#pragma unroll
-                for (int k = 0; k < kPre; ++k) {
-                    const int c = et + NE * k;
-                    pre[k] = (c < nwin_next) ? window_dual(a, nb.bh, nb.q0 * kCR - a.shift + c) : -INFINITY;
-                }
-            }
             const int i = b.i0 + r;
-            const bool active = i < a.L_own && on_mask(a.mask_own, a.H, a.L_own, b.bh, i);
+            const float so = vw[a.maxwin + r];        // previous own dual; -inf marks an inactive row
+            const bool active = i < a.L_own && so != -INFINITY;
             float o = 0.f, acc0 = 0.f, acc1 = 0.f, M = -INFINITY;
-            if (!kFirst && active) o = a.off_own[(size_t)b.bh * a.Lr_own + i];
+            if (!kFirst && active) o = so;
             const int lo = i - a.w - wbase;               // band of this lane, window coordinates
             const int wlo = b.i0 + qd * 32 - a.w - wbase; // union over the warp
             const int whi = wlo + 31 + 2 * a.w;
@@ -368,28 +373,24 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
                 }
             }
             float acc_s = acc0 + acc1;
-            if (has_next) {  // park the prefetched window duals for the next block
-                float* nvw = s.vwin + ((gi + 1 - g_begin) & 1) * a.maxwin;
-#pragma unroll
-                for (int k = 0; k < kPre; ++k)
-                    if (et + NE * k < nwin_next) nvw[et + NE * k] = pre[k];
-                for (int c = et + NE * kPre; c < nwin_next; c += NE)
-                    nvw[c] = window_dual(a, nb.bh, nb.q0 * kCR - a.shift + c);
-            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.v_empty[vs]);  // window slot free for the producer
             if (et == 0) ST_TRACE(33 + min(gi - g_begin, 7));
-            // combine the column parts of every row (fixed order 0, 1, .., kParts-1)
+            // combine the column parts of every row (fixed order 0, 1, .., kParts-1); the partials
+            // are double-buffered by block parity, so one barrier per block suffices
+            float* part = s.part + ((gi - g_begin) & 1) * 768;
             if (half > 0) {
-                s.part[(half - 1) * 256 + r] = acc_s;
-                s.part[(half - 1) * 256 + 128 + r] = M;
+                part[(half - 1) * 256 + r] = acc_s;
+                part[(half - 1) * 256 + 128 + r] = M;
             }
             named_bar(2, NE);
             if (half == 0 && i < a.L_own) {
                 float u = 0.f;
 #pragma unroll
                 for (int pp = 1; pp < kParts; ++pp) {
-                    const float s1 = s.part[(pp - 1) * 256 + r];
+                    const float s1 = part[(pp - 1) * 256 + r];
                     if (kFirst) {
-                        const float M1 = s.part[(pp - 1) * 256 + 128 + r];
+                        const float M1 = part[(pp - 1) * 256 + 128 + r];
                         const float Mx = fmaxf(M, M1);
                         acc_s = (M == -INFINITY ? 0.f : acc_s * ex2(M - Mx)) +
                                 (M1 == -INFINITY ? 0.f : s1 * ex2(M1 - Mx));
@@ -418,6 +419,7 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
                     }
                 }
                 a.out_own[(size_t)b.bh * a.Lr_own + i] = u;
+                a.pad_own[(size_t)b.bh * a.pad_ld_own + a.pad_off + i] = active ? u : -INFINITY;
             }
         }
     }
@@ -528,6 +530,22 @@ __global__ void k_pack(const TIn* __restrict__ X, int BH, int L, int Lr, int Lp,
 }
 
 // ---------------------------------------------------------------------------
+// Padded masked dual buffers [BH][pad_ld]: entry pad_off + j holds the dual of column j when it is
+// active, -inf otherwise (also on the guards j < 0, j >= L), so the producer can bulk-copy any
+// window.  init: 0 on active entries (the cold start); refresh: copy from a standard [BH][Lr] vector.
+// ---------------------------------------------------------------------------
+__global__ void k_pad_fill(float* __restrict__ pad, const float* __restrict__ src, int BH, int H, int L, int Lr,
+                           int pad_ld, int pad_off, const uint8_t* __restrict__ mask) {
+    const long n = (long)BH * pad_ld;
+    for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long)gridDim.x * blockDim.x) {
+        const int bh = (int)(t / pad_ld), j = (int)(t % pad_ld) - pad_off;
+        float x = -INFINITY;
+        if (j >= 0 && j < L && on_mask(mask, H, L, bh, j)) x = src ? src[(size_t)bh * Lr + j] : 0.f;
+        pad[t] = x;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Work lists: active 128-row blocks (any active row) in (head, block) order.
 // ---------------------------------------------------------------------------
 __global__ void k_block_flags(const uint8_t* __restrict__ mask, int H, int BH, int L, int NB, int* __restrict__ flags) {
@@ -584,7 +602,7 @@ long long phase_launch_count(bool reset) {
 size_t phase_smem_bytes(const PhaseArgs& a) {
     const int nst = 512 / a.CR;
     return (size_t)a.NA * a.npl * 128 * a.row_bytes + (size_t)a.NSK * a.npl * a.CR * a.row_bytes +
-           (size_t)(2 * a.maxwin + 768) * 4 + (size_t)(4 + 2 * a.NSK + 2 * nst) * 8 + 16;
+           (size_t)(kNV * (a.maxwin + 128) + 1536) * 4 + (size_t)(2 * kNV + 4 + 2 * a.NSK + 2 * nst) * 8 + 16;
 }
 
 template <int kNPL, int kCR, int kEW>
@@ -623,6 +641,15 @@ cudaError_t launch_pack(int dtype, const void* X, int BH, int L, int Lr, int Lp,
     const unsigned nb = (unsigned)((total + 255) / 256);
     if (dtype == 0) k_pack<float><<<nb, 256, 0, s>>>((const float*)X, BH, L, Lr, Lp, d, shift, p0, p1, p2);
     else k_pack<__nv_bfloat16><<<nb, 256, 0, s>>>((const __nv_bfloat16*)X, BH, L, Lr, Lp, d, shift, p0, p1, p2);
+    ++g_phase_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pad_fill(float* pad, const float* src, int BH, int H, int L, int Lr, int pad_ld, int pad_off,
+                            const uint8_t* mask, cudaStream_t s) {
+    const long n = (long)BH * pad_ld;
+    const int nb = (int)std::min<long>((n + 255) / 256, 148L * 8);
+    k_pad_fill<<<nb, 256, 0, s>>>(pad, src, BH, H, L, Lr, pad_ld, pad_off, mask);
     ++g_phase_launches;
     return cudaGetLastError();
 }

@@ -23,7 +23,10 @@ struct PhaseArgs {
     const uint8_t* mask_other;  // [B, L_other] or null
     const uint8_t* A_pack[3];   // packed planes of the own side  [BH][Lp_own][d] bf16
     const uint8_t* B_pack[3];   // packed planes of the other side
-    const float* dual_other;    // [BH][Lr_other]
+    const float* dual_other;    // [BH][Lr_other] (read only for the dustbin entry)
+    const float* pad_other;     // [BH][pad_ld_other] masked padded duals of the other side (see launch_pad_fill)
+    float* pad_own;             // [BH][pad_ld_own] same for the own side: previous duals in, new duals out
+    int pad_ld_own, pad_ld_other, pad_off;
     const float* off_own;       // [BH][Lr_own] previous dual of the own side
     float* out_own;             // [BH][Lr_own]
     const int* work;            // active (head, block) list
@@ -50,6 +53,9 @@ cudaError_t launch_dustbin(const DustArgs& a, bool first, int BH, cudaStream_t s
 // layout, row r stored at packed row r + shift (other packed rows zero).
 cudaError_t launch_pack(int dtype, const void* X, int BH, int L, int Lr, int Lp, int d, int shift, uint8_t* p0,
                         uint8_t* p1, uint8_t* p2, cudaStream_t s);
+// pad[bh][pad_off + j] = active(j) ? (src ? src[bh][j] : 0) : -inf; guards -inf
+cudaError_t launch_pad_fill(float* pad, const float* src, int BH, int H, int L, int Lr, int pad_ld, int pad_off,
+                            const uint8_t* mask, cudaStream_t s);
 cudaError_t launch_compact(const int* flags, int n, int* work, int* count, cudaStream_t s);
 cudaError_t launch_worklist(const uint8_t* mask, int H, int BH, int L, int NB, int* flags, int* work, int* count,
                             cudaStream_t s);

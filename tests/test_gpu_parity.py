@@ -437,3 +437,35 @@ def test_certificate_eta_decays_and_selector_is_first_feasible():
     s = certificates.select_tail_depth(t["Q"], t["K"], t["V"], t["G"], spec, float(eta[1].max()) * 1.01, 4,
                                        operator_norm_bound=1.0)
     assert s.used_sufficient_bound and s.selected == 1
+
+
+@pytest.mark.parametrize("dtype,w,d,mask,dustbin", [("f32", 20, 64, "uniform_len", 0), ("bf16", 20, 128, "uniform_len", 0),
+                                                    ("bf16", 64, 64, "none", 0), ("f32", 64, 64, "uniform_len", 0),
+                                                    ("f32", 16, 32, "none", 1)])
+def test_workspace_contents_do_not_matter(dtype, w, d, mask, dustbin):
+    """The caller-owned workspace is scratch: a forward + backward on a workspace full of NaN bytes
+    must be bit-identical to one on a zeroed workspace (guards against reads of never-written
+    cells, e.g. window duals past the band or padded rows)."""
+    cfg = configs.Config(0, B=2, H=2, L=300, d=d, w=w, eps=0.2, T=8, R=2, dtype=dtype, mask=mask, dustbin=dustbin)
+    inp = configs.make_inputs(cfg)
+    b = inp.bits or {}
+    shp = (cfg.B, cfg.H, cfg.rows, d)
+    Q, K, V, G = (_dev(getattr(inp, k), b.get(k)).reshape(shp) for k in ("Q", "K", "V", "G"))
+    rm = None if inp.row_mask is None else torch.from_numpy(inp.row_mask).cuda()
+    spec = band.BandSpec(batch=cfg.B, heads=cfg.H, seq_q=cfg.L, seq_k=cfg.L, head_dim=d, half_band=w,
+                         base_depth=cfg.T, tail_depth=2, epsilon=cfg.eps, dtype=dtype, dustbin=dustbin,
+                         dustbin_cost=cfg.dustbin_cost)
+    outs = []
+    for fill in (0, 255):
+        ws = band.Workspace()
+        ws._buf = torch.full((spec.workspace_bytes() + 4096,), fill, dtype=torch.uint8, device="cuda")
+        run = band.run_surrogate(Q, K, V, spec, rm, rm, workspace=ws)
+        cot = band.r2_backward(run, G, workspace=ws)
+        torch.cuda.synchronize()
+        u, v, _ = run.tail_duals(inp.row_mask, inp.row_mask)  # the saved state's meaningful words
+        outs.append([x.clone() for x in (run.output, cot.grad_q, cot.grad_k, cot.grad_v, cot.d_eps)] +
+                    [torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64)),
+                     torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64))])
+    for name, a, c in zip(("O", "dQ", "dK", "dV", "d_eps", "u", "v"), *outs):
+        bad = torch.nonzero(a.reshape(-1).view(torch.uint8) != c.reshape(-1).view(torch.uint8)).flatten()
+        assert bad.numel() == 0, (name, bad.numel(), bad[:8].tolist())
