@@ -130,6 +130,7 @@ struct TcPlan {
     int npl, CR, shift, NA, NSK, row_bytes, maxwin, Lpq, Lpk, NBq, NBk;
     size_t smem;
 };
+int num_sms();
 TcPlan tc_plan(const st_desc* d, const Dims& m) {
     TcPlan p;
     if (d->flags & ST_FLAG_GENERIC) return p;
@@ -150,8 +151,10 @@ TcPlan tc_plan(const st_desc* d, const Dims& m) {
     const int nchunk = (int)((128 + 2 * m.w + p.CR - 1) / p.CR);  // window chunks of one block
     p.maxwin = nchunk * p.CR;
     const size_t kMax = 227 * 1024;
-    for (int NA = 2; NA >= 1; --NA)
-        for (int extra = 128 / p.CR + 1; extra >= 0; --extra) {
+    const int na_max = getenv("ST_PHASE_NA") ? atoi(getenv("ST_PHASE_NA")) : 2;
+    const int ex_max = getenv("ST_PHASE_EXTRA") ? atoi(getenv("ST_PHASE_EXTRA")) : 128 / p.CR + 1;
+    for (int NA = na_max; NA >= 1; --NA)
+        for (int extra = ex_max; extra >= 0; --extra) {
             st::PhaseArgs a{};
             a.CR = p.CR;
             a.NA = NA;
@@ -159,6 +162,7 @@ TcPlan tc_plan(const st_desc* d, const Dims& m) {
             a.npl = p.npl;
             a.row_bytes = p.row_bytes;
             a.maxwin = p.maxwin;
+            a.wl_cap = (int)((m.BH * std::max(p.NBq, p.NBk) + num_sms() - 1) / num_sms());
             const size_t sm = st::phase_smem_bytes(a);
             if (sm <= kMax) {
                 p.NA = NA;
@@ -190,6 +194,30 @@ bool fused_ok(const st_desc* d, const Dims& m) {
     g.Wf = (int)m.Wf;
     return st::fstep_smem_bytes(g) <= 227 * 1024 && !getenv("ST_NO_FUSED");
 }
+// Development timeline of one row half-step launch (ST_TRACE_PHASE=<step>): per-block globaltimer
+// stamps of the producer, MMA and epilogue roles for the first 4 CTAs, printed to stderr.  Blocks.
+unsigned long long* phase_trace_begin(long t, cudaStream_t st) {
+    static unsigned long long* buf = nullptr;
+    const char* e = getenv("ST_TRACE_PHASE");
+    if (!e || t != atol(e)) return nullptr;
+    if (!buf && cudaMalloc(&buf, 16 * 64 * 8) != cudaSuccess) return nullptr;
+    cudaMemsetAsync(buf, 0, 16 * 64 * 8, st);
+    return buf;
+}
+void phase_trace_dump(const unsigned long long* dbuf) {
+    unsigned long long h[16 * 64];
+    if (cudaMemcpy(h, dbuf, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return;
+    for (int c = 0; c < 4; ++c) {
+        const unsigned long long t0 = h[c * 64];
+        fprintf(stderr, "CTA %d blocks %llu end %lld ns\n", c, h[c * 64 + 42], (long long)(h[c * 64 + 41] - t0));
+        for (int k = 0; k < 7; ++k)
+            fprintf(stderr, "  blk %d prodA %6lld mmaA %6lld mmaDone %6lld epiStart %6lld epiEnd %6lld\n", k,
+                    (long long)(h[c * 64 + 1 + k] - t0), (long long)(h[c * 64 + 9 + k] - t0),
+                    (long long)(h[c * 64 + 17 + k] - t0), (long long)(h[c * 64 + 25 + k] - t0),
+                    (long long)(h[c * 64 + 33 + k] - t0));
+    }
+}
+
 WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
     WsLayout w;
     size_t o = 0;
@@ -424,12 +452,14 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
         pr.NSK = tp.NSK;
         pr.row_bytes = tp.row_bytes;
         pr.maxwin = tp.maxwin;
+        pr.wl_cap = (int)((m.BH * std::max(tp.NBq, tp.NBk) + num_sms() - 1) / num_sms());
         pr.H = g.H;
         pr.w = g.w;
         pr.dustbin = g.dustbin;
         pr.c2 = g.c2;
         pr.sd2 = g.sd2;
         pr.err = err;
+        pr.dbg = getenv("ST_PHASE_DBG") ? atoi(getenv("ST_PHASE_DBG")) : 0;
         st::PhaseArgs pc = pr;
         // row phase: own = queries (A = Q block), other = keys (B = K window)
         pr.NB = tp.NBq;
@@ -463,8 +493,9 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
             pr.c2 = pc.c2 = g.c2 * lam;
             pr.sd2 = pc.sd2 = dr.sd2 = dc.sd2 = g.sd2 * lam;
             pr.dual_other = v_prev; pr.off_own = u_prev; pr.out_own = u_out;
-            pr.trace = nullptr;
+            pr.trace = phase_trace_begin(t, st);
             ST_CUDA(st::launch_phase(pr, t == 1, grid, st));
+            if (pr.trace) phase_trace_dump(pr.trace);
             if (g.dustbin) {
                 dr.dual_other = v_prev; dr.off_own = u_prev; dr.out_own = u_out;
                 ST_CUDA(st::launch_dustbin(dr, t == 1, g.BH, st));

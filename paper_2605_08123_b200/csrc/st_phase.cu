@@ -53,6 +53,7 @@ struct Smem {
     uint64_t* t_full;
     uint64_t* t_empty;
     uint32_t* tmem_base;
+    int* wl;          // [wl_cap] this CTA's slice of the work list (no global loads on the block path)
 };
 
 __device__ __forceinline__ Smem carve(uint8_t* base, const PhaseArgs& a, int nst) {
@@ -67,12 +68,13 @@ __device__ __forceinline__ Smem carve(uint8_t* base, const PhaseArgs& a, int nst
     s.v_empty = bars + kNV;
     bars += 2 * kNV;
     s.a_full = bars;
-    s.a_empty = bars + 2;
-    s.k_full = bars + 4;
+    s.a_empty = bars + a.NA;
+    s.k_full = bars + 2 * a.NA;
     s.k_empty = s.k_full + a.NSK;
     s.t_full = s.k_empty + a.NSK;
     s.t_empty = s.t_full + nst;
     s.tmem_base = (uint32_t*)(s.t_empty + nst);
+    s.wl = (int*)(s.tmem_base + 4);
     return s;
 }
 
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
     const uint32_t blk_bytes = 128u * a.row_bytes, chk_bytes = (uint32_t)kCR * a.row_bytes;
 
     if (threadIdx.x == 0) {
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < a.NA; ++k) {
             mbar_init(&s.a_full[k], 1);
             mbar_init(&s.a_empty[k], 1);
         }
@@ -142,22 +144,24 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
         tc_alloc(s.tmem_base, 512);
         tc_relinquish();
     }
+    const int n = *a.nwork;
+    const int g_begin = (int)((long long)n * blockIdx.x / gridDim.x);
+    const int g_end = min((int)((long long)n * (blockIdx.x + 1) / gridDim.x), g_begin + a.wl_cap);
+    for (int k = threadIdx.x; k < g_end - g_begin; k += blockDim.x) s.wl[k] = a.work[g_begin + k];
+    if (threadIdx.x == 0 && (int)((long long)n * (blockIdx.x + 1) / gridDim.x) - g_begin > a.wl_cap)
+        atomicOr(a.err, 16);  // cannot happen: wl_cap = ceil(max work / grid)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *s.tmem_base;
     if (threadIdx.x == 0) ST_TRACE(0);
 
-    const int n = *a.nwork;
-    const int g_begin = (int)((long long)n * blockIdx.x / gridDim.x);
-    const int g_end = (int)((long long)n * (blockIdx.x + 1) / gridDim.x);
-
     if (warp == 0) {
         // ------------------------------------------------------------ producer (warp-uniform loop)
         int last_bh = -1, last_q = -1;
         uint32_t kseq = 0;
         for (int gi = g_begin; gi < g_end; ++gi) {
-            const Blk b = block_of(a, a.work[gi]);
+            const Blk b = block_of(a, s.wl[gi - g_begin]);
             {   // masked window duals of the other side + previous own duals (padded buffers, -inf guards)
                 const int vs = (gi - g_begin) % kNV;
                 const uint32_t vn = (gi - g_begin) / kNV;
@@ -221,7 +225,7 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
         uint32_t last_seq = 0, rel_seq = 0, tseq = 0;
         bool have = false;
         for (int gi = g_begin; gi < g_end; ++gi) {
-            const Blk b = block_of(a, a.work[gi]);
+            const Blk b = block_of(a, s.wl[gi - g_begin]);
             const int ab = (gi - g_begin) % a.NA;
             const uint32_t an = (gi - g_begin) / a.NA;
             mbar_wait(&s.a_full[ab], an & 1);
@@ -254,7 +258,7 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
                 if (elect_one()) {
 #pragma unroll
                     for (int pr = 0; pr < kNP; ++pr)
-                        for (int kk = 0; kk < ksteps; ++kk) {
+                        for (int kk = 0; kk < ((a.dbg & 2) ? 1 : ksteps); ++kk) {
                             const uint64_t adk = ad0 + (uint64_t)pa_[pr] * a_plane + (uint64_t)(kk * 16);
 #pragma unroll
                             for (int c = 0; c < kG; ++c)
@@ -281,7 +285,7 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
             // release ring slots the next block of this CTA does not need
             uint32_t keep_from = last_seq + 1;
             if (gi + 1 < g_end) {
-                const Blk nb = block_of(a, a.work[gi + 1]);
+                const Blk nb = block_of(a, s.wl[gi + 1 - g_begin]);
                 if (nb.bh == last_bh && nb.q0 <= last_q) keep_from = last_seq - (uint32_t)(last_q - nb.q0);
             }
             if (elect_one()) {
@@ -301,7 +305,7 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
         const int et = threadIdx.x - 64;          // 0 .. NE-1
         uint32_t tseq = 0;
         for (int gi = g_begin; gi < g_end; ++gi) {
-            const Blk b = block_of(a, a.work[gi]);
+            const Blk b = block_of(a, s.wl[gi - g_begin]);
             const int vs = (gi - g_begin) % kNV;
             mbar_wait(&s.v_full[vs], ((gi - g_begin) / kNV) & 1);
             const float* vw = s.vwin + (size_t)vs * (a.maxwin + 128);
@@ -334,7 +338,7 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s.t_empty[ts]);
                 ++tseq;
-                if (!any || !active) continue;
+                if (!any || !active || (a.dbg & 1)) continue;
                 if (kFirst) {
                     float m = -INFINITY;
 #pragma unroll
@@ -602,7 +606,7 @@ long long phase_launch_count(bool reset) {
 size_t phase_smem_bytes(const PhaseArgs& a) {
     const int nst = 512 / a.CR;
     return (size_t)a.NA * a.npl * 128 * a.row_bytes + (size_t)a.NSK * a.npl * a.CR * a.row_bytes +
-           (size_t)(kNV * (a.maxwin + 128) + 1536) * 4 + (size_t)(2 * kNV + 4 + 2 * a.NSK + 2 * nst) * 8 + 16;
+           (size_t)(kNV * (a.maxwin + 128) + 1536) * 4 + (size_t)(2 * kNV + 2 * a.NA + 2 * a.NSK + 2 * nst) * 8 + 16 + (size_t)a.wl_cap * 4;
 }
 
 template <int kNPL, int kCR, int kEW>

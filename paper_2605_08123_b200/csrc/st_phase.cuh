@@ -31,8 +31,10 @@ struct PhaseArgs {
     float* out_own;             // [BH][Lr_own]
     const int* work;            // active (head, block) list
     const int* nwork;
+    int wl_cap;                 // max work items per CTA (SMEM copy of the CTA's work-list slice)
     int* err;
     unsigned long long* trace;  // debug timeline (null in production)
+    int dbg;                    // development ablations (ST_PHASE_DBG): 1 = skip epilogue math, 2 = one MMA K-step
 };
 
 struct DustArgs {
