@@ -16,17 +16,18 @@ def bench(cid, iters=3, L=None):
     Q, K, V, G = dev(inp.Q, 'Q'), dev(inp.K, 'K'), dev(inp.V, 'V'), dev(inp.G, 'G')
     rm = None if inp.row_mask is None else torch.from_numpy(inp.row_mask).cuda()
     run = band.run_surrogate(Q, K, V, spec, rm, rm)
-    band.r2_backward(run, G)
+    mode = os.environ.get("BWD_MODE", "one_reference")
+    band.r2_backward(run, G, mode=mode)
     torch.cuda.synchronize()
     e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     tf, tb = [], []
     for _ in range(iters):
         e[0].record(); run = band.run_surrogate(Q, K, V, spec, rm, rm, validate=False, saved=run.saved, out=run.output)
-        e[1].record(); band.r2_backward(run, G); e[2].record(); torch.cuda.synchronize()
+        e[1].record(); band.r2_backward(run, G, mode=mode); e[2].record(); torch.cuda.synchronize()
         tf.append(e[0].elapsed_time(e[1])); tb.append(e[1].elapsed_time(e[2]))
     cells = cfg.nominal_cell_steps()
     t = min(tf) + min(tb)
-    print(f"config {cid} L={cfg.L}: fwd {min(tf):.3f} ms bwd {min(tb):.3f} ms -> {cells/(t*1e-3):.3e} band-cells/s", flush=True)
+    print(f"config {cid} L={cfg.L} [{mode}]: fwd {min(tf):.3f} ms bwd {min(tb):.3f} ms -> {cells/(t*1e-3):.3e} band-cells/s", flush=True)
 
 for cid in [int(x) for x in sys.argv[1:]]:
     bench(cid)
