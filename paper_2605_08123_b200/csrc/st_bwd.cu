@@ -904,6 +904,271 @@ __global__ void __launch_bounds__(256) k_bwdG(Geo g, BT<TIn> a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Window-chunked vector stages (R6 dQ, C6 dK (+C5), C1 dV, RO output, RW / CW) for dustbin-free
+// bands with w % 16 == 0.  The band tile is read in its sheared view: cell (row i0 + r, window
+// column c = r + k) sits at base + r (Wf - 1) + c, so 32 consecutive window columns of one row are
+// 128 contiguous, 16-byte aligned bytes, and one chunk of the window is a [128][32] strip.  Per
+// chunk of kWC = 32 window columns (NSTG-deep cp.async ring of S / Z strips + the chunk's 32
+// operand rows; NSTG = 2 and one WT buffer keep two CTAs per SM):
+//   phase 1 (2 threads per row, rotated column order: bank-conflict free) the weight W of every cell
+//           (0 off the band), stored transposed WT[c][r]; row partials (g_v, d_eps, v0b) in registers
+//   phase 2 dense tile GEMM out[128][D] += W X over the chunk: thread = 4 rows x D/8 columns, per
+//           window column one LDS.128 of W and D/32 LDS.128 of X feed 4 D/8 FMAs; warps whose 16
+//           rows miss the chunk skip it
+// Every operand row is read once per block (no per-row window redundancy), every reduction has a
+// fixed order (increasing window column), and the kernel is independent of the band width beyond
+// the chunk count.
+// ---------------------------------------------------------------------------
+constexpr int kWC = 32;  // window columns per chunk
+
+// 16-byte global -> shared async copy (LDGSTS); src_bytes = 0 zero-fills the destination
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sm100::smem_u32(dst)), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int D, class TIn>
+__host__ __device__ constexpr size_t bwdW_stage_floats(bool z) {
+    return (size_t)(z ? 2 : 1) * 128 * kWC + (size_t)kWC * D * sizeof(TIn) / 4;
+}
+template <int D, class TIn>
+static size_t bwdW_smem_bytes(const Geo& g, bool z, int nstg) {
+    const int Nw = 128 + 2 * g.w;
+    return ((size_t)nstg * bwdW_stage_floats<D, TIn>(z) + kWC * 128 + 5 * (size_t)Nw) * 4 + 128;
+}
+bool bwdW_supported(const Geo& g) {
+    return !g.dustbin && g.w >= 16 && g.w % 16 == 0 && (g.d == 32 || g.d == 64 || g.d == 128) &&
+           !getenv("ST_NO_BWDW");
+}
+
+template <int kOp, bool kDirect, int D, class TIn, int NSTG>
+__global__ void __launch_bounds__(256) k_bwdW(Geo g, BT<TIn> a) {
+    extern __shared__ __align__(128) float smw[];
+    __shared__ float sacc[2][128], sdacc[2][128];
+    constexpr bool kRow = kOp < 10;
+    constexpr bool kNeedZ = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RW || kOp == CW);
+    constexpr int CPT = D / 8;  // output columns per thread
+    const int Lo = kRow ? g.Lq : g.Lk, Lx = kRow ? g.Lk : g.Lq;
+    const int Lro = kRow ? g.Lrq : g.Lrk, Lrx = kRow ? g.Lrk : g.Lrq;
+    const int Lpo = kRow ? g.Lqp : g.Lkp;
+    const uint8_t* mo = kRow ? g.row_mask : g.col_mask;
+    const uint8_t* mx = kRow ? g.col_mask : g.row_mask;
+    const int bh = blockIdx.y, i0 = blockIdx.x * 128, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const size_t bo = (size_t)bh * Lro, bx = (size_t)bh * Lrx;
+    auto on_o = [&](int k) { return k < Lo && (mo == nullptr || mo[(size_t)(bh / g.H) * Lo + k] != 0); };
+    auto on_x = [&](int k) { return k >= 0 && k < Lx && (mx == nullptr || mx[(size_t)(bh / g.H) * Lx + k] != 0); };
+    const int r = tid & 127, hh = tid >> 7, i = i0 + r;
+    const bool active = on_o(i);
+    float* vo = (kOp == R6 || kOp == RW) ? a.dQ : kOp == C1 ? a.dV : kOp == RO ? a.O : a.dK;
+    if (!__syncthreads_or(active)) {
+        if (hh == 0 && i < Lo) {
+            if (kOp == R6 || kOp == RW) a.deps_part[bo + i] = 0.f;
+            if (kOp == C1) a.g_v[bo + i] = 0.f;
+            if (kOp == C6 && a.fuse_c5) a.v0b[bo + i] = 0.f;
+            for (int x = 0; x < D; ++x) vo[(bo + i) * D + x] = 0.f;
+        }
+        return;
+    }
+    const int Wf = g.Wf, Nw = 128 + 2 * g.w, NCH = Nw / kWC;
+    const size_t stf = bwdW_stage_floats<D, TIn>(kNeedZ);
+    float* WT = smw + NSTG * stf;     // [kWC][128]
+    float* wv = WT + kWC * 128;       // [5][Nw]
+    const float* Sb = (kRow ? a.S2 : a.S2T) + ((size_t)bh * Lpo + i0) * Wf;
+    const float* Zb = kNeedZ ? (kRow ? a.Z : a.ZT) + ((size_t)bh * Lpo + i0) * Wf : nullptr;
+    const TIn* osrc = (kOp == R6 || kOp == RW) ? a.K : (kOp == C1) ? a.dO : (kOp == RO) ? a.V : a.Q;
+    auto stS = [&](int s) { return smw + (size_t)s * stf; };
+    auto stZ = [&](int s) { return smw + (size_t)s * stf + 128 * kWC; };
+    auto stX = [&](int s) { return reinterpret_cast<TIn*>(smw + (size_t)s * stf + (kNeedZ ? 2 : 1) * 128 * kWC); };
+    auto issue = [&](int j) {  // all threads: one chunk's strips (8 x 16 B per row and band) + operand rows
+        const int s = j % NSTG, c0 = j * kWC;
+        float* S = stS(s);
+        float* Z = stZ(s);
+        for (int e = tid; e < 128 * (kWC / 4); e += 256) {
+            const int rr = e / (kWC / 4), sg = (e % (kWC / 4)) * 4;
+            cp_async16(S + rr * kWC + sg, Sb + (size_t)rr * (Wf - 1) + c0 + sg, 16u);
+            if (kNeedZ) cp_async16(Z + rr * kWC + sg, Zb + (size_t)rr * (Wf - 1) + c0 + sg, 16u);
+        }
+        constexpr int SPR = D * (int)sizeof(TIn) / 16;  // 16-byte segments per operand row
+        const int xb0 = i0 - g.w + c0;
+        TIn* X = stX(s);
+        for (int e = tid; e < kWC * SPR; e += 256) {
+            const int row = e / SPR, sg = e % SPR, x = xb0 + row;
+            const bool ok = x >= 0 && x < Lx;  // rows outside the sequence: zero-filled
+            cp_async16(reinterpret_cast<uint8_t*>(X) + (size_t)row * D * sizeof(TIn) + sg * 16,
+                       reinterpret_cast<const uint8_t*>(osrc + (bx + (ok ? x : 0)) * D) + sg * 16, ok ? 16u : 0u);
+        }
+        cp_async_commit();
+    };
+    for (int j = 0; j < NSTG - 1; ++j) {  // prologue (empty groups past the end keep the count uniform)
+        if (j < NCH) issue(j);
+        else cp_async_commit();
+    }
+    // window vectors (other side), c <-> x = i0 - w + c; 0 where invalid (the band carries -inf there)
+    //   R6: v2, beta|v1, delta|v0, v2b(=g_v), v1b     C6: u2, alpha|u1, -, u2b, u1b     C1 / RO: u2 / v2
+    for (int c = tid; c < Nw; c += 256) {
+        const int x = i0 - g.w + c;
+        float w0 = 0.f, w1 = 0.f, w2 = 0.f, w3 = 0.f, w4 = 0.f;
+        if (on_x(x)) {
+            if (kRow) {
+                w0 = a.v2[bx + x];
+                if (kOp == R6) {
+                    const float v1 = a.v1[bx + x], v0 = a.v0[bx + x];
+                    w1 = kDirect ? v1 : ex2(v1 - w0);
+                    w2 = kDirect ? v0 : ex2(v0 - w0);
+                    w3 = a.g_v[bx + x];
+                    w4 = a.v1b[bx + x];
+                }
+            } else {
+                w0 = a.u2[bx + x];
+                if (kOp == C6) {
+                    const float u1 = a.u1[bx + x];
+                    w1 = kDirect ? u1 : ex2(u1 - w0);
+                    w3 = a.u2b[bx + x];
+                    w4 = a.u1b[bx + x];
+                }
+            }
+        }
+        wv[c] = w0;
+        wv[Nw + c] = w1;
+        wv[2 * Nw + c] = w2;
+        wv[3 * Nw + c] = w3;
+        wv[4 * Nw + c] = w4;
+    }
+    float o2 = 0.f, o1 = 0.f, o0 = 0.f, ob2 = 0.f, ob1 = 0.f;
+    if (active) {
+        if (kRow) {
+            o2 = a.u2[bo + i];
+            o1 = a.u1[bo + i];
+            if (kOp == R6) {
+                ob2 = a.u2b[bo + i];
+                ob1 = a.u1b[bo + i];
+            }
+        } else {
+            o2 = a.v2[bo + i];
+            o1 = a.v1[bo + i];
+            o0 = a.v0[bo + i];
+            if (kOp == C6) {
+                ob2 = a.g_v[bo + i];
+                ob1 = a.v1b[bo + i];
+            }
+        }
+    }
+    // one-reference modifiers of the own index: R6 alpha_i; C6 beta_j, delta_j
+    const float ma = active ? ex2(o1 - o2) : 0.f, mb = (active && !kRow) ? ex2(o0 - o2) : 0.f;
+    __syncthreads();  // window vectors visible
+    float acc = 0.f, dacc = 0.f;
+    const int rg = tid >> 3, cg = tid & 7;
+    const int wr0 = warp * 16;  // phase-2 rows of this warp: [wr0, wr0 + 16)
+    float accv[4][CPT];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < CPT; ++e) accv[q][e] = 0.f;
+    for (int j = 0; j < NCH; ++j) {
+        const int s = j % NSTG, c0 = j * kWC;
+        cp_async_wait<NSTG - 2>();  // this thread's copies of chunk j landed
+        __syncthreads();            // everyone's; and every thread is past the previous chunk's phase 2
+        if (j + NSTG - 1 < NCH) issue(j + NSTG - 1);  // into the stage the previous chunk used
+        else cp_async_commit();
+        const float* S = stS(s);
+        const float* Z = stZ(s);
+        const TIn* X = stX(s);
+        // ---- phase 1: weights of this thread's 16 columns of row r (rotated: conflict-free)
+        float* wt = WT;  // single buffer: every thread finished the previous chunk's phase 2 (barrier above)
+#pragma unroll 4
+        for (int jj = 0; jj < kWC / 2; ++jj) {
+            const int cl = (r + 16 * hh + jj) & (kWC - 1);
+            const int c = c0 + cl;
+            const float s2 = S[r * kWC + cl];
+            float wgt = 0.f;
+            if (active && (unsigned)(c - r) < (unsigned)Wf && s2 != -INFINITY) {
+                const float p = (kOp == RW || kOp == CW) ? 0.f : ex2(s2 + o2 + wv[c]);
+                if (kOp == RW || kOp == CW) {  // the band already holds Sbar
+                    wgt = Z[r * kWC + cl];
+                    if (kOp == RW) dacc += wgt * (s2 * kLn2);
+                } else if (kOp == RO) {
+                    wgt = p;
+                } else if (kOp == C1) {
+                    acc += p * Z[r * kWC + cl];
+                    wgt = p;
+                } else if (kOp == R6) {
+                    const float z = Z[r * kWC + cl];
+                    if (kDirect) {
+                        wgt = sbar_of(true, s2, p, z, o1, o2, wv[2 * Nw + c], wv[Nw + c], wv[c], ob2, ob1,
+                                      wv[3 * Nw + c], wv[4 * Nw + c]);
+                    } else {  // Sbar = P22 (Z - v2b_j - beta_j u2b_i - alpha_i beta_j v1b_j - alpha_i delta_j u1b_i)
+                        const float bj = wv[Nw + c], dj = wv[2 * Nw + c];
+                        wgt = p * (z - wv[3 * Nw + c] - bj * ob2 - ma * bj * wv[4 * Nw + c] - ma * dj * ob1);
+                    }
+                    dacc += wgt * (s2 * kLn2);
+                } else {  // C6: own = column j, window = rows i
+                    const float z = Z[r * kWC + cl];
+                    if (kDirect) {
+                        wgt = sbar_of(true, s2, p, z, wv[Nw + c], wv[c], o0, o1, o2, wv[3 * Nw + c], wv[4 * Nw + c],
+                                      ob2, ob1);
+                        if (a.fuse_c5) acc += ex2(s2 + wv[Nw + c] + o0) * wv[4 * Nw + c];  // C5: P10 u1b
+                    } else {  // alpha_i = wv[Nw + c], beta_j = ma, delta_j = mb
+                        const float ai = wv[Nw + c];
+                        wgt = p * (z - ob2 - ma * wv[3 * Nw + c] - ai * ma * ob1 - ai * mb * wv[4 * Nw + c]);
+                        acc += p * ai * wv[4 * Nw + c];  // C5: P22 alpha_i u1b_i (used when fuse_c5)
+                    }
+                }
+            }
+            wt[cl * 128 + r] = wgt;
+        }
+        __syncthreads();  // WT of this chunk complete
+        // ---- phase 2: out[4 rg + q][4 cg + 32 m ..] += sum_c W[row][c] X[c][..]
+        if (c0 <= wr0 + 15 + 2 * g.w && c0 + kWC - 1 >= wr0) {
+            const float* wrow = wt + 4 * rg;
+            const TIn* xr = X + 4 * cg;
+#pragma unroll 4
+            for (int cl = 0; cl < kWC; ++cl) {
+                const float4 w4 = *reinterpret_cast<const float4*>(wrow + cl * 128);
+                const float wq[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                for (int m = 0; m < CPT / 4; ++m) {
+                    const float4 x4 = ld4f<TIn>(xr + cl * D + 32 * m);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        accv[q][4 * m + 0] = fmaf(wq[q], x4.x, accv[q][4 * m + 0]);
+                        accv[q][4 * m + 1] = fmaf(wq[q], x4.y, accv[q][4 * m + 1]);
+                        accv[q][4 * m + 2] = fmaf(wq[q], x4.z, accv[q][4 * m + 2]);
+                        accv[q][4 * m + 3] = fmaf(wq[q], x4.w, accv[q][4 * m + 3]);
+                    }
+                }
+            }
+        }
+    }
+    sacc[hh][r] = acc;
+    sdacc[hh][r] = dacc;
+    __syncthreads();
+    if (hh == 0 && i < Lo) {
+        if (kOp == C1) a.g_v[bo + i] = active ? sacc[0][r] + sacc[1][r] : 0.f;
+        if (kOp == R6 || kOp == RW) a.deps_part[bo + i] = active ? sdacc[0][r] + sdacc[1][r] : 0.f;
+        if (kOp == C6 && a.fuse_c5) {  // v0b_j = -delta_j sum_i P22 alpha_i u1b_i  (direct: -sum P10 u1b)
+            const float s5 = sacc[0][r] + sacc[1][r];
+            a.v0b[bo + i] = !active ? 0.f : kDirect ? -s5 : -ex2(a.v0[bo + i] - a.v2[bo + i]) * s5;
+        }
+    }
+    const float sc = (kOp == C1 || kOp == RO) ? 1.f : g.inv_qk;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int ii = i0 + 4 * rg + q;
+        if (ii >= Lo) continue;
+#pragma unroll
+        for (int m = 0; m < CPT / 4; ++m) {
+            const int col = 4 * cg + 32 * m;
+            *reinterpret_cast<float4*>(vo + (bo + ii) * D + col) =
+                make_float4(accv[q][4 * m] * sc, accv[q][4 * m + 1] * sc, accv[q][4 * m + 2] * sc,
+                            accv[q][4 * m + 3] * sc);
+        }
+    }
+}
+
 // Zd_i = dO_i . V_dustbin (rows) and ZdT_j = dO_dustbin . V_j (columns)
 template <class TIn>
 __global__ void k_dust_dots(Geo g, const TIn* __restrict__ dO, const TIn* __restrict__ V, float* Zd, float* ZdT) {
@@ -1004,7 +1269,25 @@ template <int kOp, bool kDirect, int D, class TIn>
 static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
     const bool row = kOp < 10;
     constexpr bool kVec = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RO || kOp == RW || kOp == CW);
-    if (kVec && D <= 64 && bwdT_smem_bytes(g) <= 227 * 1024 && !getenv("ST_NO_BWDV")) {
+    const bool narrow_ok = kVec && D <= 64 && bwdT_smem_bytes(g) <= 227 * 1024 && !getenv("ST_NO_BWDV");
+    if constexpr (kVec) {
+        // wide bands (no 128-row band tile in SMEM): the window-chunked vector stage over sheared band
+        // strips; narrow bands keep the 128-row tile kernel (the strips would read the 2x wider window)
+        if (!narrow_ok && bwdW_supported(g)) {
+            constexpr bool kZ = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RW || kOp == CW);
+            static const int nstg = getenv("ST_BWDW_NSTG") ? atoi(getenv("ST_BWDW_NSTG")) : 2;
+            const size_t smem = bwdW_smem_bytes<D, TIn>(g, kZ, nstg == 3 ? 3 : 2);
+            if (smem <= 227 * 1024) {
+                auto k = nstg == 3 ? k_bwdW<kOp, kDirect, D, TIn, 3> : k_bwdW<kOp, kDirect, D, TIn, 2>;
+                cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e != cudaSuccess) return e;
+                const int n = row ? g.Lq : g.Lk;
+                k<<<dim3((n + 127) / 128, g.BH), 256, smem, s>>>(g, a);
+                return cudaGetLastError();
+            }
+        }
+    }
+    if (narrow_ok) {
         // 128-row weights + register-tiled band GEMM (operands as f32)
         const size_t smem = bwdT_smem_bytes(g);
         auto k = k_bwdV<kOp, kDirect, D, TIn>;

@@ -469,3 +469,16 @@ def test_workspace_contents_do_not_matter(dtype, w, d, mask, dustbin):
     for name, a, c in zip(("O", "dQ", "dK", "dV", "d_eps", "u", "v"), *outs):
         bad = torch.nonzero(a.reshape(-1).view(torch.uint8) != c.reshape(-1).view(torch.uint8)).flatten()
         assert bad.numel() == 0, (name, bad.numel(), bad[:8].tolist())
+
+
+@pytest.mark.parametrize("dtype,d,w,mask,mode", [("f32", 32, 112, "uniform_len", "one_reference"),
+                                                 ("f32", 64, 96, "none", "direct_four_plan"),
+                                                 ("bf16", 128, 80, "uniform_len", "one_reference")])
+def test_wide_band_window_chunked_stages_parity(dtype, d, w, mask, mode):
+    """Bands too wide for a 128-row SMEM tile run the window-chunked vector stages (k_bwdW: sheared
+    band strips, dense chunk GEMMs): f32 and bf16 operands, masks (edge blocks, inactive rows), both
+    adjoint schedules, against the oracle."""
+    cfg = configs.Config(0, B=2, H=1, L=700, d=d, w=w, eps=0.1, T=12, R=2, dtype=dtype, mask=mask)
+    inp = configs.make_inputs(cfg)
+    tol = BF16_TOL if dtype == "bf16" else FP32_TOL
+    check_against_oracle(cfg, inp, tol, tol, mode=mode)
