@@ -1169,6 +1169,133 @@ __global__ void __launch_bounds__(256) k_bwdW(Geo g, BT<TIn> a) {
     }
 }
 
+// Window-chunked scalar sweeps (R1, R12, R2, R4, C3, C5) over the sheared band strips, for the bands
+// whose 128-row tile does not fit SMEM: 2 threads per row (rotated columns), NSTG-deep cp.async ring
+// of [128][32] S (and Z) strips, one barrier per chunk, 2-3 CTAs per SM.
+template <int kOp, bool kDirect, class TIn, int NSTG>
+__global__ void __launch_bounds__(256) k_sweepW(Geo g, BT<TIn> a) {
+    extern __shared__ __align__(128) float smw[];
+    __shared__ float sacc[2][128], sacc2[2][128];
+    constexpr bool kRow = kOp < 10;
+    constexpr bool kNeedZ = (kOp == R1 || kOp == R12);
+    const int Lo = kRow ? g.Lq : g.Lk, Lx = kRow ? g.Lk : g.Lq;
+    const int Lro = kRow ? g.Lrq : g.Lrk, Lrx = kRow ? g.Lrk : g.Lrq;
+    const int Lpo = kRow ? g.Lqp : g.Lkp;
+    const uint8_t* mo = kRow ? g.row_mask : g.col_mask;
+    const uint8_t* mx = kRow ? g.col_mask : g.row_mask;
+    const int bh = blockIdx.y, i0 = blockIdx.x * 128, tid = threadIdx.x;
+    const size_t bo = (size_t)bh * Lro, bx = (size_t)bh * Lrx;
+    auto on_o = [&](int k) { return k < Lo && (mo == nullptr || mo[(size_t)(bh / g.H) * Lo + k] != 0); };
+    auto on_x = [&](int k) { return k >= 0 && k < Lx && (mx == nullptr || mx[(size_t)(bh / g.H) * Lx + k] != 0); };
+    const int r = tid & 127, hh = tid >> 7, i = i0 + r;
+    const bool active = on_o(i);
+    auto put = [&](float val) {
+        if (kOp == R1 || kOp == R12) a.g_u[bo + i] = val;
+        if (kOp == R2) a.u2b[bo + i] = val;
+        if (kOp == R4) a.u1b[bo + i] = val;
+        if (kOp == C3) a.v1b[bo + i] = val;
+        if (kOp == C5) a.v0b[bo + i] = val;
+    };
+    if (!__syncthreads_or(active)) {
+        if (hh == 0 && i < Lo) {
+            put(0.f);
+            if (kOp == R12) a.u2b[bo + i] = 0.f;
+        }
+        return;
+    }
+    const int Wf = g.Wf, Nw = 128 + 2 * g.w, NCH = Nw / kWC;
+    constexpr int STF = (kNeedZ ? 2 : 1) * 128 * kWC;
+    float* wv = smw + NSTG * STF;  // [4][Nw]: x2, x1, g_v|u2b, v1b|u1b
+    const float* Sb = (kRow ? a.S2 : a.S2T) + ((size_t)bh * Lpo + i0) * Wf;
+    const float* Zb = kNeedZ ? a.Z + ((size_t)bh * Lpo + i0) * Wf : nullptr;
+    auto issue = [&](int j) {
+        float* S = smw + (size_t)(j % NSTG) * STF;
+        const int c0 = j * kWC;
+        for (int e = tid; e < 128 * (kWC / 4); e += 256) {
+            const int rr = e / (kWC / 4), sg = (e % (kWC / 4)) * 4;
+            cp_async16(S + rr * kWC + sg, Sb + (size_t)rr * (Wf - 1) + c0 + sg, 16u);
+            if (kNeedZ) cp_async16(S + 128 * kWC + rr * kWC + sg, Zb + (size_t)rr * (Wf - 1) + c0 + sg, 16u);
+        }
+        cp_async_commit();
+    };
+    for (int j = 0; j < NSTG - 1; ++j) {
+        if (j < NCH) issue(j);
+        else cp_async_commit();
+    }
+    for (int c = tid; c < Nw; c += 256) {
+        const int x = i0 - g.w + c;
+        float w0 = 0.f, w1 = 0.f, w3 = 0.f, w4 = 0.f;
+        if (on_x(x)) {
+            if (kRow) {
+                w0 = a.v2[bx + x];
+                w1 = a.v1[bx + x];
+                if (kOp == R2 || kOp == R12) w3 = a.g_v[bx + x];
+                if (kOp == R4) w4 = a.v1b[bx + x];
+            } else {
+                w0 = a.u2[bx + x];
+                w1 = a.u1[bx + x];
+                if (kOp == C3) w3 = a.u2b[bx + x];
+                if (kOp == C5) w4 = a.u1b[bx + x];
+            }
+        }
+        wv[c] = w0;
+        wv[Nw + c] = w1;
+        wv[2 * Nw + c] = w3;
+        wv[3 * Nw + c] = w4;
+    }
+    float o2 = 0.f, o1 = 0.f, o0 = 0.f;
+    if (active) {
+        o2 = kRow ? a.u2[bo + i] : a.v2[bo + i];
+        o1 = kRow ? a.u1[bo + i] : a.v1[bo + i];
+        if (!kRow) o0 = a.v0[bo + i];
+    }
+    float acc = 0.f, acc2 = 0.f;
+    for (int j = 0; j < NCH; ++j) {
+        cp_async_wait<NSTG - 2>();
+        __syncthreads();  // chunk j visible (and the window vectors, j = 0); chunk j - 1 fully consumed
+        if (j + NSTG - 1 < NCH) issue(j + NSTG - 1);
+        else cp_async_commit();
+        const float* S = smw + (size_t)(j % NSTG) * STF;
+        const float* Z = S + 128 * kWC;
+        const int c0 = j * kWC;
+        if (!active || c0 > r + 2 * g.w || c0 + kWC - 1 < r) continue;  // this row's band misses the chunk
+#pragma unroll 4
+        for (int jj = 0; jj < kWC / 2; ++jj) {
+            const int cl = (r + 16 * hh + jj) & (kWC - 1);
+            const int c = c0 + cl;
+            const float s2 = S[r * kWC + cl];
+            if ((unsigned)(c - r) >= (unsigned)Wf || s2 == -INFINITY) continue;
+            const float x2 = wv[c], x1 = wv[Nw + c];
+            const float p = ex2(s2 + o2 + x2);
+            if (kOp == R1) acc += p * Z[r * kWC + cl];
+            else if (kOp == R12) {
+                acc += p * Z[r * kWC + cl];
+                acc2 += p * wv[2 * Nw + c];
+            } else if (kOp == R2) acc += p * wv[2 * Nw + c];
+            else if (kOp == R4) acc += kDirect ? ex2(s2 + o1 + x1) * wv[3 * Nw + c] : p * ex2(x1 - x2) * wv[3 * Nw + c];
+            else if (kOp == C3) acc += (kDirect ? ex2(s2 + x2 + o1) : p) * wv[2 * Nw + c];
+            else acc += kDirect ? ex2(s2 + x1 + o0) * wv[3 * Nw + c] : p * ex2(x1 - x2) * wv[3 * Nw + c];
+        }
+    }
+    sacc[hh][r] = acc;
+    sacc2[hh][r] = acc2;
+    __syncthreads();
+    if (hh == 0 && i < Lo) {
+        acc = sacc[0][r] + sacc[1][r];
+        acc2 = sacc2[0][r] + sacc2[1][r];
+        if (kOp == R12) a.u2b[bo + i] = active ? acc - acc2 : 0.f;
+        float val = 0.f;
+        if (active) {
+            if (kOp == R1 || kOp == R12) val = acc;
+            if (kOp == R2) val = a.g_u[bo + i] - acc;
+            if (kOp == R4) val = kDirect ? -acc : -ex2(o1 - o2) * acc;
+            if (kOp == C3) val = kDirect ? -acc : -ex2(o1 - o2) * acc;
+            if (kOp == C5) val = kDirect ? -acc : -ex2(o0 - o2) * acc;
+        }
+        put(val);
+    }
+}
+
 // Zd_i = dO_i . V_dustbin (rows) and ZdT_j = dO_dustbin . V_j (columns)
 template <class TIn>
 __global__ void k_dust_dots(Geo g, const TIn* __restrict__ dO, const TIn* __restrict__ V, float* Zd, float* ZdT) {
@@ -1300,6 +1427,20 @@ static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
         const int n = row ? g.Lq : g.Lk;
         k<<<dim3((n + 127) / 128, g.BH), 256, smem, s>>>(g, a);
         return cudaGetLastError();
+    }
+    if constexpr (!kVec) {
+        // scalar sweeps over bands whose 128-row tile does not fit SMEM: window-chunked strips
+        if (bwdT_op_smem(g, kOp, D) > 227 * 1024 && bwdW_supported(g)) {
+            constexpr bool kZ = (kOp == R1 || kOp == R12);
+            constexpr int NS = 3;
+            const size_t smem = ((size_t)NS * (kZ ? 2 : 1) * 128 * kWC + 4 * (size_t)(128 + 2 * g.w)) * 4 + 128;
+            auto k = k_sweepW<kOp, kDirect, TIn, NS>;
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            const int n = row ? g.Lq : g.Lk;
+            k<<<dim3((n + 127) / 128, g.BH), 256, smem, s>>>(g, a);
+            return cudaGetLastError();
+        }
     }
     const int rb = pick_rb(g, kOp, D, (int)sizeof(TIn));
     if (rb == 0) return cudaErrorNotSupported;
