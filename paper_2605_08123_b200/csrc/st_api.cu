@@ -182,6 +182,7 @@ struct WsLayout {
     size_t vb2, part[2], partm;  // fused-step ping-pong duals and column partials
     size_t fs_flags, fs_work, fs_cnt, fs_part[2], fs_partm;  // persistent solve: work list, tagged partials
     size_t tail_u, tail_v;  // generic-R adjoint: (R+1) row / column cotangent vectors
+    size_t dpart;           // dustbin line partials [BH][8][129]
     size_t bytes;
 };
 
@@ -253,6 +254,7 @@ WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
     w.v1b = take(rk);
     w.v0b = take(rk);
     w.err = take(sizeof(int));
+    w.dpart = take(sizeof(float) * (size_t)m.BH * 8 * 129);
     w.tail_u = take(rq * (size_t)(m.R + 1));
     w.tail_v = take(rk * (size_t)(m.R + 1));
     for (int p = 0; p < 3; ++p) w.qp[p] = w.kp[p] = 0;
@@ -645,7 +647,7 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
     }
     if (st::bwdT_supported(g) && !(desc->flags & ST_FLAG_GENERIC)) {
         ST_CUDA(st::launch_output_tile(g, desc->dtype, S2, u_prev, v_prev, V, O, st));
-        if (g.dustbin) ST_CUDA(st::launch_output(g, desc->dtype, S2, u_prev, v_prev, V, O, st, 1));
+        if (g.dustbin) ST_CUDA(st::launch_output(g, desc->dtype, S2, u_prev, v_prev, V, O, st, 1, (float*)(ws + wl.dpart)));
     } else {
         ST_CUDA(st::launch_output(g, desc->dtype, S2, u_prev, v_prev, V, O, st));
     }
@@ -732,6 +734,9 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
         t.ZT = ZT;
         t.Zd = (float*)(ws + wl.Zd);
         t.ZdT = (float*)(ws + wl.ZdT);
+        p.Zd = t.Zd;
+        p.ZdT = t.ZdT;
+        p.dpart = (float*)(ws + wl.dpart);
         if (!haveT) ST_CUDA(st::launch_transpose_band(g, p.S2, S2T, st, -INFINITY));
         if (dual) {
             ST_CUDA(st::launch_band_dual(g, desc->dtype, true, dO, V, Z, ZT, st));

@@ -791,6 +791,164 @@ __device__ __forceinline__ float sbar_cell(bool direct, float s2, float u1i, flo
 enum { RB_GU = 0, RB_U2B = 1, RB_U1B = 2, RB_DQ = 3 };
 enum { CB_GV = 0, CB_V1B = 1, CB_V0B = 2, CB_DK = 3 };
 
+// ---------------------------------------------------------------------------
+// The dustbin row / column of the spoke support (full-length lines): each line is split over
+// kDustSplit CTAs per head (one cell per thread; vector terms warp-cooperative), partials in a fixed
+// order, then one combine CTA per head.  Cell scores are the constant sd2 on active cells and the
+// corner; Z of a line cell comes from the precomputed dustbin dots (Zd / ZdT) and the corner dot.
+//   row line (own = dustbin row Lq):    RB_GU, RB_U2B, RB_U1B, RB_DQ (d_eps part; dQ_L = 0), kRO (O_L)
+//   column line (own = dustbin col Lk): CB_GV (+dV_L), CB_V1B, CB_V0B, CB_DK (dK_L = 0)
+// ---------------------------------------------------------------------------
+constexpr int kDustSplit = 8;
+constexpr int kRO = 9;  // forward transport output of the dustbin row
+
+template <bool kCol, int kOp, bool kDirect, class TIn>
+__global__ void __launch_bounds__(256) k_dust_line(Geo g, BwdArgs<TIn> a, const float* __restrict__ Zd,
+                                                   const float* __restrict__ ZdT, float* __restrict__ part) {
+    __shared__ float wsum[8];
+    __shared__ float vsum[8][128];
+    const int s = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int n = kCol ? g.Lq + 1 : g.Lk + 1;  // cells of the line (last = corner)
+    const int chunk = (n + kDustSplit - 1) / kDustSplit;
+    const int c_lo = s * chunk, c_hi = min(n, c_lo + chunk);
+    const size_t ro = (size_t)bh * g.Lrq, co = (size_t)bh * g.Lrk;
+    constexpr bool kVecOut = (kOp == kRO) || (kCol && kOp == CB_GV);
+    constexpr bool kNeedZ = kCol ? (kOp == CB_GV) : (kOp == RB_GU || kOp == RB_DQ);
+    // own duals of the line
+    const size_t own = kCol ? co + g.Lk : ro + g.Lq;
+    const float o2 = kCol ? a.v2[own] : a.u2[own];
+    const float o1 = kCol ? a.v1[own] : a.u1[own];
+    const float o0 = kCol ? a.v0[own] : 0.f;
+    float zc = 0.f;  // corner dot dO_dustbin . V_dustbin
+    if (kNeedZ) {
+        for (int x = lane; x < g.d; x += 32) zc += ldf(a.dO + (ro + g.Lq) * g.d + x) * ldf(a.V + (co + g.Lk) * g.d + x);
+        zc = warp_sum(zc);
+    }
+    const float sd2 = g.sd2;
+    float acc = 0.f;
+    float vacc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int b0 = c_lo + wid * 32; b0 < c_hi; b0 += 256) {
+        const int t = b0 + lane;  // other-side index of this lane's cell (t == Lq / Lk: the corner)
+        float contrib = 0.f, vw = 0.f;
+        if (t < c_hi) {
+            const bool corner = kCol ? t == g.Lq : t == g.Lk;
+            const bool on = corner || (kCol ? row_on(g, bh, t) : col_on(g, bh, t));
+            if (on) {
+                if (kCol) {
+                    const size_t oi = ro + t;
+                    const float u2i = a.u2[oi];
+                    const float p = ex2(sd2 + u2i + o2);
+                    if (kOp == CB_GV) {
+                        const float z = corner ? zc : Zd[(size_t)bh * g.Lqp + t];
+                        contrib = p * z;
+                        vw = p;
+                    } else if (kOp == CB_V1B) {
+                        contrib = (kDirect ? ex2(sd2 + u2i + o1) : p) * a.u2b[oi];
+                    } else if (kOp == CB_V0B) {
+                        const float u1i = a.u1[oi];
+                        contrib = (kDirect ? ex2(sd2 + u1i + o0) : p * ex2(u1i - u2i)) * a.u1b[oi];
+                    }
+                } else {
+                    const size_t oj = co + t;
+                    const float v2j = a.v2[oj];
+                    const float p = ex2(sd2 + o2 + v2j);
+                    if (kOp == kRO) {
+                        vw = p;
+                    } else if (kOp == RB_GU) {
+                        contrib = p * (corner ? zc : ZdT[(size_t)bh * g.Lkp + t]);
+                    } else if (kOp == RB_U2B) {
+                        contrib = p * a.g_v[oj];
+                    } else if (kOp == RB_U1B) {
+                        const float v1j = a.v1[oj];
+                        contrib = (kDirect ? ex2(sd2 + o1 + v1j) : p * ex2(v1j - v2j)) * a.v1b[oj];
+                    } else if (kOp == RB_DQ) {
+                        const float z = corner ? zc : ZdT[(size_t)bh * g.Lkp + t];
+                        const float sb = sbar_cell(kDirect, sd2, o1, o2, a.v0[oj], a.v1[oj], v2j, z, a.u2b[ro + g.Lq],
+                                                   a.u1b[ro + g.Lq], a.g_v[oj], a.v1b[oj]);
+                        contrib = sb * (sd2 * kLn2);
+                    }
+                }
+            }
+        }
+        acc += contrib;
+        if (kVecOut) {  // vector term: sum over this batch's cells of vw * (V_j | dO_i)
+            const TIn* X = kCol ? a.dO + ro * g.d : a.V + co * g.d;
+            const int cnt = min(32, c_hi - b0);
+            for (int q = 0; q < cnt; ++q) {
+                const float wq = __shfl_sync(0xffffffffu, vw, q);
+                if (wq == 0.f) continue;
+                const TIn* xr = X + (size_t)(b0 + q) * g.d;
+#pragma unroll
+                for (int m = 0; m < 4; ++m)
+                    if (lane + 32 * m < g.d) vacc[m] = fmaf(wq, ldf(xr + lane + 32 * m), vacc[m]);
+            }
+        }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) wsum[wid] = acc;
+    if (kVecOut) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+            if (lane + 32 * m < g.d) vsum[wid][lane + 32 * m] = vacc[m];
+    }
+    __syncthreads();
+    float* out = part + ((size_t)bh * kDustSplit + s) * 129;
+    if (tid == 0) {
+        float t = 0.f;
+        for (int w = 0; w < 8; ++w) t += wsum[w];
+        out[0] = t;
+    }
+    if (kVecOut && tid < g.d) {
+        float t = 0.f;
+        for (int w = 0; w < 8; ++w) t += vsum[w][tid];
+        out[1 + tid] = t;
+    }
+}
+
+template <bool kCol, int kOp, bool kDirect, class TIn>
+__global__ void __launch_bounds__(128) k_dust_line_fin(Geo g, BwdArgs<TIn> a, const float* __restrict__ part,
+                                                       float* __restrict__ O) {
+    const int bh = blockIdx.x, tid = threadIdx.x;
+    const size_t ro = (size_t)bh * g.Lrq, co = (size_t)bh * g.Lrk;
+    const float* pp = part + (size_t)bh * kDustSplit * 129;
+    const size_t own = kCol ? co + g.Lk : ro + g.Lq;
+    if (tid == 0) {
+        float tot = 0.f;
+        for (int s = 0; s < kDustSplit; ++s) tot += pp[s * 129];
+        if (kCol) {
+            if (kOp == CB_GV) a.g_v[own] = tot;
+            if (kOp == CB_V1B) a.v1b[own] = kDirect ? -tot : -ex2(a.v1[own] - a.v2[own]) * tot;
+            if (kOp == CB_V0B) a.v0b[own] = kDirect ? -tot : -ex2(a.v0[own] - a.v2[own]) * tot;
+        } else {
+            if (kOp == RB_GU) a.g_u[own] = tot;
+            if (kOp == RB_U2B) a.u2b[own] = a.g_u[own] - tot;
+            if (kOp == RB_U1B) a.u1b[own] = kDirect ? -tot : -ex2(a.u1[own] - a.u2[own]) * tot;
+            if (kOp == RB_DQ) a.deps_part[own] = tot;
+        }
+    }
+    for (int x = tid; x < g.d; x += 128) {
+        float v = 0.f;
+        if (kOp == kRO || (kCol && kOp == CB_GV))
+            for (int s = 0; s < kDustSplit; ++s) v += pp[s * 129 + 1 + x];
+        if (kOp == kRO) O[own * g.d + x] = v;
+        if (kCol && kOp == CB_GV) a.dV[own * g.d + x] = v;
+        if (kCol && kOp == CB_DK) a.dK[own * g.d + x] = 0.f;  // constant cost: no dK of the dustbin key
+        if (!kCol && kOp == RB_DQ) a.dQ[own * g.d + x] = 0.f;
+    }
+}
+
+void add_launches(long long n);
+
+template <bool kCol, int kOp, bool kDirect, class TIn>
+static void dust_line(const Geo& g, const BwdArgs<TIn>& a, const float* Zd, const float* ZdT, float* part, float* O,
+                      cudaStream_t s) {
+    if (!(kCol && kOp == CB_DK))
+        k_dust_line<kCol, kOp, kDirect, TIn><<<dim3(kDustSplit, g.BH), 256, 0, s>>>(g, a, Zd, ZdT, part);
+    k_dust_line_fin<kCol, kOp, kDirect, TIn><<<g.BH, 128, 0, s>>>(g, a, part, O);
+    add_launches(2);
+}
+
+
 template <int kOp, bool kDirect, class TIn>
 __global__ void __launch_bounds__(256) k_bwd_row(Geo g, BwdArgs<TIn> a, int last_only) {
     __shared__ float sh_vec[8][128];
@@ -1192,7 +1350,20 @@ cudaError_t launch_col_step(const Geo& g, bool first, const float* S2, const flo
 }
 
 cudaError_t launch_output(const Geo& g, int dtype, const float* S2, const float* u, const float* v, const void* V,
-                          float* O, cudaStream_t s, int last_only) {
+                          float* O, cudaStream_t s, int last_only, float* dpart) {
+    if (last_only && dpart != nullptr && g.d <= 128) {  // the dustbin row: split line kernel
+        auto go = [&](auto tag) {
+            using TIn = decltype(tag);
+            BwdArgs<TIn> a{};
+            a.u1 = a.u2 = u;
+            a.v0 = a.v1 = a.v2 = v;
+            a.V = (const TIn*)V;
+            dust_line<false, kRO, false, TIn>(g, a, nullptr, nullptr, dpart, O, s);
+        };
+        if (dtype == 0) go(float{});
+        else go(__nv_bfloat16{});
+        return cudaGetLastError();
+    }
     const unsigned nb = nblocks((long)g.BH * (last_only ? 1 : g.Lrq), 8);
     if (dtype == 0) k_output<float><<<nb, 256, 0, s>>>(g, S2, u, v, (const float*)V, O, last_only);
     else k_output<__nv_bfloat16><<<nb, 256, 0, s>>>(g, S2, u, v, (const __nv_bfloat16*)V, O, last_only);
@@ -1298,6 +1469,22 @@ static BwdArgs<TIn> bwd_args(const BwdPtrs& p) {
 template <class TIn, bool kD>
 static cudaError_t dust_stage_t(const Geo& g, const BwdPtrs& p, int stage, cudaStream_t s) {
     const BwdArgs<TIn> a = bwd_args<TIn>(p);
+    if (p.dpart != nullptr && g.d <= 128) {  // split line kernels
+        switch (stage) {
+            case 0:
+                dust_line<false, RB_GU, kD, TIn>(g, a, p.Zd, p.ZdT, p.dpart, nullptr, s);
+                dust_line<true, CB_GV, kD, TIn>(g, a, p.Zd, p.ZdT, p.dpart, nullptr, s);
+                break;
+            case 1: dust_line<false, RB_U2B, kD, TIn>(g, a, p.Zd, p.ZdT, p.dpart, nullptr, s); break;
+            case 2: dust_line<true, CB_V1B, kD, TIn>(g, a, p.Zd, p.ZdT, p.dpart, nullptr, s); break;
+            case 3: dust_line<false, RB_U1B, kD, TIn>(g, a, p.Zd, p.ZdT, p.dpart, nullptr, s); break;
+            case 4: dust_line<true, CB_V0B, kD, TIn>(g, a, p.Zd, p.ZdT, p.dpart, nullptr, s); break;
+            default:
+                dust_line<false, RB_DQ, kD, TIn>(g, a, p.Zd, p.ZdT, p.dpart, nullptr, s);
+                dust_line<true, CB_DK, kD, TIn>(g, a, p.Zd, p.ZdT, p.dpart, nullptr, s);
+        }
+        return cudaGetLastError();
+    }
     const unsigned nb = nblocks(g.BH, 8);
     switch (stage) {
         case 0:

@@ -13,6 +13,8 @@ struct BwdPtrs {
     float *g_u, *g_v, *u2b, *v1b, *u1b, *v0b;
     const void *Q, *K, *V, *dO;
     float *dQ, *dK, *dV, *deps_part;
+    const float *Zd = nullptr, *ZdT = nullptr;  // dustbin dots (tile backward)
+    float* dpart = nullptr;                     // [BH][8][129] dustbin line partials (null: generic kernels)
 };
 
 // extra bands of the tile backward (st_bwd.cu)
@@ -122,7 +124,7 @@ cudaError_t launch_stepT(const Geo& g, bool first, const float* S2, const float*
 cudaError_t launch_col_step(const Geo& g, bool first, const float* S2, const float* u, const float* v_prev,
                             float* v_out, int* err, cudaStream_t s);
 cudaError_t launch_output(const Geo& g, int dtype, const float* S2, const float* u, const float* v, const void* V,
-                          float* O, cudaStream_t s, int last_only = 0);
+                          float* O, cudaStream_t s, int last_only = 0, float* dpart = nullptr);
 cudaError_t launch_gauges(const Geo& g, const float* u_slots, int nslots, float* gauge, cudaStream_t s);
 cudaError_t launch_backward(const Geo& g, int dtype, const BwdPtrs& p, bool direct, cudaStream_t s);
 cudaError_t launch_deps_reduce(const Geo& g, const float* part, float* out, cudaStream_t s, int i_begin = 0,
