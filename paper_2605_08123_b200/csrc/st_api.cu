@@ -622,17 +622,10 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
             dr.sd2 = dc.sd2 = gs.sd2;
             if (tile) {
                 // fp32 path: bulk-copied band tiles, in-thread reductions; columns via the transposed band
+                // (dustbin problems: the dustbin row / column ride in the same launches)
                 ST_CUDA(st::launch_stepT(gs, t == 1, S2, v_prev, u_prev, u_out, err, st));
-                if (g.dustbin) {
-                    dr.dual_other = v_prev; dr.off_own = u_prev; dr.out_own = u_out;
-                    ST_CUDA(st::launch_dustbin(dr, t == 1, g.BH, st));
-                }
                 halo(0, u_out);
                 ST_CUDA(st::launch_stepT(gts, t == 1, S2T, u_out, v_prev, v_out, err, st));
-                if (g.dustbin) {
-                    dc.dual_other = u_out; dc.off_own = v_prev; dc.out_own = v_out;
-                    ST_CUDA(st::launch_dustbin(dc, t == 1, g.BH, st));
-                }
                 halo(1, v_out);
             } else {
                 ST_CUDA(st::launch_row_step(gs, t == 1, S2, v_prev, u_prev, u_out, err, st));

@@ -266,6 +266,43 @@ __global__ void __launch_bounds__(128) k_stepT(Geo g, const float* __restrict__ 
                                                const float* off_own, float* out_own, int* err) {
     extern __shared__ __align__(16) float smf[];
     __shared__ __align__(8) uint64_t bar;
+    if (g.dustbin && blockIdx.x == gridDim.x - 1) {
+        // the extra CTA column: the own side's dustbin dual (a full-length line over the other side's
+        // active duals and the corner, constant score sd2), same launch as the band rows
+        __shared__ float red[4];
+        const int bh = blockIdx.y, t = threadIdx.x, lane = t & 31, wid = t >> 5;
+        const float* dual = dual_other + (size_t)bh * g.Lrk;
+        const int n = g.Lk + 1;
+        float off;
+        if (kFirst) {
+            float m = -INFINITY;
+            for (int j = t; j < n; j += 128)
+                if (j == g.Lk || col_on(g, bh, j)) m = fmaxf(m, g.sd2 + dual[j]);
+            m = warp_max(m);
+            if (lane == 0) red[wid] = m;
+            __syncthreads();
+            off = -fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+            __syncthreads();
+        } else {
+            off = off_own[(size_t)bh * g.Lrq + g.Lq];
+        }
+        float sum = 0.f;
+        for (int j = t; j < n; j += 128)
+            if (j == g.Lk || col_on(g, bh, j)) sum += ex2(g.sd2 + dual[j] + off);
+        sum = warp_sum(sum);
+        if (lane == 0) red[wid] = sum;
+        __syncthreads();
+        if (t == 0) {
+            const float tot = (red[0] + red[1]) + (red[2] + red[3]);
+            float u = off - lg2(tot);
+            if (!(tot > 0.f) || !isfinite(u)) {
+                atomicOr(err, 8);
+                u = 0.f;
+            }
+            out_own[(size_t)bh * g.Lrq + g.Lq] = u;
+        }
+        return;
+    }
     const int bh = blockIdx.y, i0 = blockIdx.x * 128, r = threadIdx.x, i = i0 + r;
     const bool active = i < g.Lq && row_on(g, bh, i);
     if (!__syncthreads_or(active)) {
@@ -1289,7 +1326,8 @@ cudaError_t launch_stepT(const Geo& g, bool first, const float* S2, const float*
         if (e != cudaSuccess) return e;
         cur = smem;
     }
-    k<<<dim3((g.Lq + 127) / 128, g.BH), 128, smem, s>>>(g, S2, dual_other, off_own, out_own, err);
+    // dustbin problems: one more CTA column computes the own dustbin dual in the same launch
+    k<<<dim3((g.Lq + 127) / 128 + (g.dustbin ? 1 : 0), g.BH), 128, smem, s>>>(g, S2, dual_other, off_own, out_own, err);
     ++g_launches;
     return cudaGetLastError();
 }

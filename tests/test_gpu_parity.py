@@ -482,3 +482,25 @@ def test_wide_band_window_chunked_stages_parity(dtype, d, w, mask, mode):
     inp = configs.make_inputs(cfg)
     tol = BF16_TOL if dtype == "bf16" else FP32_TOL
     check_against_oracle(cfg, inp, tol, tol, mode=mode)
+
+
+# bf16 inputs on the dustbin config: the tensor-core solve accumulates config 3's large scores
+# (|s2| ~ 115) in fp32 inside the MMA, ~1e-4 relative per score, which the score-sensitive dQ / dK
+# amplify to ~1e-3 (the reference's own f32 instantiation sits at ~4e-4 there).  Stated bound:
+BF16_DUSTBIN_GRAD_TOL = 2e-3
+
+
+@pytest.mark.parametrize("dtype,mode", [("f32", "direct_four_plan"), ("f32", "one_reference"),
+                                        ("bf16", "one_reference")])
+def test_dustbin_line_kernels_parity(dtype, mode):
+    """The dustbin row / column (full-length lines, split over CTAs with fixed-order partials, and the
+    dustbin duals riding in the half-step launches) in both adjoint schedules and both input dtypes,
+    with masked examples, against the oracle."""
+    cfg = configs.CONFIGS[3].replace(B=2, H=2, L=640, dtype=dtype)
+    inp = configs.make_inputs(cfg)
+    if dtype == "bf16":
+        check_against_oracle(cfg, inp, BF16_TOL, BF16_DUSTBIN_GRAD_TOL, mode=mode)
+        return
+    g, r, _ = check_against_oracle(cfg, inp, FP32_TOL, FP32_GRAD_TOL, mode=mode)
+    assert np.abs(g["dQ"][:, cfg.L]).max() == 0.0
+    assert np.abs(g["dK"][:, cfg.L]).max() == 0.0
