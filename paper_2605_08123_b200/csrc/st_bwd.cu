@@ -284,6 +284,15 @@ __global__ void __launch_bounds__(128) k_bwdT(Geo g, BT<TIn> a) {
 // GEMM: thread = 4 own rows x (D/8) columns, per band step 4 broadcast W loads
 // + D/32 LDS.128 of the operand row feed 4 D/8 FMAs.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 ffma2w(float2 a, float2 b, float2 c) {  // FFMA2 (packed fp32, sm_100)
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "mov.b64 rc, {%6, %7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+
 template <int kOp, bool kDirect, int D, class TIn>
 __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
     extern __shared__ __align__(16) float smf[];
@@ -486,31 +495,31 @@ __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
     // ---- phase 2: band GEMM.  thread = rows 4 rg .. 4 rg + 3, column chunks {4 cg + 32 m}
     if (g.dbg & 1) return;  // timing studies only (ST_BWD_DBG)
     const int rg = tid >> 3, cg = tid & 7;
-    float accv[4][CPT];
+    float2 accv[4][CPT / 2];  // column pairs (FFMA2)
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int e = 0; e < CPT; ++e) accv[q][e] = 0.f;
+        for (int e = 0; e < CPT / 2; ++e) accv[q][e] = make_float2(0.f, 0.f);
     const float* wrow = tS + (4 * rg) * Wf;
     // band step kk feeds rows q with cell k = kk - q; only the first / last 3 steps need the
     // k in [0, Wf) guard, the interior runs check-free
     auto step = [&](int kk, bool guard) {
-        float wq[4];
+        float2 wq[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int k = kk - q;
-            wq[q] = (!guard || (k >= 0 && k < Wf)) ? wrow[q * Wf + k] : 0.f;
+            const float wk = (!guard || (k >= 0 && k < Wf)) ? wrow[q * Wf + k] : 0.f;
+            wq[q] = make_float2(wk, wk);
         }
         const float* xr = ops + (4 * rg + kk) * D + 4 * cg;
 #pragma unroll
         for (int m = 0; m < CPT / 4; ++m) {
             const float4 x4 = *reinterpret_cast<const float4*>(xr + 32 * m);
+            const float2 xa = make_float2(x4.x, x4.y), xb = make_float2(x4.z, x4.w);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                accv[q][4 * m + 0] = fmaf(wq[q], x4.x, accv[q][4 * m + 0]);
-                accv[q][4 * m + 1] = fmaf(wq[q], x4.y, accv[q][4 * m + 1]);
-                accv[q][4 * m + 2] = fmaf(wq[q], x4.z, accv[q][4 * m + 2]);
-                accv[q][4 * m + 3] = fmaf(wq[q], x4.w, accv[q][4 * m + 3]);
+                accv[q][2 * m + 0] = ffma2w(xa, wq[q], accv[q][2 * m + 0]);
+                accv[q][2 * m + 1] = ffma2w(xb, wq[q], accv[q][2 * m + 1]);
             }
         }
     };
@@ -529,8 +538,8 @@ __global__ void __launch_bounds__(256) k_bwdV(Geo g, BT<TIn> a) {
 #pragma unroll
         for (int m = 0; m < CPT / 4; ++m) {
             const int col = 4 * cg + 32 * m;
-            float4 o4 = make_float4(accv[q][4 * m] * sc, accv[q][4 * m + 1] * sc, accv[q][4 * m + 2] * sc,
-                                    accv[q][4 * m + 3] * sc);
+            float4 o4 = make_float4(accv[q][2 * m].x * sc, accv[q][2 * m].y * sc, accv[q][2 * m + 1].x * sc,
+                                    accv[q][2 * m + 1].y * sc);
             if (dsrc != nullptr && g.dustbin) {  // + p_dust * (V | dO)_dustbin
                 const TIn* dr = dsrc + (bx + Lx) * D + col;
                 o4.x = fmaf(pdq, ldf(dr), o4.x);
@@ -920,7 +929,7 @@ __global__ void __launch_bounds__(256) k_bwdG(Geo g, BT<TIn> a) {
 // fixed order (increasing window column), and the kernel is independent of the band width beyond
 // the chunk count.
 // ---------------------------------------------------------------------------
-constexpr int kWC = 32;  // window columns per chunk
+constexpr int kWC = 16;  // window columns per chunk
 
 // 16-byte global -> shared async copy (LDGSTS); src_bytes = 0 zero-fills the destination
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
@@ -938,7 +947,8 @@ __host__ __device__ constexpr size_t bwdW_stage_floats(bool z) {
 template <int D, class TIn>
 static size_t bwdW_smem_bytes(const Geo& g, bool z, int nstg) {
     const int Nw = 128 + 2 * g.w;
-    return ((size_t)nstg * bwdW_stage_floats<D, TIn>(z) + kWC * 128 + 5 * (size_t)Nw) * 4 + 128;
+    const size_t xf = sizeof(TIn) == 4 ? 0 : (size_t)kWC * D;  // f32 copy of a bf16 operand chunk
+    return ((size_t)nstg * bwdW_stage_floats<D, TIn>(z) + kWC * 128 + xf + 5 * (size_t)Nw) * 4 + 128;
 }
 bool bwdW_supported(const Geo& g) {
     return !g.dustbin && g.w >= 16 && g.w % 16 == 0 && (g.d == 32 || g.d == 64 || g.d == 128) &&
@@ -946,7 +956,7 @@ bool bwdW_supported(const Geo& g) {
 }
 
 template <int kOp, bool kDirect, int D, class TIn, int NSTG>
-__global__ void __launch_bounds__(256) k_bwdW(Geo g, BT<TIn> a) {
+__global__ void __launch_bounds__(256, (D <= 64 ? 3 : 2)) k_bwdW(Geo g, BT<TIn> a) {
     extern __shared__ __align__(128) float smw[];
     __shared__ float sacc[2][128], sdacc[2][128];
     constexpr bool kRow = kOp < 10;
@@ -976,7 +986,8 @@ __global__ void __launch_bounds__(256) k_bwdW(Geo g, BT<TIn> a) {
     const int Wf = g.Wf, Nw = 128 + 2 * g.w, NCH = Nw / kWC;
     const size_t stf = bwdW_stage_floats<D, TIn>(kNeedZ);
     float* WT = smw + NSTG * stf;     // [kWC][128]
-    float* wv = WT + kWC * 128;       // [5][Nw]
+    float* Xf = WT + kWC * 128;       // [kWC][D] f32 operand chunk (bf16 inputs: converted once per chunk)
+    float* wv = Xf + (sizeof(TIn) == 4 ? 0 : kWC * D);  // [5][Nw]
     const float* Sb = (kRow ? a.S2 : a.S2T) + ((size_t)bh * Lpo + i0) * Wf;
     const float* Zb = kNeedZ ? (kRow ? a.Z : a.ZT) + ((size_t)bh * Lpo + i0) * Wf : nullptr;
     const TIn* osrc = (kOp == R6 || kOp == RW) ? a.K : (kOp == C1) ? a.dO : (kOp == RO) ? a.V : a.Q;
@@ -1063,11 +1074,11 @@ __global__ void __launch_bounds__(256) k_bwdW(Geo g, BT<TIn> a) {
     float acc = 0.f, dacc = 0.f;
     const int rg = tid >> 3, cg = tid & 7;
     const int wr0 = warp * 16;  // phase-2 rows of this warp: [wr0, wr0 + 16)
-    float accv[4][CPT];
+    float2 accv[4][CPT / 2];  // column pairs (FFMA2: half the issue slots of the chunk GEMM)
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int e = 0; e < CPT; ++e) accv[q][e] = 0.f;
+        for (int e = 0; e < CPT / 2; ++e) accv[q][e] = make_float2(0.f, 0.f);
     for (int j = 0; j < NCH; ++j) {
         const int s = j % NSTG, c0 = j * kWC;
         cp_async_wait<NSTG - 2>();  // this thread's copies of chunk j landed
@@ -1076,12 +1087,20 @@ __global__ void __launch_bounds__(256) k_bwdW(Geo g, BT<TIn> a) {
         else cp_async_commit();
         const float* S = stS(s);
         const float* Z = stZ(s);
-        const TIn* X = stX(s);
+        const float* X;  // the chunk's operand rows as f32
+        if constexpr (sizeof(TIn) == 4) {
+            X = reinterpret_cast<const float*>(stX(s));
+        } else {  // one conversion per element instead of one per row group (read again after phase 1's barrier)
+            const TIn* Xb = stX(s);
+            for (int e = 4 * tid; e < kWC * D; e += 4 * 256)
+                *reinterpret_cast<float4*>(Xf + e) = ld4f<TIn>(Xb + e);
+            X = Xf;
+        }
         // ---- phase 1: weights of this thread's 16 columns of row r (rotated: conflict-free)
         float* wt = WT;  // single buffer: every thread finished the previous chunk's phase 2 (barrier above)
 #pragma unroll 4
         for (int jj = 0; jj < kWC / 2; ++jj) {
-            const int cl = (r + 16 * hh + jj) & (kWC - 1);
+            const int cl = (r + (kWC / 2) * hh + jj) & (kWC - 1);
             const int c = c0 + cl;
             const float s2 = S[r * kWC + cl];
             float wgt = 0.f;
@@ -1124,20 +1143,20 @@ __global__ void __launch_bounds__(256) k_bwdW(Geo g, BT<TIn> a) {
         // ---- phase 2: out[4 rg + q][4 cg + 32 m ..] += sum_c W[row][c] X[c][..]
         if (c0 <= wr0 + 15 + 2 * g.w && c0 + kWC - 1 >= wr0) {
             const float* wrow = wt + 4 * rg;
-            const TIn* xr = X + 4 * cg;
+            const float* xr = X + 4 * cg;
 #pragma unroll 4
             for (int cl = 0; cl < kWC; ++cl) {
                 const float4 w4 = *reinterpret_cast<const float4*>(wrow + cl * 128);
-                const float wq[4] = {w4.x, w4.y, w4.z, w4.w};
+                const float2 wq[4] = {make_float2(w4.x, w4.x), make_float2(w4.y, w4.y), make_float2(w4.z, w4.z),
+                                      make_float2(w4.w, w4.w)};
 #pragma unroll
                 for (int m = 0; m < CPT / 4; ++m) {
-                    const float4 x4 = ld4f<TIn>(xr + cl * D + 32 * m);
+                    const float4 x4 = *reinterpret_cast<const float4*>(xr + cl * D + 32 * m);
+                    const float2 xa = make_float2(x4.x, x4.y), xb = make_float2(x4.z, x4.w);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        accv[q][4 * m + 0] = fmaf(wq[q], x4.x, accv[q][4 * m + 0]);
-                        accv[q][4 * m + 1] = fmaf(wq[q], x4.y, accv[q][4 * m + 1]);
-                        accv[q][4 * m + 2] = fmaf(wq[q], x4.z, accv[q][4 * m + 2]);
-                        accv[q][4 * m + 3] = fmaf(wq[q], x4.w, accv[q][4 * m + 3]);
+                        accv[q][2 * m + 0] = ffma2w(xa, wq[q], accv[q][2 * m + 0]);
+                        accv[q][2 * m + 1] = ffma2w(xb, wq[q], accv[q][2 * m + 1]);
                     }
                 }
             }
@@ -1163,8 +1182,8 @@ __global__ void __launch_bounds__(256) k_bwdW(Geo g, BT<TIn> a) {
         for (int m = 0; m < CPT / 4; ++m) {
             const int col = 4 * cg + 32 * m;
             *reinterpret_cast<float4*>(vo + (bo + ii) * D + col) =
-                make_float4(accv[q][4 * m] * sc, accv[q][4 * m + 1] * sc, accv[q][4 * m + 2] * sc,
-                            accv[q][4 * m + 3] * sc);
+                make_float4(accv[q][2 * m].x * sc, accv[q][2 * m].y * sc, accv[q][2 * m + 1].x * sc,
+                            accv[q][2 * m + 1].y * sc);
         }
     }
 }
@@ -1173,7 +1192,7 @@ __global__ void __launch_bounds__(256) k_bwdW(Geo g, BT<TIn> a) {
 // whose 128-row tile does not fit SMEM: 2 threads per row (rotated columns), NSTG-deep cp.async ring
 // of [128][32] S (and Z) strips, one barrier per chunk, 2-3 CTAs per SM.
 template <int kOp, bool kDirect, class TIn, int NSTG>
-__global__ void __launch_bounds__(256) k_sweepW(Geo g, BT<TIn> a) {
+__global__ void __launch_bounds__(256, 4) k_sweepW(Geo g, BT<TIn> a) {
     extern __shared__ __align__(128) float smw[];
     __shared__ float sacc[2][128], sacc2[2][128];
     constexpr bool kRow = kOp < 10;
@@ -1261,7 +1280,7 @@ __global__ void __launch_bounds__(256) k_sweepW(Geo g, BT<TIn> a) {
         if (!active || c0 > r + 2 * g.w || c0 + kWC - 1 < r) continue;  // this row's band misses the chunk
 #pragma unroll 4
         for (int jj = 0; jj < kWC / 2; ++jj) {
-            const int cl = (r + 16 * hh + jj) & (kWC - 1);
+            const int cl = (r + (kWC / 2) * hh + jj) & (kWC - 1);
             const int c = c0 + cl;
             const float s2 = S[r * kWC + cl];
             if ((unsigned)(c - r) >= (unsigned)Wf || s2 == -INFINITY) continue;
@@ -1403,9 +1422,11 @@ static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
         if (!narrow_ok && bwdW_supported(g)) {
             constexpr bool kZ = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RW || kOp == CW);
             static const int nstg = getenv("ST_BWDW_NSTG") ? atoi(getenv("ST_BWDW_NSTG")) : 2;
-            const size_t smem = bwdW_smem_bytes<D, TIn>(g, kZ, nstg == 3 ? 3 : 2);
+            const int ns = nstg >= 4 ? 4 : nstg == 3 ? 3 : 2;
+            const size_t smem = bwdW_smem_bytes<D, TIn>(g, kZ, ns);
             if (smem <= 227 * 1024) {
-                auto k = nstg == 3 ? k_bwdW<kOp, kDirect, D, TIn, 3> : k_bwdW<kOp, kDirect, D, TIn, 2>;
+                auto k = ns == 4 ? k_bwdW<kOp, kDirect, D, TIn, 4>
+                                 : ns == 3 ? k_bwdW<kOp, kDirect, D, TIn, 3> : k_bwdW<kOp, kDirect, D, TIn, 2>;
                 cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 if (e != cudaSuccess) return e;
                 const int n = row ? g.Lq : g.Lk;
@@ -1432,9 +1453,10 @@ static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
         // scalar sweeps over bands whose 128-row tile does not fit SMEM: window-chunked strips
         if (bwdT_op_smem(g, kOp, D) > 227 * 1024 && bwdW_supported(g)) {
             constexpr bool kZ = (kOp == R1 || kOp == R12);
-            constexpr int NS = 3;
+            static const int ns_env = getenv("ST_SWEEPW_NSTG") ? atoi(getenv("ST_SWEEPW_NSTG")) : 3;
+            const int NS = ns_env >= 4 ? 4 : ns_env == 2 ? 2 : 3;
             const size_t smem = ((size_t)NS * (kZ ? 2 : 1) * 128 * kWC + 4 * (size_t)(128 + 2 * g.w)) * 4 + 128;
-            auto k = k_sweepW<kOp, kDirect, TIn, NS>;
+            auto k = NS == 4 ? k_sweepW<kOp, kDirect, TIn, 4> : NS == 2 ? k_sweepW<kOp, kDirect, TIn, 2> : k_sweepW<kOp, kDirect, TIn, 3>;
             cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
             const int n = row ? g.Lq : g.Lk;
