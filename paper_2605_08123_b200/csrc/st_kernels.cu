@@ -119,7 +119,8 @@ struct BandMma {
     static constexpr int CP = D <= 64 ? 2 : 1;   // key column tiles per warp pass (B fragments in registers)
     static constexpr int NWARP = 8;
     static constexpr int P = D + 4;               // SMEM pitch (doubles): conflict-free A fragment loads
-    static size_t smem() { return (size_t)128 * P * 8; }
+    static constexpr int RB = D <= 64 ? 128 : 64; // query rows per CTA (d = 128: 64 rows -> 3 CTAs / SM)
+    static size_t smem() { return (size_t)RB * P * 8; }
 };
 
 // Warp pass = CP key column tiles (8 keys each, B fragments converted to f64
@@ -130,12 +131,12 @@ template <class TIn, bool kZ, int D>
 __global__ void __launch_bounds__(256) k_band_mma(Geo g, const TIn* __restrict__ A, const TIn* __restrict__ B,
                                                   float* __restrict__ out, float* __restrict__ outT) {
     using M = BandMma<D>;
-    constexpr int CP = M::CP, P = M::P, KS = D / 4;
-    extern __shared__ __align__(16) double sqa[];  // [128][P] query rows of the block, f64
-    const int bh = blockIdx.y, i0 = blockIdx.x * 128, j0 = i0 - g.w;
+    constexpr int CP = M::CP, P = M::P, KS = D / 4, RB = M::RB, NRT = RB / 8;
+    extern __shared__ __align__(16) double sqa[];  // [RB][P] query rows of the block, f64
+    const int bh = blockIdx.y, i0 = blockIdx.x * RB, j0 = i0 - g.w;
     const TIn* Ah = A + (size_t)bh * g.Lrq * D;
     const TIn* Bh = B + (size_t)bh * g.Lrk * D;
-    for (int e = threadIdx.x; e < 128 * (D / 4); e += 256) {
+    for (int e = threadIdx.x; e < RB * (D / 4); e += 256) {
         const int r = e / (D / 4), x = (e % (D / 4)) * 4;
         const int i = i0 + r;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(256) k_band_mma(Geo g, const TIn* __restrict__
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
     const int CT = (7 + 2 * g.w) / 8 + 1;     // column tiles one row tile touches
-    const int NCT = 15 + CT;                  // column tiles of the block window
+    const int NCT = NRT - 1 + CT;             // column tiles of the block window
     const int npass = (NCT + CP - 1) / CP;
     for (int pass = warp; pass < npass; pass += M::NWARP) {
         const int c0 = pass * CP;
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(256) k_band_mma(Geo g, const TIn* __restrict__
             }
         }
         // row tiles touching column tiles [c0, c0 + CP): ri in [c0 - CT + 1, c0 + CP - 1]
-        const int rlo = max(0, c0 - CT + 1), rhi = min(15, c0 + CP - 1);
+        const int rlo = max(0, c0 - CT + 1), rhi = min(NRT - 1, c0 + CP - 1);
         // two row tiles per iteration: 2*CP independent accumulation chains per warp
         for (int ri = rlo; ri <= rhi; ri += 2) {
             const bool two = ri + 1 <= rhi;
@@ -1236,7 +1237,7 @@ static cudaError_t launch_band_mma(const Geo& g, const void* A, const void* B, f
     auto kern = k_band_mma<TIn, kZ, D>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<dim3((g.Lq + 127) / 128, g.BH), 256, smem, s>>>(g, (const TIn*)A, (const TIn*)B, out, outT);
+    kern<<<dim3((g.Lq + M::RB - 1) / M::RB, g.BH), 256, smem, s>>>(g, (const TIn*)A, (const TIn*)B, out, outT);
     ++g_launches;
     return cudaGetLastError();
 }
