@@ -301,6 +301,58 @@ int num_sms() {
     return n;
 }
 
+// One tcgen05 band write pass (bf16 operand planes): the score band (cot = false, s2 = q.k c2) or
+// the cotangent band (cot = true, dO.v) of the own side -- rows = queries (col = false) or keys
+// (col = true, the transposed band).  The SMEM plan is refitted for the transpose tiles.
+cudaError_t tc_band_pass(const TcPlan& tp, const Dims& m, const st::Geo& g, bool col, bool cot, const uint8_t* A_pack,
+                         const uint8_t* B_pack, float* pad_own, float* pad_other, float* out, int* err, cudaStream_t st) {
+    st::PhaseArgs a{};
+    a.npl = 1;
+    a.CR = tp.CR;
+    a.shift = tp.shift;
+    a.row_bytes = tp.row_bytes;
+    a.maxwin = tp.maxwin;
+    a.H = g.H;
+    a.w = g.w;
+    a.c2 = g.c2;
+    a.err = err;
+    a.NB = col ? tp.NBk : tp.NBq;
+    a.L_own = col ? g.Lk : g.Lq;
+    a.L_other = col ? g.Lq : g.Lk;
+    a.Lr_own = col ? g.Lrk : g.Lrq;
+    a.Lr_other = col ? g.Lrq : g.Lrk;
+    a.Lp_own = col ? tp.Lpk : tp.Lpq;
+    a.Lp_other = col ? tp.Lpq : tp.Lpk;
+    a.mask_own = col ? g.col_mask : g.row_mask;
+    a.mask_other = col ? g.row_mask : g.col_mask;
+    a.A_pack[0] = A_pack;
+    a.B_pack[0] = B_pack;
+    a.pad_own = pad_own;
+    a.pad_other = pad_other;
+    a.pad_ld_own = tp.CR + a.Lp_own;
+    a.pad_ld_other = tp.CR + a.Lp_other;
+    a.pad_off = tp.CR;
+    a.work = nullptr;
+    a.nwork_all = (int)(m.BH * a.NB);
+    a.band_out = out;
+    a.band_ld = col ? g.Lkp : g.Lqp;
+    a.Wf = g.Wf;
+    const int grid = std::min(num_sms(), a.nwork_all);
+    a.wl_cap = (a.nwork_all + grid - 1) / grid;
+    const int nchunk = tp.maxwin / tp.CR;
+    for (int ew : {16, 8}) {
+        if (tp.CR == 64 && ew == 16) continue;
+        a.ew_write = ew;
+        for (int na = 2; na >= 1; --na)
+            for (int extra = 2; extra >= 0; --extra) {
+                a.NA = na;
+                a.NSK = nchunk + extra;
+                if (st::phase_smem_bytes(a) <= 227 * 1024) return st::launch_phase_band(a, cot, grid, st);
+            }
+    }
+    return cudaErrorNotSupported;
+}
+
 #define ST_CUDA(call)                                                                  \
     do {                                                                               \
         cudaError_t e_ = (call);                                                       \
@@ -519,8 +571,17 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
             u_prev = u_out;
             v_prev = v_out;
         }
-        if (dualT) ST_CUDA(st::launch_band_dual(g, desc->dtype, false, Q, K, S2, S2T_ws, st));
-        else ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));  // transport application
+        if (tp.npl == 1 && !getenv("ST_NO_TCBAND")) {
+            // the stored score band (transport application, backward reuse) from the packed planes on
+            // tcgen05 -- the same fp32-accumulated scores the solve used; the transposed band from the
+            // column geometry.  Activity: the padded duals (-inf on inactive rows / columns).
+            ST_CUDA(tc_band_pass(tp, m, g, false, false, qp[0], kp[0], pad_u, pad_v, S2, err, st));
+            if (dualT) ST_CUDA(tc_band_pass(tp, m, g, true, false, kp[0], qp[0], pad_v, pad_u, S2T_ws, err, st));
+        } else if (dualT) {
+            ST_CUDA(st::launch_band_dual(g, desc->dtype, false, Q, K, S2, S2T_ws, st));
+        } else {
+            ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));  // transport application
+        }
     } else {
         if (dualT) ST_CUDA(st::launch_band_dual(g, desc->dtype, false, Q, K, S2, S2T_ws, st));
         else ST_CUDA(st::launch_scores(g, desc->dtype, Q, K, S2, st));
@@ -708,7 +769,25 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
     if (generic_tail && !tiled) return fail(ST_NOT_SUPPORTED, "the generic tail adjoint needs d in {32, 64, 128}");
     const bool dual = tiled && st::band_dual_supported(g);
     bool haveT = reuse == 2;
-    if (!reuse) {
+    // bf16 planes: the bands on tcgen05 (the forward's solve and band used the same scores)
+    const TcPlan tpb = tc_plan(desc, m);
+    const bool tcb = tiled && dual && tpb.ok && tpb.npl == 1 && !getenv("ST_NO_TCBAND");
+    float* pad_u = tcb ? (float*)(ws + wl.pad_u) : nullptr;
+    float* pad_v = tcb ? (float*)(ws + wl.pad_v) : nullptr;
+    uint8_t* qp0 = tcb ? (uint8_t*)(ws + wl.qp[0]) : nullptr;
+    uint8_t* kp0 = tcb ? (uint8_t*)(ws + wl.kp[0]) : nullptr;
+    int* errp = (int*)(ws + wl.err);
+    if (tcb) {
+        ST_CUDA(st::launch_pad_fill(pad_u, nullptr, g.BH, g.H, g.Lq, g.Lrq, tpb.CR + tpb.Lpq, tpb.CR, row_mask, st));
+        ST_CUDA(st::launch_pad_fill(pad_v, nullptr, g.BH, g.H, g.Lk, g.Lrk, tpb.CR + tpb.Lpk, tpb.CR, col_mask, st));
+        if (!reuse) {
+            ST_CUDA(st::launch_pack(desc->dtype, Q, g.BH, g.Lq, g.Lrq, tpb.Lpq, g.d, tpb.shift, qp0, nullptr, nullptr, st));
+            ST_CUDA(st::launch_pack(desc->dtype, K, g.BH, g.Lk, g.Lrk, tpb.Lpk, g.d, tpb.shift, kp0, nullptr, nullptr, st));
+            ST_CUDA(tc_band_pass(tpb, m, g, false, false, qp0, kp0, pad_u, pad_v, (float*)p.S2, errp, st));
+            ST_CUDA(tc_band_pass(tpb, m, g, true, false, kp0, qp0, pad_v, pad_u, (float*)(ws + wl.S2T), errp, st));
+            haveT = true;
+        }
+    } else if (!reuse) {
         if (dual) {
             ST_CUDA(st::launch_band_dual(g, desc->dtype, false, Q, K, (float*)p.S2, (float*)(ws + wl.S2T), st));
             haveT = true;
@@ -731,7 +810,12 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
         p.ZdT = t.ZdT;
         p.dpart = (float*)(ws + wl.dpart);
         if (!haveT) ST_CUDA(st::launch_transpose_band(g, p.S2, S2T, st, -INFINITY));
-        if (dual) {
+        if (tcb) {  // Z = dO V^T on tcgen05 (bf16 products exact, fp32 accumulation)
+            ST_CUDA(st::launch_pack(desc->dtype, dO, g.BH, g.Lq, g.Lrq, tpb.Lpq, g.d, tpb.shift, qp0, nullptr, nullptr, st));
+            ST_CUDA(st::launch_pack(desc->dtype, V, g.BH, g.Lk, g.Lrk, tpb.Lpk, g.d, tpb.shift, kp0, nullptr, nullptr, st));
+            ST_CUDA(tc_band_pass(tpb, m, g, false, true, qp0, kp0, pad_u, pad_v, Z, errp, st));
+            ST_CUDA(tc_band_pass(tpb, m, g, true, true, kp0, qp0, pad_v, pad_u, ZT, errp, st));
+        } else if (dual) {
             ST_CUDA(st::launch_band_dual(g, desc->dtype, true, dO, V, Z, ZT, st));
         } else {
             ST_CUDA(st::launch_zband(g, desc->dtype, dO, V, Z, st));

@@ -54,6 +54,7 @@ struct Smem {
     uint64_t* t_empty;
     uint32_t* tmem_base;
     int* wl;          // [wl_cap] this CTA's slice of the work list (no global loads on the block path)
+    float* stage;     // band write passes: [kEW][32][33] per-warp transpose tiles
 };
 
 __device__ __forceinline__ Smem carve(uint8_t* base, const PhaseArgs& a, int nst) {
@@ -75,6 +76,7 @@ __device__ __forceinline__ Smem carve(uint8_t* base, const PhaseArgs& a, int nst
     s.t_empty = s.t_full + nst;
     s.tmem_base = (uint32_t*)(s.t_empty + nst);
     s.wl = (int*)(s.tmem_base + 4);
+    s.stage = (float*)(((uintptr_t)(s.wl + a.wl_cap) + 15) & ~(uintptr_t)15);
     return s;
 }
 
@@ -111,7 +113,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 }  // namespace
 
-template <int kNPL, int kCR, bool kFirst, int kEW>
+// kWrite = 0: the half-step.  kWrite = 1 / 2: the same tiles written out as the stored score band
+// (s2 = q.k c2, -inf off the support) / cotangent band (dO.v, 0 off the support) of the own side,
+// [BH][band_ld][Wf] (the transposed band from the column geometry); activity from the padded duals.
+template <int kNPL, int kCR, bool kFirst, int kEW, int kWrite = 0>
 __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
     constexpr int kParts = kEW / 4;         // epilogue warps per TMEM lane quadrant (column parts)
     constexpr int NE = 32 * kEW;            // epilogue threads
@@ -144,10 +149,10 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
         tc_alloc(s.tmem_base, 512);
         tc_relinquish();
     }
-    const int n = *a.nwork;
+    const int n = a.work ? *a.nwork : a.nwork_all;
     const int g_begin = (int)((long long)n * blockIdx.x / gridDim.x);
     const int g_end = min((int)((long long)n * (blockIdx.x + 1) / gridDim.x), g_begin + a.wl_cap);
-    for (int k = threadIdx.x; k < g_end - g_begin; k += blockDim.x) s.wl[k] = a.work[g_begin + k];
+    for (int k = threadIdx.x; k < g_end - g_begin; k += blockDim.x) s.wl[k] = a.work ? a.work[g_begin + k] : g_begin + k;
     if (threadIdx.x == 0 && (int)((long long)n * (blockIdx.x + 1) / gridDim.x) - g_begin > a.wl_cap)
         atomicOr(a.err, 16);  // cannot happen: wl_cap = ceil(max work / grid)
     tc_fence_before();
@@ -293,6 +298,74 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
             }
             __syncwarp();
             rel_seq = max(rel_seq, keep_from);
+        }
+    } else if constexpr (kWrite != 0) {
+        // ------------------------------------------------------------ band write epilogue
+        // A warp owns 32 rows x HC columns of each chunk; it stages them through a padded SMEM tile so
+        // that, row by row, the 32 lanes store 32 consecutive band cells (coalesced), instead of 32 rows
+        // per store instruction.  Cells outside the window (j before / after it) get the fill value.
+        constexpr int HC = kCR / kParts;
+        const int ew = warp - 2, qd = warp & 3, half = ew >> 2;
+        float* stg = s.stage + (size_t)ew * 32 * 33;
+        const float fill = kWrite == 1 ? -INFINITY : 0.f;
+        uint32_t tseq = 0;
+        for (int gi = g_begin; gi < g_end; ++gi) {
+            const Blk b = block_of(a, s.wl[gi - g_begin]);
+            const int vs = (gi - g_begin) % kNV;
+            mbar_wait(&s.v_full[vs], ((gi - g_begin) / kNV) & 1);
+            const float* vw = s.vwin + (size_t)vs * (a.maxwin + 128);
+            const int wbase = b.q0 * kCR - a.shift;
+            const int nwin = (b.q1 - b.q0 + 1) * kCR;
+            const int wlo = b.i0 + qd * 32 - a.w - wbase;  // window column of band cell k = 0, row 32 qd
+            const int i = b.i0 + qd * 32 + lane;
+            const bool act = i < a.L_own && vw[a.maxwin + qd * 32 + lane] != -INFINITY;
+            const unsigned actm = __ballot_sync(0xffffffffu, act);
+            float* obase = a.band_out + ((size_t)b.bh * a.band_ld + b.i0 + qd * 32) * a.Wf;
+            for (int q = b.q0; q <= b.q1; ++q) {
+                const int ts = tseq % NST;
+                mbar_wait(&s.t_full[ts], (tseq / NST) & 1);
+                tc_fence_after();
+                const int c0 = (q - b.q0) * kCR + half * HC;
+                const bool any = !(wlo + 31 + 2 * a.w < c0 || wlo > c0 + HC - 1);
+                float v[HC];
+                if (any) {
+                    const uint32_t taddr = tbase + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ts * kCR + half * HC);
+#pragma unroll
+                    for (int h = 0; h < HC / 32; ++h) tc_ld32(taddr + 32 * h, *reinterpret_cast<float(*)[32]>(v + 32 * h));
+                    tc_wait_ld();
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s.t_empty[ts]);
+                ++tseq;
+                if (!any) continue;
+#pragma unroll
+                for (int h = 0; h < HC / 32; ++h) {
+#pragma unroll
+                    for (int cc = 0; cc < 32; ++cc) stg[lane * 33 + cc] = v[32 * h + cc];
+                    __syncwarp();
+                    const int c = c0 + 32 * h + lane;  // this lane's window column
+                    const bool con = vw[c] != -INFINITY;
+                    for (int rr = 0; rr < 32; ++rr) {
+                        const int k = c - (wlo + rr);
+                        if ((unsigned)k <= (unsigned)(2 * a.w)) {
+                            const float x = stg[rr * 33 + lane];
+                            const bool on = ((actm >> rr) & 1u) && con;
+                            obase[(size_t)rr * a.Wf + k] = on ? (kWrite == 1 ? x * a.c2 : x) : fill;
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+            if (half == 0) {  // band cells whose column lies outside the block's window
+                for (int rr = 0; rr < 32; ++rr) {
+                    const int lo = wlo + rr;
+                    for (int k = lane; k < min(-lo, 2 * a.w + 1); k += 32) obase[(size_t)rr * a.Wf + k] = fill;
+                    for (int k = max(0, nwin - lo) + lane; k <= 2 * a.w; k += 32) obase[(size_t)rr * a.Wf + k] = fill;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.v_empty[vs]);
         }
     } else {
         // ------------------------------------------------------------ epilogue (warps 2 .. 2 + kEW)
@@ -606,7 +679,8 @@ long long phase_launch_count(bool reset) {
 size_t phase_smem_bytes(const PhaseArgs& a) {
     const int nst = 512 / a.CR;
     return (size_t)a.NA * a.npl * 128 * a.row_bytes + (size_t)a.NSK * a.npl * a.CR * a.row_bytes +
-           (size_t)(kNV * (a.maxwin + 128) + 1536) * 4 + (size_t)(2 * kNV + 2 * a.NA + 2 * a.NSK + 2 * nst) * 8 + 16 + (size_t)a.wl_cap * 4;
+           (size_t)(kNV * (a.maxwin + 128) + 1536) * 4 + (size_t)(2 * kNV + 2 * a.NA + 2 * a.NSK + 2 * nst) * 8 + 16 + (size_t)a.wl_cap * 4 +
+           (a.band_out ? (size_t)a.ew_write * 32 * 33 * 4 + 16 : 0);
 }
 
 template <int kNPL, int kCR, int kEW>
@@ -630,6 +704,25 @@ cudaError_t launch_phase(const PhaseArgs& a, bool first, int grid, cudaStream_t 
     }
     if (a.CR == 128) return ew == 8 ? launch_phase_t<3, 128, 8>(a, first, grid, s) : launch_phase_t<3, 128, 16>(a, first, grid, s);
     return launch_phase_t<3, 64, 8>(a, first, grid, s);
+}
+
+template <int kCR, int kEW, int kW>
+static cudaError_t launch_band_t(const PhaseArgs& a, int grid, cudaStream_t s) {
+    const size_t smem = phase_smem_bytes(a);
+    auto k = k_phase<1, kCR, false, kEW, kW>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k<<<grid, 64 + 32 * kEW, smem, s>>>(a);
+    ++g_phase_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_phase_band(const PhaseArgs& a, bool cotangent, int grid, cudaStream_t s) {
+    if (a.npl != 1 || a.band_out == nullptr) return cudaErrorNotSupported;  // bf16 operand planes only
+    if (a.CR == 128)
+        return a.ew_write == 8 ? (cotangent ? launch_band_t<128, 8, 2>(a, grid, s) : launch_band_t<128, 8, 1>(a, grid, s))
+                               : (cotangent ? launch_band_t<128, 16, 2>(a, grid, s) : launch_band_t<128, 16, 1>(a, grid, s));
+    return cotangent ? launch_band_t<64, 8, 2>(a, grid, s) : launch_band_t<64, 8, 1>(a, grid, s);
 }
 
 cudaError_t launch_dustbin(const DustArgs& a, bool first, int BH, cudaStream_t s) {

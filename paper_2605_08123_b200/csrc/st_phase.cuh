@@ -31,6 +31,10 @@ struct PhaseArgs {
     float* out_own;             // [BH][Lr_own]
     const int* work;            // active (head, block) list
     const int* nwork;
+    int nwork_all;              // work == null: every block 0 .. nwork_all-1 (band write passes)
+    float* band_out;            // band write passes: [BH][band_ld][Wf] (null for the half-step)
+    int band_ld, Wf;
+    int ew_write;               // band write passes: epilogue warps (16, or 8 to fit SMEM)
     int wl_cap;                 // max work items per CTA (SMEM copy of the CTA's work-list slice)
     int* err;
     unsigned long long* trace;  // debug timeline (null in production)
@@ -51,6 +55,9 @@ long long phase_launch_count(bool reset);
 size_t phase_smem_bytes(const PhaseArgs& a);
 cudaError_t launch_phase(const PhaseArgs& a, bool first, int grid, cudaStream_t s);
 cudaError_t launch_dustbin(const DustArgs& a, bool first, int BH, cudaStream_t s);
+// the score band (cotangent = false: s2 = q.k c2, -inf off the support) or the cotangent band
+// (cotangent = true: dO.v, 0 off the support) of the own side, from packed bf16 planes on tcgen05
+cudaError_t launch_phase_band(const PhaseArgs& a, bool cotangent, int grid, cudaStream_t s);
 // [BH][Lr][d] (f32 or bf16) -> npl bf16 planes [BH][Lp][d] in the K-major core-matrix
 // layout, row r stored at packed row r + shift (other packed rows zero).
 cudaError_t launch_pack(int dtype, const void* X, int BH, int L, int Lr, int Lp, int d, int shift, uint8_t* p0,
