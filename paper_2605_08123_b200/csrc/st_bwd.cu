@@ -1188,6 +1188,269 @@ __global__ void __launch_bounds__(256, (D <= 64 ? 3 : 2)) k_bwdW(Geo g, BT<TIn> 
     }
 }
 
+// ---------------------------------------------------------------------------
+// bf16 operands: the window-chunked vector stages with the chunk GEMM on tcgen05.  Per 16-column
+// window chunk: phase 1 (as k_bwdW) writes the weights as two bf16 planes W = hi + lo (16 bits of
+// mantissa: the split costs <= 2^-17 relative per weight, far inside the bf16 parity bound) in the
+// UMMA K-major core-matrix layout, the chunk's 16 operand rows are transposed into the B operand,
+// and one elected thread issues two kind::f16 MMAs (M = 128 rows, N = D, K = 16) accumulating
+// out[128][D] in TMEM (fp32).  A / B are double-buffered against the MMA (commit -> mbarrier).
+// ---------------------------------------------------------------------------
+template <int kOp, bool kDirect, int D, int NSTG>
+__global__ void __launch_bounds__(256, 2) k_bwdM(Geo g, BT<__nv_bfloat16> a) {
+    using TIn = __nv_bfloat16;
+    constexpr int KC = 16;  // NSTG: cp.async ring depth (bytes in flight per SM hide the HBM latency)
+    extern __shared__ __align__(1024) uint8_t smm[];
+    __shared__ __align__(8) uint64_t mma_bar[2];
+    __shared__ uint32_t tmem_sh;
+    __shared__ float sacc[2][128], sdacc[2][128];
+    constexpr bool kRow = kOp < 10;
+    constexpr bool kNeedZ = (kOp == R6 || kOp == C1 || kOp == C6);
+    const int Lo = kRow ? g.Lq : g.Lk, Lx = kRow ? g.Lk : g.Lq;
+    const int Lro = kRow ? g.Lrq : g.Lrk, Lrx = kRow ? g.Lrk : g.Lrq;
+    const int Lpo = kRow ? g.Lqp : g.Lkp;
+    const uint8_t* mo = kRow ? g.row_mask : g.col_mask;
+    const uint8_t* mx = kRow ? g.col_mask : g.row_mask;
+    const int bh = blockIdx.y, i0 = blockIdx.x * 128, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const size_t bo = (size_t)bh * Lro, bx = (size_t)bh * Lrx;
+    auto on_o = [&](int k) { return k < Lo && (mo == nullptr || mo[(size_t)(bh / g.H) * Lo + k] != 0); };
+    auto on_x = [&](int k) { return k >= 0 && k < Lx && (mx == nullptr || mx[(size_t)(bh / g.H) * Lx + k] != 0); };
+    const int r = tid & 127, hh = tid >> 7, i = i0 + r;
+    const bool active = on_o(i);
+    float* vo = kOp == R6 ? a.dQ : kOp == C1 ? a.dV : kOp == RO ? a.O : a.dK;
+    if (!__syncthreads_or(active)) {
+        if (hh == 0 && i < Lo) {
+            if (kOp == R6) a.deps_part[bo + i] = 0.f;
+            if (kOp == C1) a.g_v[bo + i] = 0.f;
+            if (kOp == C6 && a.fuse_c5) a.v0b[bo + i] = 0.f;
+            for (int x = 0; x < D; ++x) vo[(bo + i) * D + x] = 0.f;
+        }
+        return;
+    }
+    const int Wf = g.Wf, Nw = 128 + 2 * g.w, NCH = Nw / KC;
+    // SMEM: NSTG stages {S [128][16] f32 | Z [128][16] f32 | X [16][D] bf16}, then A [2][2 planes][128 x 16]
+    // bf16, B [2][D x 16] bf16 (K-major core matrices), then the window vectors [5][Nw]
+    constexpr int STB = (kNeedZ ? 2 : 1) * 128 * KC * 4 + KC * D * 2;  // stage bytes
+    constexpr int AB = 128 * KC * 2, BB = D * KC * 2;
+    uint8_t* Abuf = smm + NSTG * STB;
+    uint8_t* Bbuf = Abuf + 2 * 2 * AB;
+    float* wv = reinterpret_cast<float*>(Bbuf + 2 * BB);
+    const float* Sb = (kRow ? a.S2 : a.S2T) + ((size_t)bh * Lpo + i0) * Wf;
+    const float* Zb = kNeedZ ? (kRow ? a.Z : a.ZT) + ((size_t)bh * Lpo + i0) * Wf : nullptr;
+    const TIn* osrc = kOp == R6 ? a.K : (kOp == C1) ? a.dO : (kOp == RO) ? a.V : a.Q;
+    auto stS = [&](int s) { return reinterpret_cast<float*>(smm + (size_t)s * STB); };
+    auto stZ = [&](int s) { return reinterpret_cast<float*>(smm + (size_t)s * STB) + 128 * KC; };
+    auto stX = [&](int s) { return reinterpret_cast<TIn*>(smm + (size_t)s * STB + (kNeedZ ? 2 : 1) * 128 * KC * 4); };
+    auto issue = [&](int j) {
+        const int s = j % NSTG, c0 = j * KC;
+        float* S = stS(s);
+        float* Z = stZ(s);
+        for (int e = tid; e < 128 * (KC / 4); e += 256) {
+            const int rr = e / (KC / 4), sg = (e % (KC / 4)) * 4;
+            cp_async16(S + rr * KC + sg, Sb + (size_t)rr * (Wf - 1) + c0 + sg, 16u);
+            if (kNeedZ) cp_async16(Z + rr * KC + sg, Zb + (size_t)rr * (Wf - 1) + c0 + sg, 16u);
+        }
+        constexpr int SPR = D * 2 / 16;
+        const int xb0 = i0 - g.w + c0;
+        TIn* X = stX(s);
+        for (int e = tid; e < KC * SPR; e += 256) {
+            const int row = e / SPR, sg = e % SPR, x = xb0 + row;
+            const bool ok = x >= 0 && x < Lx;
+            cp_async16(reinterpret_cast<uint8_t*>(X) + (size_t)row * D * 2 + sg * 16,
+                       reinterpret_cast<const uint8_t*>(osrc + (bx + (ok ? x : 0)) * D) + sg * 16, ok ? 16u : 0u);
+        }
+        cp_async_commit();
+    };
+    if (warp == 0) {
+        sm100::tc_alloc(&tmem_sh, D < 32 ? 32 : D);
+        sm100::tc_relinquish();
+    }
+    if (tid == 0) {
+        sm100::mbar_init(&mma_bar[0], 1);
+        sm100::mbar_init(&mma_bar[1], 1);
+        sm100::fence_mbar_init();
+    }
+    for (int j = 0; j < NSTG - 1; ++j) {
+        if (j < NCH) issue(j);
+        else cp_async_commit();
+    }
+    for (int c = tid; c < Nw; c += 256) {
+        const int x = i0 - g.w + c;
+        float w0 = 0.f, w1 = 0.f, w2 = 0.f, w3 = 0.f, w4 = 0.f;
+        if (on_x(x)) {
+            if (kRow) {
+                w0 = a.v2[bx + x];
+                if (kOp == R6) {
+                    const float v1 = a.v1[bx + x], v0 = a.v0[bx + x];
+                    w1 = kDirect ? v1 : ex2(v1 - w0);
+                    w2 = kDirect ? v0 : ex2(v0 - w0);
+                    w3 = a.g_v[bx + x];
+                    w4 = a.v1b[bx + x];
+                }
+            } else {
+                w0 = a.u2[bx + x];
+                if (kOp == C6) {
+                    const float u1 = a.u1[bx + x];
+                    w1 = kDirect ? u1 : ex2(u1 - w0);
+                    w3 = a.u2b[bx + x];
+                    w4 = a.u1b[bx + x];
+                }
+            }
+        }
+        wv[c] = w0;
+        wv[Nw + c] = w1;
+        wv[2 * Nw + c] = w2;
+        wv[3 * Nw + c] = w3;
+        wv[4 * Nw + c] = w4;
+    }
+    float o2 = 0.f, o1 = 0.f, o0 = 0.f, ob2 = 0.f, ob1 = 0.f;
+    if (active) {
+        if (kRow) {
+            o2 = a.u2[bo + i];
+            o1 = a.u1[bo + i];
+            if (kOp == R6) {
+                ob2 = a.u2b[bo + i];
+                ob1 = a.u1b[bo + i];
+            }
+        } else {
+            o2 = a.v2[bo + i];
+            o1 = a.v1[bo + i];
+            o0 = a.v0[bo + i];
+            if (kOp == C6) {
+                ob2 = a.g_v[bo + i];
+                ob1 = a.v1b[bo + i];
+            }
+        }
+    }
+    const float ma = active ? ex2(o1 - o2) : 0.f, mb = (active && !kRow) ? ex2(o0 - o2) : 0.f;
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t tmem = tmem_sh;
+    const uint32_t idesc = sm100::make_idesc(128, D, 1u);
+    float acc = 0.f, dacc = 0.f;
+    // this thread's 16-byte core-matrix row of the A planes: row r, K half hh
+    const uint32_t a_off = (uint32_t)((r & ~7) * (KC * 2) + hh * 128 + (r & 7) * 16);
+    for (int j = 0; j < NCH; ++j) {
+        const int s = j % NSTG, c0 = j * KC, ab = j & 1;
+        cp_async_wait<NSTG - 2>();
+        __syncthreads();  // chunk j landed everywhere; the previous chunk's phase 1 / B build are done
+        if (j + NSTG - 1 < NCH) issue(j + NSTG - 1);
+        else cp_async_commit();
+        if (j >= 2) sm100::mbar_wait(&mma_bar[ab], (uint32_t)((j - 2) >> 1) & 1u);  // A / B[ab] free again
+        const float* S = stS(s);
+        const float* Z = stZ(s);
+        const TIn* X = stX(s);
+        uint8_t* Ahi = Abuf + ab * 2 * AB;
+        uint8_t* Alo = Ahi + AB;
+        uint8_t* Bt = Bbuf + ab * BB;
+        // ---- phase 1: 8 weights of row r (columns 8 hh .. 8 hh + 7), rotated reads, bf16 hi / lo planes
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            const int pos = (r + jj) & 7, cl = 8 * hh + pos;
+            const int c = c0 + cl;
+            const float s2 = S[r * KC + cl];
+            float wgt = 0.f;
+            if (active && (unsigned)(c - r) < (unsigned)Wf && s2 != -INFINITY) {
+                const float p = ex2(s2 + o2 + wv[c]);
+                if (kOp == RO) {
+                    wgt = p;
+                } else if (kOp == C1) {
+                    acc += p * Z[r * KC + cl];
+                    wgt = p;
+                } else if (kOp == R6) {
+                    const float z = Z[r * KC + cl];
+                    if (kDirect) {
+                        wgt = sbar_of(true, s2, p, z, o1, o2, wv[2 * Nw + c], wv[Nw + c], wv[c], ob2, ob1,
+                                      wv[3 * Nw + c], wv[4 * Nw + c]);
+                    } else {
+                        const float bj = wv[Nw + c], dj = wv[2 * Nw + c];
+                        wgt = p * (z - wv[3 * Nw + c] - bj * ob2 - ma * bj * wv[4 * Nw + c] - ma * dj * ob1);
+                    }
+                    dacc += wgt * (s2 * kLn2);
+                } else {  // C6
+                    const float z = Z[r * KC + cl];
+                    if (kDirect) {
+                        wgt = sbar_of(true, s2, p, z, wv[Nw + c], wv[c], o0, o1, o2, wv[3 * Nw + c], wv[4 * Nw + c],
+                                      ob2, ob1);
+                        if (a.fuse_c5) acc += ex2(s2 + wv[Nw + c] + o0) * wv[4 * Nw + c];
+                    } else {
+                        const float ai = wv[Nw + c];
+                        wgt = p * (z - ob2 - ma * wv[3 * Nw + c] - ai * ma * ob1 - ai * mb * wv[4 * Nw + c]);
+                        acc += p * ai * wv[4 * Nw + c];
+                    }
+                }
+            }
+            const __nv_bfloat16 hi = __float2bfloat16_rn(wgt);
+            const __nv_bfloat16 lo = __float2bfloat16_rn(wgt - __bfloat162float(hi));
+            *reinterpret_cast<__nv_bfloat16*>(Ahi + a_off + pos * 2) = hi;
+            *reinterpret_cast<__nv_bfloat16*>(Alo + a_off + pos * 2) = lo;
+        }
+        // ---- B operand: X^T of the chunk, K-major core matrices (n = output column, k = window column)
+        for (int u = tid; u < D * 2; u += 256) {
+            const int n = u >> 1, kc = u & 1;
+            __align__(16) __nv_bfloat16 e8[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) e8[e] = X[(kc * 8 + e) * D + n];
+            *reinterpret_cast<uint4*>(Bt + (n & ~7) * (KC * 2) + kc * 128 + (n & 7) * 16) = *reinterpret_cast<const uint4*>(e8);
+        }
+        sm100::fence_proxy_async_smem();  // generic SMEM writes -> visible to the tensor core
+        __syncthreads();
+        if (warp == 0) {
+            sm100::tc_fence_after();
+            if (sm100::elect_one()) {
+                const uint64_t bd = sm100::make_desc(sm100::smem_u32(Bt), 128, 8 * KC * 2);
+                sm100::mma_bf16(tmem, sm100::make_desc(sm100::smem_u32(Ahi), 128, 8 * KC * 2), bd, idesc, j > 0 ? 1u : 0u);
+                sm100::mma_bf16(tmem, sm100::make_desc(sm100::smem_u32(Alo), 128, 8 * KC * 2), bd, idesc, 1u);
+                sm100::tc_commit(&mma_bar[ab]);
+            }
+            __syncwarp();
+        }
+    }
+    // the last commit covers every earlier MMA
+    sm100::mbar_wait(&mma_bar[(NCH - 1) & 1], (uint32_t)((NCH - 1) >> 1) & 1u);
+    sm100::tc_fence_after();
+    sacc[hh][r] = acc;
+    sdacc[hh][r] = dacc;
+    __syncthreads();
+    if (hh == 0 && i < Lo) {
+        if (kOp == C1) a.g_v[bo + i] = active ? sacc[0][r] + sacc[1][r] : 0.f;
+        if (kOp == R6) a.deps_part[bo + i] = active ? sdacc[0][r] + sdacc[1][r] : 0.f;
+        if (kOp == C6 && a.fuse_c5) {
+            const float s5 = sacc[0][r] + sacc[1][r];
+            a.v0b[bo + i] = !active ? 0.f : kDirect ? -s5 : -ex2(a.v0[bo + i] - a.v2[bo + i]) * s5;
+        }
+    }
+    if (warp < 4) {  // TMEM lane quadrant = warp: thread r holds output row r
+        const float sc = (kOp == C1 || kOp == RO) ? 1.f : g.inv_qk;
+#pragma unroll
+        for (int h = 0; h < D / 32; ++h) {
+            float v[32];
+            sm100::tc_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(32 * h), v);
+            sm100::tc_wait_ld();
+            if (i < Lo) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    *reinterpret_cast<float4*>(vo + (bo + i) * D + 32 * h + 4 * q) =
+                        make_float4(v[4 * q] * sc, v[4 * q + 1] * sc, v[4 * q + 2] * sc, v[4 * q + 3] * sc);
+            }
+        }
+    }
+    sm100::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        sm100::tc_fence_after();
+        sm100::tc_dealloc(tmem, D < 32 ? 32 : D);
+    }
+}
+
+template <int D>
+static size_t bwdM_smem_bytes(const Geo& g, bool z, int nstg) {
+    const int Nw = 128 + 2 * g.w;
+    return (size_t)nstg * ((z ? 2 : 1) * 128 * 16 * 4 + 16 * D * 2) + 2 * 2 * 128 * 16 * 2 + 2 * D * 16 * 2 +
+           (size_t)5 * Nw * 4 + 1024;
+}
+
 // Window-chunked scalar sweeps (R1, R12, R2, R4, C3, C5) over the sheared band strips, for the bands
 // whose 128-row tile does not fit SMEM: 2 threads per row (rotated columns), NSTG-deep cp.async ring
 // of [128][32] S (and Z) strips, one barrier per chunk, 2-3 CTAs per SM.
@@ -1419,6 +1682,20 @@ static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
     if constexpr (kVec) {
         // wide bands (no 128-row band tile in SMEM): the window-chunked vector stage over sheared band
         // strips; narrow bands keep the 128-row tile kernel (the strips would read the 2x wider window)
+        if constexpr (std::is_same<TIn, __nv_bfloat16>::value && (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RO)) {
+            if (!narrow_ok && bwdW_supported(g) && !getenv("ST_NO_BWDM")) {  // chunk GEMM on tcgen05
+                constexpr bool kZ = (kOp == R6 || kOp == C1 || kOp == C6);
+                static const int nsm = getenv("ST_BWDM_NSTG") ? atoi(getenv("ST_BWDM_NSTG")) : 2;
+                const int ns = nsm >= 6 ? 6 : nsm >= 4 ? 4 : 2;
+                const size_t smem = bwdM_smem_bytes<D>(g, kZ, ns);
+                auto k = ns == 6 ? k_bwdM<kOp, kDirect, D, 6> : ns == 4 ? k_bwdM<kOp, kDirect, D, 4> : k_bwdM<kOp, kDirect, D, 2>;
+                cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e != cudaSuccess) return e;
+                const int n = row ? g.Lq : g.Lk;
+                k<<<dim3((n + 127) / 128, g.BH), 256, smem, s>>>(g, a);
+                return cudaGetLastError();
+            }
+        }
         if (!narrow_ok && bwdW_supported(g)) {
             constexpr bool kZ = (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RW || kOp == CW);
             static const int nstg = getenv("ST_BWDW_NSTG") ? atoi(getenv("ST_BWDW_NSTG")) : 2;
