@@ -1196,10 +1196,14 @@ __global__ void __launch_bounds__(256, (D <= 64 ? 3 : 2)) k_bwdW(Geo g, BT<TIn> 
 // and one elected thread issues two kind::f16 MMAs (M = 128 rows, N = D, K = 16) accumulating
 // out[128][D] in TMEM (fp32).  A / B are double-buffered against the MMA (commit -> mbarrier).
 // ---------------------------------------------------------------------------
-template <int kOp, bool kDirect, int D, int NSTG>
-__global__ void __launch_bounds__(256, 2) k_bwdM(Geo g, BT<__nv_bfloat16> a) {
-    using TIn = __nv_bfloat16;
-    constexpr int KC = 16;  // NSTG: cp.async ring depth (bytes in flight per SM hide the HBM latency)
+// fp32 operands: W and X both split into three bf16 planes (hi, mid, lo) and the six products of
+// order <= 2^-16 (hh, hm, mh, hl, mm, lh), i.e. fp32-accurate products at bf16 tensor rate.
+template <int kOp, bool kDirect, int D, int NSTG, class TIn = __nv_bfloat16>
+__global__ void __launch_bounds__(256, 2) k_bwdM(Geo g, BT<TIn> a) {
+    constexpr bool kF32 = sizeof(TIn) == 4;
+    constexpr int WP = kF32 ? 3 : 2;   // weight planes
+    constexpr int XP = kF32 ? 3 : 1;   // operand planes
+    constexpr int KC = 16;  // NSTG: cp.async ring depth
     extern __shared__ __align__(1024) uint8_t smm[];
     __shared__ __align__(8) uint64_t mma_bar[2];
     __shared__ uint32_t tmem_sh;
@@ -1230,11 +1234,11 @@ __global__ void __launch_bounds__(256, 2) k_bwdM(Geo g, BT<__nv_bfloat16> a) {
     const int Wf = g.Wf, Nw = 128 + 2 * g.w, NCH = Nw / KC;
     // SMEM: NSTG stages {S [128][16] f32 | Z [128][16] f32 | X [16][D] bf16}, then A [2][2 planes][128 x 16]
     // bf16, B [2][D x 16] bf16 (K-major core matrices), then the window vectors [5][Nw]
-    constexpr int STB = (kNeedZ ? 2 : 1) * 128 * KC * 4 + KC * D * 2;  // stage bytes
-    constexpr int AB = 128 * KC * 2, BB = D * KC * 2;
-    uint8_t* Abuf = smm + NSTG * STB;
-    uint8_t* Bbuf = Abuf + 2 * 2 * AB;
-    float* wv = reinterpret_cast<float*>(Bbuf + 2 * BB);
+    constexpr int STB = (kNeedZ ? 2 : 1) * 128 * KC * 4 + KC * D * (int)sizeof(TIn);  // stage bytes
+    constexpr int AB = 128 * KC * 2, BB = D * KC * 2;  // one bf16 plane of A / B
+    uint8_t* Abuf = smm + NSTG * STB;                  // [2][WP][AB]
+    uint8_t* Bbuf = Abuf + 2 * WP * AB;                // [2][XP][BB]
+    float* wv = reinterpret_cast<float*>(Bbuf + 2 * XP * BB);
     const float* Sb = (kRow ? a.S2 : a.S2T) + ((size_t)bh * Lpo + i0) * Wf;
     const float* Zb = kNeedZ ? (kRow ? a.Z : a.ZT) + ((size_t)bh * Lpo + i0) * Wf : nullptr;
     const TIn* osrc = kOp == R6 ? a.K : (kOp == C1) ? a.dO : (kOp == RO) ? a.V : a.Q;
@@ -1250,13 +1254,13 @@ __global__ void __launch_bounds__(256, 2) k_bwdM(Geo g, BT<__nv_bfloat16> a) {
             cp_async16(S + rr * KC + sg, Sb + (size_t)rr * (Wf - 1) + c0 + sg, 16u);
             if (kNeedZ) cp_async16(Z + rr * KC + sg, Zb + (size_t)rr * (Wf - 1) + c0 + sg, 16u);
         }
-        constexpr int SPR = D * 2 / 16;
+        constexpr int SPR = D * (int)sizeof(TIn) / 16;
         const int xb0 = i0 - g.w + c0;
         TIn* X = stX(s);
         for (int e = tid; e < KC * SPR; e += 256) {
             const int row = e / SPR, sg = e % SPR, x = xb0 + row;
             const bool ok = x >= 0 && x < Lx;
-            cp_async16(reinterpret_cast<uint8_t*>(X) + (size_t)row * D * 2 + sg * 16,
+            cp_async16(reinterpret_cast<uint8_t*>(X) + (size_t)row * D * sizeof(TIn) + sg * 16,
                        reinterpret_cast<const uint8_t*>(osrc + (bx + (ok ? x : 0)) * D) + sg * 16, ok ? 16u : 0u);
         }
         cp_async_commit();
@@ -1341,9 +1345,8 @@ __global__ void __launch_bounds__(256, 2) k_bwdM(Geo g, BT<__nv_bfloat16> a) {
         const float* S = stS(s);
         const float* Z = stZ(s);
         const TIn* X = stX(s);
-        uint8_t* Ahi = Abuf + ab * 2 * AB;
-        uint8_t* Alo = Ahi + AB;
-        uint8_t* Bt = Bbuf + ab * BB;
+        uint8_t* Ap = Abuf + ab * WP * AB;
+        uint8_t* Bt = Bbuf + ab * XP * BB;
         // ---- phase 1: 8 weights of row r (columns 8 hh .. 8 hh + 7), rotated reads, bf16 hi / lo planes
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
@@ -1382,26 +1385,55 @@ __global__ void __launch_bounds__(256, 2) k_bwdM(Geo g, BT<__nv_bfloat16> a) {
                 }
             }
             const __nv_bfloat16 hi = __float2bfloat16_rn(wgt);
-            const __nv_bfloat16 lo = __float2bfloat16_rn(wgt - __bfloat162float(hi));
-            *reinterpret_cast<__nv_bfloat16*>(Ahi + a_off + pos * 2) = hi;
-            *reinterpret_cast<__nv_bfloat16*>(Alo + a_off + pos * 2) = lo;
+            const float r1 = wgt - __bfloat162float(hi);  // exact in fp32
+            const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+            *reinterpret_cast<__nv_bfloat16*>(Ap + a_off + pos * 2) = hi;
+            *reinterpret_cast<__nv_bfloat16*>(Ap + AB + a_off + pos * 2) = mid;
+            if (WP == 3)
+                *reinterpret_cast<__nv_bfloat16*>(Ap + 2 * AB + a_off + pos * 2) =
+                    __float2bfloat16_rn(r1 - __bfloat162float(mid));
         }
         // ---- B operand: X^T of the chunk, K-major core matrices (n = output column, k = window column)
         for (int u = tid; u < D * 2; u += 256) {
             const int n = u >> 1, kc = u & 1;
-            __align__(16) __nv_bfloat16 e8[8];
+            const uint32_t boff = (n & ~7) * (KC * 2) + kc * 128 + (n & 7) * 16;
+            if constexpr (!kF32) {
+                __align__(16) __nv_bfloat16 e8[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) e8[e] = X[(kc * 8 + e) * D + n];
-            *reinterpret_cast<uint4*>(Bt + (n & ~7) * (KC * 2) + kc * 128 + (n & 7) * 16) = *reinterpret_cast<const uint4*>(e8);
+                for (int e = 0; e < 8; ++e) e8[e] = X[(kc * 8 + e) * D + n];
+                *reinterpret_cast<uint4*>(Bt + boff) = *reinterpret_cast<const uint4*>(e8);
+            } else {
+                __align__(16) __nv_bfloat16 h8[8], m8[8], l8[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const float x = X[(kc * 8 + e) * D + n];
+                    h8[e] = __float2bfloat16_rn(x);
+                    const float r1 = x - __bfloat162float(h8[e]);
+                    m8[e] = __float2bfloat16_rn(r1);
+                    l8[e] = __float2bfloat16_rn(r1 - __bfloat162float(m8[e]));
+                }
+                *reinterpret_cast<uint4*>(Bt + boff) = *reinterpret_cast<const uint4*>(h8);
+                *reinterpret_cast<uint4*>(Bt + BB + boff) = *reinterpret_cast<const uint4*>(m8);
+                *reinterpret_cast<uint4*>(Bt + 2 * BB + boff) = *reinterpret_cast<const uint4*>(l8);
+            }
         }
         sm100::fence_proxy_async_smem();  // generic SMEM writes -> visible to the tensor core
         __syncthreads();
         if (warp == 0) {
             sm100::tc_fence_after();
             if (sm100::elect_one()) {
-                const uint64_t bd = sm100::make_desc(sm100::smem_u32(Bt), 128, 8 * KC * 2);
-                sm100::mma_bf16(tmem, sm100::make_desc(sm100::smem_u32(Ahi), 128, 8 * KC * 2), bd, idesc, j > 0 ? 1u : 0u);
-                sm100::mma_bf16(tmem, sm100::make_desc(sm100::smem_u32(Alo), 128, 8 * KC * 2), bd, idesc, 1u);
+                // (A plane, B plane) products: bf16 operands (hi, lo) x X; fp32 the six of order <= 2^-16
+                constexpr int NP = kF32 ? 6 : 2;
+                constexpr int pa_[6] = {0, 0, 1, 0, 1, 2};
+                constexpr int pb_[6] = {0, 1, 0, 2, 1, 0};
+                constexpr int qa_[2] = {0, 1};
+#pragma unroll
+                for (int pr = 0; pr < NP; ++pr) {
+                    const int pa = kF32 ? pa_[pr] : qa_[pr], pb = kF32 ? pb_[pr] : 0;
+                    sm100::mma_bf16(tmem, sm100::make_desc(sm100::smem_u32(Ap + pa * AB), 128, 8 * KC * 2),
+                                    sm100::make_desc(sm100::smem_u32(Bt + pb * BB), 128, 8 * KC * 2), idesc,
+                                    (j > 0 || pr > 0) ? 1u : 0u);
+                }
                 sm100::tc_commit(&mma_bar[ab]);
             }
             __syncwarp();
@@ -1444,11 +1476,12 @@ __global__ void __launch_bounds__(256, 2) k_bwdM(Geo g, BT<__nv_bfloat16> a) {
     }
 }
 
-template <int D>
+template <int D, class TIn>
 static size_t bwdM_smem_bytes(const Geo& g, bool z, int nstg) {
     const int Nw = 128 + 2 * g.w;
-    return (size_t)nstg * ((z ? 2 : 1) * 128 * 16 * 4 + 16 * D * 2) + 2 * 2 * 128 * 16 * 2 + 2 * D * 16 * 2 +
-           (size_t)5 * Nw * 4 + 1024;
+    const int wp = sizeof(TIn) == 4 ? 3 : 2, xp = sizeof(TIn) == 4 ? 3 : 1;
+    return (size_t)nstg * ((z ? 2 : 1) * 128 * 16 * 4 + 16 * D * sizeof(TIn)) + (size_t)2 * wp * 128 * 16 * 2 +
+           (size_t)2 * xp * D * 16 * 2 + (size_t)5 * Nw * 4 + 1024;
 }
 
 // Window-chunked scalar sweeps (R1, R12, R2, R4, C3, C5) over the sheared band strips, for the bands
@@ -1682,13 +1715,19 @@ static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
     if constexpr (kVec) {
         // wide bands (no 128-row band tile in SMEM): the window-chunked vector stage over sheared band
         // strips; narrow bands keep the 128-row tile kernel (the strips would read the 2x wider window)
-        if constexpr (std::is_same<TIn, __nv_bfloat16>::value && (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RO)) {
-            if (!narrow_ok && bwdW_supported(g) && !getenv("ST_NO_BWDM")) {  // chunk GEMM on tcgen05
+        if constexpr (kOp == R6 || kOp == C1 || kOp == C6 || kOp == RO) {
+            // chunk GEMM on tcgen05 for bf16 operands on wide bands.  The fp32 variant (3-plane split,
+            // six products) passes parity but measured slower than the CUDA-core kernels on config 2
+            // (0.368 vs 0.288 ms backward), so it is opt-in (ST_BWDM_F32=1)
+            const bool f32 = std::is_same<TIn, float>::value;
+            static const bool f32_on = getenv("ST_BWDM_F32") != nullptr;
+            if ((f32 ? f32_on : !narrow_ok) && bwdW_supported(g) && !getenv("ST_NO_BWDM")) {
                 constexpr bool kZ = (kOp == R6 || kOp == C1 || kOp == C6);
                 static const int nsm = getenv("ST_BWDM_NSTG") ? atoi(getenv("ST_BWDM_NSTG")) : 2;
                 const int ns = nsm >= 6 ? 6 : nsm >= 4 ? 4 : 2;
-                const size_t smem = bwdM_smem_bytes<D>(g, kZ, ns);
-                auto k = ns == 6 ? k_bwdM<kOp, kDirect, D, 6> : ns == 4 ? k_bwdM<kOp, kDirect, D, 4> : k_bwdM<kOp, kDirect, D, 2>;
+                const size_t smem = bwdM_smem_bytes<D, TIn>(g, kZ, ns);
+                auto k = ns == 6 ? k_bwdM<kOp, kDirect, D, 6, TIn>
+                                 : ns == 4 ? k_bwdM<kOp, kDirect, D, 4, TIn> : k_bwdM<kOp, kDirect, D, 2, TIn>;
                 cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                 if (e != cudaSuccess) return e;
                 const int n = row ? g.Lq : g.Lk;
