@@ -1552,6 +1552,8 @@ __global__ void __launch_bounds__(256, 4) k_sweepW(Geo g, BT<TIn> a) {
                 if (kOp == C3) w3 = a.u2b[bx + x];
                 if (kOp == C5) w4 = a.u1b[bx + x];
             }
+            // one-reference R4 / C5: the window side's modifier beta_j / alpha_i folded in once per column
+            if (!kDirect && (kOp == R4 || kOp == C5)) w4 *= ex2(w1 - w0);
         }
         wv[c] = w0;
         wv[Nw + c] = w1;
@@ -1587,9 +1589,9 @@ __global__ void __launch_bounds__(256, 4) k_sweepW(Geo g, BT<TIn> a) {
                 acc += p * Z[r * kWC + cl];
                 acc2 += p * wv[2 * Nw + c];
             } else if (kOp == R2) acc += p * wv[2 * Nw + c];
-            else if (kOp == R4) acc += kDirect ? ex2(s2 + o1 + x1) * wv[3 * Nw + c] : p * ex2(x1 - x2) * wv[3 * Nw + c];
+            else if (kOp == R4) acc += kDirect ? ex2(s2 + o1 + x1) * wv[3 * Nw + c] : p * wv[3 * Nw + c];
             else if (kOp == C3) acc += (kDirect ? ex2(s2 + x2 + o1) : p) * wv[2 * Nw + c];
-            else acc += kDirect ? ex2(s2 + x1 + o0) * wv[3 * Nw + c] : p * ex2(x1 - x2) * wv[3 * Nw + c];
+            else acc += kDirect ? ex2(s2 + x1 + o0) * wv[3 * Nw + c] : p * wv[3 * Nw + c];
         }
     }
     sacc[hh][r] = acc;
@@ -1767,7 +1769,7 @@ static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
     }
     if constexpr (!kVec) {
         // scalar sweeps over bands whose 128-row tile does not fit SMEM: window-chunked strips
-        if (bwdT_op_smem(g, kOp, D) > 227 * 1024 && bwdW_supported(g)) {
+        if ((bwdT_op_smem(g, kOp, D) > 227 * 1024 || g.Wf > 129) && bwdW_supported(g)) {
             constexpr bool kZ = (kOp == R1 || kOp == R12);
             static const int ns_env = getenv("ST_SWEEPW_NSTG") ? atoi(getenv("ST_SWEEPW_NSTG")) : 3;
             const int NS = ns_env >= 4 ? 4 : ns_env == 2 ? 2 : 3;
