@@ -215,16 +215,21 @@ def test_bf16_full_size_properties(cid):
     assert np.all(np.isfinite(g1["dQ"])) and np.all(np.isfinite(g1["dK"]))
 
 
-def test_band_reuse_matches_recompute():
+@pytest.mark.parametrize("cid,L", [(2, None), (4, 2048), (5, 2048)])
+def test_band_reuse_matches_recompute(cid, L):
     """ST_FLAG_REUSE_BAND (backward consumes the forward's score band, as r2_backward(run.scaled, ...)
-    does) gives bit-identical gradients to recomputing the band in a fresh workspace."""
-    cfg = configs.CONFIGS[2].replace(B=1)
+    does) gives bit-identical gradients to recomputing the band in a fresh workspace: fp32 (f64 DMMA
+    band) and bf16 (tcgen05 band write passes, configs 4 / 5 geometry)."""
+    cfg = configs.CONFIGS[cid].replace(B=1)
+    if L:
+        cfg = cfg.replace(L=L, H=2)
     inp = configs.make_inputs(cfg)
     spec = band.BandSpec(batch=cfg.B, heads=cfg.H, seq_q=cfg.L, seq_k=cfg.L, head_dim=cfg.d, half_band=cfg.w,
-                         base_depth=cfg.T, tail_depth=cfg.R, epsilon=cfg.eps)
+                         base_depth=cfg.T, tail_depth=cfg.R, epsilon=cfg.eps, dtype=cfg.dtype)
     shp = (cfg.B, cfg.H, cfg.rows, cfg.d)
-    Q, K, V, G = (torch.from_numpy(x).cuda().reshape(shp) for x in (inp.Q, inp.K, inp.V, inp.G))
-    rm = torch.from_numpy(inp.row_mask).cuda()
+    b_ = inp.bits or {}
+    Q, K, V, G = (_dev(getattr(inp, k), b_.get(k)).reshape(shp) for k in ("Q", "K", "V", "G"))
+    rm = None if inp.row_mask is None else torch.from_numpy(inp.row_mask).cuda()
     ws = band.Workspace()
     run = band.run_surrogate(Q, K, V, spec, rm, rm, workspace=ws)
     a = band.r2_backward(run, G, workspace=ws)           # reuses the band
