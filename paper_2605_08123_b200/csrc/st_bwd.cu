@@ -1100,7 +1100,7 @@ __global__ void __launch_bounds__(256, (D <= 64 ? 3 : 2)) k_bwdW(Geo g, BT<TIn> 
         float* wt = WT;  // single buffer: every thread finished the previous chunk's phase 2 (barrier above)
 #pragma unroll 4
         for (int jj = 0; jj < kWC / 2; ++jj) {
-            const int cl = (r + (kWC / 2) * hh + jj) & (kWC - 1);
+            const int cl = (r + (kWC / 2) * hh + jj + (r >> 4)) & (kWC - 1);  // conflict-free (kWC = 16)
             const int c = c0 + cl;
             const float s2 = S[r * kWC + cl];
             float wgt = 0.f;
@@ -1234,7 +1234,8 @@ __global__ void __launch_bounds__(256, 2) k_bwdM(Geo g, BT<TIn> a) {
     const int Wf = g.Wf, Nw = 128 + 2 * g.w, NCH = Nw / KC;
     // SMEM: NSTG stages {S [128][16] f32 | Z [128][16] f32 | X [16][D] bf16}, then A [2][2 planes][128 x 16]
     // bf16, B [2][D x 16] bf16 (K-major core matrices), then the window vectors [5][Nw]
-    constexpr int STB = (kNeedZ ? 2 : 1) * 128 * KC * 4 + KC * D * (int)sizeof(TIn);  // stage bytes
+    constexpr int SP = KC + 4;  // strip row pitch (floats): with the rotation below, conflict-free phase-1 reads
+    constexpr int STB = (kNeedZ ? 2 : 1) * 128 * SP * 4 + KC * D * (int)sizeof(TIn);  // stage bytes
     constexpr int AB = 128 * KC * 2, BB = D * KC * 2;  // one bf16 plane of A / B
     uint8_t* Abuf = smm + NSTG * STB;                  // [2][WP][AB]
     uint8_t* Bbuf = Abuf + 2 * WP * AB;                // [2][XP][BB]
@@ -1243,16 +1244,16 @@ __global__ void __launch_bounds__(256, 2) k_bwdM(Geo g, BT<TIn> a) {
     const float* Zb = kNeedZ ? (kRow ? a.Z : a.ZT) + ((size_t)bh * Lpo + i0) * Wf : nullptr;
     const TIn* osrc = kOp == R6 ? a.K : (kOp == C1) ? a.dO : (kOp == RO) ? a.V : a.Q;
     auto stS = [&](int s) { return reinterpret_cast<float*>(smm + (size_t)s * STB); };
-    auto stZ = [&](int s) { return reinterpret_cast<float*>(smm + (size_t)s * STB) + 128 * KC; };
-    auto stX = [&](int s) { return reinterpret_cast<TIn*>(smm + (size_t)s * STB + (kNeedZ ? 2 : 1) * 128 * KC * 4); };
+    auto stZ = [&](int s) { return reinterpret_cast<float*>(smm + (size_t)s * STB) + 128 * SP; };
+    auto stX = [&](int s) { return reinterpret_cast<TIn*>(smm + (size_t)s * STB + (kNeedZ ? 2 : 1) * 128 * SP * 4); };
     auto issue = [&](int j) {
         const int s = j % NSTG, c0 = j * KC;
         float* S = stS(s);
         float* Z = stZ(s);
         for (int e = tid; e < 128 * (KC / 4); e += 256) {
             const int rr = e / (KC / 4), sg = (e % (KC / 4)) * 4;
-            cp_async16(S + rr * KC + sg, Sb + (size_t)rr * (Wf - 1) + c0 + sg, 16u);
-            if (kNeedZ) cp_async16(Z + rr * KC + sg, Zb + (size_t)rr * (Wf - 1) + c0 + sg, 16u);
+            cp_async16(S + rr * SP + sg, Sb + (size_t)rr * (Wf - 1) + c0 + sg, 16u);
+            if (kNeedZ) cp_async16(Z + rr * SP + sg, Zb + (size_t)rr * (Wf - 1) + c0 + sg, 16u);
         }
         constexpr int SPR = D * (int)sizeof(TIn) / 16;
         const int xb0 = i0 - g.w + c0;
@@ -1350,19 +1351,19 @@ __global__ void __launch_bounds__(256, 2) k_bwdM(Geo g, BT<TIn> a) {
         // ---- phase 1: 8 weights of row r (columns 8 hh .. 8 hh + 7), rotated reads, bf16 hi / lo planes
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
-            const int pos = (r + jj) & 7, cl = 8 * hh + pos;
+            const int pos = (r + jj + 2 * (r >> 3)) & 7, cl = 8 * hh + pos;
             const int c = c0 + cl;
-            const float s2 = S[r * KC + cl];
+            const float s2 = S[r * SP + cl];
             float wgt = 0.f;
             if (active && (unsigned)(c - r) < (unsigned)Wf && s2 != -INFINITY) {
                 const float p = ex2(s2 + o2 + wv[c]);
                 if (kOp == RO) {
                     wgt = p;
                 } else if (kOp == C1) {
-                    acc += p * Z[r * KC + cl];
+                    acc += p * Z[r * SP + cl];
                     wgt = p;
                 } else if (kOp == R6) {
-                    const float z = Z[r * KC + cl];
+                    const float z = Z[r * SP + cl];
                     if (kDirect) {
                         wgt = sbar_of(true, s2, p, z, o1, o2, wv[2 * Nw + c], wv[Nw + c], wv[c], ob2, ob1,
                                       wv[3 * Nw + c], wv[4 * Nw + c]);
@@ -1372,7 +1373,7 @@ __global__ void __launch_bounds__(256, 2) k_bwdM(Geo g, BT<TIn> a) {
                     }
                     dacc += wgt * (s2 * kLn2);
                 } else {  // C6
-                    const float z = Z[r * KC + cl];
+                    const float z = Z[r * SP + cl];
                     if (kDirect) {
                         wgt = sbar_of(true, s2, p, z, wv[Nw + c], wv[c], o0, o1, o2, wv[3 * Nw + c], wv[4 * Nw + c],
                                       ob2, ob1);
@@ -1480,7 +1481,7 @@ template <int D, class TIn>
 static size_t bwdM_smem_bytes(const Geo& g, bool z, int nstg) {
     const int Nw = 128 + 2 * g.w;
     const int wp = sizeof(TIn) == 4 ? 3 : 2, xp = sizeof(TIn) == 4 ? 3 : 1;
-    return (size_t)nstg * ((z ? 2 : 1) * 128 * 16 * 4 + 16 * D * sizeof(TIn)) + (size_t)2 * wp * 128 * 16 * 2 +
+    return (size_t)nstg * ((z ? 2 : 1) * 128 * 20 * 4 + 16 * D * sizeof(TIn)) + (size_t)2 * wp * 128 * 16 * 2 +
            (size_t)2 * xp * D * 16 * 2 + (size_t)5 * Nw * 4 + 1024;
 }
 
@@ -1578,7 +1579,7 @@ __global__ void __launch_bounds__(256, 4) k_sweepW(Geo g, BT<TIn> a) {
         if (!active || c0 > r + 2 * g.w || c0 + kWC - 1 < r) continue;  // this row's band misses the chunk
 #pragma unroll 4
         for (int jj = 0; jj < kWC / 2; ++jj) {
-            const int cl = (r + (kWC / 2) * hh + jj) & (kWC - 1);
+            const int cl = (r + (kWC / 2) * hh + jj + (r >> 4)) & (kWC - 1);  // conflict-free (kWC = 16)
             const int c = c0 + cl;
             const float s2 = S[r * kWC + cl];
             if ((unsigned)(c - r) >= (unsigned)Wf || s2 == -INFINITY) continue;
