@@ -150,6 +150,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--e2e-depth", type=int, default=3, help="pipeline depth of the e2e H2D / compute / D2H overlap")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -312,10 +313,10 @@ def main():
         h2d = sum(x.numel() * x.element_size() for x in (hQ, hK, hV, hG)) + \
             sum(0 if x is None else x.numel() for x in (hrm, hcm))
         d2h = sum(x.numel() * x.element_size() for x in outs_h) + deps_h.numel() * 4
-        # Pipelined 2 deep: step k's H2D (copy stream), fwd+bwd (compute stream) and D2H (d2h stream)
+        # Pipelined nb deep: step k's H2D (copy stream), fwd+bwd (compute stream) and D2H (d2h stream)
         # overlap steps k-1 / k+1; device inputs and outputs are double-buffered and ordered by events.
         # Every step still copies its own inputs in and its results out inside the timed region.
-        nb = 2
+        nb = max(2, args.e2e_depth)
         din = [tuple(torch.empty_like(x) for x in (Q, K, V, G)) for _ in range(nb)]
         dms = [(None if rm is None else torch.empty_like(rm), None if cm is None else torch.empty_like(cm))
                for _ in range(nb)]
@@ -371,7 +372,7 @@ def main():
             dist.all_reduce(t2, op=dist.ReduceOp.MAX)
         e2e = {"value": cells * world / (float(t2.item()) * 1e-3), "unit": "band-cells/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": float(t2.item()),
-               "pipeline": "2-deep: H2D / fwd+bwd / D2H of consecutive steps overlap on 3 streams (pinned host buffers)"}
+               "pipeline": f"{nb}-deep: H2D / fwd+bwd / D2H of consecutive steps overlap on 3 streams (pinned host buffers)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
