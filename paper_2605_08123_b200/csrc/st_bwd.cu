@@ -1198,8 +1198,9 @@ __global__ void __launch_bounds__(256, (D <= 64 ? 3 : 2)) k_bwdW(Geo g, BT<TIn> 
 // ---------------------------------------------------------------------------
 // fp32 operands: W and X both split into three bf16 planes (hi, mid, lo) and the six products of
 // order <= 2^-16 (hh, hm, mh, hl, mm, lh), i.e. fp32-accurate products at bf16 tensor rate.
+// C1 / RO read one window vector: smaller SMEM, three CTAs per SM
 template <int kOp, bool kDirect, int D, int NSTG, class TIn = __nv_bfloat16>
-__global__ void __launch_bounds__(256, 2) k_bwdM(Geo g, BT<TIn> a) {
+__global__ void __launch_bounds__(256, (kOp == C1 || kOp == RO) ? 3 : 2) k_bwdM(Geo g, BT<TIn> a) {
     constexpr bool kF32 = sizeof(TIn) == 4;
     constexpr int WP = kF32 ? 3 : 2;   // weight planes
     constexpr int XP = kF32 ? 3 : 1;   // operand planes
@@ -1303,10 +1304,12 @@ __global__ void __launch_bounds__(256, 2) k_bwdM(Geo g, BT<TIn> a) {
             }
         }
         wv[c] = w0;
-        wv[Nw + c] = w1;
-        wv[2 * Nw + c] = w2;
-        wv[3 * Nw + c] = w3;
-        wv[4 * Nw + c] = w4;
+        if (kOp == R6 || kOp == C6) {
+            wv[Nw + c] = w1;
+            wv[2 * Nw + c] = w2;
+            wv[3 * Nw + c] = w3;
+            wv[4 * Nw + c] = w4;
+        }
     }
     float o2 = 0.f, o1 = 0.f, o0 = 0.f, ob2 = 0.f, ob1 = 0.f;
     if (active) {
@@ -1478,11 +1481,11 @@ __global__ void __launch_bounds__(256, 2) k_bwdM(Geo g, BT<TIn> a) {
 }
 
 template <int D, class TIn>
-static size_t bwdM_smem_bytes(const Geo& g, bool z, int nstg) {
+static size_t bwdM_smem_bytes(const Geo& g, bool z, int nstg, int nvec) {
     const int Nw = 128 + 2 * g.w;
     const int wp = sizeof(TIn) == 4 ? 3 : 2, xp = sizeof(TIn) == 4 ? 3 : 1;
     return (size_t)nstg * ((z ? 2 : 1) * 128 * 20 * 4 + 16 * D * sizeof(TIn)) + (size_t)2 * wp * 128 * 16 * 2 +
-           (size_t)2 * xp * D * 16 * 2 + (size_t)5 * Nw * 4 + 1024;
+           (size_t)2 * xp * D * 16 * 2 + (size_t)nvec * Nw * 4 + 1024;
 }
 
 // Window-chunked scalar sweeps (R1, R12, R2, R4, C3, C5) over the sheared band strips, for the bands
@@ -1728,7 +1731,7 @@ static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
                 constexpr bool kZ = (kOp == R6 || kOp == C1 || kOp == C6);
                 static const int nsm = getenv("ST_BWDM_NSTG") ? atoi(getenv("ST_BWDM_NSTG")) : 2;
                 const int ns = nsm >= 6 ? 6 : nsm >= 4 ? 4 : 2;
-                const size_t smem = bwdM_smem_bytes<D, TIn>(g, kZ, ns);
+                const size_t smem = bwdM_smem_bytes<D, TIn>(g, kZ, ns, (kOp == R6 || kOp == C6) ? 5 : 1);
                 auto k = ns == 6 ? k_bwdM<kOp, kDirect, D, 6, TIn>
                                  : ns == 4 ? k_bwdM<kOp, kDirect, D, 4, TIn> : k_bwdM<kOp, kDirect, D, 2, TIn>;
                 cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
