@@ -1,21 +1,29 @@
 #!/usr/bin/env python
 """Benchmark: fwd+bwd band-cells/s of the banded balanced Sinkhorn attention operator.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config 2]
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config 4]
 
-Workload (BASELINE.json metric on configs[1] = config 2): B=8, H=4, L=2048,
-d=64, half band 64 (W=129), eps=0.05, T=50, R=2, fp32, valid lengths uniform in
-[L/2, L] masked out of support and marginals; seeded synthetic inputs.
-A step = st_forward + st_backward (one-reference schedule) over the batch.
-value = B*H*L*W*(T+R) * n_gpus / max-over-ranks(device time per step)
-(weak scaling: every rank runs its own full config-2 batch, no collective in the
-operator -- batch x head partitioning).  Rank 0 prints ONE JSON line.
+Workload (BASELINE.json metric; the largest single-GPU config = config 4):
+B=4, H=8, L=32768, d=128, half band 128 (W=257), eps=0.05, T=100, R=2, bf16
+Q/K/V/dO (N(0,1)/sqrt(d), seeded), fp32 duals and accumulation.  A step =
+st_forward + st_backward (one-reference schedule) over the whole batch.
+
+    value = B*H*L*W*(T+R) / max-over-ranks(device time per step)
+
+Multi-GPU (torchrun): the B*H independent (b, h) problems of the ONE config are
+split contiguously over the ranks (shard.head_partition) -- strong scaling,
+no collective in the operator.  Rank 0 prints ONE JSON line.
+
+--impl reference: the reference algorithm on the host cores (the oracle port,
+tests/oracle_ref.py -> oracle/build/libstoc.so; the product library is never
+loaded on that arm), on a stated bounded sample of the same workload.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import statistics
 import sys
 import threading
@@ -23,9 +31,13 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM, FALLBACK_BF16 = 6650.0, 1590.0
+EX2_PER_CLK_SM, N_SM = 16, 148          # MUFU.EX2 issue rate (15.85 measured, tools/bench_mufu.cu)
+# CPU sample per reference step: rows of each sampled head (full L for configs 1-3)
+SAMPLE_ROWS = {4: 4096, 5: 4096}
 
 
 def peaks():
@@ -37,52 +49,76 @@ def peaks():
         return FALLBACK_HBM, FALLBACK_BF16, "fallback (B200_PROFILING.md)"
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
+
+
 def workload_str(cfg):
     return (f"config{cfg.cid}: B={cfg.B},H={cfg.H},L={cfg.L},d={cfg.d},W={cfg.Wf}(|i-j|<={cfg.w}),eps={cfg.eps},"
             f"T={cfg.T},R={cfg.R},{cfg.dtype}" + (",masked" if cfg.mask != "none" else "")
             + (",dustbin" if cfg.dustbin else ""))
 
 
+def config_obj(cfg, world):
+    return {"workload": workload_str(cfg), "seed": 0, "mode": "one_reference",
+            "parallelism": (f"batch x head: the {cfg.B * cfg.H} (b,h) problems split contiguously over {world} GPU(s), "
+                            "no operator collective"),
+            "l2": "inputs > L2 (126 MB) and a 256 MiB flush write between timed steps"}
+
+
 # ---------------------------------------------------------------------------
 # reference arm: the reference algorithm (CPU restatement, f32 template mode,
-# tile_block=128) on the host cores -- the reference cannot be compiled here
-# (Eigen3 / vendored headers absent), so the oracle port runs.
+# tile_block=128) on the host cores.  Imports only tests/oracle_ref.py.
 # ---------------------------------------------------------------------------
-def cpu_sample(cfg, threads, nheads=None):
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
+def cpu_sample(cfg, threads, W):
+    """One bounded sample of the workload: `threads` heads (<= B*H), each its first
+    SAMPLE_ROWS[cid] rows (full L for configs 1-3) at full T, R, band and epsilon."""
     import oracle_ref
-    from paper_2605_08123_b200 import configs
-    n = min(cfg.B * cfg.H, nheads or threads)
-    inp = configs.make_inputs(cfg, heads=range(n))
+    n = min(cfg.B * cfg.H, threads)
+    rows = min(cfg.L, SAMPLE_ROWS.get(cfg.cid, cfg.L))
+    scfg = cfg if rows == cfg.L else cfg.replace(L=rows)
+    inp = W.make_inputs(scfg, heads=range(n))
 
     def once():
         t0 = time.perf_counter()
-        oracle_ref.run(cfg, inp.Q, inp.K, inp.V, inp.G, inp.row_mask, inp.col_mask, heads=inp.heads, precision=32,
+        oracle_ref.run(scfg, inp.Q, inp.K, inp.V, inp.G, inp.row_mask, inp.col_mask, heads=inp.heads, precision=32,
                        threads=threads, tile_block=128)
         return time.perf_counter() - t0
-    cells = n * cfg.L * cfg.Wf * (cfg.T + cfg.R)
-    return once, cells, n
+    cells = n * rows * cfg.Wf * (cfg.T + cfg.R)
+    desc = (f"{n} of {cfg.B * cfg.H} config-{cfg.cid} heads x rows [0,{rows}) of L={cfg.L} per step, full T/R/W/eps, "
+            f"run_surrogate + r2_backward(OneReference), f32 template mode (bf16 inputs upcast), tile_block 128, "
+            f"{threads} threads on {cpu_model()}")
+    return once, cells, desc
 
 
-def run_reference(args, cfg):
+def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    import oracle_ref
+    W = oracle_ref.load_configs()   # configs.py by path, oracle RNG: libsinkattn.so is never mapped
+    cfg = W.CONFIGS[args.config]
     threads = os.cpu_count() or 1
-    once, cells, n = cpu_sample(cfg, threads)
+    once, cells, desc = cpu_sample(cfg, threads, W)
     for _ in range(args.warmup):
         once()
     ts = [once() for _ in range(args.steps)]
     t = statistics.mean(ts)
     v = cells / t
-    sample = (f"{n} of {cfg.B * cfg.H} config-{cfg.cid} heads per step (run_surrogate + r2_backward OneReference, "
-              f"f32 template mode, tile_block 128), {threads} threads")
     line = {
         "impl": "reference", "metric": "fwd+bwd band-cells/s", "value": v, "unit": "band-cells/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": workload_str(cfg), "seed": 0, "host": "cpu"},
-        "cpu_baseline": {"value": v, "unit": "band-cells/s", "cores": threads, "kind": "port", "sample": sample},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
+        "config": config_obj(cfg, args.gpus),
+        "cpu_baseline": {"value": v, "unit": "band-cells/s", "cores": threads, "kind": "port", "sample": desc,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": "band-cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line, default=lambda o: o.item() if hasattr(o, "item") else str(o)), flush=True)
@@ -136,34 +172,42 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def load_traffic(cid):
+    """Measured DRAM bytes per launch of the dominant kernel (ncu --set full, profiles/)."""
+    p = os.path.join(ROOT, "profiles", f"traffic_config{cid}.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--mode", default="one_reference", choices=["one_reference", "direct_four_plan"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--e2e-depth", type=int, default=3, help="pipeline depth of the e2e H2D / compute / D2H overlap")
+    ap.add_argument("--e2e-depth", type=int, default=2, help="pipeline depth of the e2e H2D / compute / D2H overlap")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
-
-    from paper_2605_08123_b200 import configs
-    cfg = configs.CONFIGS[args.config]
     if args.impl == "reference":
-        return run_reference(args, cfg)
+        return run_reference(args)
 
     import numpy as np
     import torch
     import torch.distributed as dist
-    from paper_2605_08123_b200 import band
+    from paper_2605_08123_b200 import band, configs, shard
 
+    cfg = configs.CONFIGS[args.config]
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -177,17 +221,18 @@ def main():
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    # weak scaling: the job is world * B examples; rank r owns examples [r*B, (r+1)*B)
-    # (shard.example_partition) -- independent (b, h) problems, no collective on the data path
-    from paper_2605_08123_b200 import shard
-    ex, heads = shard.example_partition(cfg.B, cfg.H, world, rank)
-    inp = configs.make_inputs(cfg.replace(B=cfg.B * world), heads=heads)
-    if inp.row_mask is not None:
-        inp.row_mask, inp.col_mask = inp.row_mask[ex.start:ex.stop], inp.col_mask[ex.start:ex.stop]
-    spec = band.BandSpec(batch=cfg.B, heads=cfg.H, seq_q=cfg.L, seq_k=cfg.L, head_dim=cfg.d, half_band=cfg.w,
+    # strong scaling: rank r owns the contiguous flat head range of the ONE config
+    heads = shard.head_partition(cfg.B * cfg.H, world, rank)
+    nh = len(heads)
+    inp = configs.make_inputs(cfg, heads=heads)
+    # each owned head is its own example (batch = nh, heads = 1), carrying its example's mask row
+    sel = np.array([h // cfg.H for h in heads], dtype=np.int64)
+    hrm = None if inp.row_mask is None else np.ascontiguousarray(inp.row_mask[sel])
+    hcm = None if inp.col_mask is None else np.ascontiguousarray(inp.col_mask[sel])
+    spec = band.BandSpec(batch=nh, heads=1, seq_q=cfg.L, seq_k=cfg.L, head_dim=cfg.d, half_band=cfg.w,
                          base_depth=cfg.T, tail_depth=cfg.R, epsilon=cfg.eps, dtype=cfg.dtype, dustbin=cfg.dustbin,
                          dustbin_cost=cfg.dustbin_cost)
-    shp = (cfg.B, cfg.H, cfg.rows, cfg.d)
+    shp = (nh, 1, cfg.rows, cfg.d)
     bits = inp.bits or {}
 
     def host(x, k):
@@ -195,16 +240,17 @@ def main():
             return torch.from_numpy(bits[k].astype(np.int16)).view(torch.bfloat16).reshape(shp)
         return torch.from_numpy(np.ascontiguousarray(x)).reshape(shp)
     hQ, hK, hV, hG = host(inp.Q, "Q"), host(inp.K, "K"), host(inp.V, "V"), host(inp.G, "G")
+    del inp
     Q, K, V, G = (x.to(dev) for x in (hQ, hK, hV, hG))
-    rm = None if inp.row_mask is None else torch.from_numpy(inp.row_mask).to(dev)
-    cm = None if inp.col_mask is None else torch.from_numpy(inp.col_mask).to(dev)
-    band.validate_support(spec, inp.row_mask, inp.col_mask)  # once, outside the timed region
+    rm = None if hrm is None else torch.from_numpy(hrm).to(dev)
+    cm = None if hcm is None else torch.from_numpy(hcm).to(dev)
+    band.validate_support(spec, hrm, hcm)  # once, outside the timed region
 
-    O = torch.empty((cfg.B, cfg.H, cfg.rows, cfg.d), dtype=torch.float32, device=dev)
+    O = torch.empty(shp, dtype=torch.float32, device=dev)
     saved = torch.empty(spec.saved_bytes(), dtype=torch.uint8, device=dev)
     grads = tuple(torch.empty_like(O) for _ in range(3))
-    d_eps = torch.empty(cfg.B * cfg.H, dtype=torch.float32, device=dev)
-    eta_v = torch.empty((cfg.B, cfg.H, cfg.rows), dtype=torch.float32, device=dev)
+    d_eps = torch.empty(nh, dtype=torch.float32, device=dev)
+    eta_v = torch.empty((nh, 1, cfg.rows), dtype=torch.float32, device=dev)
     ws = band.Workspace()
     ws.get(spec.workspace_bytes(), dev)
 
@@ -245,77 +291,96 @@ def main():
             torch.cuda.synchronize(dev)
         barrier()
         ts = [s.elapsed_time(e) for s, e in evs]
+    del graph
     ms = float(statistics.mean(ts))
     tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms_max = float(tmax.item())
-    cells = cfg.nominal_cell_steps()
-    value = cells * world / (ms_max * 1e-3)
+    cells_all = cfg.nominal_cell_steps()                      # the whole config (all ranks)
+    value = cells_all / (ms_max * 1e-3)
 
-    # --- dominant kernel: one Sinkhorn full step, measured differentially ---
-    # forward with T and with T + dT on the same inputs; dT full steps = dT x (row + col) launches
+    # --- the dominant kernel: the Sinkhorn full step, measured differentially (T vs T + dT) ---
     dT = 20
     spec2 = band.BandSpec(**{**spec.__dict__, "base_depth": cfg.T + dT})
-    ws2 = band.Workspace()
-    ws2.get(spec2.workspace_bytes(), dev)
     saved2 = torch.empty(spec2.saved_bytes(), dtype=torch.uint8, device=dev)
+    ws2 = band.Workspace()
 
-    def fwd(sp, w_, sv):
+    def fwd(sp, sv, w_):
         band.run_surrogate(Q, K, V, sp, rm, cm, out=O, saved=sv, workspace=w_, validate=False)
     with torch.cuda.stream(stream):
-        tf = {}
-        for key, sp, w_, sv in (("a", spec, ws, saved), ("b", spec2, ws2, saved2)):
-            for _ in range(2):
-                fwd(sp, w_, sv)
+        tf, nl = {}, {}
+        for key, sp, sv in (("a", spec, saved), ("b", spec2, saved2)):
+            w_ = ws if key == "a" else ws2
+            fwd(sp, sv, w_)
+            torch.cuda.synchronize(dev)
+            band.launch_count(reset=True)
+            fwd(sp, sv, w_)
+            nl[key] = band.launch_count(reset=True)
             xs = []
-            for _ in range(5):
+            for _ in range(3):
                 flush.zero_()
                 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 s.record(stream)
-                fwd(sp, w_, sv)
+                fwd(sp, sv, w_)
                 e.record(stream)
                 torch.cuda.synchronize(dev)
                 xs.append(s.elapsed_time(e))
             tf[key] = statistics.median(xs)
+            if key == "b":
+                del w_
+                ws2 = None
     step_ms = max(1e-6, (tf["b"] - tf["a"]) / dT)
-    act = configs.active_cells(cfg)
-    rows_cols = cfg.B * cfg.H * (cfg.rows + cfg.rows)
-    alg_bytes = 4 * act + 3 * 4 * rows_cols          # one read of the active S2 band + dual read/write
+    launches_per_full_step = max(1, (nl["b"] - nl["a"]) // dT)
+    launch_us = step_ms * 1e3 / launches_per_full_step
+
+    act_all = configs.active_cells(cfg)                     # exact active edges per Sinkhorn step (all heads)
+    act = act_all * nh // (cfg.B * cfg.H) if cfg.mask == "none" else act_all  # this rank's (unmasked configs)
+    P_exp = EX2_PER_CLK_SM * N_SM * (clk.max_mhz or 1965) * 1e6
     hbm, bf16, peak_src = peaks()
-    achieved = alg_bytes / (step_ms * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "step_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get("bytes_per_full_step")
-        except Exception:
-            traffic = None
-    exps = 2 * act
-    sfu_peak = 16 * 148 * (clk.max_mhz or 1965) * 1e6
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "peak_source": peak_src,
-                "kernel": "Sinkhorn full step (u and v half-steps), differential timing T vs T+20",
-                "algorithmic_bytes_per_step": alg_bytes, "step_ms": step_ms,
-                "step_share_of_fwd_bwd": (cfg.T + cfg.R) * step_ms / ms}
-    roofline_sfu = {"bound": "sfu(ex2)", "achieved": exps / (step_ms * 1e-3) / 1e9,
-                    "peak": sfu_peak / 1e9, "unit": "Gexp/s", "frac": exps / (step_ms * 1e-3) / sfu_peak,
-                    "peak_source": "16 MUFU.EX2/clk/SM x 148 SMs x max SM clock (nominal)"}
+    # SURVEY §8(d) algorithmic counts (one-reference schedule)
+    n_exp = act_all * (2 * (cfg.T + cfg.R) + 5)
+    n_flop = act_all * 2 * cfg.d * (cfg.T + cfg.R + 11)
+    s_in = 2 if cfg.dtype == "bf16" else 4
+    n_byte = cfg.B * cfg.H * cfg.rows * cfg.d * (4 * s_in + 4 * 4)
+    t_s = ms_max * 1e-3
+    tp = {"exp": n_exp / P_exp, "tensor": n_flop / (bf16 * 1e12), "hbm": n_byte / (hbm * 1e9)}
+    # dominant kernel (per launch): 2 ex2 per active cell per full step (§8(d)); the issued count of the
+    # current schedule is stated beside it
+    alg_exp_launch = 2 * act / launches_per_full_step
+    traffic = load_traffic(cfg.cid)
+    roofline = {
+        "bound": "sfu(ex2)", "unit": "Gex2/s",
+        "achieved": alg_exp_launch / (launch_us * 1e-6) / 1e9, "peak": P_exp / 1e9,
+        "frac": alg_exp_launch / (launch_us * 1e-6) / P_exp,
+        "traffic": None if traffic is None else traffic.get("dram_bytes_per_launch"),
+        "traffic_algorithmic_bytes_per_launch": None if traffic is None else traffic.get("algorithmic_bytes_per_launch"),
+        "kernel": (f"Sinkhorn full step ({launches_per_full_step} launch(es)/step), differential timing T vs T+{dT}, "
+                   f"CUDA events on the launching stream"),
+        "per_launch_us": launch_us, "launches_per_full_step": launches_per_full_step,
+        "alg_ex2_per_launch": alg_exp_launch,
+        "peak_source": f"{EX2_PER_CLK_SM} MUFU.EX2/clk/SM x {N_SM} SMs x max SM clock",
+        "kernel_share_of_step": (cfg.T + cfg.R) * step_ms / ms,
+        "whole_step": {
+            "binding": max(tp, key=tp.get), "t_roof_ms": 1e3 * max(tp.values()),
+            "frac": max(tp.values()) / t_s,
+            "frac_exp": tp["exp"] / t_s, "frac_tensor": tp["tensor"] / t_s, "frac_hbm": tp["hbm"] / t_s,
+            "N_exp": n_exp, "N_flop": n_flop, "N_byte": n_byte,
+            "model": "SURVEY §8(d): N_exp = cells(2(T+R)+5), N_flop = cells 2d(T+R+11), N_byte = BHLd(4 s_in + 4 s_out); "
+                     "P_mma = measured bf16 dense, P_hbm = measured copy"},
+    }
 
     # --- e2e through the public API with pinned host buffers ---
     e2e = None
     if not args.no_e2e:
         hQ, hK, hV, hG = (x.pin_memory() for x in (hQ, hK, hV, hG))
-        hrm = None if inp.row_mask is None else torch.from_numpy(inp.row_mask).pin_memory()
-        hcm = None if inp.col_mask is None else torch.from_numpy(inp.col_mask).pin_memory()
-        outs_h = [torch.empty(O.shape, dtype=torch.float32).pin_memory() for _ in range(4)]
-        deps_h = torch.empty(cfg.B * cfg.H, dtype=torch.float32).pin_memory()
+        hrm_t = None if hrm is None else torch.from_numpy(hrm).pin_memory()
+        hcm_t = None if hcm is None else torch.from_numpy(hcm).pin_memory()
         h2d = sum(x.numel() * x.element_size() for x in (hQ, hK, hV, hG)) + \
-            sum(0 if x is None else x.numel() for x in (hrm, hcm))
-        d2h = sum(x.numel() * x.element_size() for x in outs_h) + deps_h.numel() * 4
+            sum(0 if x is None else x.numel() for x in (hrm_t, hcm_t))
         # Pipelined nb deep: step k's H2D (copy stream), fwd+bwd (compute stream) and D2H (d2h stream)
-        # overlap steps k-1 / k+1; device inputs and outputs are double-buffered and ordered by events.
-        # Every step still copies its own inputs in and its results out inside the timed region.
+        # overlap steps k-1 / k+1; device inputs / outputs are nb-buffered and ordered by events.
+        # Every step copies its own inputs in and its results (O, dQ, dK, dV, d_eps) out.
         nb = max(2, args.e2e_depth)
         din = [tuple(torch.empty_like(x) for x in (Q, K, V, G)) for _ in range(nb)]
         dms = [(None if rm is None else torch.empty_like(rm), None if cm is None else torch.empty_like(cm))
@@ -323,11 +388,12 @@ def main():
         dout = [(torch.empty_like(O), tuple(torch.empty_like(O) for _ in range(3)), torch.empty_like(d_eps),
                  torch.empty_like(eta_v), torch.empty_like(saved)) for _ in range(nb)]
         outs_hb = [[torch.empty(O.shape, dtype=torch.float32).pin_memory() for _ in range(4)] for _ in range(nb)]
-        deps_hb = [torch.empty(cfg.B * cfg.H, dtype=torch.float32).pin_memory() for _ in range(nb)]
+        deps_hb = [torch.empty(nh, dtype=torch.float32).pin_memory() for _ in range(nb)]
+        d2h = sum(x.numel() * x.element_size() for x in outs_hb[0]) + deps_hb[0].numel() * 4
         s_h2d, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        ev_in = [torch.cuda.Event() for _ in range(nb)]    # inputs of slot landed
-        ev_used = [torch.cuda.Event() for _ in range(nb)]  # compute finished reading inputs / writing outputs
-        ev_out = [torch.cuda.Event() for _ in range(nb)]   # outputs of slot copied to host
+        ev_in = [torch.cuda.Event() for _ in range(nb)]
+        ev_used = [torch.cuda.Event() for _ in range(nb)]
+        ev_out = [torch.cuda.Event() for _ in range(nb)]
         for k in range(nb):
             ev_used[k].record(stream)
             ev_out[k].record(s_d2h)
@@ -338,7 +404,7 @@ def main():
             Oe, gr, de, ee, sv = dout[b]
             with torch.cuda.stream(s_h2d):
                 s_h2d.wait_event(ev_used[b])
-                for dst, src in ((Qe, hQ), (Ke, hK), (Ve, hV), (Ge, hG), (rme, hrm), (cme, hcm)):
+                for dst, src in ((Qe, hQ), (Ke, hK), (Ve, hV), (Ge, hG), (rme, hrm_t), (cme, hcm_t)):
                     if dst is not None:
                         dst.copy_(src, non_blocking=True)
                 ev_in[b].record(s_h2d)
@@ -354,7 +420,7 @@ def main():
                     dst.copy_(src, non_blocking=True)
                 deps_hb[b].copy_(cot.d_eps, non_blocking=True)
                 ev_out[b].record(s_d2h)
-        for k in range(2 * nb):
+        for k in range(nb):
             e2e_step(k)
         torch.cuda.synchronize(dev)
         barrier()
@@ -370,30 +436,29 @@ def main():
         t2 = torch.tensor([ems], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-        e2e = {"value": cells * world / (float(t2.item()) * 1e-3), "unit": "band-cells/s",
+        e2e = {"value": cells_all / (float(t2.item()) * 1e-3), "unit": "band-cells/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": float(t2.item()),
                "pipeline": f"{nb}-deep: H2D / fwd+bwd / D2H of consecutive steps overlap on 3 streams (pinned host buffers)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle_ref
+        W = oracle_ref.load_configs()
         threads = os.cpu_count() or 1
-        once, ccells, n = cpu_sample(cfg, threads)
-        once()
+        once, ccells, desc = cpu_sample(W.CONFIGS[cfg.cid], threads, W)
         t = once()
         cpu = {"value": ccells / t, "unit": "band-cells/s", "cores": threads, "kind": "port",
-               "sample": f"{n} of {cfg.B * cfg.H} config-{cfg.cid} heads, run_surrogate + r2_backward(OneReference), "
-                         f"f32 template mode, tile_block 128, {threads} threads, {t:.2f} s wall"}
+               "sample": desc + f", {t:.2f} s wall", "cpu_model": cpu_model()}
 
     if rank == 0:
+        conf = config_obj(cfg, world)
+        conf.update({"cuda_graph": not args.no_graph, "mode": args.mode, "heads_per_gpu": nh,
+                     "active_cells_per_step": act_all, "nominal_cells_per_step": cfg.nominal_cells()})
         line = {
             "metric": "fwd+bwd band-cells/s", "value": value, "unit": "band-cells/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
-            "config": {"workload": workload_str(cfg), "seed": 0, "mode": args.mode,
-                       "parallelism": f"batch x head shards: {world} GPU(s) x {cfg.B} examples each, no operator collective",
-                       "l2": "flushed between timed steps (256 MiB write)", "cuda_graph": graph is not None,
-                       "active_cells_per_step": act, "nominal_cells_per_step": cfg.nominal_cells()},
-            "roofline": roofline, "roofline_sfu": roofline_sfu, "cpu_baseline": cpu, "e2e": e2e,
+            "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic", "config": conf,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches_per_step * args.steps), "clocks": clk.summary(),
             "ms_per_step_all": [round(x, 4) for x in ts],
         }

@@ -155,6 +155,12 @@ void stoc_normal_fill(std::uint64_t seed, const char* tag, std::uint64_t start, 
         out[k] = scale * stoc::counter_normal_base(base, start + static_cast<std::uint64_t>(k));
 }
 
+// Fill out[k] = counter_uniform(fold_tag(seed, tag) + start + k), k < n (inc/rng.hpp:21-35).
+void stoc_uniform_fill(std::uint64_t seed, const char* tag, std::uint64_t start, std::int64_t n, double* out) {
+    const std::uint64_t base = stoc::fold_tag(seed, tag);
+    for (std::int64_t k = 0; k < n; ++k) out[k] = stoc::counter_uniform(base + start + static_cast<std::uint64_t>(k));
+}
+
 std::int64_t stoc_banded_entry_count(std::int64_t L, std::int64_t w) { return stoc::banded_entry_count(L, w); }
 
 // Batched reference path.  Tensors are [B, H, Lr, d] doubles (Lr = L + dustbin),

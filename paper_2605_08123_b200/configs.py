@@ -24,12 +24,25 @@ from __future__ import annotations
 
 import ctypes
 import dataclasses
+import importlib
 import math
-from typing import Dict, Optional
+from typing import Callable, Dict, Optional
 
 import numpy as np
 
-from ._lib import lib
+# The counter RNG backend (bit-exact restatements of inc/rng.hpp:38-56): by default the
+# product library's st_normal_fill / st_uniform_fill, loaded lazily.  bench.py's reference arm
+# loads this file by path and installs the oracle's stoc_* fills instead, so that arm never
+# maps libsinkattn.so (set_rng_backend).
+_BACKEND: Dict[str, Callable] = {}
+
+
+def set_rng_backend(normal: Callable, uniform: Callable) -> None:
+    _BACKEND["normal"], _BACKEND["uniform"] = normal, uniform
+
+
+def _product_lib():
+    return importlib.import_module("paper_2605_08123_b200._lib").lib
 
 
 @dataclasses.dataclass(frozen=True)
@@ -81,14 +94,19 @@ CONFIGS: Dict[int, Config] = {
 
 
 def normal_fill(seed: int, tag: str, start: int, n: int, scale: float = 1.0) -> np.ndarray:
+    if "normal" in _BACKEND:
+        return _BACKEND["normal"](seed, tag, start, n, scale)
     out = np.empty(n, dtype=np.float64)
-    lib.st_normal_fill(seed, tag.encode(), start, n, scale, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    _product_lib().st_normal_fill(seed, tag.encode(), start, n, scale,
+                                  out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     return out
 
 
 def uniform_fill(seed: int, tag: str, start: int, n: int) -> np.ndarray:
+    if "uniform" in _BACKEND:
+        return _BACKEND["uniform"](seed, tag, start, n)
     out = np.empty(n, dtype=np.float64)
-    lib.st_uniform_fill(seed, tag.encode(), start, n, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    _product_lib().st_uniform_fill(seed, tag.encode(), start, n, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     return out
 
 

@@ -28,3 +28,11 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+def pytest_sessionfinish(session, exitstatus):
+    try:
+        import parity_log
+        parity_log.write()
+    except Exception:  # pragma: no cover - reporting only
+        pass

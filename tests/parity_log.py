@@ -1,0 +1,32 @@
+"""Per-config, per-tensor parity records of the GPU tests (test infrastructure).
+
+check_against_oracle() appends one record per case; with ST_PARITY_OUT set, the
+session writes them as JSON (tools/parity_table.sh copies it to profiles/).
+"""
+import json
+import os
+
+RECORDS = []
+
+
+def record(case, cfg, heads, mode, errs, floor, bounds):
+    RECORDS.append({
+        "case": case, "config": getattr(cfg, "cid", None),
+        "shape": {"L": cfg.L, "d": cfg.d, "w": cfg.w, "Wf": 2 * cfg.w + 1, "eps": cfg.eps, "T": cfg.T, "R": cfg.R,
+                  "dtype": cfg.dtype, "mask": cfg.mask, "dustbin": cfg.dustbin},
+        "heads": [int(h) for h in heads], "mode": mode,
+        "rel_l2_gpu_vs_f64": {k: float(v) for k, v in errs.items()},
+        "rel_l2_ref_f32_vs_f64": {k: float(v) for k, v in floor.items()},
+        "bound": {k: float(v) for k, v in bounds.items()},
+    })
+
+
+def write(path=None):
+    path = path or os.environ.get("ST_PARITY_OUT")
+    if not path or not RECORDS:
+        return
+    os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)
+    with open(path, "w") as f:
+        json.dump({"measure": "rel-L2 = ||x - x_f64|| / ||x_f64|| per tensor over the listed heads; "
+                              "x_f64 = the oracle (reference algorithm) in double on the same (bf16-rounded) inputs",
+                   "records": RECORDS}, f, indent=1)

@@ -18,6 +18,7 @@ import pytest
 import torch
 
 import oracle_ref
+import parity_log
 from paper_2605_08123_b200 import band, configs
 
 FP32_TOL = 1e-5
@@ -89,7 +90,8 @@ def oracle(cfg, inp, **kw):
 KEYS = ("O", "dQ", "dK", "dV", "eta_v", "d_eps")
 
 
-def check_against_oracle(cfg, inp, tol_o, tol_g, mode="one_reference", eps_schedule=None):
+def check_against_oracle(cfg, inp, tol_o, tol_g, mode="one_reference", eps_schedule=None, case=None,
+                         bounds_override=None):
     g = gpu_run(cfg, inp, mode=mode, eps_schedule=eps_schedule)
     m = 1 if mode == "direct_four_plan" else 0
     r = oracle(cfg, inp, precision=64, mode=m, eps_schedule=eps_schedule)
@@ -98,13 +100,17 @@ def check_against_oracle(cfg, inp, tol_o, tol_g, mode="one_reference", eps_sched
     floor = {k: rel(r32[k], r[k]) for k in KEYS}
     print(f"config {cfg.cid} L={cfg.L} heads={len(inp.heads)} mode={mode} rel-L2 gpu / ref-f32:",
           {k: f"{errs[k]:.2e}/{floor[k]:.2e}" for k in KEYS})
-    assert np.all(np.isfinite(g["O"])) and np.all(np.isfinite(g["dQ"]))
+    bounds = {}
     for k in KEYS:
         tol = tol_o if k in ("O", "dV") else (max(DEPS_TOL, tol_g) if k == "d_eps" else tol_g)
         # d_eps (EXT, no reference pin) is a cancellation-heavy scalar sum of +-Sbar*S: within 3x of the
         # reference's own f32 instantiation (config 3 with scores |s2| ~ 115 sits at ~1e-3 there)
-        bound = max(tol, (3.0 if k == "d_eps" else 1.5) * floor[k])
-        assert errs[k] <= bound, (k, errs[k], bound, errs)
+        bounds[k] = max(tol, (3.0 if k == "d_eps" else 1.5) * floor[k])
+    bounds.update(bounds_override or {})
+    parity_log.record(case or f"config{cfg.cid}", cfg, inp.heads, mode, errs, floor, bounds)
+    assert np.all(np.isfinite(g["O"])) and np.all(np.isfinite(g["dQ"]))
+    for k in KEYS:
+        assert errs[k] <= bounds[k], (k, errs[k], bounds[k], errs)
     # saved tail duals (centered gauge ledger) against the oracle's centered trace
     nh = len(inp.heads)
     for rr in range(3):
@@ -199,20 +205,45 @@ def test_deterministic_and_linear_in_G():
         assert rel(r3[k], 0.5 * r1[k] - 2.0 * r2[k]) < 1e-5, k
 
 
-@pytest.mark.parametrize("cid", [4, 5])
-def test_bf16_full_size_properties(cid):
-    """Full BASELINE sizes: finite, dV(dO=1) = column sums of P22 = 1, modes agree."""
+@pytest.mark.parametrize("cid,heads", [(4, (0, 1)), (5, (0,))])
+def test_bf16_full_baseline_shape_parity(cid, heads):
+    """Configs 4 / 5 at their full BASELINE shapes (L = 32768 / 131072, the full band, T, eps) on a
+    seeded head subset: 512 / 1024 row blocks per launch, i.e. several blocks per
+    persistent CTA, so the cross-block chunk reuse and ring bookkeeping of the half-step kernel run
+    exactly as in the benchmark.  Stated bf16 bound: BF16_TOL = 1e-4 rel-L2 on O, dQ, dK, dV, eta."""
     cfg = configs.CONFIGS[cid]
-    heads = range(0, cfg.B * cfg.H)
-    inp = configs.make_inputs(cfg, heads=heads)
-    shp = (cfg.B, cfg.H, cfg.rows, cfg.d)
-    ones = torch.ones(shp, dtype=torch.bfloat16, device="cuda")
-    g = gpu_run(cfg, inp, G=ones)
-    assert np.all(np.isfinite(g["O"]))
-    colsum = g["dV"]  # every head-dim column equals sum_i P22_ij
-    assert np.abs(colsum - 1.0).max() < 1e-3, np.abs(colsum - 1.0).max()
-    g1 = gpu_run(cfg, inp)
-    assert np.all(np.isfinite(g1["dQ"])) and np.all(np.isfinite(g1["dK"]))
+    inp = configs.make_inputs(cfg, heads=range(heads[0], heads[-1] + 1))
+    check_against_oracle(cfg, inp, BF16_TOL, BF16_TOL, case=f"config{cid}-full-L")
+
+
+def test_bf16_many_blocks_per_cta_parity():
+    """Config-4 geometry (d = 128, W = 257) with 8 heads x 64 blocks = 512 blocks > 2 x 148 CTAs."""
+    cfg = configs.CONFIGS[4].replace(L=8192)
+    inp = configs.make_inputs(cfg, heads=range(8))
+    check_against_oracle(cfg, inp, BF16_TOL, BF16_TOL, case="config4-L8192-8heads")
+
+
+@pytest.mark.parametrize("cid", [4, 5])
+def test_bf16_full_size_row_sums(cid):
+    """Every head of the full configs: the row sums of the tail plan P22 (O with V = 1) are close to 1.
+    The final column half-step forces the COLUMN sums to 1 for any u, so the row sums are the check
+    that reaches the row solve; their deviation must stay within 2x of the oracle's on head 0 (+1e-4)."""
+    cfg = configs.CONFIGS[cid]
+    inp = configs.make_inputs(cfg)
+    ones_bits = np.full_like(inp.bits["V"], 0x3F80)           # bf16 1.0
+    inp.V = np.ones_like(inp.V)
+    inp.bits = {**inp.bits, "V": ones_bits}
+    g = gpu_run(cfg, inp, duals=False)
+    assert np.all(np.isfinite(g["O"])) and np.all(np.isfinite(g["dQ"])) and np.all(np.isfinite(g["dK"]))
+    rows = g["O"][:, :, 0]
+    assert np.array_equal(g["O"][:, :, 0], g["O"][:, :, -1])
+    dev = np.abs(rows - 1.0).max(axis=1)
+    sub = configs.make_inputs(cfg, heads=range(1))
+    r = oracle_ref.run(cfg, sub.Q, sub.K, np.ones_like(sub.V), sub.G, heads=sub.heads, precision=64, backward=False)
+    ref_dev = float(np.abs(r["O"][0, :, 0] - 1.0).max())
+    print(f"config {cid}: max |rowsum(P22) - 1| per head {dev.max():.3e} (oracle head 0: {ref_dev:.3e})")
+    assert abs(float(dev[0]) - ref_dev) <= 0.05 * ref_dev + 1e-4
+    assert dev.max() <= 2 * ref_dev + 1e-4, dev
 
 
 @pytest.mark.parametrize("cid,L", [(2, None), (4, 2048), (5, 2048)])
@@ -509,3 +540,32 @@ def test_dustbin_line_kernels_parity(dtype, mode):
     g, r, _ = check_against_oracle(cfg, inp, FP32_TOL, FP32_GRAD_TOL, mode=mode)
     assert np.abs(g["dQ"][:, cfg.L]).max() == 0.0
     assert np.abs(g["dK"][:, cfg.L]).max() == 0.0
+
+
+def _ref_fixtures():
+    import glob
+    import os
+    return sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_config*.npz")))
+
+
+@pytest.mark.parametrize("path", _ref_fixtures(), ids=lambda p: p.rsplit("/", 1)[-1])
+def test_gpu_matches_reference_golden(path):
+    """The CUDA path against the REFERENCE'S OWN outputs (tests/golden/ref_*.npz, made by the
+    unmodified reference through oracle/_ref, tests/golden/make_ref_golden.py), per config."""
+    import os
+    z = np.load(path)
+    cid = int(os.path.basename(path).split("config")[1][0])
+    cfg = configs.CONFIGS[cid].replace(L=int(z["L"]))
+    inp = configs.make_inputs(cfg, heads=range(len(z["heads"])))
+    g = gpu_run(cfg, inp)
+    keys = [str(k) for k in z["keys"]]
+    floor = dict(zip(keys, z["floor"]))
+    errs, bounds = {}, {}
+    for k in keys:
+        errs[k] = rel(g[k], z[k])
+        bounds[k] = BF16_TOL if cfg.dtype == "bf16" else max(FP32_TOL, 1.5 * floor[k])
+    parity_log.record(f"ref-golden-config{cid}-L{cfg.L}", cfg, inp.heads, "one_reference", errs, floor, bounds)
+    print(f"reference golden config {cid} L={cfg.L}: rel-L2 gpu / ref-f32:",
+          {k: f"{errs[k]:.2e}/{floor[k]:.2e}" for k in keys})
+    for k in keys:
+        assert errs[k] <= bounds[k], (k, errs[k], bounds[k])
