@@ -175,6 +175,35 @@ TcPlan tc_plan(const st_desc* d, const Dims& m) {
     return p;
 }
 
+// Full-step solve (k_fstep16): bf16 planes, 128-column chunks, the block's window (<= 3 chunks)
+// resident in TMEM next to one free slot, no dustbin / sequence-sharding hook.  SMEM plan: NA, NSK.
+struct FsPlan {
+    bool ok = false;
+    int NA, NSK;
+};
+FsPlan fstep_plan(const st_desc* d, const TcPlan& tp, const Dims& m) {
+    FsPlan f;
+    if (!tp.ok || tp.npl != 1 || tp.CR != 128 || d->dustbin || tp.maxwin / tp.CR > 3 || getenv("ST_NO_FSTEP16")) return f;
+    for (int NA = 2; NA >= 1; --NA)
+        for (int extra = 2; extra >= 0; --extra) {
+            st::PhaseArgs a{};
+            a.CR = tp.CR;
+            a.NA = NA;
+            a.NSK = tp.maxwin / tp.CR + extra;
+            a.npl = 1;
+            a.row_bytes = tp.row_bytes;
+            a.maxwin = tp.maxwin;
+            a.wl_cap = (int)((m.BH * std::max(tp.NBq, tp.NBk) + num_sms() - 1) / num_sms());
+            if (st::fstep16_smem_bytes(a) <= 227 * 1024) {
+                f.ok = true;
+                f.NA = NA;
+                f.NSK = a.NSK;
+                return f;
+            }
+        }
+    return f;
+}
+
 struct WsLayout {
     size_t Z, ZT, Zd, ZdT;  // tile backward bands
     size_t S2, S2T, u, v, g_u, u2b, u1b, deps, g_v, v1b, v0b, err;
@@ -183,6 +212,7 @@ struct WsLayout {
     size_t fs_flags, fs_work, fs_cnt, fs_part[2], fs_partm;  // persistent solve: work list, tagged partials
     size_t tail_u, tail_v;  // generic-R adjoint: (R+1) row / column cotangent vectors
     size_t dpart;           // dustbin line partials [BH][8][129]
+    size_t fpart;           // full-step bf16 solve: column partials [BH][NBq][maxwin]
     size_t bytes;
 };
 
@@ -285,6 +315,9 @@ WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
         w.cnt = take(sizeof(int) * 2);
         w.pad_u = take(sizeof(float) * (size_t)m.BH * (tp.CR + tp.Lpq));
         w.pad_v = take(sizeof(float) * (size_t)m.BH * (tp.CR + tp.Lpk));
+        w.fpart = take(sizeof(float) * (size_t)m.BH * tp.NBq * tp.maxwin);
+    } else {
+        w.fpart = 0;
     }
     w.bytes = o;
     return w;
@@ -366,7 +399,8 @@ extern "C" {
 const char* st_last_error(void) { return g_err.c_str(); }
 
 int64_t st_launch_count(int32_t reset) {
-    return (int64_t)(st::launch_count(reset != 0) + st::phase_launch_count(reset != 0));
+    return (int64_t)(st::launch_count(reset != 0) + st::phase_launch_count(reset != 0) +
+                     st::fstep16_launch_count(reset != 0));
 }
 
 size_t st_saved_bytes(const st_desc* desc) {
@@ -538,7 +572,28 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
         dr.L_own = g.Lq; dr.L_other = g.Lk; dr.Lr_own = g.Lrq; dr.Lr_other = g.Lrk; dr.mask_other = col_mask;
         dc.L_own = g.Lk; dc.L_other = g.Lq; dc.Lr_own = g.Lrk; dc.Lr_other = g.Lrq; dc.mask_other = row_mask;
         const int grid = std::min(num_sms(), (int)(m.BH * std::max(tp.NBq, tp.NBk)));
-        for (long t = 1; t <= T + R; ++t) {
+        const FsPlan fp = hook ? FsPlan{} : fstep_plan(desc, tp, m);
+        if (fp.ok) {
+            // ---- one tcgen05 score evaluation per full step (k_fstep16) + the column-dual merge
+            float* fpart = (float*)(ws + wl.fpart);
+            ST_CUDA(cudaMemsetAsync(fpart, 0, sizeof(float) * (size_t)m.BH * tp.NBq * tp.maxwin, st));
+            st::PhaseArgs pf = pr;
+            pf.NA = fp.NA;
+            pf.NSK = fp.NSK;
+            for (long t = 1; t <= T + R; ++t) {
+                const long r = t - T;
+                float* u_out = (sv && r >= 0 && r < sl.ns) ? slot_u(r) : u_ws;
+                float* v_out = (sv && r >= 0 && r < sl.ns) ? slot_v(r) : v_ws;
+                pf.c2 = g.c2 * step_scale(desc, t);
+                pf.out_own = u_out;
+                ST_CUDA(st::launch_fstep16(pf, fpart, t == 1, grid, st));
+                ST_CUDA(st::launch_vmerge(fpart, pad_v, v_out, g.BH, g.H, g.Lq, g.Lk, g.Lrk, tp.NBq, tp.maxwin, g.w,
+                                          tp.CR, tp.shift, tp.Lpk, pad_ld_k, tp.CR, col_mask, err, st));
+                u_prev = u_out;
+                v_prev = v_out;
+            }
+        }
+        for (long t = 1; !fp.ok && t <= T + R; ++t) {
             const long r = t - T;
             float* u_out = (sv && r >= 0 && r < sl.ns) ? slot_u(r) : u_ws;
             float* v_out = (sv && r >= 0 && r < sl.ns) ? slot_v(r) : v_ws;

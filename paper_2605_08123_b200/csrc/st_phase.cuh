@@ -65,6 +65,14 @@ cudaError_t launch_pack(int dtype, const void* X, int BH, int L, int Lr, int Lp,
 // pad[bh][pad_off + j] = active(j) ? (src ? src[bh][j] : 0) : -inf; guards -inf
 cudaError_t launch_pad_fill(float* pad, const float* src, int BH, int H, int L, int Lr, int pad_ld, int pad_off,
                             const uint8_t* mask, cudaStream_t s);
+// Full-step bf16 solve (st_fstep16.cu): one S evaluation per Sinkhorn step.  part: column partials
+// [BH][NB][maxwin]; k_vmerge folds them into the padded column duals (and v_out when non-null).
+size_t fstep16_smem_bytes(const PhaseArgs& a);
+long long fstep16_launch_count(bool reset);
+cudaError_t launch_fstep16(const PhaseArgs& a, float* part, bool first, int grid, cudaStream_t s);
+cudaError_t launch_vmerge(const float* part, float* pad_v, float* v_out, int BH, int H, int Lq, int Lk, int Lrk, int NB,
+                          int maxwin, int w, int CR, int shift, int Lp_other, int pad_ld, int pad_off,
+                          const uint8_t* col_mask, int* err, cudaStream_t s);
 cudaError_t launch_compact(const int* flags, int n, int* work, int* count, cudaStream_t s);
 cudaError_t launch_worklist(const uint8_t* mask, int H, int BH, int L, int NB, int* flags, int* work, int* count,
                             cudaStream_t s);

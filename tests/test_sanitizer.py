@@ -1,0 +1,29 @@
+"""compute-sanitizer (memcheck, racecheck, synccheck) over small forward + backward cases that
+cover every kernel family: the fp32 persistent solve and tile stages (config 1 / 2 geometry),
+the dustbin line kernels (config 3), the tcgen05 full-step solve with more row blocks than CTAs
+(config 4 geometry) and the half-step + window-chunked stages (config 5 geometry).
+Logs go to $ST_SANITIZER_OUT (default gpurun_out/sanitizer); SURVEY §5."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+@pytest.mark.parametrize("case", ["c1", "c2", "c3", "bf16", "bf16w"])
+def test_compute_sanitizer_clean(tool, case):
+    out = os.environ.get("ST_SANITIZER_OUT", os.path.join(ROOT, "gpurun_out", "sanitizer"))
+    os.makedirs(out, exist_ok=True)
+    log = os.path.join(out, f"{tool}_{case}.log")
+    cmd = [SAN, "--tool", tool, "--error-exitcode", "97", "--log-file", log,
+           sys.executable, os.path.join(ROOT, "tools", "sanitize_case.py"), case]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
+    text = open(log).read() if os.path.exists(log) else ""
+    assert p.returncode == 0, (p.returncode, text[-3000:], p.stderr[-2000:])
+    assert "ERROR SUMMARY: 0 errors" in text or "RACECHECK SUMMARY: 0 hazards" in text or "0 errors" in text, text[-2000:]
