@@ -45,15 +45,16 @@ using namespace sm100;
 namespace {
 
 constexpr int kNV = 3;     // dual-window ring slots
-constexpr int kEW = 16;    // epilogue warps
-constexpr int kParts = 4;  // column parts per lane quadrant
+constexpr int kPH = 3;     // epilogue warps per 16-lane half of a TMEM lane quadrant
+constexpr int kEW = 8 * kPH;  // epilogue warps
+constexpr int kSlc = 4;    // 32-column slices per 128-column chunk
 
 struct FSmem {
     uint8_t* A;       // [NA][128 * row_bytes]
     uint8_t* K;       // [NSK][CR * row_bytes]
     float* vwin;      // [kNV][maxwin + 128]
-    float* rowp;      // [2][2][kParts][128]: row partial (sum, max) per part, by block parity
-    float* colp;      // [2][4][maxwin]: column partials per lane quadrant, by block parity
+    float* rowp;      // [2][kPH][128]: row partial (sum, max) per sub-warp (one buffer: two barriers per block)
+    float* colp;      // [8][maxwin]: column partials per 16-lane half quadrant
     uint64_t* v_full;
     uint64_t* v_empty;
     uint64_t* a_full;
@@ -73,8 +74,8 @@ __device__ __forceinline__ FSmem fcarve(uint8_t* base, const PhaseArgs& a, int n
     s.K = s.A + (size_t)a.NA * blk;
     s.vwin = (float*)(s.K + (size_t)a.NSK * chk);
     s.rowp = s.vwin + kNV * (a.maxwin + 128);
-    s.colp = s.rowp + 2 * 2 * kParts * 128;
-    uint64_t* bars = (uint64_t*)(s.colp + 2 * 4 * a.maxwin);
+    s.colp = s.rowp + 2 * kPH * 128;
+    uint64_t* bars = (uint64_t*)(s.colp + 8 * a.maxwin);
     s.v_full = bars;
     s.v_empty = bars + kNV;
     bars += 2 * kNV;
@@ -125,7 +126,6 @@ template <bool kFirst, bool kRecompute>
 __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float* __restrict__ part_out) {
     constexpr int NE = 32 * kEW;
     constexpr int kCR = 128;
-    constexpr int HC = kCR / kParts;  // 32 columns per warp per chunk
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     constexpr int NST = 512 / kCR;
     const FSmem s = fcarve(smem_raw, a, NST);
@@ -232,39 +232,47 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float
             const bool same = have && b.bh == last_bh;
             const int new_start = same ? max(b.q0, last_q + 1) : b.q0;
             const uint32_t next_seq = have ? last_seq + 1 : 0;
-            constexpr int kG = 2;
-            for (int q0 = b.q0; q0 <= b.q1; q0 += kG) {
-                const int ng = min(kG, b.q1 - q0 + 1);
-                uint64_t bd[kG];
-                uint32_t dt[kG];
+            // chunks are issued as soon as their TMEM slot is free; a chunk whose successor's slot
+            // (and K chunk) are ready too is paired with it (independent accumulators hide the
+            // dependent-MMA latency of a lone chain)
+            auto seq_of = [&](int q) {
+                return (same && q <= last_q) ? last_seq - (uint32_t)(last_q - q) : next_seq + (uint32_t)(q - new_start);
+            };
+            for (int q = b.q0; q <= b.q1;) {
+                const uint32_t sq0 = seq_of(q);
+                mbar_wait(&s.k_full[sq0 % a.NSK], (sq0 / a.NSK) & 1);
+                mbar_wait(&s.t_empty[tseq % NST], ((tseq / NST) & 1) ^ 1);
+                int ng = 1;
+                if (q + 1 <= b.q1) {
+                    const uint32_t sq1 = seq_of(q + 1), t1 = tseq + 1;
+                    bool ok = mbar_test(&s.k_full[sq1 % a.NSK], (sq1 / a.NSK) & 1) &&
+                              mbar_test(&s.t_empty[t1 % NST], ((t1 / NST) & 1) ^ 1);
+                    ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
+                    if (ok) ng = 2;
+                }
+                uint64_t bd[2];
+                uint32_t dt[2];
 #pragma unroll
-                for (int c = 0; c < kG; ++c) {
-                    if (c < ng) {
-                        const int q = q0 + c;
-                        const uint32_t seq = (same && q <= last_q) ? last_seq - (uint32_t)(last_q - q)
-                                                                   : next_seq + (uint32_t)(q - new_start);
-                        const int sl = seq % a.NSK;
-                        mbar_wait(&s.k_full[sl], (seq / a.NSK) & 1);
-                        const uint32_t tq = tseq + c;
-                        mbar_wait(&s.t_empty[tq % NST], ((tq / NST) & 1) ^ 1);
-                        bd[c] = make_desc(smem_u32(s.K + (size_t)sl * chk_bytes), 128, sbo);
-                        dt[c] = tbase + (uint32_t)((tq % NST) * kCR);
-                    }
+                for (int c = 0; c < 2; ++c) {
+                    const uint32_t sq = seq_of(q + c);
+                    bd[c] = make_desc(smem_u32(s.K + (size_t)(sq % a.NSK) * chk_bytes), 128, sbo);
+                    dt[c] = tbase + (uint32_t)(((tseq + c) % NST) * kCR);
                 }
                 tc_fence_after();
                 if (elect_one()) {
                     for (int kk = 0; kk < ksteps; ++kk) {
 #pragma unroll
-                        for (int c = 0; c < kG; ++c)
+                        for (int c = 0; c < 2; ++c)
                             if (c < ng && (kk == 0 || !(a.dbg & 2)))
                                 mma_bf16(dt[c], ad0 + (uint64_t)(kk * 16), bd[c] + (uint64_t)(kk * 16), idesc, kk > 0);
                     }
 #pragma unroll
-                    for (int c = 0; c < kG; ++c)
+                    for (int c = 0; c < 2; ++c)
                         if (c < ng) tc_commit(&s.t_full[(tseq + c) % NST]);
                 }
                 __syncwarp();
                 tseq += ng;
+                q += ng;
             }
             if (elect_one()) tc_commit(&s.a_empty[ab]);
             __syncwarp();
@@ -286,157 +294,415 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float
         }
     } else {
         // ------------------------------------------------------------ epilogue
-        const int ew = warp - 2;
-        const int qd = warp & 3;       // TMEM lane quadrant (warp_id % 4)
-        const int part = ew >> 2;      // column part 0..3
-        const int r = qd * 32 + lane;  // row inside the block
+        // 24 warps: warp % 4 = TMEM lane quadrant; g = (warp - 2) / 4 in 0..5 picks the 16-lane half
+        // (g & 1) of the quadrant and the sub-warp k = g >> 1 of that half.  A half's band union is
+        // cut into 32-column slices; sub-warp k takes slices s_lo + k, s_lo + k + 3, ... (3 of the 9
+        // slices of an interior config-4 block).  Tiles are read with tcgen05.ld.16x256b: thread
+        // t holds rows t1 = t >> 2 and t1 + 8 and columns 8m + 2 t0 + {0, 1} (t0 = t & 3), so a
+        // column sum is an in-thread sum over two rows plus a 3-stage butterfly over t1.
+        const int qd = warp & 3;
+        const int g6 = (warp - 2) >> 2;
+        const int half = g6 & 1;
+        const int sub = g6 >> 1;
+        const int t0 = lane & 3, t1 = lane >> 2;
+        const int rbase = qd * 32 + half * 16;
+        const int ra = rbase + t1, rb = ra + 8;   // the thread's two rows (inside the block)
         const int et = threadIdx.x - 64;
+        const float2 c2v = make_float2(a.c2, a.c2);
         uint32_t tseq = 0;
         for (int gi = g_begin; gi < g_end; ++gi) {
             const Blk b = fblock_of(a, s.wl[gi - g_begin]);
-            const int par = (gi - g_begin) & 1;
             const int vs = (gi - g_begin) % kNV;
             mbar_wait(&s.v_full[vs], ((gi - g_begin) / kNV) & 1);
             const float* vw = s.vwin + (size_t)vs * (a.maxwin + 128);
             const int wbase = b.q0 * kCR - a.shift;
             const int nch = b.q1 - b.q0 + 1;
-            const int i = b.i0 + r;
-            const float so = vw[a.maxwin + r];
-            const bool active = i < a.L_own && so != -INFINITY;
-            const float o = (!kFirst && active) ? so : 0.f;
-            const int lo = i - a.w - wbase;                // band of this lane, window coordinates
-            const int wlo = b.i0 + qd * 32 - a.w - wbase;  // union over the warp
-            const int whi = wlo + 31 + 2 * a.w;
-            const int ilo = wlo + 31, ihi = wlo + 2 * a.w;  // intersection over the warp
-            // ---- row pass: e = ex2(s2 + v + o), written back over S (later steps)
-            // kRec: the column pass recomputes e instead (the cold start always does: its online
-            // per-part max would leave earlier slices relative to a stale max)
-            constexpr bool kRec = kRecompute || kFirst;
-            float acc0 = 0.f, acc1 = 0.f, M = -INFINITY;
-            for (int q = 0; q < nch; ++q) {
-                const int ts = (tseq + q) % NST;
-                mbar_wait(&s.t_full[ts], ((tseq + q) / NST) & 1);
-                tc_fence_after();
-                const int c0 = q * kCR + part * HC;
-                const bool any = !(whi < c0 || wlo > c0 + HC - 1);
-                if (!any) continue;
-                const bool inner = (c0 >= ilo) && (c0 + HC - 1 <= ihi);
-                const uint32_t taddr = tbase + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ts * kCR + part * HC);
-                float v[32];
-                tc_ld32(taddr, v);
-                tc_wait_ld();
-                if (a.dbg & 1) {  // ablation: no row math
-                } else if (!active) {  // no early exit: tcgen05.st below is warp-collective
+            const int nsl = nch * kSlc;
+            int ib[2];
+            bool act[2];
+            float ov[2];
+            int lov[2];
 #pragma unroll
-                    for (int cc = 0; cc < HC; ++cc) v[cc] = 0.f;
-                } else if (kFirst) {
-                    float m = -INFINITY;
-#pragma unroll
-                    for (int cc = 0; cc < HC; ++cc) {
-                        const int c = c0 + cc;
-                        const float x = fmaf(v[cc], a.c2, vw[c]);
-                        v[cc] = ((unsigned)(c - lo) <= (unsigned)(2 * a.w)) ? x : -INFINITY;
-                        m = fmaxf(m, v[cc]);
-                    }
-                    if (m > M) {
-                        const float sc = (M == -INFINITY) ? 0.f : ex2(M - m);
-                        acc0 *= sc;
-                        acc1 *= sc;
-                        M = m;
-                    }
-                    if (M != -INFINITY) {
-#pragma unroll
-                        for (int cc = 0; cc < HC; cc += 2) {
-                            acc0 += ex2(v[cc] - M);
-                            acc1 += ex2(v[cc + 1] - M);
-                        }
-                    }
-                } else if (inner) {
-#pragma unroll
-                    for (int cc = 0; cc < HC; cc += 4) {
-                        const float4 w4 = *reinterpret_cast<const float4*>(vw + c0 + cc);
-                        v[cc + 0] = ex2(fmaf(v[cc + 0], a.c2, w4.x) + o);
-                        v[cc + 1] = ex2(fmaf(v[cc + 1], a.c2, w4.y) + o);
-                        v[cc + 2] = ex2(fmaf(v[cc + 2], a.c2, w4.z) + o);
-                        v[cc + 3] = ex2(fmaf(v[cc + 3], a.c2, w4.w) + o);
-                        acc0 += v[cc + 0] + v[cc + 2];
-                        acc1 += v[cc + 1] + v[cc + 3];
-                    }
-                } else {
-#pragma unroll
-                    for (int cc = 0; cc < HC; ++cc) {
-                        const int c = c0 + cc;
-                        float x = fmaf(v[cc], a.c2, vw[c]) + o;
-                        x = ((unsigned)(c - lo) <= (unsigned)(2 * a.w)) ? x : -INFINITY;
-                        v[cc] = ex2(x);
-                        if (cc & 1) acc1 += v[cc];
-                        else acc0 += v[cc];
-                    }
-                }
-                if (!kRec) tc_st32(taddr, v);
+            for (int h = 0; h < 2; ++h) {
+                const int rr = h ? rb : ra;
+                ib[h] = b.i0 + rr;
+                const float so = vw[a.maxwin + rr];
+                act[h] = ib[h] < a.L_own && so != -INFINITY;
+                ov[h] = (!kFirst && act[h]) ? so : 0.f;
+                lov[h] = ib[h] - a.w - wbase;               // band start of the row, window coordinates
             }
-            if (!kRec) tc_wait_st();
-            // ---- row sums: combine the 4 column parts in fixed order
-            float* rp = s.rowp + (size_t)par * 2 * kParts * 128;
-            rp[part * 128 + r] = acc0 + acc1;
-            if (kFirst) rp[(kParts + part) * 128 + r] = M;
-            named_bar(2, NE);
-            float rsum = 0.f, Mall = -INFINITY;
-            if (kFirst) {
+            const float2 o2a = make_float2(ov[0], ov[0]), o2b = make_float2(ov[1], ov[1]);
+            const int wlo = b.i0 + rbase - a.w - wbase;     // union over the half's 16 rows
+            const int whi = wlo + 15 + 2 * a.w;
+            const int ilo = wlo + 15, ihi = wlo + 2 * a.w;  // intersection
+            const int s_lo = wlo < 0 ? 0 : (wlo >> 5);
+            const int s_hi = min(nsl - 1, whi >> 5);
+            if (!kFirst && !kRecompute && a.w == 128 && nch == 3 && wbase == b.i0 - 128 && a.dbg == 0) {
+                // ================= interior block, w = 128: 3 chunks, the half's band union is the 9
+                // slices qd .. qd + 8 (window column of row r's band start = r); sub-warp k owns slices
+                // qd + k + 3j (j < 3), of which qd and qd + 8 are the only partial (edge) ones.
+                // Inactive rows carry o = -inf, so every exponential of theirs is 0 without a branch.
+                const float oa = act[0] ? ov[0] : -INFINITY, ob = act[1] ? ov[1] : -INFINITY;
+                const float2 oa2 = make_float2(oa, oa), ob2 = make_float2(ob, ob);
+                const uint32_t tl = tbase + ((uint32_t)rbase << 16);
+                float2 acc_a = make_float2(0.f, 0.f), acc_b = make_float2(0.f, 0.f);
+                int waited = -1;
 #pragma unroll
-                for (int p = 0; p < kParts; ++p) Mall = fmaxf(Mall, rp[(kParts + p) * 128 + r]);
+                for (int j = 0; j < 3; ++j) {
+                    const int sl = qd + sub + 3 * j;
+                    const int q = sl >> 2;
+                    const int ts = (tseq + q) & (NST - 1);
+                    if (q > waited) {
+                        mbar_wait(&s.t_full[ts], ((tseq + q) / NST) & 1);
+                        tc_fence_after();
+                        waited = q;
+                    }
+                    const uint32_t taddr = tl + (uint32_t)(ts * kCR + (sl & 3) * 32);
+                    float x[16];
+                    tc_ld16x256(taddr, x);
+                    const float* vp = vw + sl * 32 + 2 * t0;
+                    float2 vv[4];
 #pragma unroll
-                for (int p = 0; p < kParts; ++p) {
-                    const float Mp = rp[(kParts + p) * 128 + r];
-                    rsum += (Mp == -INFINITY) ? 0.f : rp[p * 128 + r] * ex2(Mp - Mall);
-                }
-            } else {
-#pragma unroll
-                for (int p = 0; p < kParts; ++p) rsum += rp[p * 128 + r];
-            }
-            float u = 0.f, wgt = 0.f;
-            if (active) {
-                u = kFirst ? (-Mall - lg2(rsum)) : (o - lg2(rsum));
-                if (!(rsum > 0.f) || !isfinite(u)) {
-                    atomicOr(a.err, 4);
-                    u = 0.f;
-                } else {
-                    wgt = 1.f / rsum;
-                }
-            }
-            if (part == 0 && i < a.L_own) {
-                a.out_own[(size_t)b.bh * a.Lr_own + i] = u;
-                a.pad_own[(size_t)b.bh * a.pad_ld_own + a.pad_off + i] = active ? u : -INFINITY;
-            }
-            // ---- column pass: c_Ij = sum_i e_ij / r_i over the warp's 32 rows, per column
-            const float off = kFirst ? -Mall : o;
-            float* cp = s.colp + (size_t)par * 4 * a.maxwin + (size_t)qd * a.maxwin;
-            for (int q = 0; q < nch; ++q) {
-                const int ts = (tseq + q) % NST;
-                const int c0 = q * kCR + part * HC;
-                const bool any = !(whi < c0 || wlo > c0 + HC - 1);
-                float val = 0.f;
-                if (any) {
-                    tc_fence_after();
-                    const uint32_t taddr = tbase + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ts * kCR + part * HC);
-                    float v[32];
-                    tc_ld32(taddr, v);
+                    for (int mm = 0; mm < 4; ++mm) vv[mm] = *reinterpret_cast<const float2*>(vp + 8 * mm);
                     tc_wait_ld();
-                    if (kRec) {
+                    const bool edge = (j == 0 && sub == 0) || (j == 2 && sub == 2);
+                    if (edge) {  // band check: window column - row in [0, 2w]
+                        const int cb = sl * 32 + 2 * t0;
 #pragma unroll
-                        for (int cc = 0; cc < HC; ++cc) {
-                            const int c = c0 + cc;
-                            float x = fmaf(v[cc], a.c2, vw[c]) + off;
-                            x = ((unsigned)(c - lo) <= (unsigned)(2 * a.w) && active) ? x : -INFINITY;
-                            v[cc] = ex2(x) * wgt;
+                        for (int mm = 0; mm < 4; ++mm) {
+                            float2 za = __ffma2_rn(make_float2(x[4 * mm], x[4 * mm + 1]), c2v, __fadd2_rn(vv[mm], oa2));
+                            float2 zb = __ffma2_rn(make_float2(x[4 * mm + 2], x[4 * mm + 3]), c2v, __fadd2_rn(vv[mm], ob2));
+                            const int c = cb + 8 * mm;
+                            za.x = (unsigned)(c - ra) <= 256u ? za.x : -INFINITY;
+                            za.y = (unsigned)(c + 1 - ra) <= 256u ? za.y : -INFINITY;
+                            zb.x = (unsigned)(c - rb) <= 256u ? zb.x : -INFINITY;
+                            zb.y = (unsigned)(c + 1 - rb) <= 256u ? zb.y : -INFINITY;
+                            x[4 * mm] = ex2(za.x);
+                            x[4 * mm + 1] = ex2(za.y);
+                            x[4 * mm + 2] = ex2(zb.x);
+                            x[4 * mm + 3] = ex2(zb.y);
+                            acc_a = __fadd2_rn(acc_a, make_float2(x[4 * mm], x[4 * mm + 1]));
+                            acc_b = __fadd2_rn(acc_b, make_float2(x[4 * mm + 2], x[4 * mm + 3]));
                         }
                     } else {
 #pragma unroll
-                        for (int cc = 0; cc < HC; ++cc) v[cc] *= wgt;
+                        for (int mm = 0; mm < 4; ++mm) {
+                            const float2 za = __ffma2_rn(make_float2(x[4 * mm], x[4 * mm + 1]), c2v, __fadd2_rn(vv[mm], oa2));
+                            const float2 zb = __ffma2_rn(make_float2(x[4 * mm + 2], x[4 * mm + 3]), c2v, __fadd2_rn(vv[mm], ob2));
+                            x[4 * mm] = ex2(za.x);
+                            x[4 * mm + 1] = ex2(za.y);
+                            x[4 * mm + 2] = ex2(zb.x);
+                            x[4 * mm + 3] = ex2(zb.y);
+                            acc_a = __fadd2_rn(acc_a, make_float2(x[4 * mm], x[4 * mm + 1]));
+                            acc_b = __fadd2_rn(acc_b, make_float2(x[4 * mm + 2], x[4 * mm + 3]));
+                        }
                     }
-                    val = (a.dbg & 4) ? v[0] : colsum32(v, lane);
+                    tc_st16x256(taddr, x);
                 }
-                cp[c0 + lane] = val;
+                tc_wait_st();
+                float sa = acc_a.x + acc_a.y, sb = acc_b.x + acc_b.y;
+                sa += __shfl_xor_sync(0xffffffffu, sa, 1);
+                sb += __shfl_xor_sync(0xffffffffu, sb, 1);
+                sa += __shfl_xor_sync(0xffffffffu, sa, 2);
+                sb += __shfl_xor_sync(0xffffffffu, sb, 2);
+                if (t0 == 0) {
+                    s.rowp[sub * 128 + ra] = sa;
+                    s.rowp[sub * 128 + rb] = sb;
+                }
+                named_bar(2, NE);
+                float ra_sum = 0.f, rb_sum = 0.f;
+#pragma unroll
+                for (int p = 0; p < kPH; ++p) {
+                    ra_sum += s.rowp[p * 128 + ra];
+                    rb_sum += s.rowp[p * 128 + rb];
+                }
+                float wa_ = 0.f, wb_ = 0.f;
+                {
+                    float ua = 0.f, ub = 0.f;
+                    if (act[0]) {
+                        ua = ov[0] - lg2(ra_sum);
+                        if (!(ra_sum > 0.f) || !isfinite(ua)) { atomicOr(a.err, 4); ua = 0.f; } else wa_ = 1.f / ra_sum;
+                    }
+                    if (act[1]) {
+                        ub = ov[1] - lg2(rb_sum);
+                        if (!(rb_sum > 0.f) || !isfinite(ub)) { atomicOr(a.err, 4); ub = 0.f; } else wb_ = 1.f / rb_sum;
+                    }
+                    if (sub == 0 && t0 == 0) {
+                        const size_t uo = (size_t)b.bh * a.Lr_own, po = (size_t)b.bh * a.pad_ld_own + a.pad_off;
+                        if (ib[0] < a.L_own) {
+                            a.out_own[uo + ib[0]] = ua;
+                            a.pad_own[po + ib[0]] = act[0] ? ua : -INFINITY;
+                        }
+                        if (ib[1] < a.L_own) {
+                            a.out_own[uo + ib[1]] = ub;
+                            a.pad_own[po + ib[1]] = act[1] ? ub : -INFINITY;
+                        }
+                    }
+                }
+                const float2 wa2 = make_float2(wa_, wa_), wb2 = make_float2(wb_, wb_);
+                float* cp = s.colp + (size_t)(qd * 2 + half) * a.maxwin;
+                const int ccol = 16 * ((lane >> 4) & 1) + 8 * ((lane >> 3) & 1) + 2 * t0 + ((lane >> 2) & 1);
+                const bool u4 = (lane & 16) != 0, u3 = (lane & 8) != 0, u2 = (lane & 4) != 0;
+                // the half's 3 slices outside its union (0 .. qd-1, qd+9 .. 11): one per sub-warp
+                cp[32 * (sub < qd ? sub : sub + 9) + ccol] = 0.f;
+                int rel = 0;  // chunks released by this warp so far
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    const int sl = qd + sub + 3 * j;
+                    const int q = sl >> 2;
+                    for (; rel < q; ++rel) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&s.t_empty[(tseq + rel) & (NST - 1)]);
+                    }
+                    const uint32_t taddr = tl + (uint32_t)(((tseq + q) & (NST - 1)) * kCR + (sl & 3) * 32);
+                    tc_fence_after();
+                    float x[16];
+                    tc_ld16x256(taddr, x);
+                    tc_wait_ld();
+                    float y[8];
+#pragma unroll
+                    for (int mm = 0; mm < 4; ++mm) {
+                        const float2 pr = __ffma2_rn(make_float2(x[4 * mm + 2], x[4 * mm + 3]), wb2,
+                                                     __fmul2_rn(make_float2(x[4 * mm], x[4 * mm + 1]), wa2));
+                        y[2 * mm] = pr.x;
+                        y[2 * mm + 1] = pr.y;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const float send = u4 ? y[k] : y[k + 4];
+                        const float keep = u4 ? y[k + 4] : y[k];
+                        y[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                    }
+#pragma unroll
+                    for (int k = 0; k < 2; ++k) {
+                        const float send = u3 ? y[k] : y[k + 2];
+                        const float keep = u3 ? y[k + 2] : y[k];
+                        y[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                    }
+                    const float send = u2 ? y[0] : y[1];
+                    const float keep = u2 ? y[1] : y[0];
+                    cp[sl * 32 + ccol] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+                }
+                for (; rel < 3; ++rel) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&s.t_empty[(tseq + rel) & (NST - 1)]);
+                }
+                tseq += 3;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s.v_empty[vs]);
+                named_bar(2, NE);
+                float* dst = part_out + ((size_t)b.bh * a.NB + b.blk) * a.maxwin;
+                if (et < 3 * kCR) {
+                    float sum = 0.f;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) sum += s.colp[(size_t)k * a.maxwin + et];
+                    dst[et] = sum;
+                }
+                continue;
+            }
+            // ---- row pass: e = ex2(s2 + v + o), written back over S (later steps; kRec: not stored,
+            // the column pass recomputes -- always so for the cold start, whose online max would
+            // leave earlier slices relative to a stale max)
+            constexpr bool kRec = kRecompute || kFirst;
+            float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+            float Mx[2] = {-INFINITY, -INFINITY};
+            int waited = -1;
+            for (int sl = s_lo + sub; sl <= s_hi; sl += kPH) {
+                const int q = sl >> 2;
+                const int ts = (tseq + q) % NST;
+                if (q > waited) {
+                    mbar_wait(&s.t_full[ts], ((tseq + q) / NST) & 1);
+                    tc_fence_after();
+                    waited = q;
+                }
+                const int c0 = sl * 32;
+                const bool inner = (c0 >= ilo) && (c0 + 31 <= ihi);
+                const uint32_t taddr = tbase + ((uint32_t)rbase << 16) + (uint32_t)(ts * kCR + (sl & 3) * 32);
+                float x[16];
+                tc_ld16x256(taddr, x);
+                tc_wait_ld();
+                if (a.dbg & 1) {
+                } else if (kFirst) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        float y[8];
+                        float m = -INFINITY;
+#pragma unroll
+                        for (int mm = 0; mm < 4; ++mm)
+#pragma unroll
+                            for (int c = 0; c < 2; ++c) {
+                                const int col = c0 + 8 * mm + 2 * t0 + c;
+                                const float z = fmaf(x[4 * mm + 2 * h + c], a.c2, vw[col]);
+                                y[2 * mm + c] = (act[h] && (unsigned)(col - lov[h]) <= (unsigned)(2 * a.w)) ? z : -INFINITY;
+                                m = fmaxf(m, y[2 * mm + c]);
+                            }
+                        if (m > Mx[h]) {
+                            const float sc = (Mx[h] == -INFINITY) ? 0.f : ex2(Mx[h] - m);
+                            acc[h].x *= sc;
+                            acc[h].y *= sc;
+                            Mx[h] = m;
+                        }
+                        if (Mx[h] != -INFINITY) {
+#pragma unroll
+                            for (int k = 0; k < 8; k += 2) {
+                                acc[h].x += ex2(y[k] - Mx[h]);
+                                acc[h].y += ex2(y[k + 1] - Mx[h]);
+                            }
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int mm = 0; mm < 4; ++mm) {
+                        const float2 vv = *reinterpret_cast<const float2*>(vw + c0 + 8 * mm + 2 * t0);
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            float2 z = __ffma2_rn(make_float2(x[4 * mm + 2 * h], x[4 * mm + 2 * h + 1]), c2v,
+                                                  __fadd2_rn(vv, h ? o2b : o2a));
+                            if (!inner || !act[h]) {
+                                const int col = c0 + 8 * mm + 2 * t0;
+                                z.x = (act[h] && (unsigned)(col - lov[h]) <= (unsigned)(2 * a.w)) ? z.x : -INFINITY;
+                                z.y = (act[h] && (unsigned)(col + 1 - lov[h]) <= (unsigned)(2 * a.w)) ? z.y : -INFINITY;
+                            }
+                            const float2 e = make_float2(ex2(z.x), ex2(z.y));
+                            x[4 * mm + 2 * h] = e.x;
+                            x[4 * mm + 2 * h + 1] = e.y;
+                            acc[h] = __fadd2_rn(acc[h], e);
+                        }
+                    }
+                }
+                if (!kRec) tc_st16x256(taddr, x);
+            }
+            if (!kRec) tc_wait_st();
+            // ---- row sums: over t0 (4 threads share a row), then over the 3 sub-warps in fixed order
+            float rs[2], rm[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float sm = acc[h].x + acc[h].y, M = Mx[h];
+#pragma unroll
+                for (int o = 1; o <= 2; o <<= 1) {
+                    const float s2 = __shfl_xor_sync(0xffffffffu, sm, o);
+                    if (kFirst) {
+                        const float M2 = __shfl_xor_sync(0xffffffffu, M, o);
+                        const float Mn = fmaxf(M, M2);
+                        sm = (M == -INFINITY ? 0.f : sm * ex2(M - Mn)) + (M2 == -INFINITY ? 0.f : s2 * ex2(M2 - Mn));
+                        M = Mn;
+                    } else {
+                        sm += s2;
+                    }
+                }
+                rs[h] = sm;
+                rm[h] = M;
+            }
+            if (t0 == 0) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int rr = h ? rb : ra;
+                    s.rowp[sub * 128 + rr] = rs[h];
+                    if (kFirst) s.rowp[(kPH + sub) * 128 + rr] = rm[h];
+                }
+            }
+            named_bar(2, NE);
+            float wgt[2], Mall[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int rr = h ? rb : ra;
+                float rsum = 0.f, Ma = -INFINITY;
+                if (kFirst) {
+#pragma unroll
+                    for (int p = 0; p < kPH; ++p) Ma = fmaxf(Ma, s.rowp[(kPH + p) * 128 + rr]);
+#pragma unroll
+                    for (int p = 0; p < kPH; ++p) {
+                        const float Mp = s.rowp[(kPH + p) * 128 + rr];
+                        rsum += (Mp == -INFINITY) ? 0.f : s.rowp[p * 128 + rr] * ex2(Mp - Ma);
+                    }
+                } else {
+#pragma unroll
+                    for (int p = 0; p < kPH; ++p) rsum += s.rowp[p * 128 + rr];
+                }
+                float u = 0.f;
+                wgt[h] = 0.f;
+                Mall[h] = Ma;
+                if (act[h]) {
+                    u = kFirst ? (-Ma - lg2(rsum)) : (ov[h] - lg2(rsum));
+                    if (!(rsum > 0.f) || !isfinite(u)) {
+                        atomicOr(a.err, 4);
+                        u = 0.f;
+                    } else {
+                        wgt[h] = 1.f / rsum;
+                    }
+                }
+                if (sub == 0 && t0 == 0 && ib[h] < a.L_own) {
+                    a.out_own[(size_t)b.bh * a.Lr_own + ib[h]] = u;
+                    a.pad_own[(size_t)b.bh * a.pad_ld_own + a.pad_off + ib[h]] = act[h] ? u : -INFINITY;
+                }
+            }
+            // ---- column pass: c_Ij = sum_i e_ij / r_i over the half's 16 rows, per column.  Every
+            // slice of the window is written by exactly one sub-warp of the half (zeros outside the
+            // union); a chunk's TMEM slot is released by each warp once it is done with that chunk.
+            const float2 wa = make_float2(wgt[0], wgt[0]), wb = make_float2(wgt[1], wgt[1]);
+            float* cp = s.colp + (size_t)(qd * 2 + half) * a.maxwin;
+            const int ph = (((s_lo + sub) % kPH) + kPH) % kPH;
+            const int ccol = 16 * ((lane >> 4) & 1) + 8 * ((lane >> 3) & 1) + 2 * t0 + ((lane >> 2) & 1);
+            for (int q = 0; q < nch; ++q) {
+                const int ts = (tseq + q) % NST;
+#pragma unroll
+                for (int j = 0; j < kSlc; ++j) {
+                    const int sl = q * kSlc + j;
+                    if (sl % kPH != ph) continue;
+                    const int c0 = sl * 32;
+                    float val = 0.f;
+                    if (sl >= s_lo && sl <= s_hi) {
+                        tc_fence_after();
+                        const uint32_t taddr = tbase + ((uint32_t)rbase << 16) + (uint32_t)(ts * kCR + j * 32);
+                        float x[16];
+                        tc_ld16x256(taddr, x);
+                        tc_wait_ld();
+                        if (kRec) {
+#pragma unroll
+                            for (int mm = 0; mm < 4; ++mm)
+#pragma unroll
+                                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                                    for (int c = 0; c < 2; ++c) {
+                                        const int col = c0 + 8 * mm + 2 * t0 + c;
+                                        float z = fmaf(x[4 * mm + 2 * h + c], a.c2, vw[col]) + (kFirst ? -Mall[h] : ov[h]);
+                                        z = (act[h] && (unsigned)(col - lov[h]) <= (unsigned)(2 * a.w)) ? z : -INFINITY;
+                                        x[4 * mm + 2 * h + c] = ex2(z);
+                                    }
+                        }
+                        float y[8];
+#pragma unroll
+                        for (int mm = 0; mm < 4; ++mm) {
+                            const float2 p = __ffma2_rn(make_float2(x[4 * mm + 2], x[4 * mm + 3]), wb,
+                                                        __fmul2_rn(make_float2(x[4 * mm], x[4 * mm + 1]), wa));
+                            y[2 * mm] = p.x;
+                            y[2 * mm + 1] = p.y;
+                        }
+                        if (a.dbg & 4) {
+                            val = y[0];
+                        } else {
+                            const bool u4 = (lane & 16) != 0, u3 = (lane & 8) != 0, u2 = (lane & 4) != 0;
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const float send = u4 ? y[k] : y[k + 4];
+                                const float keep = u4 ? y[k + 4] : y[k];
+                                y[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                            }
+#pragma unroll
+                            for (int k = 0; k < 2; ++k) {
+                                const float send = u3 ? y[k] : y[k + 2];
+                                const float keep = u3 ? y[k + 2] : y[k];
+                                y[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                            }
+                            const float send = u2 ? y[0] : y[1];
+                            const float keep = u2 ? y[1] : y[0];
+                            val = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+                        }
+                    }
+                    cp[c0 + ccol] = val;
+                }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s.t_empty[ts]);
@@ -445,11 +711,14 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.v_empty[vs]);  // window duals no longer needed
             named_bar(2, NE);
-            // ---- combine the 4 lane quadrants in fixed order; store the block's column partials
-            const float* cb = s.colp + (size_t)par * 4 * a.maxwin;
+            // ---- combine the 8 half-quadrant partials in fixed order; store the block's column partials
             float* dst = part_out + ((size_t)b.bh * a.NB + b.blk) * a.maxwin;
-            for (int c = et; c < nch * kCR; c += NE)
-                dst[c] = ((cb[c] + cb[a.maxwin + c]) + cb[2 * a.maxwin + c]) + cb[3 * a.maxwin + c];
+            for (int c = et; c < nch * kCR; c += NE) {
+                float sum = 0.f;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) sum += s.colp[(size_t)k * a.maxwin + c];
+                dst[c] = sum;
+            }
         }
     }
     tc_fence_before();
@@ -505,7 +774,7 @@ long long fstep16_launch_count(bool reset) {
 size_t fstep16_smem_bytes(const PhaseArgs& a) {
     const int nst = 512 / a.CR;
     return (size_t)a.NA * 128 * a.row_bytes + (size_t)a.NSK * a.CR * a.row_bytes +
-           (size_t)(kNV * (a.maxwin + 128) + 2 * 2 * kParts * 128 + 2 * 4 * a.maxwin) * 4 +
+           (size_t)(kNV * (a.maxwin + 128) + 2 * kPH * 128 + 8 * a.maxwin) * 4 +
            (size_t)(2 * kNV + 2 * a.NA + 2 * a.NSK + 2 * nst) * 8 + 16 + (size_t)a.wl_cap * 4;
 }
 
