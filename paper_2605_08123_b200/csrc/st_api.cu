@@ -249,6 +249,33 @@ void phase_trace_dump(const unsigned long long* dbuf) {
     }
 }
 
+// Development timeline of one k_fstep16 launch (ST_TRACE_FSTEP=<step>): per-block globaltimer stamps
+// of the MMA warp and of epilogue warp 2 for the first 8 blocks of CTAs 0..3, printed to stderr.
+unsigned long long* fstep_trace_begin(long t, cudaStream_t st) {
+    static unsigned long long* buf = nullptr;
+    const char* e = getenv("ST_TRACE_FSTEP");
+    if (!e || t != atol(e)) return nullptr;
+    if (!buf && cudaMalloc(&buf, 4 * 64 * 8) != cudaSuccess) return nullptr;
+    cudaMemsetAsync(buf, 0, 4 * 64 * 8, st);
+    return buf;
+}
+void fstep_trace_dump(const unsigned long long* dbuf) {
+    unsigned long long h[4 * 64];
+    if (cudaMemcpy(h, dbuf, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return;
+    for (int c = 0; c < 4; ++c) {
+        const unsigned long long t0 = h[c * 64 + 57];
+        fprintf(stderr, "CTA %d end %lld ns  blk4 rounds: %lld %lld | %lld %lld | %lld %lld\n", c, (long long)(h[c * 64] - t0),
+                (long long)(h[c * 64 + 58] - t0), (long long)(h[c * 64 + 59] - t0), (long long)(h[c * 64 + 60] - t0),
+                (long long)(h[c * 64 + 61] - t0), (long long)(h[c * 64 + 62] - t0), (long long)(h[c * 64 + 63] - t0));
+        for (int k = 0; k < 8; ++k)
+            fprintf(stderr, "  blk %d mma %6lld-%6lld  epi start %6lld vfull %6lld rowend %6lld colend %6lld bar %6lld\n", k,
+                    (long long)(h[c * 64 + 1 + k] - t0), (long long)(h[c * 64 + 9 + k] - t0),
+                    (long long)(h[c * 64 + 17 + k] - t0), (long long)(h[c * 64 + 25 + k] - t0),
+                    (long long)(h[c * 64 + 33 + k] - t0), (long long)(h[c * 64 + 41 + k] - t0),
+                    (long long)(h[c * 64 + 49 + k] - t0));
+    }
+}
+
 WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
     WsLayout w;
     size_t o = 0;
@@ -586,7 +613,9 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
                 float* v_out = (sv && r >= 0 && r < sl.ns) ? slot_v(r) : v_ws;
                 pf.c2 = g.c2 * step_scale(desc, t);
                 pf.out_own = u_out;
+                pf.trace = fstep_trace_begin(t, st);
                 ST_CUDA(st::launch_fstep16(pf, fpart, t == 1, grid, st));
+                if (pf.trace) fstep_trace_dump(pf.trace);
                 ST_CUDA(st::launch_vmerge(fpart, pad_v, v_out, g.BH, g.H, g.Lq, g.Lk, g.Lrk, tp.NBq, tp.maxwin, g.w,
                                           tp.CR, tp.shift, tp.Lpk, pad_ld_k, tp.CR, col_mask, err, st));
                 u_prev = u_out;

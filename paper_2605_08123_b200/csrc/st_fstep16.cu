@@ -28,11 +28,13 @@
 //   warp 1   MMA issuer: M=128, N=CR, K=16 per instruction into a ring of
 //            512/CR TMEM slots; a block's chunks stay resident until its column
 //            pass released them
-//   warps 2..17  epilogue: 4 lane quadrants x 4 column parts (32 columns of every
-//            chunk each)
+//   warps 2..9   epilogue: one warp per 16-lane half of a TMEM lane quadrant; it owns
+//            whole rows (16 of them), so row sums need no cross-warp combine and the
+//            column pass follows the row pass without a CTA barrier
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "st_common.cuh"
 #include "st_phase.cuh"
@@ -45,16 +47,16 @@ using namespace sm100;
 namespace {
 
 constexpr int kNV = 3;     // dual-window ring slots
-constexpr int kPH = 3;     // epilogue warps per 16-lane half of a TMEM lane quadrant
-constexpr int kEW = 8 * kPH;  // epilogue warps
+constexpr int kEW = 16;    // epilogue warps: two per 16-lane half of a TMEM lane quadrant
 constexpr int kSlc = 4;    // 32-column slices per 128-column chunk
+constexpr int kG = 3;      // tiles per epilogue round (shared TMEM-load wait, interleaved math)
 
 struct FSmem {
     uint8_t* A;       // [NA][128 * row_bytes]
     uint8_t* K;       // [NSK][CR * row_bytes]
     float* vwin;      // [kNV][maxwin + 128]
-    float* rowp;      // [2][kPH][128]: row partial (sum, max) per sub-warp (one buffer: two barriers per block)
-    float* colp;      // [8][maxwin]: column partials per 16-lane half quadrant
+    float* colp;      // [2][8][maxwin]: column partials per 16-lane half quadrant, by block parity
+    float* rowx;      // [8][2][16]: row-sum exchange of the two warps of a half quadrant
     uint64_t* v_full;
     uint64_t* v_empty;
     uint64_t* a_full;
@@ -64,7 +66,7 @@ struct FSmem {
     uint64_t* t_full;
     uint64_t* t_empty;
     uint32_t* tmem_base;
-    int* wl;
+    int4* bd;         // [wl_cap] block descriptors of this CTA's work-list slice: (bh, blk, q0, q1)
 };
 
 __device__ __forceinline__ FSmem fcarve(uint8_t* base, const PhaseArgs& a, int nst) {
@@ -73,9 +75,9 @@ __device__ __forceinline__ FSmem fcarve(uint8_t* base, const PhaseArgs& a, int n
     s.A = base;
     s.K = s.A + (size_t)a.NA * blk;
     s.vwin = (float*)(s.K + (size_t)a.NSK * chk);
-    s.rowp = s.vwin + kNV * (a.maxwin + 128);
-    s.colp = s.rowp + 2 * kPH * 128;
-    uint64_t* bars = (uint64_t*)(s.colp + 8 * a.maxwin);
+    s.colp = s.vwin + kNV * (a.maxwin + 128);
+    s.rowx = s.colp + 2 * 8 * a.maxwin;
+    uint64_t* bars = (uint64_t*)(s.rowx + 8 * 2 * 16);
     s.v_full = bars;
     s.v_empty = bars + kNV;
     bars += 2 * kNV;
@@ -86,7 +88,7 @@ __device__ __forceinline__ FSmem fcarve(uint8_t* base, const PhaseArgs& a, int n
     s.t_full = s.k_empty + a.NSK;
     s.t_empty = s.t_full + nst;
     s.tmem_base = (uint32_t*)(s.t_empty + nst);
-    s.wl = (int*)(s.tmem_base + 4);
+    s.bd = (int4*)(s.tmem_base + 4);
     return s;
 }
 
@@ -103,6 +105,34 @@ __device__ __forceinline__ Blk fblock_of(const PhaseArgs& a, int g) {
     b.q1 = min(nq - 1, (b.i0 + 128 + a.w + a.shift + a.CR - 1) / a.CR - 1);
     return b;
 }
+
+__device__ __forceinline__ Blk bdesc(int4 d) {
+    Blk b;
+    b.bh = d.x;
+    b.blk = d.y;
+    b.i0 = d.y * 128;
+    b.q0 = d.z;
+    b.q1 = d.w;
+    return b;
+}
+
+__device__ __forceinline__ unsigned long long fgtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// development timeline (ST_TRACE_PHASE=<step>): trace[cta * 64 + slot] for CTAs 0..3
+#ifdef ST_FSTEP_TRACE
+#define FS_TRACE(slot) FS_TRACE_ON(slot)
+#else
+#define FS_TRACE(slot) \
+    do {               \
+    } while (0)
+#endif
+#define FS_TRACE_ON(slot)                                                                                 \
+    do {                                                                                               \
+        if (a.trace && blockIdx.x < 4 && (slot) < 64) a.trace[blockIdx.x * 64 + (slot)] = fgtimer(); \
+    } while (0)
 
 // Lane c of the warp returns sum over the 32 lanes of x[c] (x is destroyed):
 // a transpose butterfly, 31 shuffles per 32 x 32 tile, fixed association order.
@@ -158,20 +188,25 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float
     const int n = a.work ? *a.nwork : a.nwork_all;
     const int g_begin = (int)((long long)n * blockIdx.x / gridDim.x);
     const int g_end = min((int)((long long)n * (blockIdx.x + 1) / gridDim.x), g_begin + a.wl_cap);
-    for (int k = threadIdx.x; k < g_end - g_begin; k += blockDim.x) s.wl[k] = a.work ? a.work[g_begin + k] : g_begin + k;
+    for (int k = threadIdx.x; k < g_end - g_begin; k += blockDim.x) {
+        const int g = a.work ? a.work[g_begin + k] : g_begin + k;
+        const Blk b = fblock_of(a, g);
+        s.bd[k] = make_int4(b.bh, b.blk, b.q0, b.q1);
+    }
     if (threadIdx.x == 0 && (int)((long long)n * (blockIdx.x + 1) / gridDim.x) - g_begin > a.wl_cap)
         atomicOr(a.err, 16);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *s.tmem_base;
+    if (threadIdx.x == 0) FS_TRACE(57);
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
         int last_bh = -1, last_q = -1;
         uint32_t kseq = 0;
         for (int gi = g_begin; gi < g_end; ++gi) {
-            const Blk b = fblock_of(a, s.wl[gi - g_begin]);
+            const Blk b = bdesc(s.bd[gi - g_begin]);
             {
                 const int vs = (gi - g_begin) % kNV;
                 const uint32_t vn = (gi - g_begin) / kNV;
@@ -223,7 +258,7 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float
         uint32_t last_seq = 0, rel_seq = 0, tseq = 0;
         bool have = false;
         for (int gi = g_begin; gi < g_end; ++gi) {
-            const Blk b = fblock_of(a, s.wl[gi - g_begin]);
+            const Blk b = bdesc(s.bd[gi - g_begin]);
             const int ab = (gi - g_begin) % a.NA;
             const uint32_t an = (gi - g_begin) / a.NA;
             mbar_wait(&s.a_full[ab], an & 1);
@@ -238,6 +273,7 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float
             auto seq_of = [&](int q) {
                 return (same && q <= last_q) ? last_seq - (uint32_t)(last_q - q) : next_seq + (uint32_t)(q - new_start);
             };
+            if (lane == 0 && gi - g_begin < 8) FS_TRACE(1 + (gi - g_begin));
             for (int q = b.q0; q <= b.q1;) {
                 const uint32_t sq0 = seq_of(q);
                 mbar_wait(&s.k_full[sq0 % a.NSK], (sq0 / a.NSK) & 1);
@@ -276,6 +312,7 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float
             }
             if (elect_one()) tc_commit(&s.a_empty[ab]);
             __syncwarp();
+            if (lane == 0 && gi - g_begin < 8) FS_TRACE(9 + (gi - g_begin));
             if (b.q1 >= new_start) last_seq = next_seq + (uint32_t)(b.q1 - new_start);
             if (!same) last_q = -1;
             last_q = max(last_q, b.q1);
@@ -283,7 +320,7 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float
             have = true;
             uint32_t keep_from = last_seq + 1;
             if (gi + 1 < g_end) {
-                const Blk nb = fblock_of(a, s.wl[gi + 1 - g_begin]);
+                const Blk nb = bdesc(s.bd[gi + 1 - g_begin]);
                 if (nb.bh == last_bh && nb.q0 <= last_q) keep_from = last_seq - (uint32_t)(last_q - nb.q0);
             }
             if (elect_one()) {
@@ -294,435 +331,475 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float
         }
     } else {
         // ------------------------------------------------------------ epilogue
-        // 24 warps: warp % 4 = TMEM lane quadrant; g = (warp - 2) / 4 in 0..5 picks the 16-lane half
-        // (g & 1) of the quadrant and the sub-warp k = g >> 1 of that half.  A half's band union is
-        // cut into 32-column slices; sub-warp k takes slices s_lo + k, s_lo + k + 3, ... (3 of the 9
-        // slices of an interior config-4 block).  Tiles are read with tcgen05.ld.16x256b: thread
-        // t holds rows t1 = t >> 2 and t1 + 8 and columns 8m + 2 t0 + {0, 1} (t0 = t & 3), so a
-        // column sum is an in-thread sum over two rows plus a 3-stage butterfly over t1.
-        const int qd = warp & 3;
-        const int g6 = (warp - 2) >> 2;
-        const int half = g6 & 1;
-        const int sub = g6 >> 1;
+        // warp w (2..17): lane quadrant qd = w % 4, g = (w - 2) / 4: half hf = g & 1 -> rows rbase ..
+        // rbase + 15, part pt = g >> 1 (the two warps of a half split its slices).  Tiles of 16 rows x
+        // 32 columns are read with tcgen05.ld.16x256b: thread t holds rows rA = rbase + t1 and
+        // rB = rA + 8 and columns 8m + 2 t0 + {0, 1} (t0 = t & 3, t1 = t >> 2).
+        const int qd = warp & 3, hf = ((warp - 2) >> 2) & 1, pt = (warp - 2) >> 3;
+        const int hq = qd * 2 + hf;  // half-quadrant id (pair barrier 3 + hq)
         const int t0 = lane & 3, t1 = lane >> 2;
-        const int rbase = qd * 32 + half * 16;
-        const int ra = rbase + t1, rb = ra + 8;   // the thread's two rows (inside the block)
+        const int rbase = qd * 32 + hf * 16;
+        const int rA = rbase + t1, rB = rA + 8;
         const int et = threadIdx.x - 64;
+        const uint32_t tl = tbase + ((uint32_t)rbase << 16);
+        const int ccol = 16 * ((lane >> 4) & 1) + 8 * ((lane >> 3) & 1) + 2 * t0 + ((lane >> 2) & 1);
+        const bool u4 = (lane & 16) != 0, u3 = (lane & 8) != 0, u2 = (lane & 4) != 0;
         const float2 c2v = make_float2(a.c2, a.c2);
+        const int bandw = 2 * a.w;
+        constexpr bool kRec = kRecompute || kFirst;  // cold start: e recomputed in the column pass
         uint32_t tseq = 0;
         for (int gi = g_begin; gi < g_end; ++gi) {
-            const Blk b = fblock_of(a, s.wl[gi - g_begin]);
+            const Blk b = bdesc(s.bd[gi - g_begin]);
+            const int par = (gi - g_begin) & 1;
             const int vs = (gi - g_begin) % kNV;
-            mbar_wait(&s.v_full[vs], ((gi - g_begin) / kNV) & 1);
-            const float* vw = s.vwin + (size_t)vs * (a.maxwin + 128);
             const int wbase = b.q0 * kCR - a.shift;
             const int nch = b.q1 - b.q0 + 1;
             const int nsl = nch * kSlc;
-            int ib[2];
-            bool act[2];
-            float ov[2];
-            int lov[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int rr = h ? rb : ra;
-                ib[h] = b.i0 + rr;
-                const float so = vw[a.maxwin + rr];
-                act[h] = ib[h] < a.L_own && so != -INFINITY;
-                ov[h] = (!kFirst && act[h]) ? so : 0.f;
-                lov[h] = ib[h] - a.w - wbase;               // band start of the row, window coordinates
-            }
-            const float2 o2a = make_float2(ov[0], ov[0]), o2b = make_float2(ov[1], ov[1]);
-            const int wlo = b.i0 + rbase - a.w - wbase;     // union over the half's 16 rows
-            const int whi = wlo + 15 + 2 * a.w;
-            const int ilo = wlo + 15, ihi = wlo + 2 * a.w;  // intersection
+            const int iA = b.i0 + rA, iB = iA + 8;
+            const int loA = iA - a.w - wbase, loB = loA + 8;  // band start of each row, window coordinates
+            const int wlo = b.i0 + rbase - a.w - wbase;       // union over the warp's 16 rows
             const int s_lo = wlo < 0 ? 0 : (wlo >> 5);
-            const int s_hi = min(nsl - 1, whi >> 5);
+            const int s_hi = min(nsl - 1, (wlo + 15 + bandw) >> 5);
+            // tiles whose 32 columns lie in every row's band need no mask
+            const int in_lo = (wlo + 15 + 31) >> 5, in_hi = (wlo + bandw - 31) >> 5;  // ceil / floor (arithmetic shifts)
+            const bool trc = warp == 2 && lane == 0 && gi - g_begin < 8;
+            if (trc) FS_TRACE(17 + (gi - g_begin));
+            mbar_wait(&s.v_full[vs], ((gi - g_begin) / kNV) & 1);
+            if (trc) FS_TRACE(25 + (gi - g_begin));
+            const float* vw = s.vwin + (size_t)vs * (a.maxwin + 128);
+            const float soA = vw[a.maxwin + rA], soB = vw[a.maxwin + rB];
+            const bool actA = iA < a.L_own && soA != -INFINITY, actB = iB < a.L_own && soB != -INFINITY;
+            // offsets; inactive rows get -inf so every exponential of theirs is 0 without a branch
+            const float oA = actA ? (kFirst ? 0.f : soA) : -INFINITY, oB = actB ? (kFirst ? 0.f : soB) : -INFINITY;
+            const float2 oA2 = make_float2(oA, oA), oB2 = make_float2(oB, oB);
             if (!kFirst && !kRecompute && a.w == 128 && nch == 3 && wbase == b.i0 - 128 && a.dbg == 0) {
-                // ================= interior block, w = 128: 3 chunks, the half's band union is the 9
-                // slices qd .. qd + 8 (window column of row r's band start = r); sub-warp k owns slices
-                // qd + k + 3j (j < 3), of which qd and qd + 8 are the only partial (edge) ones.
-                // Inactive rows carry o = -inf, so every exponential of theirs is 0 without a branch.
-                const float oa = act[0] ? ov[0] : -INFINITY, ob = act[1] ? ov[1] : -INFINITY;
-                const float2 oa2 = make_float2(oa, oa), ob2 = make_float2(ob, ob);
-                const uint32_t tl = tbase + ((uint32_t)rbase << 16);
-                float2 acc_a = make_float2(0.f, 0.f), acc_b = make_float2(0.f, 0.f);
-                int waited = -1;
+                // ============ interior block, w = 128: the half's union is the 9 slices qd .. qd + 8 (row r's
+                // band starts at window column r); part 0 owns slices qd .. qd + 3, part 1 qd + 4 .. qd + 8
+                // (both warps of a half share one SMSP, so the 4 : 5 split costs no MUFU throughput); only
+                // qd and qd + 8 are partial.  TMEM is read ONCE for 8 of the 9 tiles: their exponentials
+                // stay in registers for the column pass, and chunk slots are released as soon as their
+                // tiles are loaded.  Part 1's last tile goes back to TMEM (register budget of 18 warps).
+                auto fast = [&](auto PTc) {
+                constexpr int P = decltype(PTc)::value;
+                constexpr int j0 = P ? 4 : 0;
+                float e[4][16];
+                float2 accA = make_float2(0.f, 0.f), accB = make_float2(0.f, 0.f);
+                // part 0: rounds {0,1}, {2,3}; part 1: {4,5,8}, {6,7} -- part 1's last tile (slice qd + 8) is
+                // exponentiated first and goes back to TMEM at once, so at most 4 tiles (64 registers) stay
+                // live.  Round 1's TMEM loads are issued before round 0's exponentials (one wait::ld each).
+                float x8[16];
+                // tile k of the warp (j = j0 + k; k = 4 is part 1's TMEM-resident slice qd + 8)
+                auto tile_addr = [&](int k) {
+                    const int sl = qd + j0 + k;
+                    return tl + (uint32_t)(((tseq + (sl >> 2)) & (NST - 1)) * kCR + (sl & 3) * 32);
+                };
+                auto exp_tile = [&](float (&ej)[16], int k) {
+                    const int j = j0 + k;
+                    const int cb = (qd + j) * 32 + 2 * t0;
+                    const bool edge = (j == 0) || (j == 8);
 #pragma unroll
-                for (int j = 0; j < 3; ++j) {
-                    const int sl = qd + sub + 3 * j;
-                    const int q = sl >> 2;
-                    const int ts = (tseq + q) & (NST - 1);
-                    if (q > waited) {
-                        mbar_wait(&s.t_full[ts], ((tseq + q) / NST) & 1);
-                        tc_fence_after();
-                        waited = q;
-                    }
-                    const uint32_t taddr = tl + (uint32_t)(ts * kCR + (sl & 3) * 32);
-                    float x[16];
-                    tc_ld16x256(taddr, x);
-                    const float* vp = vw + sl * 32 + 2 * t0;
-                    float2 vv[4];
-#pragma unroll
-                    for (int mm = 0; mm < 4; ++mm) vv[mm] = *reinterpret_cast<const float2*>(vp + 8 * mm);
-                    tc_wait_ld();
-                    const bool edge = (j == 0 && sub == 0) || (j == 2 && sub == 2);
-                    if (edge) {  // band check: window column - row in [0, 2w]
-                        const int cb = sl * 32 + 2 * t0;
-#pragma unroll
-                        for (int mm = 0; mm < 4; ++mm) {
-                            float2 za = __ffma2_rn(make_float2(x[4 * mm], x[4 * mm + 1]), c2v, __fadd2_rn(vv[mm], oa2));
-                            float2 zb = __ffma2_rn(make_float2(x[4 * mm + 2], x[4 * mm + 3]), c2v, __fadd2_rn(vv[mm], ob2));
+                    for (int mm = 0; mm < 4; ++mm) {
+                        const float2 vv = *reinterpret_cast<const float2*>(vw + cb + 8 * mm);
+                        float2 za = __ffma2_rn(make_float2(ej[4 * mm], ej[4 * mm + 1]), c2v, __fadd2_rn(vv, oA2));
+                        float2 zb = __ffma2_rn(make_float2(ej[4 * mm + 2], ej[4 * mm + 3]), c2v, __fadd2_rn(vv, oB2));
+                        if (edge) {  // partial slices: band check window column - row in [0, 2w]
                             const int c = cb + 8 * mm;
-                            za.x = (unsigned)(c - ra) <= 256u ? za.x : -INFINITY;
-                            za.y = (unsigned)(c + 1 - ra) <= 256u ? za.y : -INFINITY;
-                            zb.x = (unsigned)(c - rb) <= 256u ? zb.x : -INFINITY;
-                            zb.y = (unsigned)(c + 1 - rb) <= 256u ? zb.y : -INFINITY;
-                            x[4 * mm] = ex2(za.x);
-                            x[4 * mm + 1] = ex2(za.y);
-                            x[4 * mm + 2] = ex2(zb.x);
-                            x[4 * mm + 3] = ex2(zb.y);
-                            acc_a = __fadd2_rn(acc_a, make_float2(x[4 * mm], x[4 * mm + 1]));
-                            acc_b = __fadd2_rn(acc_b, make_float2(x[4 * mm + 2], x[4 * mm + 3]));
+                            za.x = (unsigned)(c - loA) <= 256u ? za.x : -INFINITY;
+                            za.y = (unsigned)(c + 1 - loA) <= 256u ? za.y : -INFINITY;
+                            zb.x = (unsigned)(c - loB) <= 256u ? zb.x : -INFINITY;
+                            zb.y = (unsigned)(c + 1 - loB) <= 256u ? zb.y : -INFINITY;
                         }
-                    } else {
-#pragma unroll
-                        for (int mm = 0; mm < 4; ++mm) {
-                            const float2 za = __ffma2_rn(make_float2(x[4 * mm], x[4 * mm + 1]), c2v, __fadd2_rn(vv[mm], oa2));
-                            const float2 zb = __ffma2_rn(make_float2(x[4 * mm + 2], x[4 * mm + 3]), c2v, __fadd2_rn(vv[mm], ob2));
-                            x[4 * mm] = ex2(za.x);
-                            x[4 * mm + 1] = ex2(za.y);
-                            x[4 * mm + 2] = ex2(zb.x);
-                            x[4 * mm + 3] = ex2(zb.y);
-                            acc_a = __fadd2_rn(acc_a, make_float2(x[4 * mm], x[4 * mm + 1]));
-                            acc_b = __fadd2_rn(acc_b, make_float2(x[4 * mm + 2], x[4 * mm + 3]));
-                        }
+                        const float2 ea = make_float2(ex2(za.x), ex2(za.y));
+                        const float2 eb = make_float2(ex2(zb.x), ex2(zb.y));
+                        ej[4 * mm] = ea.x;
+                        ej[4 * mm + 1] = ea.y;
+                        ej[4 * mm + 2] = eb.x;
+                        ej[4 * mm + 3] = eb.y;
+                        accA = __fadd2_rn(accA, ea);
+                        accB = __fadd2_rn(accB, eb);
                     }
-                    tc_st16x256(taddr, x);
+                };
+                const int qlast0 = P ? 2 : ((qd + 1) >> 2);   // last chunk of round 0
+                const int qlast1 = P ? ((qd + 7) >> 2) : ((qd + 3) >> 2);
+                for (int q = 0; q <= qlast0; ++q) mbar_wait(&s.t_full[(tseq + q) & (NST - 1)], ((tseq + q) / NST) & 1);
+                tc_fence_after();
+                if (warp == 2 && lane == 0 && gi - g_begin == 4) FS_TRACE(58);
+                tc_ld16x256(tile_addr(0), e[0]);
+                tc_ld16x256(tile_addr(1), e[1]);
+                if (P) tc_ld16x256(tile_addr(4), x8);
+                tc_wait_ld();
+                if (warp == 2 && lane == 0 && gi - g_begin == 4) FS_TRACE(59);
+                for (int q = qlast0 + 1; q <= qlast1; ++q) mbar_wait(&s.t_full[(tseq + q) & (NST - 1)], ((tseq + q) / NST) & 1);
+                tc_fence_after();
+                tc_ld16x256(tile_addr(2), e[2]);
+                tc_ld16x256(tile_addr(3), e[3]);
+                exp_tile(e[0], 0);
+                exp_tile(e[1], 1);
+                if (P) {
+                    exp_tile(x8, 4);
+                    tc_st16x256(tile_addr(4), x8);
                 }
-                tc_wait_st();
-                float sa = acc_a.x + acc_a.y, sb = acc_b.x + acc_b.y;
-                sa += __shfl_xor_sync(0xffffffffu, sa, 1);
-                sb += __shfl_xor_sync(0xffffffffu, sb, 1);
-                sa += __shfl_xor_sync(0xffffffffu, sa, 2);
-                sb += __shfl_xor_sync(0xffffffffu, sb, 2);
+                tc_wait_ld();
+                if (P) tc_wait_st();
+                if (warp == 2 && lane == 0 && gi - g_begin == 4) FS_TRACE(60);
+                // every tile loaded: release the chunks (part 1 keeps chunk 2 for its TMEM-resident tile)
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0)
+                    for (int q = 0; q < (P ? 2 : 3); ++q) mbar_arrive(&s.t_empty[(tseq + q) & (NST - 1)]);
+                exp_tile(e[2], 2);
+                exp_tile(e[3], 3);
+                // ---- row sums: over t0, then the two parts of the half in fixed order (part 0 + part 1)
+                float sA = accA.x + accA.y, sB = accB.x + accB.y;
+                sA += __shfl_xor_sync(0xffffffffu, sA, 1);
+                sB += __shfl_xor_sync(0xffffffffu, sB, 1);
+                sA += __shfl_xor_sync(0xffffffffu, sA, 2);
+                sB += __shfl_xor_sync(0xffffffffu, sB, 2);
+                float* rx = s.rowx + hq * 32;
                 if (t0 == 0) {
-                    s.rowp[sub * 128 + ra] = sa;
-                    s.rowp[sub * 128 + rb] = sb;
+                    rx[P * 16 + t1] = sA;
+                    rx[P * 16 + t1 + 8] = sB;
                 }
-                named_bar(2, NE);
-                float ra_sum = 0.f, rb_sum = 0.f;
-#pragma unroll
-                for (int p = 0; p < kPH; ++p) {
-                    ra_sum += s.rowp[p * 128 + ra];
-                    rb_sum += s.rowp[p * 128 + rb];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s.v_empty[vs]);  // window duals no longer needed
+                named_bar(3 + hq, 64);
+                sA = rx[t1] + rx[16 + t1];
+                sB = rx[t1 + 8] + rx[16 + t1 + 8];
+                float wA = 0.f, wB = 0.f, uA = 0.f, uB = 0.f;
+                if (actA) {
+                    uA = oA - lg2(sA);
+                    if (!(sA > 0.f) || !isfinite(uA)) { atomicOr(a.err, 4); uA = 0.f; } else wA = 1.f / sA;
                 }
-                float wa_ = 0.f, wb_ = 0.f;
-                {
-                    float ua = 0.f, ub = 0.f;
-                    if (act[0]) {
-                        ua = ov[0] - lg2(ra_sum);
-                        if (!(ra_sum > 0.f) || !isfinite(ua)) { atomicOr(a.err, 4); ua = 0.f; } else wa_ = 1.f / ra_sum;
+                if (actB) {
+                    uB = oB - lg2(sB);
+                    if (!(sB > 0.f) || !isfinite(uB)) { atomicOr(a.err, 4); uB = 0.f; } else wB = 1.f / sB;
+                }
+                if (P == 0 && t0 == 0) {
+                    const size_t uo = (size_t)b.bh * a.Lr_own, po = (size_t)b.bh * a.pad_ld_own + a.pad_off;
+                    if (iA < a.L_own) {
+                        a.out_own[uo + iA] = uA;
+                        a.pad_own[po + iA] = actA ? uA : -INFINITY;
                     }
-                    if (act[1]) {
-                        ub = ov[1] - lg2(rb_sum);
-                        if (!(rb_sum > 0.f) || !isfinite(ub)) { atomicOr(a.err, 4); ub = 0.f; } else wb_ = 1.f / rb_sum;
-                    }
-                    if (sub == 0 && t0 == 0) {
-                        const size_t uo = (size_t)b.bh * a.Lr_own, po = (size_t)b.bh * a.pad_ld_own + a.pad_off;
-                        if (ib[0] < a.L_own) {
-                            a.out_own[uo + ib[0]] = ua;
-                            a.pad_own[po + ib[0]] = act[0] ? ua : -INFINITY;
-                        }
-                        if (ib[1] < a.L_own) {
-                            a.out_own[uo + ib[1]] = ub;
-                            a.pad_own[po + ib[1]] = act[1] ? ub : -INFINITY;
-                        }
+                    if (iB < a.L_own) {
+                        a.out_own[uo + iB] = uB;
+                        a.pad_own[po + iB] = actB ? uB : -INFINITY;
                     }
                 }
-                const float2 wa2 = make_float2(wa_, wa_), wb2 = make_float2(wb_, wb_);
-                float* cp = s.colp + (size_t)(qd * 2 + half) * a.maxwin;
-                const int ccol = 16 * ((lane >> 4) & 1) + 8 * ((lane >> 3) & 1) + 2 * t0 + ((lane >> 2) & 1);
-                const bool u4 = (lane & 16) != 0, u3 = (lane & 8) != 0, u2 = (lane & 4) != 0;
-                // the half's 3 slices outside its union (0 .. qd-1, qd+9 .. 11): one per sub-warp
-                cp[32 * (sub < qd ? sub : sub + 9) + ccol] = 0.f;
-                int rel = 0;  // chunks released by this warp so far
-#pragma unroll
-                for (int j = 0; j < 3; ++j) {
-                    const int sl = qd + sub + 3 * j;
-                    const int q = sl >> 2;
-                    for (; rel < q; ++rel) {
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&s.t_empty[(tseq + rel) & (NST - 1)]);
-                    }
-                    const uint32_t taddr = tl + (uint32_t)(((tseq + q) & (NST - 1)) * kCR + (sl & 3) * 32);
-                    tc_fence_after();
-                    float x[16];
-                    tc_ld16x256(taddr, x);
-                    tc_wait_ld();
+                if (trc) FS_TRACE(33 + (gi - g_begin));
+                // ---- column pass from registers (part 1's slice qd + 8 re-read from TMEM last)
+                const float2 wA2 = make_float2(wA, wA), wB2 = make_float2(wB, wB);
+                float* cp = s.colp + ((size_t)par * 8 + (size_t)hq) * a.maxwin;
+                if (P == 0) {
+                    for (int sl = 0; sl < qd; ++sl) cp[sl * 32 + ccol] = 0.f;
+                    for (int sl = qd + 9; sl < 12; ++sl) cp[sl * 32 + ccol] = 0.f;
+                }
+                auto col_tile = [&](const float (&ej)[16], int k) {
                     float y[8];
 #pragma unroll
                     for (int mm = 0; mm < 4; ++mm) {
-                        const float2 pr = __ffma2_rn(make_float2(x[4 * mm + 2], x[4 * mm + 3]), wb2,
-                                                     __fmul2_rn(make_float2(x[4 * mm], x[4 * mm + 1]), wa2));
+                        const float2 pr = __ffma2_rn(make_float2(ej[4 * mm + 2], ej[4 * mm + 3]), wB2,
+                                                     __fmul2_rn(make_float2(ej[4 * mm], ej[4 * mm + 1]), wA2));
                         y[2 * mm] = pr.x;
                         y[2 * mm + 1] = pr.y;
                     }
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const float send = u4 ? y[k] : y[k + 4];
-                        const float keep = u4 ? y[k + 4] : y[k];
-                        y[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                    for (int i2 = 0; i2 < 4; ++i2) {
+                        const float send = u4 ? y[i2] : y[i2 + 4];
+                        const float keep = u4 ? y[i2 + 4] : y[i2];
+                        y[i2] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
                     }
 #pragma unroll
-                    for (int k = 0; k < 2; ++k) {
-                        const float send = u3 ? y[k] : y[k + 2];
-                        const float keep = u3 ? y[k + 2] : y[k];
-                        y[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                    for (int i2 = 0; i2 < 2; ++i2) {
+                        const float send = u3 ? y[i2] : y[i2 + 2];
+                        const float keep = u3 ? y[i2 + 2] : y[i2];
+                        y[i2] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
                     }
                     const float send = u2 ? y[0] : y[1];
                     const float keep = u2 ? y[1] : y[0];
-                    cp[sl * 32 + ccol] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+                    cp[(qd + j0 + k) * 32 + ccol] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+                };
+                if (P) {  // start the TMEM re-read of slice qd + 8 first; it lands while tiles 0..3 reduce
+                    tc_fence_after();
+                    tc_ld16x256(tile_addr(4), x8);
                 }
-                for (; rel < 3; ++rel) {
+                col_tile(e[0], 0);
+                col_tile(e[1], 1);
+                col_tile(e[2], 2);
+                col_tile(e[3], 3);
+                if (P) {
+                    tc_wait_ld();
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&s.t_empty[(tseq + rel) & (NST - 1)]);
+                    if (lane == 0) mbar_arrive(&s.t_empty[(tseq + 2) & (NST - 1)]);
+                    col_tile(x8, 4);
                 }
+                };
+                if (pt) fast(std::integral_constant<int, 1>{});
+                else fast(std::integral_constant<int, 0>{});
                 tseq += 3;
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&s.v_empty[vs]);
+                if (trc) FS_TRACE(41 + (gi - g_begin));
                 named_bar(2, NE);
+                if (trc) FS_TRACE(49 + (gi - g_begin));
+                const float* cb8 = s.colp + (size_t)par * 8 * a.maxwin;
                 float* dst = part_out + ((size_t)b.bh * a.NB + b.blk) * a.maxwin;
                 if (et < 3 * kCR) {
                     float sum = 0.f;
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) sum += s.colp[(size_t)k * a.maxwin + et];
+                    for (int k = 0; k < 8; ++k) sum += cb8[(size_t)k * a.maxwin + et];
                     dst[et] = sum;
                 }
                 continue;
             }
-            // ---- row pass: e = ex2(s2 + v + o), written back over S (later steps; kRec: not stored,
-            // the column pass recomputes -- always so for the cold start, whose online max would
-            // leave earlier slices relative to a stale max)
-            constexpr bool kRec = kRecompute || kFirst;
-            float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-            float Mx[2] = {-INFINITY, -INFINITY};
-            int waited = -1;
-            for (int sl = s_lo + sub; sl <= s_hi; sl += kPH) {
-                const int q = sl >> 2;
-                const int ts = (tseq + q) % NST;
-                if (q > waited) {
-                    mbar_wait(&s.t_full[ts], ((tseq + q) / NST) & 1);
-                    tc_fence_after();
-                    waited = q;
+            if (pt == 1) {
+                // generic blocks run on the first warp of each pair; the second only keeps the barrier
+                // and slot protocols (one arrival per chunk and per window) and joins the combine
+                __syncwarp();
+                if (lane == 0) {
+                    for (int q = 0; q < nch; ++q) mbar_arrive(&s.t_empty[(tseq + q) & (NST - 1)]);
+                    mbar_arrive(&s.v_empty[vs]);
                 }
-                const int c0 = sl * 32;
-                const bool inner = (c0 >= ilo) && (c0 + 31 <= ihi);
-                const uint32_t taddr = tbase + ((uint32_t)rbase << 16) + (uint32_t)(ts * kCR + (sl & 3) * 32);
-                float x[16];
-                tc_ld16x256(taddr, x);
-                tc_wait_ld();
-                if (a.dbg & 1) {
-                } else if (kFirst) {
+                tseq += nch;
+                named_bar(2, NE);
+                const float* cb8 = s.colp + (size_t)par * 8 * a.maxwin;
+                float* dst = part_out + ((size_t)b.bh * a.NB + b.blk) * a.maxwin;
+                for (int c = et; c < nch * kCR; c += NE) {
+                    float sum = 0.f;
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        float y[8];
-                        float m = -INFINITY;
+                    for (int k = 0; k < 8; ++k) sum += cb8[(size_t)k * a.maxwin + c];
+                    dst[c] = sum;
+                }
+                continue;
+            }
+            // ---- row pass: e = ex2(s2 + v + o) over the warp's union slices, written back over S
+            float2 accA = make_float2(0.f, 0.f), accB = make_float2(0.f, 0.f);
+            float MA = -INFINITY, MB = -INFINITY;  // cold start: running row maxima
+            int waited = -1;
+            for (int g0 = s_lo; g0 <= s_hi; g0 += kG) {
+                // kG tiles per round: their TMEM loads share one wait, their exponentials interleave
+                const int gl = min(s_hi, g0 + kG - 1);
+                const int qh = gl >> 2;
+                if (qh > waited) {
+                    for (int q = waited + 1; q <= qh; ++q) mbar_wait(&s.t_full[(tseq + q) & (NST - 1)], ((tseq + q) / NST) & 1);
+                    tc_fence_after();
+                    waited = qh;
+                }
+                float x[kG][16];
+                float2 vv[kG][4];
+#pragma unroll
+                for (int k = 0; k < kG; ++k) {
+                    const int sl = min(g0 + k, gl);
+                    tc_ld16x256(tl + (uint32_t)(((tseq + (sl >> 2)) & (NST - 1)) * kCR + (sl & 3) * 32), x[k]);
+#pragma unroll
+                    for (int mm = 0; mm < 4; ++mm)
+                        vv[k][mm] = *reinterpret_cast<const float2*>(vw + sl * 32 + 2 * t0 + 8 * mm);
+                }
+                tc_wait_ld();
+#pragma unroll
+                for (int k = 0; k < kG; ++k) {
+                    const int sl = g0 + k;
+                    if (sl > gl) break;
+                    const int cb = sl * 32 + 2 * t0;
+                    if (kFirst) {
+                        float mA = -INFINITY, mB = -INFINITY;
+#pragma unroll
+                        for (int mm = 0; mm < 4; ++mm) {
+                            const int c = cb + 8 * mm;
+                            float2 za = __ffma2_rn(make_float2(x[k][4 * mm], x[k][4 * mm + 1]), c2v, vv[k][mm]);
+                            float2 zb = __ffma2_rn(make_float2(x[k][4 * mm + 2], x[k][4 * mm + 3]), c2v, vv[k][mm]);
+                            za.x = (actA && (unsigned)(c - loA) <= (unsigned)bandw) ? za.x : -INFINITY;
+                            za.y = (actA && (unsigned)(c + 1 - loA) <= (unsigned)bandw) ? za.y : -INFINITY;
+                            zb.x = (actB && (unsigned)(c - loB) <= (unsigned)bandw) ? zb.x : -INFINITY;
+                            zb.y = (actB && (unsigned)(c + 1 - loB) <= (unsigned)bandw) ? zb.y : -INFINITY;
+                            x[k][4 * mm] = za.x;
+                            x[k][4 * mm + 1] = za.y;
+                            x[k][4 * mm + 2] = zb.x;
+                            x[k][4 * mm + 3] = zb.y;
+                            mA = fmaxf(mA, fmaxf(za.x, za.y));
+                            mB = fmaxf(mB, fmaxf(zb.x, zb.y));
+                        }
+                        if (mA > MA) {
+                            const float sc = (MA == -INFINITY) ? 0.f : ex2(MA - mA);
+                            accA.x *= sc;
+                            accA.y *= sc;
+                            MA = mA;
+                        }
+                        if (mB > MB) {
+                            const float sc = (MB == -INFINITY) ? 0.f : ex2(MB - mB);
+                            accB.x *= sc;
+                            accB.y *= sc;
+                            MB = mB;
+                        }
+#pragma unroll
+                        for (int mm = 0; mm < 4; ++mm) {
+                            if (MA != -INFINITY)
+                                accA = __fadd2_rn(accA, make_float2(ex2(x[k][4 * mm] - MA), ex2(x[k][4 * mm + 1] - MA)));
+                            if (MB != -INFINITY)
+                                accB = __fadd2_rn(accB, make_float2(ex2(x[k][4 * mm + 2] - MB), ex2(x[k][4 * mm + 3] - MB)));
+                        }
+                    } else {
+                        const bool inner = sl >= in_lo && sl <= in_hi;
+#pragma unroll
+                        for (int mm = 0; mm < 4; ++mm) {
+                            float2 za = __ffma2_rn(make_float2(x[k][4 * mm], x[k][4 * mm + 1]), c2v, __fadd2_rn(vv[k][mm], oA2));
+                            float2 zb = __ffma2_rn(make_float2(x[k][4 * mm + 2], x[k][4 * mm + 3]), c2v, __fadd2_rn(vv[k][mm], oB2));
+                            if (!inner) {
+                                const int c = cb + 8 * mm;
+                                za.x = (unsigned)(c - loA) <= (unsigned)bandw ? za.x : -INFINITY;
+                                za.y = (unsigned)(c + 1 - loA) <= (unsigned)bandw ? za.y : -INFINITY;
+                                zb.x = (unsigned)(c - loB) <= (unsigned)bandw ? zb.x : -INFINITY;
+                                zb.y = (unsigned)(c + 1 - loB) <= (unsigned)bandw ? zb.y : -INFINITY;
+                            }
+                            const float2 ea = make_float2(ex2(za.x), ex2(za.y));
+                            const float2 eb = make_float2(ex2(zb.x), ex2(zb.y));
+                            x[k][4 * mm] = ea.x;
+                            x[k][4 * mm + 1] = ea.y;
+                            x[k][4 * mm + 2] = eb.x;
+                            x[k][4 * mm + 3] = eb.y;
+                            accA = __fadd2_rn(accA, ea);
+                            accB = __fadd2_rn(accB, eb);
+                        }
+                        tc_st16x256(tl + (uint32_t)(((tseq + (sl >> 2)) & (NST - 1)) * kCR + (sl & 3) * 32), x[k]);
+                    }
+                }
+            }
+            if (!kRec) tc_wait_st();
+            if (trc) FS_TRACE(33 + (gi - g_begin));
+            // ---- row sums over the 4 threads (t0) sharing a row: u and the column weights 1 / r
+            float sA = accA.x + accA.y, sB = accB.x + accB.y;
+#pragma unroll
+            for (int o = 1; o <= 2; o <<= 1) {
+                const float pA = __shfl_xor_sync(0xffffffffu, sA, o), pB = __shfl_xor_sync(0xffffffffu, sB, o);
+                if (kFirst) {
+                    const float qA = __shfl_xor_sync(0xffffffffu, MA, o), qB = __shfl_xor_sync(0xffffffffu, MB, o);
+                    const float nA = fmaxf(MA, qA), nB = fmaxf(MB, qB);
+                    sA = (MA == -INFINITY ? 0.f : sA * ex2(MA - nA)) + (qA == -INFINITY ? 0.f : pA * ex2(qA - nA));
+                    sB = (MB == -INFINITY ? 0.f : sB * ex2(MB - nB)) + (qB == -INFINITY ? 0.f : pB * ex2(qB - nB));
+                    MA = nA;
+                    MB = nB;
+                } else {
+                    sA += pA;
+                    sB += pB;
+                }
+            }
+            float wA = 0.f, wB = 0.f, uA = 0.f, uB = 0.f;
+            if (actA) {
+                uA = kFirst ? (-MA - lg2(sA)) : (oA - lg2(sA));
+                if (!(sA > 0.f) || !isfinite(uA)) { atomicOr(a.err, 4); uA = 0.f; } else wA = 1.f / sA;
+            }
+            if (actB) {
+                uB = kFirst ? (-MB - lg2(sB)) : (oB - lg2(sB));
+                if (!(sB > 0.f) || !isfinite(uB)) { atomicOr(a.err, 4); uB = 0.f; } else wB = 1.f / sB;
+            }
+            if (t0 == 0) {
+                const size_t uo = (size_t)b.bh * a.Lr_own, po = (size_t)b.bh * a.pad_ld_own + a.pad_off;
+                if (iA < a.L_own) {
+                    a.out_own[uo + iA] = uA;
+                    a.pad_own[po + iA] = actA ? uA : -INFINITY;
+                }
+                if (iB < a.L_own) {
+                    a.out_own[uo + iB] = uB;
+                    a.pad_own[po + iB] = actB ? uB : -INFINITY;
+                }
+            }
+            // ---- column pass: c_Ij = sum_i e_ij / r_i over the warp's 16 rows, per column
+            const float2 wA2 = make_float2(wA, wA), wB2 = make_float2(wB, wB);
+            const float offA = kFirst ? -MA : oA, offB = kFirst ? -MB : oB;
+            float* cp = s.colp + ((size_t)par * 8 + (size_t)(qd * 2 + hf)) * a.maxwin;
+            for (int sl = 0; sl < s_lo; ++sl) cp[sl * 32 + ccol] = 0.f;
+            for (int sl = s_hi + 1; sl < nsl; ++sl) cp[sl * 32 + ccol] = 0.f;
+            int rel = 0;  // chunks this warp released
+            for (int g0 = s_lo; g0 <= s_hi; g0 += kG) {
+                const int gl = min(s_hi, g0 + kG - 1);
+                for (; rel < (g0 >> 2); ++rel) {  // chunks wholly before this round: done
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&s.t_empty[(tseq + rel) & (NST - 1)]);
+                }
+                tc_fence_after();
+                float x[kG][16];
+#pragma unroll
+                for (int k = 0; k < kG; ++k) {
+                    const int sl = min(g0 + k, gl);
+                    tc_ld16x256(tl + (uint32_t)(((tseq + (sl >> 2)) & (NST - 1)) * kCR + (sl & 3) * 32), x[k]);
+                }
+                tc_wait_ld();
+                float y[kG][8];
+#pragma unroll
+                for (int k = 0; k < kG; ++k) {
+                    const int sl = min(g0 + k, gl);
+                    if (kRec) {
+                        const int cb = sl * 32 + 2 * t0;
 #pragma unroll
                         for (int mm = 0; mm < 4; ++mm)
 #pragma unroll
                             for (int c = 0; c < 2; ++c) {
-                                const int col = c0 + 8 * mm + 2 * t0 + c;
-                                const float z = fmaf(x[4 * mm + 2 * h + c], a.c2, vw[col]);
-                                y[2 * mm + c] = (act[h] && (unsigned)(col - lov[h]) <= (unsigned)(2 * a.w)) ? z : -INFINITY;
-                                m = fmaxf(m, y[2 * mm + c]);
+                                const int col = cb + 8 * mm + c;
+                                float za = fmaf(x[k][4 * mm + c], a.c2, vw[col]) + offA;
+                                float zb = fmaf(x[k][4 * mm + 2 + c], a.c2, vw[col]) + offB;
+                                za = (actA && (unsigned)(col - loA) <= (unsigned)bandw) ? za : -INFINITY;
+                                zb = (actB && (unsigned)(col - loB) <= (unsigned)bandw) ? zb : -INFINITY;
+                                x[k][4 * mm + c] = ex2(za);
+                                x[k][4 * mm + 2 + c] = ex2(zb);
                             }
-                        if (m > Mx[h]) {
-                            const float sc = (Mx[h] == -INFINITY) ? 0.f : ex2(Mx[h] - m);
-                            acc[h].x *= sc;
-                            acc[h].y *= sc;
-                            Mx[h] = m;
-                        }
-                        if (Mx[h] != -INFINITY) {
-#pragma unroll
-                            for (int k = 0; k < 8; k += 2) {
-                                acc[h].x += ex2(y[k] - Mx[h]);
-                                acc[h].y += ex2(y[k + 1] - Mx[h]);
-                            }
-                        }
                     }
-                } else {
 #pragma unroll
                     for (int mm = 0; mm < 4; ++mm) {
-                        const float2 vv = *reinterpret_cast<const float2*>(vw + c0 + 8 * mm + 2 * t0);
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            float2 z = __ffma2_rn(make_float2(x[4 * mm + 2 * h], x[4 * mm + 2 * h + 1]), c2v,
-                                                  __fadd2_rn(vv, h ? o2b : o2a));
-                            if (!inner || !act[h]) {
-                                const int col = c0 + 8 * mm + 2 * t0;
-                                z.x = (act[h] && (unsigned)(col - lov[h]) <= (unsigned)(2 * a.w)) ? z.x : -INFINITY;
-                                z.y = (act[h] && (unsigned)(col + 1 - lov[h]) <= (unsigned)(2 * a.w)) ? z.y : -INFINITY;
-                            }
-                            const float2 e = make_float2(ex2(z.x), ex2(z.y));
-                            x[4 * mm + 2 * h] = e.x;
-                            x[4 * mm + 2 * h + 1] = e.y;
-                            acc[h] = __fadd2_rn(acc[h], e);
-                        }
+                        const float2 pr = __ffma2_rn(make_float2(x[k][4 * mm + 2], x[k][4 * mm + 3]), wB2,
+                                                     __fmul2_rn(make_float2(x[k][4 * mm], x[k][4 * mm + 1]), wA2));
+                        y[k][2 * mm] = pr.x;
+                        y[k][2 * mm + 1] = pr.y;
                     }
                 }
-                if (!kRec) tc_st16x256(taddr, x);
-            }
-            if (!kRec) tc_wait_st();
-            // ---- row sums: over t0 (4 threads share a row), then over the 3 sub-warps in fixed order
-            float rs[2], rm[2];
+                // reduce over t1 (lane bits 2..4): after the 3 stages lane holds column ccol
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                float sm = acc[h].x + acc[h].y, M = Mx[h];
+                for (int j = 0; j < 4; ++j)
 #pragma unroll
-                for (int o = 1; o <= 2; o <<= 1) {
-                    const float s2 = __shfl_xor_sync(0xffffffffu, sm, o);
-                    if (kFirst) {
-                        const float M2 = __shfl_xor_sync(0xffffffffu, M, o);
-                        const float Mn = fmaxf(M, M2);
-                        sm = (M == -INFINITY ? 0.f : sm * ex2(M - Mn)) + (M2 == -INFINITY ? 0.f : s2 * ex2(M2 - Mn));
-                        M = Mn;
-                    } else {
-                        sm += s2;
+                    for (int k = 0; k < kG; ++k) {
+                        const float send = u4 ? y[k][j] : y[k][j + 4];
+                        const float keep = u4 ? y[k][j + 4] : y[k][j];
+                        y[k][j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
                     }
-                }
-                rs[h] = sm;
-                rm[h] = M;
-            }
-            if (t0 == 0) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int rr = h ? rb : ra;
-                    s.rowp[sub * 128 + rr] = rs[h];
-                    if (kFirst) s.rowp[(kPH + sub) * 128 + rr] = rm[h];
+                for (int j = 0; j < 2; ++j)
+#pragma unroll
+                    for (int k = 0; k < kG; ++k) {
+                        const float send = u3 ? y[k][j] : y[k][j + 2];
+                        const float keep = u3 ? y[k][j + 2] : y[k][j];
+                        y[k][j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                    }
+#pragma unroll
+                for (int k = 0; k < kG; ++k) {
+                    const float send = u2 ? y[k][0] : y[k][1];
+                    const float keep = u2 ? y[k][1] : y[k][0];
+                    const float val = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+                    if (g0 + k <= gl) cp[(g0 + k) * 32 + ccol] = val;
                 }
             }
-            named_bar(2, NE);
-            float wgt[2], Mall[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int rr = h ? rb : ra;
-                float rsum = 0.f, Ma = -INFINITY;
-                if (kFirst) {
-#pragma unroll
-                    for (int p = 0; p < kPH; ++p) Ma = fmaxf(Ma, s.rowp[(kPH + p) * 128 + rr]);
-#pragma unroll
-                    for (int p = 0; p < kPH; ++p) {
-                        const float Mp = s.rowp[(kPH + p) * 128 + rr];
-                        rsum += (Mp == -INFINITY) ? 0.f : s.rowp[p * 128 + rr] * ex2(Mp - Ma);
-                    }
-                } else {
-#pragma unroll
-                    for (int p = 0; p < kPH; ++p) rsum += s.rowp[p * 128 + rr];
-                }
-                float u = 0.f;
-                wgt[h] = 0.f;
-                Mall[h] = Ma;
-                if (act[h]) {
-                    u = kFirst ? (-Ma - lg2(rsum)) : (ov[h] - lg2(rsum));
-                    if (!(rsum > 0.f) || !isfinite(u)) {
-                        atomicOr(a.err, 4);
-                        u = 0.f;
-                    } else {
-                        wgt[h] = 1.f / rsum;
-                    }
-                }
-                if (sub == 0 && t0 == 0 && ib[h] < a.L_own) {
-                    a.out_own[(size_t)b.bh * a.Lr_own + ib[h]] = u;
-                    a.pad_own[(size_t)b.bh * a.pad_ld_own + a.pad_off + ib[h]] = act[h] ? u : -INFINITY;
-                }
-            }
-            // ---- column pass: c_Ij = sum_i e_ij / r_i over the half's 16 rows, per column.  Every
-            // slice of the window is written by exactly one sub-warp of the half (zeros outside the
-            // union); a chunk's TMEM slot is released by each warp once it is done with that chunk.
-            const float2 wa = make_float2(wgt[0], wgt[0]), wb = make_float2(wgt[1], wgt[1]);
-            float* cp = s.colp + (size_t)(qd * 2 + half) * a.maxwin;
-            const int ph = (((s_lo + sub) % kPH) + kPH) % kPH;
-            const int ccol = 16 * ((lane >> 4) & 1) + 8 * ((lane >> 3) & 1) + 2 * t0 + ((lane >> 2) & 1);
-            for (int q = 0; q < nch; ++q) {
-                const int ts = (tseq + q) % NST;
-#pragma unroll
-                for (int j = 0; j < kSlc; ++j) {
-                    const int sl = q * kSlc + j;
-                    if (sl % kPH != ph) continue;
-                    const int c0 = sl * 32;
-                    float val = 0.f;
-                    if (sl >= s_lo && sl <= s_hi) {
-                        tc_fence_after();
-                        const uint32_t taddr = tbase + ((uint32_t)rbase << 16) + (uint32_t)(ts * kCR + j * 32);
-                        float x[16];
-                        tc_ld16x256(taddr, x);
-                        tc_wait_ld();
-                        if (kRec) {
-#pragma unroll
-                            for (int mm = 0; mm < 4; ++mm)
-#pragma unroll
-                                for (int h = 0; h < 2; ++h)
-#pragma unroll
-                                    for (int c = 0; c < 2; ++c) {
-                                        const int col = c0 + 8 * mm + 2 * t0 + c;
-                                        float z = fmaf(x[4 * mm + 2 * h + c], a.c2, vw[col]) + (kFirst ? -Mall[h] : ov[h]);
-                                        z = (act[h] && (unsigned)(col - lov[h]) <= (unsigned)(2 * a.w)) ? z : -INFINITY;
-                                        x[4 * mm + 2 * h + c] = ex2(z);
-                                    }
-                        }
-                        float y[8];
-#pragma unroll
-                        for (int mm = 0; mm < 4; ++mm) {
-                            const float2 p = __ffma2_rn(make_float2(x[4 * mm + 2], x[4 * mm + 3]), wb,
-                                                        __fmul2_rn(make_float2(x[4 * mm], x[4 * mm + 1]), wa));
-                            y[2 * mm] = p.x;
-                            y[2 * mm + 1] = p.y;
-                        }
-                        if (a.dbg & 4) {
-                            val = y[0];
-                        } else {
-                            const bool u4 = (lane & 16) != 0, u3 = (lane & 8) != 0, u2 = (lane & 4) != 0;
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                const float send = u4 ? y[k] : y[k + 4];
-                                const float keep = u4 ? y[k + 4] : y[k];
-                                y[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-                            }
-#pragma unroll
-                            for (int k = 0; k < 2; ++k) {
-                                const float send = u3 ? y[k] : y[k + 2];
-                                const float keep = u3 ? y[k + 2] : y[k];
-                                y[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-                            }
-                            const float send = u2 ? y[0] : y[1];
-                            const float keep = u2 ? y[1] : y[0];
-                            val = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-                        }
-                    }
-                    cp[c0 + ccol] = val;
-                }
+            for (; rel < nch; ++rel) {
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&s.t_empty[ts]);
+                if (lane == 0) mbar_arrive(&s.t_empty[(tseq + rel) & (NST - 1)]);
             }
             tseq += nch;
+            if (trc) FS_TRACE(41 + (gi - g_begin));
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.v_empty[vs]);  // window duals no longer needed
             named_bar(2, NE);
+            if (trc) FS_TRACE(49 + (gi - g_begin));
             // ---- combine the 8 half-quadrant partials in fixed order; store the block's column partials
+            const float* cb8 = s.colp + (size_t)par * 8 * a.maxwin;
             float* dst = part_out + ((size_t)b.bh * a.NB + b.blk) * a.maxwin;
             for (int c = et; c < nch * kCR; c += NE) {
                 float sum = 0.f;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) sum += s.colp[(size_t)k * a.maxwin + c];
+                for (int k = 0; k < 8; ++k) sum += cb8[(size_t)k * a.maxwin + c];
                 dst[c] = sum;
             }
         }
     }
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) FS_TRACE(0);
     if (warp == 1) {
         tc_fence_after();
         tc_dealloc(tbase, 512);
@@ -774,8 +851,8 @@ long long fstep16_launch_count(bool reset) {
 size_t fstep16_smem_bytes(const PhaseArgs& a) {
     const int nst = 512 / a.CR;
     return (size_t)a.NA * 128 * a.row_bytes + (size_t)a.NSK * a.CR * a.row_bytes +
-           (size_t)(kNV * (a.maxwin + 128) + 2 * kPH * 128 + 8 * a.maxwin) * 4 +
-           (size_t)(2 * kNV + 2 * a.NA + 2 * a.NSK + 2 * nst) * 8 + 16 + (size_t)a.wl_cap * 4;
+           (size_t)(kNV * (a.maxwin + 128) + 2 * 8 * a.maxwin + 8 * 2 * 16) * 4 +
+           (size_t)(2 * kNV + 2 * a.NA + 2 * a.NSK + 2 * nst) * 8 + 16 + (size_t)a.wl_cap * 16;
 }
 
 template <bool kFirst, bool kRec>
