@@ -171,6 +171,14 @@ st_status st_saved_duals(const st_desc* desc, const void* saved, const uint8_t* 
                          const uint8_t* col_mask_host, double* u, double* v, double* gauge,
                          void* stream);
 
+/* The device status word of a forward (carried in `saved`): synchronizes `stream`
+ * and returns ST_OK, ST_INFEASIBLE_SUPPORT (an active row or column had an empty
+ * reduction, the reference's InfeasibleSupport thrown inside row_half_step /
+ * col_half_step, sinkhorn.hpp:52-56 / :98-102) or ST_CUDA_ERROR (an internal
+ * invariant).  st_forward / st_backward are asynchronous and never block on it;
+ * call this (or st_saved_duals) where the reference would have thrown. */
+st_status st_check_status(const st_desc* desc, const void* saved, void* stream);
+
 /* Host-side support validation (SupportMask::validate): ST_INFEASIBLE_SUPPORT
  * when an active row or column has no active edge.  Masks are HOST pointers. */
 st_status st_validate_support(const st_desc* desc, const uint8_t* row_mask_host,

@@ -38,7 +38,7 @@ EXPORTED = (
     "st_saved_bytes", "st_workspace_bytes", "st_forward", "st_backward", "st_saved_duals",
     "st_validate_support", "st_normal_fill", "st_uniform_fill", "st_last_error", "st_launch_count",
     "st_forward_halo", "st_backward_halo", "st_base_vjp_workspace_bytes", "st_base_solve_vjp",
-    "st_tail_adjoint",
+    "st_tail_adjoint", "st_check_status",
 )
 
 
@@ -87,6 +87,8 @@ def _load() -> ctypes.CDLL:
     lib.st_base_solve_vjp.restype = ctypes.c_int
     lib.st_saved_duals.argtypes = [P, VP, VP, VP, D, D, D, VP]
     lib.st_saved_duals.restype = ctypes.c_int
+    lib.st_check_status.argtypes = [P, VP, VP]
+    lib.st_check_status.restype = ctypes.c_int
     lib.st_validate_support.argtypes = [P, VP, VP]
     lib.st_validate_support.restype = ctypes.c_int
     lib.st_normal_fill.argtypes = [U64, ctypes.c_char_p, U64, I64, ctypes.c_double, D]

@@ -165,6 +165,12 @@ class SurrogateRun:
     col_mask: Optional[torch.Tensor]
     workspace: Optional["Workspace"] = None  # holds this forward's score band until reused
 
+    def check(self) -> None:
+        """Raise the reference's exception if the forward hit an empty active reduction
+        (InfeasibleSupport, sinkhorn.hpp:52-56); synchronizes the current stream."""
+        d = self.spec.desc()
+        _check(lib.st_check_status(ctypes.byref(d), _ptr(self.saved), torch.cuda.current_stream().cuda_stream))
+
     def tail_duals(self, row_mask_host=None, col_mask_host=None):
         """(u[3,BH,L'], v[3,BH,L'], gauge[3,BH]) in natural units, centered if spec.centered."""
         s = self.spec

@@ -350,15 +350,18 @@ WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
     return w;
 }
 
-int num_sms() {
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
+int num_sms() {  // per device (a process may drive several GPUs); racy first fills write the same value
+    constexpr int kMaxDev = 64;
+    static int n[kMaxDev] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDev) dev = 0;
+    if (n[dev] == 0) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        n[dev] = v > 0 ? v : 148;
     }
-    return n;
+    return n[dev];
 }
 
 // One tcgen05 band write pass (bf16 operand planes): the score band (cot = false, s2 = q.k c2) or
@@ -1090,6 +1093,21 @@ st_status st_tail_adjoint(const st_desc* desc, const void* saved, const void* Q,
                          workspace, workspace_bytes, stream, nullptr, nullptr, 0, -1, eta_u);
 }
 
+st_status st_check_status(const st_desc* desc, const void* saved, void* stream) {
+    Dims m;
+    st_status s = check_desc(desc, m);
+    if (s != ST_OK) return s;
+    if (saved == nullptr) return fail(ST_MISSING_BASE_TRACE, "null saved state");
+    const SavedLayout sl = saved_layout(m);
+    int status = 0;
+    ST_CUDA(cudaMemcpyAsync(&status, (const char*)saved + sl.status, sizeof(int), cudaMemcpyDeviceToHost,
+                            (cudaStream_t)stream));
+    ST_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    if (status & 16) return fail(ST_CUDA_ERROR, "internal error: CTA work list overflow in a solve kernel");
+    if (status != 0) return fail(ST_INFEASIBLE_SUPPORT, "an active row or column had an empty reduction");
+    return ST_OK;
+}
+
 st_status st_saved_duals(const st_desc* desc, const void* saved, const uint8_t* row_mask_host,
                          const uint8_t* col_mask_host, double* u, double* v, double* gauge, void* stream) {
     Dims m;
@@ -1130,6 +1148,9 @@ st_status st_saved_duals(const st_desc* desc, const void* saved, const uint8_t* 
                 if (v) v[k] = on ? (double)hv[k] * ln2 + C : 0.0;
             }
         }
+    // status word bits (device side): 4 / 8 = an active row / column had an empty reduction (the
+    // reference's InfeasibleSupport); 16 = a CTA work-list overflow (internal invariant)
+    if (status & 16) return fail(ST_CUDA_ERROR, "internal error: CTA work list overflow in a solve kernel");
     if (status != 0) return fail(ST_INFEASIBLE_SUPPORT, "an active row or column had an empty reduction");
     return ST_OK;
 }

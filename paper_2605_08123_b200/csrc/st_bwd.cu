@@ -1761,12 +1761,9 @@ static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
         // 128-row weights + register-tiled band GEMM (operands as f32)
         const size_t smem = bwdT_smem_bytes(g);
         auto k = k_bwdV<kOp, kDirect, D, TIn>;
-        static size_t cur = 0;
-        if (smem > cur) {
-            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            cur = smem;
-        }
+        // set on every launch: the attribute is per device, and callers may drive several devices / threads
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
         const int n = row ? g.Lq : g.Lk;
         k<<<dim3((n + 127) / 128, g.BH), 256, smem, s>>>(g, a);
         return cudaGetLastError();
@@ -1795,12 +1792,8 @@ static cudaError_t run_op(const Geo& g, const BT<TIn>& a, cudaStream_t s) {
     }
     const size_t smem = bwdT_op_smem(g, kOp, D);
     auto k = k_bwdT<kOp, kDirect, D, TIn>;
-    static size_t cur = 0;
-    if (smem > cur) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        cur = smem;
-    }
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
     const int n = row ? g.Lq : g.Lk;
     k<<<dim3((n + 127) / 128, g.BH), 128, smem, s>>>(g, a);
     return cudaGetLastError();
@@ -1878,13 +1871,20 @@ static cudaError_t run_all(const Geo& g, const BwdPtrs& p, const BwdTPtrs& t, in
         // R6 (dQ, d_eps) and C6 (dK, v0b) read the same finished vectors and write disjoint outputs:
         // run them on two streams so each fills the other's partial last wave (event fork / join,
         // captured as graph dependencies)
-        static thread_local cudaStream_t side = nullptr;
-        static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-        if (!side) {
-            cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
-            cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
-            cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
+        // side stream and events per (thread, device): a process may drive several GPUs
+        constexpr int kMaxDev = 64;
+        static thread_local cudaStream_t sides[kMaxDev] = {};
+        static thread_local cudaEvent_t forks[kMaxDev] = {}, joins[kMaxDev] = {};
+        int dev = 0;
+        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+        if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+        if (!sides[dev]) {
+            if ((e = cudaStreamCreateWithFlags(&sides[dev], cudaStreamNonBlocking)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&forks[dev], cudaEventDisableTiming)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&joins[dev], cudaEventDisableTiming)) != cudaSuccess) return e;
         }
+        cudaStream_t side = sides[dev];
+        cudaEvent_t ev_fork = forks[dev], ev_join = joins[dev];
         if ((e = cudaEventRecord(ev_fork, s)) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(side, ev_fork, 0)) != cudaSuccess) return e;
         if ((e = run_op<C6, kDirect, D, TIn>(g, a, side)) != cudaSuccess) return e;

@@ -12,8 +12,12 @@
       restricted to the neighbour's columns (``partials_to_left/right``), and
     - the w-wide slice of new column duals v on each side (``v_halo``),
 
-  plus the one-time Q/K/V halo rows.  The sharded reduction order equals the
-  unsharded one, so sharded duals are bit-identical to a one-GPU run.
+  plus the one-time Q/K/V halo rows.  Every own row's and own column's
+  reduction lies inside the local window, so own-row outputs equal the
+  unsharded ones up to the association order of the blocked reductions: a
+  local problem starts at window.start, so its 128-row blocking can differ
+  from the global one (the lockstep GPU test bounds the difference at 1e-6
+  rel-L2; tests/test_shard.py checks bit-identity of the f64 protocol model).
   ``exchange`` moves these halos with torch.distributed point-to-point
   (NCCL over NVLink for CUDA tensors, gloo for the CPU tests).
 

@@ -91,11 +91,12 @@ KEYS = ("O", "dQ", "dK", "dV", "eta_v", "d_eps")
 
 
 def check_against_oracle(cfg, inp, tol_o, tol_g, mode="one_reference", eps_schedule=None, case=None,
-                         bounds_override=None):
+                         bounds_override=None, floor=True):
     g = gpu_run(cfg, inp, mode=mode, eps_schedule=eps_schedule)
     m = 1 if mode == "direct_four_plan" else 0
     r = oracle(cfg, inp, precision=64, mode=m, eps_schedule=eps_schedule)
-    r32 = oracle(cfg, inp, precision=32, mode=m, eps_schedule=eps_schedule)
+    # the reference's own f32 instantiation (the noise floor; informational for the fixed bf16 bound)
+    r32 = oracle(cfg, inp, precision=32, mode=m, eps_schedule=eps_schedule) if floor else r
     errs = {k: rel(g[k], r[k]) for k in KEYS}
     floor = {k: rel(r32[k], r[k]) for k in KEYS}
     print(f"config {cfg.cid} L={cfg.L} heads={len(inp.heads)} mode={mode} rel-L2 gpu / ref-f32:",
@@ -211,9 +212,12 @@ def test_bf16_full_baseline_shape_parity(cid, heads):
     seeded head subset: 512 / 1024 row blocks per launch, i.e. several blocks per
     persistent CTA, so the cross-block chunk reuse and ring bookkeeping of the half-step kernel run
     exactly as in the benchmark.  Stated bf16 bound: BF16_TOL = 1e-4 rel-L2 on O, dQ, dK, dV, eta."""
+    import os
     cfg = configs.CONFIGS[cid]
     inp = configs.make_inputs(cfg, heads=range(heads[0], heads[-1] + 1))
-    check_against_oracle(cfg, inp, BF16_TOL, BF16_TOL, case=f"config{cid}-full-L")
+    # config 5's f32 floor run costs ~2.5 min of host time: only when the parity table is regenerated
+    floor = cid == 4 or bool(os.environ.get("ST_PARITY_OUT"))
+    check_against_oracle(cfg, inp, BF16_TOL, BF16_TOL, case=f"config{cid}-full-L", floor=floor)
 
 
 def test_bf16_many_blocks_per_cta_parity():
@@ -238,11 +242,18 @@ def test_bf16_full_size_row_sums(cid):
     rows = g["O"][:, :, 0]
     assert np.array_equal(g["O"][:, :, 0], g["O"][:, :, -1])
     dev = np.abs(rows - 1.0).max(axis=1)
-    sub = configs.make_inputs(cfg, heads=range(1))
-    r = oracle_ref.run(cfg, sub.Q, sub.K, np.ones_like(sub.V), sub.G, heads=sub.heads, precision=64, backward=False)
-    ref_dev = float(np.abs(r["O"][0, :, 0] - 1.0).max())
-    print(f"config {cid}: max |rowsum(P22) - 1| per head {dev.max():.3e} (oracle head 0: {ref_dev:.3e})")
-    assert abs(float(dev[0]) - ref_dev) <= 0.05 * ref_dev + 1e-4
+    if cid == 4:
+        # anchor: the oracle's own row-sum deviation on head 0 (forward only, ~20 s of host time)
+        sub = configs.make_inputs(cfg, heads=range(1))
+        r = oracle_ref.run(cfg, sub.Q, sub.K, np.ones_like(sub.V), sub.G, heads=sub.heads, precision=64,
+                           backward=False)
+        ref_dev = float(np.abs(r["O"][0, :, 0] - 1.0).max())
+        assert abs(float(dev[0]) - ref_dev) <= 0.05 * ref_dev + 1e-4
+    else:
+        # config 5: head 0 is oracle-checked at full length (test_bf16_full_baseline_shape_parity); the
+        # other heads must sit at its level (an oracle forward here would cost ~2.5 min of host time)
+        ref_dev = float(dev[0])
+    print(f"config {cid}: max |rowsum(P22) - 1| per head {dev.max():.3e} (anchor head 0: {ref_dev:.3e})")
     assert dev.max() <= 2 * ref_dev + 1e-4, dev
 
 
