@@ -419,28 +419,35 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float
                         accB = __fadd2_rn(accB, eb);
                     }
                 };
-                const int qlast0 = P ? 2 : ((qd + 1) >> 2);   // last chunk of round 0
-                const int qlast1 = P ? ((qd + 7) >> 2) : ((qd + 3) >> 2);
-                for (int q = 0; q <= qlast0; ++q) mbar_wait(&s.t_full[(tseq + q) & (NST - 1)], ((tseq + q) / NST) & 1);
+                // part 1 first exponentiates its TMEM-resident tile 8 (slice qd + 8, chunk 2) and stores it
+                // back before any register tile is loaded, so at most 4 tiles (64 registers) are ever live
+                if (P) {
+                    for (int q = 0; q <= 2; ++q) mbar_wait(&s.t_full[(tseq + q) & (NST - 1)], ((tseq + q) / NST) & 1);
+                    tc_fence_after();
+                    tc_ld16x256(tile_addr(4), x8);
+                    tc_wait_ld();
+                    exp_tile(x8, 4);
+                    tc_st16x256(tile_addr(4), x8);
+                    tc_wait_st();
+                }
+                const int qlast0 = (qd + j0 + 1) >> 2;  // last chunk of round 0 (tiles 0, 1)
+                const int qlast1 = (qd + j0 + 3) >> 2;
+                if (!P)
+                    for (int q = 0; q <= qlast0; ++q) mbar_wait(&s.t_full[(tseq + q) & (NST - 1)], ((tseq + q) / NST) & 1);
                 tc_fence_after();
                 if (warp == 2 && lane == 0 && gi - g_begin == 4) FS_TRACE(58);
                 tc_ld16x256(tile_addr(0), e[0]);
                 tc_ld16x256(tile_addr(1), e[1]);
-                if (P) tc_ld16x256(tile_addr(4), x8);
                 tc_wait_ld();
                 if (warp == 2 && lane == 0 && gi - g_begin == 4) FS_TRACE(59);
-                for (int q = qlast0 + 1; q <= qlast1; ++q) mbar_wait(&s.t_full[(tseq + q) & (NST - 1)], ((tseq + q) / NST) & 1);
+                if (!P)
+                    for (int q = qlast0 + 1; q <= qlast1; ++q) mbar_wait(&s.t_full[(tseq + q) & (NST - 1)], ((tseq + q) / NST) & 1);
                 tc_fence_after();
                 tc_ld16x256(tile_addr(2), e[2]);
                 tc_ld16x256(tile_addr(3), e[3]);
                 exp_tile(e[0], 0);
                 exp_tile(e[1], 1);
-                if (P) {
-                    exp_tile(x8, 4);
-                    tc_st16x256(tile_addr(4), x8);
-                }
                 tc_wait_ld();
-                if (P) tc_wait_st();
                 if (warp == 2 && lane == 0 && gi - g_begin == 4) FS_TRACE(60);
                 // every tile loaded: release the chunks (part 1 keeps chunk 2 for its TMEM-resident tile)
                 tc_fence_before();
