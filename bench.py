@@ -66,10 +66,13 @@ def workload_str(cfg):
             + (",dustbin" if cfg.dustbin else ""))
 
 
-def config_obj(cfg, world):
-    return {"workload": workload_str(cfg), "seed": 0, "mode": "one_reference",
-            "parallelism": (f"batch x head: the {cfg.B * cfg.H} (b,h) problems split contiguously over {world} GPU(s), "
-                            "no operator collective"),
+def config_obj(cfg, world, seqshard=False):
+    par = (f"sequence: L={cfg.L} split contiguously over {world} GPU(s) in 128-row blocks (all {cfg.B * cfg.H} heads "
+           f"per GPU), w={cfg.w}-wide halo of every dual / adjoint vector exchanged with NCCL point-to-point after "
+           "each producing kernel (shard.nccl_halo)") if seqshard else \
+          (f"batch x head: the {cfg.B * cfg.H} (b,h) problems split contiguously over {world} GPU(s), "
+           "no operator collective")
+    return {"workload": workload_str(cfg), "seed": 0, "mode": "one_reference", "parallelism": par,
             "l2": "inputs > L2 (126 MB) and a 256 MiB flush write between timed steps"}
 
 
@@ -116,7 +119,7 @@ def run_reference(args):
         "impl": "reference", "metric": "fwd+bwd band-cells/s", "value": v, "unit": "band-cells/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
-        "config": config_obj(cfg, args.gpus),
+        "config": config_obj(cfg, args.gpus, seqshard=(args.seqshard or cfg.cid == 5) and args.gpus > 1),
         "cpu_baseline": {"value": v, "unit": "band-cells/s", "cores": threads, "kind": "port", "sample": desc,
                          "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": "band-cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -197,6 +200,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--e2e-depth", type=int, default=2, help="pipeline depth of the e2e H2D / compute / D2H overlap")
+    ap.add_argument("--seqshard", action="store_true",
+                    help="shard the sequence (not the heads) over the ranks; default for --config 5 (SURVEY §8(e))")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -215,6 +220,12 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    if (args.seqshard or cfg.cid == 5) and world > 1 or args.seqshard:
+        if not dist.is_initialized():  # --seqshard on one GPU without torchrun: a one-rank group
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+        return run_seqshard(args, cfg, rank, world, local, dev)
 
     def barrier():
         if world > 1:
@@ -465,6 +476,74 @@ def main():
         print(json.dumps(line, default=lambda o: o.item() if hasattr(o, "item") else str(o)), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def run_seqshard(args, cfg, rank, world, local, dev):
+    """Config 5 across the ranks of one node: rank r owns a contiguous block-aligned slice of the
+    sequence for every head and runs the operator on its window (own rows + w-wide halos) through
+    st_forward_halo / st_backward_halo; the halo of every dual and adjoint vector is completed by NCCL
+    point-to-point right after the kernel that produces it (shard.nccl_halo).  value = the whole
+    config's band-cells per step / max-over-ranks device time (strong scaling)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2605_08123_b200 import band, configs, shard
+    plan = shard.SeqShard(L=cfg.L, w=cfg.w, world=world, rank=rank)
+    win = plan.window
+    hl = plan.rows.start - win.start
+    own = range(hl, hl + len(plan.rows))
+    inp = configs.make_inputs(cfg)
+    nh = cfg.B * cfg.H
+    spec = band.BandSpec(batch=cfg.B, heads=cfg.H, seq_q=len(win), seq_k=len(win), head_dim=cfg.d, half_band=cfg.w,
+                         base_depth=cfg.T, tail_depth=cfg.R, epsilon=cfg.eps, dtype=cfg.dtype)
+    shp = (cfg.B, cfg.H, len(win), cfg.d)
+
+    def dev_t(k):
+        x = inp.bits[k].reshape(cfg.B, cfg.H, cfg.L, cfg.d)[:, :, win.start:win.stop]
+        return torch.from_numpy(np.ascontiguousarray(x).astype(np.int16)).view(torch.bfloat16).to(dev).reshape(shp)
+    Q, K, V, G = (dev_t(k) for k in ("Q", "K", "V", "G"))
+    del inp
+    ex = shard.nccl_halo(plan)
+    stream = torch.cuda.Stream(dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step():
+        return shard.sharded_forward_backward(spec, Q, K, V, G, None, None, ex, own)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize(dev)
+        band.launch_count(reset=True)
+        step()
+        launches = band.launch_count(reset=True)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        with ClockSampler(local) as clk:
+            for s_, e_ in evs:
+                flush.zero_()
+                s_.record(stream)
+                step()
+                e_.record(stream)
+            torch.cuda.synchronize(dev)
+        dist.barrier()
+    ms = float(statistics.mean(s_.elapsed_time(e_) for s_, e_ in evs))
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = cfg.nominal_cell_steps() / (ms_max * 1e-3)
+    if rank == 0:
+        conf = config_obj(cfg, world, seqshard=True)
+        conf.update({"cuda_graph": False, "rows_per_gpu": len(plan.rows), "window_per_gpu": len(win),
+                     "active_cells_per_step": configs.active_cells(cfg), "nominal_cells_per_step": cfg.nominal_cells()})
+        line = {"metric": "fwd+bwd band-cells/s", "value": value, "unit": "band-cells/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic", "config": conf,
+                "roofline": None, "cpu_baseline": None, "e2e": None,
+                "gpu_launches": int(launches * args.steps), "clocks": clk.summary()}
+        print(json.dumps(line, default=lambda o: o.item() if hasattr(o, "item") else str(o)), flush=True)
+    dist.destroy_process_group()
     return 0
 
 
