@@ -817,35 +817,34 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float
 // v^t_j = v^{t-1}_j - lg2( sum_{I : rows of I meet band(j)} c_Ij ), ascending I.
 // pad_v in place (-inf stays on inactive / guard entries); v_out (standard layout).
 // ---------------------------------------------------------------------------
-__global__ void k_vmerge(const float* __restrict__ part, float* __restrict__ pad_v, float* __restrict__ v_out,
-                         int BH, int H, int Lq, int Lk, int Lrk, int NB, int maxwin, int w, int CR, int shift,
-                         int Lp_other, int pad_ld, int pad_off, const uint8_t* __restrict__ col_mask,
-                         int* __restrict__ err) {
-    const long n = (long)BH * Lk;
-    for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long)gridDim.x * blockDim.x) {
-        const int bh = (int)(t / Lk), j = (int)(t % Lk);
-        float* pv = pad_v + (size_t)bh * pad_ld + pad_off + j;
-        const float vold = *pv;
-        float v = 0.f;
-        if (vold != -INFINITY) {  // active column (the padded buffer carries the mask)
-            const int I0 = max(0, j - w) / 128, I1 = min(Lq - 1, j + w) / 128;
-            const int nq = Lp_other / CR;
-            float sum = 0.f;
-            for (int I = I0; I <= I1; ++I) {
-                const int q0 = max(0, (I * 128 - w + shift) / CR);
-                (void)nq;
-                const int wc = j - (q0 * CR - shift);
-                sum += part[((size_t)bh * NB + I) * maxwin + wc];
-            }
-            v = vold - lg2(sum);
-            if (!(sum > 0.f) || !isfinite(v)) {
-                atomicOr(err, 8);
-                v = 0.f;
-            }
-            *pv = v;
+__global__ void __launch_bounds__(256) k_vmerge(const float* __restrict__ part, float* __restrict__ pad_v,
+                                                float* __restrict__ v_out, int BH, int H, int Lq, int Lk, int Lrk,
+                                                int NB, int maxwin, int w, int CR, int shift, int Lp_other, int pad_ld,
+                                                int pad_off, const uint8_t* __restrict__ col_mask, int* __restrict__ err) {
+    // grid (ceil(Lk / 256), BH): 32-bit indices, no divisions on the element path (CR is 64 or 128)
+    const int bh = blockIdx.y;
+    const int j = blockIdx.x * 256 + threadIdx.x;
+    if (j >= Lk) return;
+    const int lcr = CR == 128 ? 7 : 6;
+    float* pv = pad_v + (size_t)bh * pad_ld + pad_off + j;
+    const float vold = *pv;
+    float v = 0.f;
+    if (vold != -INFINITY) {  // active column (the padded buffer carries the mask)
+        const int I0 = max(0, j - w) >> 7, I1 = min(Lq - 1, j + w) >> 7;
+        const float* pb = part + (size_t)bh * NB * maxwin;
+        float sum = 0.f;
+        for (int I = I0; I <= I1; ++I) {
+            const int q0 = max(0, (I * 128 - w + shift) >> lcr);  // first window chunk of block I
+            sum += pb[(size_t)I * maxwin + (j - ((q0 << lcr) - shift))];
         }
-        if (v_out) v_out[(size_t)bh * Lrk + j] = v;
+        v = vold - lg2(sum);
+        if (!(sum > 0.f) || !isfinite(v)) {
+            atomicOr(err, 8);
+            v = 0.f;
+        }
+        *pv = v;
     }
+    if (v_out) v_out[(size_t)bh * Lrk + j] = v;
 }
 
 static thread_local long long g_fs_launches = 0;
@@ -883,10 +882,8 @@ cudaError_t launch_fstep16(const PhaseArgs& a, float* part, bool first, int grid
 cudaError_t launch_vmerge(const float* part, float* pad_v, float* v_out, int BH, int H, int Lq, int Lk, int Lrk, int NB,
                           int maxwin, int w, int CR, int shift, int Lp_other, int pad_ld, int pad_off,
                           const uint8_t* col_mask, int* err, cudaStream_t s) {
-    const long n = (long)BH * Lk;
-    const int nb = (int)std::min<long>((n + 255) / 256, 148L * 16);
-    k_vmerge<<<nb, 256, 0, s>>>(part, pad_v, v_out, BH, H, Lq, Lk, Lrk, NB, maxwin, w, CR, shift, Lp_other, pad_ld,
-                                pad_off, col_mask, err);
+    k_vmerge<<<dim3((Lk + 255) / 256, BH), 256, 0, s>>>(part, pad_v, v_out, BH, H, Lq, Lk, Lrk, NB, maxwin, w, CR,
+                                                          shift, Lp_other, pad_ld, pad_off, col_mask, err);
     ++g_fs_launches;
     return cudaGetLastError();
 }
