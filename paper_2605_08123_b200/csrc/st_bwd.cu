@@ -1188,6 +1188,32 @@ __global__ void __launch_bounds__(256, (D <= 64 ? 3 : 2)) k_bwdW(Geo g, BT<TIn> 
     }
 }
 
+
+// 8 bf16 packed in 4 words (element e in word e >> 1, half e & 1): out[(rot + e) & 7] = in[e]
+__device__ __forceinline__ void rot8_bf16(uint32_t (&w)[4], int rot) {
+    if (rot & 1) {  // by one element: out[e + 1] = in[e]
+        const uint32_t t3 = w[3];
+        w[3] = __byte_perm(w[2], w[3], 0x5432);
+        w[2] = __byte_perm(w[1], w[2], 0x5432);
+        w[1] = __byte_perm(w[0], w[1], 0x5432);
+        w[0] = __byte_perm(t3, w[0], 0x5432);
+    }
+    if (rot & 2) {  // by one word
+        const uint32_t t = w[3];
+        w[3] = w[2];
+        w[2] = w[1];
+        w[1] = w[0];
+        w[0] = t;
+    }
+    if (rot & 4) {  // by two words
+        uint32_t t = w[0];
+        w[0] = w[2];
+        w[2] = t;
+        t = w[1];
+        w[1] = w[3];
+        w[3] = t;
+    }
+}
 // ---------------------------------------------------------------------------
 // bf16 operands: the window-chunked vector stages with the chunk GEMM on tcgen05.  Per 16-column
 // window chunk: phase 1 (as k_bwdW) writes the weights as two bf16 planes W = hi + lo (16 bits of
@@ -1351,10 +1377,14 @@ __global__ void __launch_bounds__(256, (kOp == C1 || kOp == RO) ? 3 : 2) k_bwdM(
         const TIn* X = stX(s);
         uint8_t* Ap = Abuf + ab * WP * AB;
         uint8_t* Bt = Bbuf + ab * XP * BB;
-        // ---- phase 1: 8 weights of row r (columns 8 hh .. 8 hh + 7), rotated reads, bf16 hi / lo planes
+        // ---- phase 1: 8 weights of row r (columns 8 hh .. 8 hh + 7), rotated reads (conflict-free strip
+        // reads), bf16 hi / lo planes; the 8 values are rotated back into column order in registers and
+        // stored as ONE 16-byte core-matrix row per plane (2-byte stores were 4-way bank-conflicted)
+        const int rot = (r + 2 * (r >> 3)) & 7;
+        uint32_t hw[4], mw[4], lw[4];  // bf16 pairs in rotated order: element jj = column (rot + jj) & 7
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
-            const int pos = (r + jj + 2 * (r >> 3)) & 7, cl = 8 * hh + pos;
+            const int pos = (rot + jj) & 7, cl = 8 * hh + pos;
             const int c = c0 + cl;
             const float s2 = S[r * SP + cl];
             float wgt = 0.f;
@@ -1391,11 +1421,25 @@ __global__ void __launch_bounds__(256, (kOp == C1 || kOp == RO) ? 3 : 2) k_bwdM(
             const __nv_bfloat16 hi = __float2bfloat16_rn(wgt);
             const float r1 = wgt - __bfloat162float(hi);  // exact in fp32
             const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-            *reinterpret_cast<__nv_bfloat16*>(Ap + a_off + pos * 2) = hi;
-            *reinterpret_cast<__nv_bfloat16*>(Ap + AB + a_off + pos * 2) = mid;
-            if (WP == 3)
-                *reinterpret_cast<__nv_bfloat16*>(Ap + 2 * AB + a_off + pos * 2) =
-                    __float2bfloat16_rn(r1 - __bfloat162float(mid));
+            const uint32_t hb = __bfloat16_as_ushort(hi), mb16 = __bfloat16_as_ushort(mid);
+            const uint32_t lb = WP == 3 ? __bfloat16_as_ushort(__float2bfloat16_rn(r1 - __bfloat162float(mid))) : 0u;
+            if (jj & 1) {
+                hw[jj >> 1] |= hb << 16;
+                mw[jj >> 1] |= mb16 << 16;
+                lw[jj >> 1] |= lb << 16;
+            } else {
+                hw[jj >> 1] = hb;
+                mw[jj >> 1] = mb16;
+                lw[jj >> 1] = lb;
+            }
+        }
+        rot8_bf16(hw, rot);
+        rot8_bf16(mw, rot);
+        *reinterpret_cast<uint4*>(Ap + a_off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(Ap + AB + a_off) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+        if (WP == 3) {
+            rot8_bf16(lw, rot);
+            *reinterpret_cast<uint4*>(Ap + 2 * AB + a_off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
         }
         // ---- B operand: X^T of the chunk, K-major core matrices (n = output column, k = window column)
         for (int u = tid; u < D * 2; u += 256) {
