@@ -94,6 +94,13 @@ typedef struct st_desc {
  * pointers (host-side registry); the caller must not have written the workspace
  * or Q/K in between.  Otherwise the band is recomputed. */
 #define ST_FLAG_REUSE_BAND 2
+/* bf16 problems whose band lines up with 64-column chunks (no dustbin, seq_q == seq_k, half_band a
+ * multiple of 64, head_dim 64 or 128 -- BASELINE configs 4 and 5) run band-free by default: the
+ * transport output and the R=2 backward recompute their score / cotangent tiles on the tensor cores
+ * and st_workspace_bytes() is O(L d), with no L x W band.  ST_FLAG_STORED_BAND selects the
+ * stored-band kernels (and their O(L W) workspace) instead; mode ST_GENERIC_TAIL and the *_halo
+ * entry points need it on such problems and return ST_NOT_SUPPORTED without it. */
+#define ST_FLAG_STORED_BAND 4
 
 /* Device bytes of the opaque saved state written by st_forward and read by
  * st_backward: fp32 tail duals u, v at steps T, T+1, T+2 plus the per-head

@@ -28,6 +28,7 @@ ST_F32 = 0
 ST_BF16 = 1
 ST_FLAG_GENERIC = 1
 ST_FLAG_REUSE_BAND = 2
+ST_FLAG_STORED_BAND = 4
 ST_MAX_STAGES = 8
 ST_ONE_REFERENCE = 0
 ST_DIRECT_FOUR_PLAN = 1

@@ -90,6 +90,7 @@ class BandSpec:
     dustbin_cost: float = 1.0
     centered: bool = True
     generic: bool = False       # force the generic (non-tensor-core) kernels (testing / ablation)
+    stored_band: bool = False   # bf16 problems that would run band-free: keep the stored-band kernels
     # EpsSchedule of the base solve (trace.hpp:12-50): ((epsilon, iterations), ...), non-increasing
     # temperatures, iterations summing to base_depth, the last stage at `epsilon`.  None: one stage.
     eps_schedule: Optional[Sequence[Tuple[float, int]]] = None
@@ -99,7 +100,8 @@ class BandSpec:
                         self.base_depth, self.tail_depth, float(self.epsilon),
                         _lib.ST_BF16 if self.dtype == "bf16" else _lib.ST_F32, int(self.dustbin),
                         float(self.dustbin_cost), int(bool(self.centered)),
-                        _lib.ST_FLAG_GENERIC if self.generic else 0)
+                        (_lib.ST_FLAG_GENERIC if self.generic else 0) |
+                        (_lib.ST_FLAG_STORED_BAND if self.stored_band else 0))
         if self.eps_schedule:
             n = len(self.eps_schedule)
             d._eps = (ctypes.c_double * n)(*[float(e) for e, _ in self.eps_schedule])  # kept alive by d
@@ -297,6 +299,8 @@ def _backward(run, G, m, grads, d_eps, eta_v, workspace, want_eta_u=False) -> Co
     if eta_v is None:
         eta_v = torch.empty((spec.batch, spec.heads, spec.cols), dtype=torch.float32, device=dev)
     wso = workspace or _default_ws
+    if want_eta_u:  # the generic tail adjoint runs on the stored-band kernels
+        spec = dataclasses.replace(spec, stored_band=True)
     ws = wso.get(spec.workspace_bytes(), dev)
     d = spec.desc()
     if wso is run.workspace and wso.last_forward is run:

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "../../include/sinkattn.h"
+#include "st_bfree.cuh"
 #include "st_kernels.cuh"
 #include "st_phase.cuh"
 
@@ -106,6 +107,9 @@ st::Geo make_geo(const st_desc* d, const Dims& m, const uint8_t* rm, const uint8
     return g;
 }
 
+struct TcPlan;
+st::BfGeo make_bfgeo(const st::Geo& g, const TcPlan& tp);
+
 // saved-state layout (fp32, base-2 raw duals): u[NS][BH][Lrq] | v[NS][BH][Lrk] | gauge[3][BH] | status int
 // with NS = max(3, R + 1) tail slots (steps T .. T+R; the generic-R adjoint reads all of them)
 constexpr long kMaxTail = 8;
@@ -175,6 +179,25 @@ TcPlan tc_plan(const st_desc* d, const Dims& m) {
     return p;
 }
 
+st::BfGeo make_bfgeo(const st::Geo& g, const TcPlan& tp) {
+    st::BfGeo b;
+    b.BH = g.BH;
+    b.H = g.H;
+    b.Lq = g.Lq;
+    b.Lk = g.Lk;
+    b.Lrq = g.Lrq;
+    b.Lrk = g.Lrk;
+    b.Lpq = tp.Lpq;
+    b.Lpk = tp.Lpk;
+    b.d = g.d;
+    b.w = g.w;
+    b.c2 = g.c2;
+    b.inv_qk = g.inv_qk;
+    b.row_mask = g.row_mask;
+    b.col_mask = g.col_mask;
+    return b;
+}
+
 // Full-step solve (k_fstep16): bf16 planes, 128-column chunks, the block's window (<= 3 chunks)
 // resident in TMEM next to one free slot, no dustbin / sequence-sharding hook.  SMEM plan: NA, NSK.
 struct FsPlan {
@@ -213,6 +236,8 @@ struct WsLayout {
     size_t tail_u, tail_v;  // generic-R adjoint: (R+1) row / column cotangent vectors
     size_t dpart;           // dustbin line partials [BH][8][129]
     size_t fpart;           // full-step bf16 solve: column partials [BH][NBq][maxwin]
+    size_t vp, gp, bfvec;   // band-free sweeps: packed V and dO planes, O(L) vector workspace
+    bool bfree;             // band-free output + backward: no S2 / S2T / Z / ZT bands in the workspace
     size_t bytes;
 };
 
@@ -276,8 +301,18 @@ void fstep_trace_dump(const unsigned long long* dbuf) {
     }
 }
 
-WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
+// Band-free transport output + R=2 backward (st_bfree.cu): bf16 planes whose 64-column chunk grid
+// lines up with every band window; square problems, no dustbin.  ST_FLAG_STORED_BAND keeps the
+// stored-band kernels (generic-R tail adjoint, base_solve_vjp and the sequence-sharded variants need them).
+bool bfree_plan(const st_desc* d, const Dims& m, const TcPlan& tp) {
+    if (!tp.ok || tp.npl != 1 || tp.shift != 0 || m.Lq != m.Lk) return false;
+    if (d->flags & (ST_FLAG_GENERIC | ST_FLAG_STORED_BAND)) return false;
+    return st::bfree_supported((int)m.d, (int)m.w, d->dustbin, m.esz);
+}
+
+WsLayout ws_layout(const Dims& m, const TcPlan& tp, bool bf) {
     WsLayout w;
+    w.bfree = bf;
     size_t o = 0;
     auto take = [&](size_t n) {
         const size_t at = o;
@@ -286,7 +321,7 @@ WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
     };
     const size_t rq = sizeof(float) * m.BH * m.Lrq, rk = sizeof(float) * m.BH * m.Lrk;
     const size_t Lqp = (m.Lq + 127) / 128 * 128, Lkp = (m.Lk + 127) / 128 * 128;
-    w.S2 = take(sizeof(float) * (size_t)m.BH * Lqp * m.Wf);
+    w.S2 = bf ? 0 : take(sizeof(float) * (size_t)m.BH * Lqp * m.Wf);
     // transposed band (fp32 tile forward and the tile backward) and the cotangent bands
     st::Geo gg{};
     gg.d = (int)m.d;
@@ -294,9 +329,9 @@ WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
     gg.Wf = (int)m.Wf;
     gg.esz = m.esz;
     gg.dustbin = m.dustbin;
-    const bool bt = st::bwdT_supported(gg);
+    const bool bt = st::bwdT_supported(gg) && !bf;
     const size_t band_q = sizeof(float) * (size_t)m.BH * Lqp * m.Wf, band_k = sizeof(float) * (size_t)m.BH * Lkp * m.Wf;
-    w.S2T = (!tp.ok || bt) ? take(band_k) : 0;
+    w.S2T = (!bf && (!tp.ok || bt)) ? take(band_k) : 0;
     w.Z = bt ? take(band_q) : 0;
     w.ZT = bt ? take(band_k) : 0;
     w.Zd = bt ? take(sizeof(float) * (size_t)m.BH * Lqp) : 0;
@@ -317,7 +352,8 @@ WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
     for (int p = 0; p < 3; ++p) w.qp[p] = w.kp[p] = 0;
     w.flags = w.work_q = w.work_k = w.cnt = w.pad_u = w.pad_v = 0;
     w.vb2 = take(rk);
-    {
+    w.part[0] = w.part[1] = w.partm = w.fs_flags = w.fs_work = w.fs_cnt = w.fs_part[0] = w.fs_part[1] = w.fs_partm = 0;
+    if (!bf) {  // fp32 fused / persistent solves
         const size_t np = sizeof(float) * (size_t)m.BH * ((m.Lq + 127) / 128) * (128 + 2 * m.w);
         w.part[0] = take(np);
         w.part[1] = take(np);
@@ -345,6 +381,12 @@ WsLayout ws_layout(const Dims& m, const TcPlan& tp) {
         w.fpart = take(sizeof(float) * (size_t)m.BH * tp.NBq * tp.maxwin);
     } else {
         w.fpart = 0;
+    }
+    w.vp = w.gp = w.bfvec = 0;
+    if (bf) {
+        w.vp = take((size_t)m.BH * tp.Lpk * tp.row_bytes);
+        w.gp = take((size_t)m.BH * tp.Lpq * tp.row_bytes);
+        w.bfvec = take(st::bfree_vec_bytes((int)m.BH, tp.Lpq, tp.Lpk));
     }
     w.bytes = o;
     return w;
@@ -442,7 +484,8 @@ size_t st_saved_bytes(const st_desc* desc) {
 size_t st_workspace_bytes(const st_desc* desc) {
     Dims m;
     if (check_desc(desc, m) != ST_OK) return 0;
-    return ws_layout(m, tc_plan(desc, m)).bytes;
+    const TcPlan tp = tc_plan(desc, m);
+    return ws_layout(m, tp, bfree_plan(desc, m, tp)).bytes;
 }
 
 // Score scale of full step t (1-based) relative to the final temperature: the band is stored at
@@ -463,7 +506,7 @@ namespace {
 struct BandKey {
     const void *Q, *K, *rm, *cm;
     st_desc d;
-    bool hasT;  // the transposed band S2T is valid too
+    int kind;  // 1: score band S2; 2: S2 and its transpose S2T; 3: packed Q / K planes only (band-free)
 };
 std::mutex g_band_mu;
 std::unordered_map<const void*, BandKey> g_band;
@@ -473,11 +516,11 @@ bool same_desc(const st_desc& a, const st_desc& b) {
            a.dustbin == b.dustbin && a.dustbin_cost == b.dustbin_cost;
 }
 void band_record(const void* ws, const void* Q, const void* K, const void* rm, const void* cm, const st_desc* d,
-                 bool hasT) {
+                 int kind) {
     std::lock_guard<std::mutex> lk(g_band_mu);
-    g_band[ws] = BandKey{Q, K, rm, cm, *d, hasT};
+    g_band[ws] = BandKey{Q, K, rm, cm, *d, kind};
 }
-// 0: nothing reusable, 1: S2 band, 2: S2 and S2T
+// 0: nothing reusable, 1: S2 band, 2: S2 and S2T, 3: packed planes
 void band_forget(const void* ws) {
     std::lock_guard<std::mutex> lk(g_band_mu);
     g_band.erase(ws);
@@ -489,7 +532,7 @@ int band_valid(const void* ws, const void* Q, const void* K, const void* rm, con
     if (it == g_band.end() || it->second.Q != Q || it->second.K != K || it->second.rm != rm || it->second.cm != cm ||
         !same_desc(it->second.d, *d))
         return 0;
-    return it->second.hasT ? 2 : 1;
+    return it->second.kind;
 }
 }  // namespace
 
@@ -507,7 +550,10 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
         if (hook) hook(user, kind, vec, kind == 0 ? m.BH * m.Lrq : m.BH * m.Lrk, stream);
     };
     const TcPlan tp = tc_plan(desc, m);
-    const WsLayout wl = ws_layout(m, tp);
+    const bool bf = bfree_plan(desc, m, tp);
+    if (bf && hook)
+        return fail(ST_NOT_SUPPORTED, "sequence sharding runs on the stored-band kernels: set ST_FLAG_STORED_BAND");
+    const WsLayout wl = ws_layout(m, tp, bf);
     if (workspace == nullptr || workspace_bytes < wl.bytes)
         return fail(ST_WORKSPACE_TOO_SMALL, "workspace smaller than st_workspace_bytes()");
     cudaStream_t st = (cudaStream_t)stream;
@@ -658,6 +704,15 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
             u_prev = u_out;
             v_prev = v_out;
         }
+        if (bf) {
+            // band-free transport application: O = P V from the packed planes, one tcgen05 sweep
+            uint8_t* vp = (uint8_t*)(ws + wl.vp);
+            ST_CUDA(st::launch_pack(desc->dtype, V, g.BH, g.Lk, g.Lrk, tp.Lpk, g.d, 0, vp, nullptr, nullptr, st));
+            ST_CUDA(st::launch_bfree_output(make_bfgeo(g, tp), qp[0], kp[0], vp, u_prev, v_prev,
+                                            (float*)(ws + wl.bfvec), O, st));
+            band_record(workspace, Q, K, row_mask, col_mask, desc, 3);
+            return ST_OK;
+        }
         if (tp.npl == 1 && !getenv("ST_NO_TCBAND")) {
             // the stored score band (transport application, backward reuse) from the packed planes on
             // tcgen05 -- the same fp32-accumulated scores the solve used; the transposed band from the
@@ -794,7 +849,7 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
     }
     // the gauge ledger (mean of the valid raw u, center() in sinkhorn.hpp:109-140) is only needed by
     // st_saved_duals, which reads the saved duals to the host anyway and computes it there in f64
-    band_record(workspace, Q, K, row_mask, col_mask, desc, dualT);
+    band_record(workspace, Q, K, row_mask, col_mask, desc, dualT ? 2 : 1);
     return ST_OK;
 }
 
@@ -818,7 +873,12 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
         return fail(ST_NOT_SUPPORTED, "the generic tail adjoint has no dustbin / sequence-sharded variant");
     if (saved == nullptr) return fail(ST_MISSING_BASE_TRACE, "backward needs the forward's saved state");
     if (!Q || !K || !V || !dO || !dQ || !dK || !dV) return fail(ST_INVALID_ARGUMENT, "null tensor pointer");
-    const WsLayout wl = ws_layout(m, tc_plan(desc, m));
+    const TcPlan tpl = tc_plan(desc, m);
+    const bool bf = bfree_plan(desc, m, tpl);
+    if (bf && (hook || generic_tail))
+        return fail(ST_NOT_SUPPORTED,
+                    "the generic tail adjoint and sequence sharding run on the stored-band kernels: set ST_FLAG_STORED_BAND");
+    const WsLayout wl = ws_layout(m, tpl, bf);
     if (workspace == nullptr || workspace_bytes < wl.bytes)
         return fail(ST_WORKSPACE_TOO_SMALL, "workspace smaller than st_workspace_bytes()");
     cudaStream_t st = (cudaStream_t)stream;
@@ -827,6 +887,41 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
     const SavedLayout sl = saved_layout(m);
     const float* su = (const float*)((const char*)saved + sl.u);
     const float* svv = (const float*)((const char*)saved + sl.v);
+    if (bf) {
+        // ---- band-free exact R=2 adjoint: six tcgen05 sweeps over the packed planes (st_bfree.cu)
+        const bool packed = (desc->flags & ST_FLAG_REUSE_BAND) && !getenv("ST_NO_REUSE") &&
+                            band_valid(workspace, Q, K, row_mask, col_mask, desc) == 3;
+        st::BfBwd b{};
+        uint8_t* qp0 = (uint8_t*)(ws + wl.qp[0]);
+        uint8_t* kp0 = (uint8_t*)(ws + wl.kp[0]);
+        uint8_t* vp0 = (uint8_t*)(ws + wl.vp);
+        uint8_t* gp0 = (uint8_t*)(ws + wl.gp);
+        if (!packed) {
+            ST_CUDA(st::launch_pack(desc->dtype, Q, g.BH, g.Lq, g.Lrq, tpl.Lpq, g.d, 0, qp0, nullptr, nullptr, st));
+            ST_CUDA(st::launch_pack(desc->dtype, K, g.BH, g.Lk, g.Lrk, tpl.Lpk, g.d, 0, kp0, nullptr, nullptr, st));
+        }
+        ST_CUDA(st::launch_pack(desc->dtype, V, g.BH, g.Lk, g.Lrk, tpl.Lpk, g.d, 0, vp0, nullptr, nullptr, st));
+        ST_CUDA(st::launch_pack(desc->dtype, dO, g.BH, g.Lq, g.Lrq, tpl.Lpq, g.d, 0, gp0, nullptr, nullptr, st));
+        b.qp = qp0;
+        b.kp = kp0;
+        b.vp = vp0;
+        b.gp = gp0;
+        b.u1 = su + (size_t)1 * m.BH * m.Lrq;
+        b.u2 = su + (size_t)2 * m.BH * m.Lrq;
+        b.v0 = svv;
+        b.v1 = svv + (size_t)1 * m.BH * m.Lrk;
+        b.v2 = svv + (size_t)2 * m.BH * m.Lrk;
+        b.V = V;
+        b.vec = (float*)(ws + wl.bfvec);
+        b.dQ = dQ;
+        b.dK = dK;
+        b.dV = dV;
+        b.deps_part = (float*)(ws + wl.deps);
+        b.eta_v = eta_v ? eta_v : (float*)(ws + wl.v0b);
+        ST_CUDA(st::launch_bfree_backward(make_bfgeo(g, tpl), b, mode == ST_DIRECT_FOUR_PLAN, st));
+        if (d_eps) ST_CUDA(st::launch_deps_reduce(g, b.deps_part, d_eps, st, 0, (int)m.Lrq));
+        return ST_OK;
+    }
     st::BwdPtrs p;
     p.S2 = (float*)(ws + wl.S2);
     p.u1 = su + (size_t)1 * m.BH * m.Lrq;
@@ -848,16 +943,17 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
     p.dQ = dQ;
     p.dK = dK;
     p.dV = dV;
-    const int reuse = (!hook && (desc->flags & ST_FLAG_REUSE_BAND) && !(desc->flags & ST_FLAG_GENERIC) && !getenv("ST_NO_REUSE"))
-                          ? band_valid(workspace, Q, K, row_mask, col_mask, desc)
-                          : 0;
+    int reuse = (!hook && (desc->flags & ST_FLAG_REUSE_BAND) && !(desc->flags & ST_FLAG_GENERIC) && !getenv("ST_NO_REUSE"))
+                    ? band_valid(workspace, Q, K, row_mask, col_mask, desc)
+                    : 0;
+    if (reuse == 3) reuse = 0;  // a band-free forward left only packed planes
     const bool tiled = st::bwdT_supported(g) && !(desc->flags & ST_FLAG_GENERIC);
     if (hook && !tiled) return fail(ST_NOT_SUPPORTED, "sequence sharding needs the tiled backward (d in {32,64,128})");
     if (generic_tail && !tiled) return fail(ST_NOT_SUPPORTED, "the generic tail adjoint needs d in {32, 64, 128}");
     const bool dual = tiled && st::band_dual_supported(g);
     bool haveT = reuse == 2;
     // bf16 planes: the bands on tcgen05 (the forward's solve and band used the same scores)
-    const TcPlan tpb = tc_plan(desc, m);
+    const TcPlan& tpb = tpl;
     const bool tcb = tiled && dual && tpb.ok && tpb.npl == 1 && !getenv("ST_NO_TCBAND");
     float* pad_u = tcb ? (float*)(ws + wl.pad_u) : nullptr;
     float* pad_v = tcb ? (float*)(ws + wl.pad_v) : nullptr;
@@ -998,7 +1094,7 @@ static BaseVjpLayout base_vjp_layout(const Dims& m, size_t base) {
 size_t st_base_vjp_workspace_bytes(const st_desc* desc) {
     Dims m;
     if (check_desc(desc, m) != ST_OK) return 0;
-    return base_vjp_layout(m, ws_layout(m, tc_plan(desc, m)).bytes).bytes;
+    return base_vjp_layout(m, ws_layout(m, tc_plan(desc, m), false).bytes).bytes;
 }
 
 st_status st_base_solve_vjp(const st_desc* desc, const void* Q, const void* K, const uint8_t* row_mask,
@@ -1009,7 +1105,7 @@ st_status st_base_solve_vjp(const st_desc* desc, const void* Q, const void* K, c
     if (s != ST_OK) return s;
     if (!Q || !K || !eta_v || !dQ || !dK) return fail(ST_INVALID_ARGUMENT, "null tensor pointer");
     if (desc->dustbin) return fail(ST_NOT_SUPPORTED, "base_solve_vjp has no dustbin variant");
-    const WsLayout wl = ws_layout(m, tc_plan(desc, m));
+    const WsLayout wl = ws_layout(m, tc_plan(desc, m), false);  // always the stored-band layout
     const BaseVjpLayout bl = base_vjp_layout(m, wl.bytes);
     if (workspace == nullptr || workspace_bytes < bl.bytes)
         return fail(ST_WORKSPACE_TOO_SMALL, "workspace smaller than st_base_vjp_workspace_bytes()");

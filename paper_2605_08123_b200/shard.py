@@ -255,8 +255,10 @@ def sharded_forward_backward(spec, Q, K, V, G, row_mask, col_mask, ex, own_rows:
     import ctypes
     from . import _lib
     from .band import _check, _ptr
+    import dataclasses
     lib = _lib.lib
     dev = Q.device
+    spec = dataclasses.replace(spec, stored_band=True)  # the halo entry points run on the stored-band kernels
     ws = torch.empty(max(spec.workspace_bytes(), 256), dtype=torch.uint8, device=dev)
     saved = torch.empty(spec.saved_bytes(), dtype=torch.uint8, device=dev)
     O = torch.empty((spec.batch, spec.heads, spec.rows, spec.head_dim), dtype=torch.float32, device=dev)
