@@ -104,7 +104,21 @@ def test_saved_state_is_O_of_L():
     s = _spec(batch=8, heads=4, seq_q=2048, seq_k=2048, head_dim=64, half_band=64)
     # 6 vectors of L per head + gauges: never the L x W plan
     assert s.saved_bytes() < 8 * 4 * (6 * 2048 * 4 + 4096)
-    assert s.workspace_bytes() >= 8 * 4 * 2048 * 129 * 4
+    assert s.workspace_bytes() >= 8 * 4 * 2048 * 129 * 4  # fp32 keeps its exact f64-DMMA score band
+
+
+def test_bf16_workspace_holds_no_band():
+    """BASELINE configs 4 / 5 run band-free: the workspace is O(L d) packed planes + O(L) vectors, far
+    below one L x W fp32 band (which ST_FLAG_STORED_BAND brings back for the stored-band kernels)."""
+    for B, H, L, d, w in ((4, 8, 32768, 128, 128), (1, 16, 131072, 64, 256)):
+        s = _spec(batch=B, heads=H, seq_q=L, seq_k=L, head_dim=d, half_band=w, dtype="bf16")
+        band_bytes = B * H * L * (2 * w + 1) * 4
+        planes = 4 * B * H * L * d * 2
+        assert s.workspace_bytes() < planes + B * H * L * 4 * 48, (s.workspace_bytes(), planes)
+        import dataclasses
+        stored = dataclasses.replace(s, stored_band=True).workspace_bytes()
+        assert stored > 4 * band_bytes  # S2, S2T, Z, ZT
+        assert s.workspace_bytes() < stored / (4 if d == 128 else 12)
 
 
 def test_config_table_matches_baseline():

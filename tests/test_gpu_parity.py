@@ -37,7 +37,8 @@ def _dev(x, bits=None):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
 
 
-def gpu_run(cfg, inp, mode="one_reference", G=None, heads_as_batch=False, eps_schedule=None, duals=True):
+def gpu_run(cfg, inp, mode="one_reference", G=None, heads_as_batch=False, eps_schedule=None, duals=True,
+            stored_band=False):
     """Run the CUDA path on the generated heads; returns numpy results [nh, L', d]."""
     nh = len(inp.heads)
     if heads_as_batch or nh != cfg.B * cfg.H:
@@ -49,7 +50,8 @@ def gpu_run(cfg, inp, mode="one_reference", G=None, heads_as_batch=False, eps_sc
         B, H, rm, cm = cfg.B, cfg.H, inp.row_mask, inp.col_mask
     spec = band.BandSpec(batch=B, heads=H, seq_q=cfg.L, seq_k=cfg.L, head_dim=cfg.d, half_band=cfg.w,
                          base_depth=cfg.T, tail_depth=cfg.R, epsilon=cfg.eps, dtype=cfg.dtype,
-                         dustbin=cfg.dustbin, dustbin_cost=cfg.dustbin_cost, eps_schedule=eps_schedule)
+                         dustbin=cfg.dustbin, dustbin_cost=cfg.dustbin_cost, eps_schedule=eps_schedule,
+                         stored_band=stored_band)
     shp = (B, H, cfg.rows, cfg.d)
     b = inp.bits or {}
     Q = _dev(inp.Q, b.get("Q")).reshape(shp)
@@ -91,8 +93,8 @@ KEYS = ("O", "dQ", "dK", "dV", "eta_v", "d_eps")
 
 
 def check_against_oracle(cfg, inp, tol_o, tol_g, mode="one_reference", eps_schedule=None, case=None,
-                         bounds_override=None, floor=True):
-    g = gpu_run(cfg, inp, mode=mode, eps_schedule=eps_schedule)
+                         bounds_override=None, floor=True, stored_band=False):
+    g = gpu_run(cfg, inp, mode=mode, eps_schedule=eps_schedule, stored_band=stored_band)
     m = 1 if mode == "direct_four_plan" else 0
     r = oracle(cfg, inp, precision=64, mode=m, eps_schedule=eps_schedule)
     # the reference's own f32 instantiation (the noise floor; informational for the fixed bf16 bound)
@@ -162,6 +164,32 @@ def test_bf16_configs_reduced_length_parity(cid, L):
     cfg = configs.CONFIGS[cid].replace(L=L)
     inp = configs.make_inputs(cfg, heads=range(0, 2))
     check_against_oracle(cfg, inp, BF16_TOL, BF16_TOL)
+
+
+@pytest.mark.parametrize("cid,L,mode", [(4, 4096, "one_reference"), (5, 4096, "direct_four_plan")])
+def test_bf16_stored_band_kernels_parity(cid, L, mode):
+    """ST_FLAG_STORED_BAND: the stored-band bf16 kernels (tcgen05 band write passes, k_bwdM / k_sweepW)
+    that the generic tail adjoint and the sequence-sharded entry points still run on, against the oracle."""
+    cfg = configs.CONFIGS[cid].replace(L=L)
+    inp = configs.make_inputs(cfg, heads=range(0, 2))
+    check_against_oracle(cfg, inp, BF16_TOL, BF16_TOL, mode=mode, stored_band=True,
+                         case=f"config{cid}-L{L}-stored-band-{mode}")
+
+
+@pytest.mark.parametrize("w,d,mask,L,mode", [(128, 128, "uniform_len", 1000, "direct_four_plan"),
+                                             (256, 64, "uniform_len", 1500, "one_reference"),
+                                             (256, 64, "none", 1100, "direct_four_plan"),
+                                             (64, 64, "uniform_len", 650, "one_reference"),
+                                             (192, 128, "none", 128, "one_reference")])
+def test_bf16_band_free_sweeps_parity(w, d, mask, L, mode):
+    """The band-free tcgen05 sweeps (st_bfree.cu: transport output, C1 / R12 / C3 / R4 / R6 / C6 with the
+    score and cotangent tiles recomputed per block, weights as bf16 hi/lo planes, MN-major operand chunks):
+    both adjoint schedules, masked rows / columns (-inf offsets), partial last blocks, edge windows, a
+    band wider than the sequence, d = 64 / 128, against the oracle."""
+    cfg = configs.Config(0, B=2, H=2, L=L, d=d, w=w, eps=0.05, T=12, R=2, dtype="bf16", mask=mask,
+                         in_scale=1 / np.sqrt(d))
+    check_against_oracle(cfg, configs.make_inputs(cfg), BF16_TOL, BF16_TOL, mode=mode,
+                         case=f"bfree-w{w}-d{d}-{mask}-{mode}")
 
 
 def test_small_shapes_and_edge_cases():
