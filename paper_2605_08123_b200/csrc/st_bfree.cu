@@ -13,10 +13,11 @@
 //            PX    acc_i += p x_j                                      (v1_bar, u1_bar)
 //            SBAR  weight = Sbar (one-reference modifier field or the four-plan form)
 //                                                  -> Y += W X_c       (dQ + d_eps;  dK + v0_bar)
-//   GEMM   the weights go to SMEM as two bf16 planes (hi + lo: 16 mantissa bits) in the UMMA
-//          K-major core-matrix layout; the chunk's operand rows X_c are the packed plane itself
-//          read MN-major (the same 8 x 16-byte core matrices), so Y[128][d] (+)= W X_c is two
-//          tcgen05.mma per 16 window columns into a TMEM accumulator.
+//   GEMM   the weights go back to TMEM over the score tile, as two bf16 planes (hi + lo: 16 mantissa
+//          bits, two K elements per 32-bit column), and are the A operand of a TS-form tcgen05.mma;
+//          the chunk's operand rows X_c are the packed plane itself read MN-major (the same 8 x 16-byte
+//          core matrices), so Y[128][d] (+)= W X_c is two tcgen05.mma per 16 window columns into a
+//          TMEM accumulator -- no SMEM staging of the weights.
 // Column stages are the same kernel on the transposed geometry (own = keys: A1 = K, B1 = Q).
 // Nothing of size L x W is written or read: HBM holds the packed planes (O(L d)), the padded
 // dual / cotangent vectors (O(L)) and the outputs.
@@ -24,8 +25,8 @@
 // Roles (persistent CTA, one per SM):
 //   warp 0      producer: 1-D bulk async copies (TMA engine) of the block operands, the window
 //               chunks and the window / own vectors
-//   warp 1      MMA issuer: polls the tile and weight barriers, issues S / Z tiles one chunk ahead
-//               of the Y accumulation
+//   warp 1      issues the S / Z tiles; warp 18 issues the Y accumulations (tcgen05.mma issue rate is
+//               the scarce resource: two issuing threads)
 //   warps 2-17  epilogue: TMEM lane quadrant x column half x chunk parity; a thread owns one row
 //               and 32 columns of every other chunk, so every row reduction is in-thread and the
 //               four parts of a row combine in a fixed order.
@@ -47,15 +48,15 @@ namespace {
 constexpr int kCR = 64;   // window chunk columns (MMA N of the score / cotangent tiles)
 constexpr int kEW = 16;   // epilogue warps
 constexpr int kNV = 2;    // vector ring slots
-constexpr int kWPlane = 128 * kCR * 2;  // bytes of one bf16 weight plane of a chunk
 
 enum { M_PV = 0, M_R12 = 1, M_PX = 2, M_SROW = 3, M_SCOL = 4 };
 
 struct SweepArgs {
-    int NA, NSK, row_bytes, maxwin;
+    int NA, NS0, NS1, row_bytes, maxwin;  // A buffers; ring slots of the B1 / B2 window chunks
     int H, NB, nblk;
     int L_own, L_other, Lr_own, Lp_own, Lp_other, w;
     int wl_cap;
+    int dbg;  // development ablations (ST_BF_DBG): 1 = no Y MMAs, 2 = one S / Z K-step, 4 = no cell math, 8 = no chunk loads (results invalid)
     float c2, scale;
     const uint8_t *A1, *B1, *A2, *B2;
     const float* wv[5];  // window vectors [BH][Lp_other]; wv[0] = exponent offsets (-inf when inactive)
@@ -66,6 +67,7 @@ struct SweepArgs {
     float* out_api;      // [BH][Lr_own] or null
     const float* fvec;   // PX: own-side factor [BH][Lp_own] (null = 1)
     const __nv_bfloat16* dot_src;  // PV: raw rows [BH][Lr_own][D] for <Y_i, src_i> (null = none)
+    unsigned long long* trace;     // development timeline (ST_BF_TRACE), null in production
 };
 
 template <int MODE, bool kDirect>
@@ -79,24 +81,22 @@ struct ModeTraits {
 
 struct BSmem {
     uint8_t* A;    // [NA][(1 + Z) * 128 * row_bytes]
-    uint8_t* B;    // [NSK][(1 + B2) * 64 * row_bytes]
-    uint8_t* W;    // [2][2 planes][128 * 64 * 2]
+    uint8_t* B0;   // [NS0][64 * row_bytes]  B1 window chunks
+    uint8_t* B1;   // [NS1][64 * row_bytes]  B2 window chunks
     float* vw;     // [kNV][NW][maxwin]
     float* vo;     // [kNV][NO][128]
     float* rowx;   // [2][4][128]
-    uint64_t *v_full, *v_empty, *a_full, *a_empty, *k_full, *k_empty, *t_full, *t_empty, *w_full, *w_empty, *y_full,
-        *y_empty;
+    uint64_t *v_full, *v_empty, *a_full, *a_empty, *k_full, *k_empty, *k2_full, *k2_empty, *t_full, *t_empty, *w_full, *y_full, *y_empty;
     uint32_t* tmem_base;
     int4* bd;
 };
 
 template <int MODE, bool kDirect>
-__host__ __device__ inline size_t bs_bytes(int NA, int NSK, int row_bytes, int maxwin, int wl_cap) {
+__host__ __device__ inline size_t bs_bytes(int NA, int NS0, int NS1, int row_bytes, int maxwin, int wl_cap) {
     using T = ModeTraits<MODE, kDirect>;
-    size_t n = (size_t)NA * (T::kZ ? 2 : 1) * 128 * row_bytes + (size_t)NSK * (T::kB2 ? 2 : 1) * kCR * row_bytes;
-    if (T::kGemm) n += 2 * 2 * kWPlane;
+    size_t n = (size_t)NA * (T::kZ ? 2 : 1) * 128 * row_bytes + (size_t)(NS0 + (T::kB2 ? NS1 : 0)) * kCR * row_bytes;
     n += (size_t)kNV * (T::NW * maxwin + T::NO * 128) * 4 + 2 * 4 * 128 * 4;
-    n += (size_t)(2 * kNV + 2 * NA + 2 * NSK + 12) * 8 + 16 + (size_t)wl_cap * 16;
+    n += (size_t)(2 * kNV + 2 * NA + 2 * NS0 + 2 * NS1 + 16) * 8 + 16 + (size_t)wl_cap * 16;
     return n;
 }
 
@@ -105,9 +105,9 @@ __device__ __forceinline__ BSmem bcarve(uint8_t* base, const SweepArgs& a) {
     using T = ModeTraits<MODE, kDirect>;
     BSmem s;
     s.A = base;
-    s.B = s.A + (size_t)a.NA * (T::kZ ? 2 : 1) * 128 * a.row_bytes;
-    s.W = s.B + (size_t)a.NSK * (T::kB2 ? 2 : 1) * kCR * a.row_bytes;
-    s.vw = (float*)(s.W + (T::kGemm ? 2 * 2 * kWPlane : 0));
+    s.B0 = s.A + (size_t)a.NA * (T::kZ ? 2 : 1) * 128 * a.row_bytes;
+    s.B1 = s.B0 + (size_t)a.NS0 * kCR * a.row_bytes;
+    s.vw = (float*)(s.B1 + (size_t)(T::kB2 ? a.NS1 : 0) * kCR * a.row_bytes);
     s.vo = s.vw + kNV * T::NW * a.maxwin;
     s.rowx = s.vo + kNV * T::NO * 128;
     uint64_t* b = (uint64_t*)(s.rowx + 2 * 4 * 128);
@@ -115,12 +115,13 @@ __device__ __forceinline__ BSmem bcarve(uint8_t* base, const SweepArgs& a) {
     s.v_empty = b; b += kNV;
     s.a_full = b; b += a.NA;
     s.a_empty = b; b += a.NA;
-    s.k_full = b; b += a.NSK;
-    s.k_empty = b; b += a.NSK;
-    s.t_full = b; b += 2;
-    s.t_empty = b; b += 2;
-    s.w_full = b; b += 2;
-    s.w_empty = b; b += 2;
+    s.k_full = b; b += a.NS0;
+    s.k_empty = b; b += a.NS0;
+    s.k2_full = b; b += a.NS1;
+    s.k2_empty = b; b += a.NS1;
+    s.t_full = b; b += 4;
+    s.t_empty = b; b += 4;
+    s.w_full = b; b += 4;
     s.y_full = b; b += 2;
     s.y_empty = b; b += 2;
     s.tmem_base = (uint32_t*)b;
@@ -148,20 +149,149 @@ __device__ __forceinline__ void tc_ldn(uint32_t taddr, float (&v)[N]) {
 
 }  // namespace
 
+// One 16-column half of a warp's slice: thread = one row.  sv / zv: the score / cotangent tile values,
+// W: the window vectors at these columns, O: the row's own scalars.  Packed (two-cell) FP32 math; the
+// band test (kEdge: slices the band boundary crosses) is the only per-cell select.  Weights leave as
+// bf16 hi / lo pairs (hw, lw: two K elements per word); row partial sums accumulate in acc2.
+template <int MODE, bool kDirect, bool kEdge, int NW, int NO>
+__device__ __forceinline__ void slice_half(const float (&sv)[16], const float (&zv)[16], const float* __restrict__ vwp,
+                                           int maxwin, int cc0, int lo, unsigned bw, const float (&O)[NO], float c2,
+                                           float2& acc2, uint32_t (&hw)[8], uint32_t (&lw)[8]) {
+    constexpr bool kGemm = MODE == M_PV || MODE == M_SROW || MODE == M_SCOL;
+    const float2 c2v = make_float2(c2, c2), a2v = make_float2(O[0], O[0]), neg1 = make_float2(-1.f, -1.f);
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+        float2 W[NW][2];
+#pragma unroll
+        for (int k = 0; k < NW; ++k) {
+            const float4 t4 = *reinterpret_cast<const float4*>(vwp + (size_t)k * maxwin + cc0 + 4 * q4);
+            W[k][0] = make_float2(t4.x, t4.y);
+            W[k][1] = make_float2(t4.z, t4.w);
+        }
+#pragma unroll
+        for (int e2 = 0; e2 < 2; ++e2) {
+            const int kx = 4 * q4 + 2 * e2;
+            const float2 s2 = make_float2(sv[kx], sv[kx + 1]);
+            bool in0 = true, in1 = true;
+            if (kEdge) {
+                in0 = (unsigned)(cc0 + kx - lo) <= bw;
+                in1 = (unsigned)(cc0 + kx + 1 - lo) <= bw;
+            }
+            float2 e0 = __fmul2_rn(s2, c2v);  // direct mode: the bare scaled score (masked)
+            float2 zz = __fadd2_rn(__ffma2_rn(s2, c2v, W[0][e2]), a2v);
+            if (kEdge) {
+                zz.x = in0 ? zz.x : -INFINITY;
+                zz.y = in1 ? zz.y : -INFINITY;
+            }
+            const float2 p = make_float2(ex2(zz.x), ex2(zz.y));
+            float2 wgt = p;
+            if constexpr (MODE == M_R12) {
+                const float2 z2 = make_float2(zv[kx], zv[kx + 1]);
+                acc2 = __ffma2_rn(p, __ffma2_rn(W[1][e2], neg1, z2), acc2);
+            } else if constexpr (MODE == M_PX) {
+                acc2 = __ffma2_rn(p, W[1][e2], acc2);
+            } else if constexpr (MODE == M_SROW) {
+                const float2 z2 = make_float2(zv[kx], zv[kx + 1]);
+                if constexpr (!kDirect) {
+                    // O = (a, u2b, alpha, au1); W = (b, v2b, beta, bv1, delta)
+                    const float2 m = __ffma2_rn(W[4][e2], make_float2(O[3], O[3]),
+                                                __ffma2_rn(W[3][e2], make_float2(O[2], O[2]),
+                                                           __ffma2_rn(W[2][e2], make_float2(O[1], O[1]), W[1][e2])));
+                    wgt = __fmul2_rn(p, __ffma2_rn(m, neg1, z2));
+                } else {
+                    // O = (u2, u1, u2b, u1b); W = (v2, v1, v0, v2b, v1b)
+                    if (kEdge) {
+                        e0.x = in0 ? e0.x : -INFINITY;
+                        e0.y = in1 ? e0.y : -INFINITY;
+                    }
+                    const float2 t21 = __fadd2_rn(e0, __fadd2_rn(W[1][e2], a2v));
+                    const float2 t11 = __fadd2_rn(e0, __fadd2_rn(W[1][e2], make_float2(O[1], O[1])));
+                    const float2 t10 = __fadd2_rn(e0, __fadd2_rn(W[2][e2], make_float2(O[1], O[1])));
+                    const float2 p21 = make_float2(ex2(t21.x), ex2(t21.y)), p11 = make_float2(ex2(t11.x), ex2(t11.y)),
+                                 p10 = make_float2(ex2(t10.x), ex2(t10.y));
+                    wgt = __fmul2_rn(p, __ffma2_rn(W[3][e2], neg1, z2));
+                    wgt = __ffma2_rn(p21, make_float2(-O[2], -O[2]), wgt);
+                    wgt = __ffma2_rn(__fmul2_rn(p11, neg1), W[4][e2], wgt);
+                    wgt = __ffma2_rn(p10, make_float2(-O[3], -O[3]), wgt);
+                }
+                acc2 = __ffma2_rn(wgt, s2, acc2);  // d_eps partial, scaled by c2 ln 2 at the end
+            } else if constexpr (MODE == M_SCOL) {
+                const float2 z2 = make_float2(zv[kx], zv[kx + 1]);
+                if constexpr (!kDirect) {
+                    // O = (a = v2, v2b, beta, bv1, delta); W = (b = u2, u2b, alpha, au1)
+                    const float2 m = __ffma2_rn(make_float2(O[4], O[4]), W[3][e2],
+                                                __ffma2_rn(make_float2(O[3], O[3]), W[2][e2],
+                                                           __ffma2_rn(make_float2(O[2], O[2]), W[1][e2], make_float2(O[1], O[1]))));
+                    wgt = __fmul2_rn(p, __ffma2_rn(m, neg1, z2));
+                    acc2 = __ffma2_rn(p, W[3][e2], acc2);
+                } else {
+                    // O = (v2, v1, v0, v2b, v1b); W = (u2, u1, u2b, u1b)
+                    if (kEdge) {
+                        e0.x = in0 ? e0.x : -INFINITY;
+                        e0.y = in1 ? e0.y : -INFINITY;
+                    }
+                    const float2 t21 = __fadd2_rn(e0, __fadd2_rn(W[0][e2], make_float2(O[1], O[1])));
+                    const float2 t11 = __fadd2_rn(e0, __fadd2_rn(W[1][e2], make_float2(O[1], O[1])));
+                    const float2 t10 = __fadd2_rn(e0, __fadd2_rn(W[1][e2], make_float2(O[2], O[2])));
+                    const float2 p21 = make_float2(ex2(t21.x), ex2(t21.y)), p11 = make_float2(ex2(t11.x), ex2(t11.y)),
+                                 p10 = make_float2(ex2(t10.x), ex2(t10.y));
+                    wgt = __fmul2_rn(p, __fadd2_rn(z2, make_float2(-O[3], -O[3])));
+                    wgt = __ffma2_rn(__fmul2_rn(p21, neg1), W[2][e2], wgt);
+                    wgt = __ffma2_rn(p11, make_float2(-O[4], -O[4]), wgt);
+                    wgt = __ffma2_rn(__fmul2_rn(p10, neg1), W[3][e2], wgt);
+                    acc2 = __ffma2_rn(p10, W[3][e2], acc2);
+                }
+            }
+            if constexpr (kGemm) {
+                const __nv_bfloat162 h2 = __floats2bfloat162_rn(wgt.x, wgt.y);  // one cvt.rn.bf16x2.f32
+                const uint32_t hb = *reinterpret_cast<const uint32_t*>(&h2);
+                const float2 hf2 = make_float2(__uint_as_float(hb << 16), __uint_as_float(hb & 0xffff0000u));
+                const float2 r2 = __ffma2_rn(hf2, neg1, wgt);  // exact residual
+                hw[2 * q4 + e2] = hb;
+                lw[2 * q4 + e2] = pack_bf16(r2.x, r2.y);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ unsigned long long bf_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// development timeline of CTA 0, blocks kTrB .. kTrB + 1 (build with -DST_BF_TRACE): slot layout in bf_trace_dump
+#ifdef ST_BF_TRACE
+#define BF_TRACE(cond, slot)                                                    \
+    do {                                                                        \
+        if (a.trace && blockIdx.x == 0 && (cond)) a.trace[(slot)] = bf_gtimer(); \
+    } while (0)
+#else
+#define BF_TRACE(cond, slot) \
+    do {                     \
+    } while (0)
+#endif
+constexpr int kTrB = 4;
+
 template <int MODE, bool kDirect, int D>
-__global__ void __launch_bounds__(64 + 32 * kEW, 1) k_bsweep(SweepArgs a) {
+__global__ void __launch_bounds__(96 + 32 * kEW, 1) k_bsweep(SweepArgs a) {
     using T = ModeTraits<MODE, kDirect>;
     constexpr bool kZ = T::kZ, kGemm = T::kGemm, kB2 = T::kB2;
     constexpr int NW = T::NW, NO = T::NO;
     constexpr int TCOLS = kCR * (kZ ? 2 : 1);  // TMEM columns of one chunk buffer (S | Z)
-    constexpr int YC = kGemm ? 2 * D : 0;      // two Y accumulators ahead of the chunk buffers
+    // Y accumulators ahead of the chunk buffers: two (the drain of a block overlaps the next block's
+    // accumulation), or one where a third chunk buffer is worth more (d = 128 with a cotangent tile)
+    constexpr int kYB = !kGemm ? 0 : (kZ && D == 128) ? 1 : 2;
+    constexpr int YC = kYB * D;
+    constexpr int NBUF = (512 - YC) / TCOLS < 4 ? (512 - YC) / TCOLS : 4;  // chunk buffers in flight
     constexpr int NE = 32 * kEW;
-    static_assert(YC + 2 * TCOLS <= 512, "TMEM budget");
+    static_assert(NBUF >= 2 && YC + NBUF * TCOLS <= 512, "TMEM budget");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const BSmem s = bcarve<MODE, kDirect>(smem_raw, a);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t blk_bytes = 128u * a.row_bytes, chk_bytes = (uint32_t)kCR * a.row_bytes;
-    const uint32_t a_stride = blk_bytes * (kZ ? 2 : 1), b_stride = chk_bytes * (kB2 ? 2 : 1);
+    const uint32_t a_stride = blk_bytes * (kZ ? 2 : 1);
+    // the ring whose chunk is also the Y operand X_c is released by the Y accumulation (long-lived)
+    constexpr bool kLong0 = MODE == M_SROW || MODE == M_SCOL, kLong1 = MODE == M_PV;
 
     if (threadIdx.x == 0) {
         for (int k = 0; k < kNV; ++k) {
@@ -172,15 +302,20 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_bsweep(SweepArgs a) {
             mbar_init(&s.a_full[k], 1);
             mbar_init(&s.a_empty[k], 1);
         }
-        for (int k = 0; k < a.NSK; ++k) {
+        for (int k = 0; k < a.NS0; ++k) {
             mbar_init(&s.k_full[k], 1);
             mbar_init(&s.k_empty[k], 1);
         }
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < a.NS1; ++k) {
+            mbar_init(&s.k2_full[k], 1);
+            mbar_init(&s.k2_empty[k], 1);
+        }
+        for (int k = 0; k < 4; ++k) {
             mbar_init(&s.t_full[k], 1);
-            mbar_init(&s.t_empty[k], kEW / 2);
+            mbar_init(&s.t_empty[k], kGemm ? 1 : kEW / 2);  // gemm: freed by the Y accumulation's commit
             mbar_init(&s.w_full[k], kEW / 2);
-            mbar_init(&s.w_empty[k], 1);
+        }
+        for (int k = 0; k < 2; ++k) {
             mbar_init(&s.y_full[k], 1);
             mbar_init(&s.y_empty[k], kEW);
         }
@@ -207,123 +342,158 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_bsweep(SweepArgs a) {
     const uint32_t tbase = *s.tmem_base;
 
     if (warp == 0) {
-        // ------------------------------------------------------------ producer
-        uint32_t cs = 0;
-        for (int bi = 0; bi < nb; ++bi) {
-            const int4 b = s.bd[bi];
-            const int i0 = b.y * 128, nch = b.w - b.z + 1, wbase = b.z * kCR, nwin = nch * kCR;
-            {
-                const int vs = bi % kNV;
-                mbar_wait(&s.v_empty[vs], ((bi / kNV) & 1) ^ 1);
-                if (elect_one()) {
-                    mbar_arrive_expect_tx(&s.v_full[vs], (uint32_t)(NW * nwin + NO * 128) * 4u);
+        // ------------------------------------------------------------ producer (one thread)
+        if (lane == 0) {
+        // three independent cursors over the CTA's (block, chunk) sequence, each advancing as soon as
+        // its buffer is free: block operands + vectors, B1 chunks (ring 0), B2 chunks (ring 1)
+        int pb = 0;                       // block cursor
+        int b0 = 0, c0 = 0, b1 = 0, c1 = 0;  // ring cursors: block, chunk within the block
+        uint32_t s0 = 0, s1 = 0;          // running chunk numbers
+        if (!kB2) b1 = nb;
+        while (pb < nb || b0 < nb || b1 < nb) {
+            bool moved = false;
+            if (pb < nb) {
+                const int vs = pb % kNV, ab = pb % a.NA;
+                bool ok = mbar_test(&s.v_empty[vs], ((pb / kNV) & 1) ^ 1) && mbar_test(&s.a_empty[ab], ((pb / a.NA) & 1) ^ 1);
+                if (ok) {
+                    {
+                        const int4 b = s.bd[pb];
+                        const int i0 = b.y * 128, nwin = (b.w - b.z + 1) * kCR, wbase = b.z * kCR;
+                        mbar_arrive_expect_tx(&s.v_full[vs], (uint32_t)(NW * nwin + NO * 128) * 4u);
 #pragma unroll
-                    for (int k = 0; k < NW; ++k)
-                        bulk_g2s(s.vw + ((size_t)vs * NW + k) * a.maxwin, a.wv[k] + (size_t)b.x * a.Lp_other + wbase,
-                                 (uint32_t)nwin * 4u, &s.v_full[vs]);
+                        for (int k = 0; k < NW; ++k)
+                            bulk_g2s(s.vw + ((size_t)vs * NW + k) * a.maxwin, a.wv[k] + (size_t)b.x * a.Lp_other + wbase,
+                                     (uint32_t)nwin * 4u, &s.v_full[vs]);
 #pragma unroll
-                    for (int k = 0; k < NO; ++k)
-                        bulk_g2s(s.vo + ((size_t)vs * NO + k) * 128, a.ov[k] + (size_t)b.x * a.Lp_own + i0, 512u,
-                                 &s.v_full[vs]);
+                        for (int k = 0; k < NO; ++k)
+                            bulk_g2s(s.vo + ((size_t)vs * NO + k) * 128, a.ov[k] + (size_t)b.x * a.Lp_own + i0, 512u,
+                                     &s.v_full[vs]);
+                        mbar_arrive_expect_tx(&s.a_full[ab], a_stride);
+                        const size_t off = ((size_t)b.x * a.Lp_own + i0) * a.row_bytes;
+                        bulk_g2s(s.A + (size_t)ab * a_stride, a.A1 + off, blk_bytes, &s.a_full[ab]);
+                        if (kZ) bulk_g2s(s.A + (size_t)ab * a_stride + blk_bytes, a.A2 + off, blk_bytes, &s.a_full[ab]);
+                    }
+                    ++pb;
+                    moved = true;
                 }
-                __syncwarp();
             }
-            const int ab = bi % a.NA;
-            mbar_wait(&s.a_empty[ab], ((bi / a.NA) & 1) ^ 1);
-            if (elect_one()) {
-                mbar_arrive_expect_tx(&s.a_full[ab], a_stride);
-                const size_t off = ((size_t)b.x * a.Lp_own + i0) * a.row_bytes;
-                bulk_g2s(s.A + (size_t)ab * a_stride, a.A1 + off, blk_bytes, &s.a_full[ab]);
-                if (kZ) bulk_g2s(s.A + (size_t)ab * a_stride + blk_bytes, a.A2 + off, blk_bytes, &s.a_full[ab]);
-            }
-            __syncwarp();
-            for (int q = b.z; q <= b.w; ++q, ++cs) {
-                const int sl = cs % a.NSK;
-                mbar_wait(&s.k_empty[sl], ((cs / a.NSK) & 1) ^ 1);
-                if (elect_one()) {
-                    mbar_arrive_expect_tx(&s.k_full[sl], b_stride);
-                    const size_t off = ((size_t)b.x * a.Lp_other + (size_t)q * kCR) * a.row_bytes;
-                    bulk_g2s(s.B + (size_t)sl * b_stride, a.B1 + off, chk_bytes, &s.k_full[sl]);
-                    if (kB2) bulk_g2s(s.B + (size_t)sl * b_stride + chk_bytes, a.B2 + off, chk_bytes, &s.k_full[sl]);
+#pragma unroll
+            for (int ring = 0; ring < (kB2 ? 2 : 1); ++ring) {
+                int& rb = ring ? b1 : b0;
+                int& rc = ring ? c1 : c0;
+                uint32_t& rs = ring ? s1 : s0;
+                if (rb >= nb) continue;
+                const int ns = ring ? a.NS1 : a.NS0;
+                uint64_t* full = ring ? s.k2_full : s.k_full;
+                uint64_t* empty = ring ? s.k2_empty : s.k_empty;
+                const int sl = rs % ns;
+                bool ok = mbar_test(&empty[sl], ((rs / ns) & 1) ^ 1);
+                if (!ok) continue;
+                const int4 b = s.bd[rb];
+                if (a.dbg & 8) {  // ablation: no window-chunk loads (stale operands)
+                    mbar_arrive(&full[sl]);
+                } else {
+                    mbar_arrive_expect_tx(&full[sl], chk_bytes);
+                    const size_t off = ((size_t)b.x * a.Lp_other + (size_t)(b.z + rc) * kCR) * a.row_bytes;
+                    bulk_g2s((ring ? s.B1 : s.B0) + (size_t)sl * chk_bytes, (ring ? a.B2 : a.B1) + off, chk_bytes, &full[sl]);
                 }
-                __syncwarp();
+                moved = true;
+                ++rs;
+                if (++rc == b.w - b.z + 1) {
+                    rc = 0;
+                    ++rb;
+                }
             }
+            if (!moved) __nanosleep(64);  // leave the issue slots of this SMSP to its epilogue warps
+        }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer
+        // ------------------------------------------------------------ S / Z tile issuer
         const uint32_t idesc_s = make_idesc(128, kCR, 1u);
-        const uint32_t idesc_y = make_idesc_bmn(128, D);
         const uint32_t sbo = (uint32_t)a.row_bytes * 8u;
-        const int ksteps = a.row_bytes / 32;
-        // S / Z cursor and Y cursor over (block, chunk); cs = running chunk number
-        int sb = 0, sc = 0, yb = 0, yc = 0;
-        uint32_t scs = 0, ycs = 0;
-        int s_nch = nb > 0 ? s.bd[0].w - s.bd[0].z + 1 : 0;
-        int y_nch = s_nch;
-        while (sb < nb || (kGemm && yb < nb)) {
-            if (sb < nb) {
-                const int ab = sb % a.NA;
-                const uint32_t sl = scs % a.NSK, tb = scs & 1;
-                bool ok = (sc > 0 || mbar_test(&s.a_full[ab], (sb / a.NA) & 1)) &&
-                          mbar_test(&s.k_full[sl], (scs / a.NSK) & 1) && mbar_test(&s.t_empty[tb], ((scs >> 1) & 1) ^ 1);
-                ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
-                if (ok) {
-                    tc_fence_after();
-                    if (elect_one()) {
-                        const uint64_t ad = make_desc(smem_u32(s.A + (size_t)ab * a_stride), 128, sbo);
-                        const uint64_t bd = make_desc(smem_u32(s.B + (size_t)sl * b_stride), 128, sbo);
-                        const uint32_t dt = tbase + YC + tb * TCOLS;
-                        for (int kk = 0; kk < ksteps; ++kk)
+        constexpr int ksteps = D / 16;
+        uint32_t scs = 0;
+        for (int sb = 0; sb < nb; ++sb) {
+            const int ab = sb % a.NA;
+            const int s_nch = s.bd[sb].w - s.bd[sb].z + 1;
+            mbar_wait(&s.a_full[ab], (sb / a.NA) & 1);
+            const uint64_t ad = make_desc(smem_u32(s.A + (size_t)ab * a_stride), 128, sbo);
+            const uint64_t ad2 = make_desc(smem_u32(s.A + (size_t)ab * a_stride + blk_bytes), 128, sbo);
+            for (int sc = 0; sc < s_nch; ++sc, ++scs) {
+                const uint32_t sl = scs % a.NS0, sl2 = kB2 ? scs % a.NS1 : 0, tb = scs % NBUF;
+                mbar_wait(&s.k_full[sl], (scs / a.NS0) & 1);
+                if (kZ) mbar_wait(&s.k2_full[sl2], (scs / a.NS1) & 1);
+                mbar_wait(&s.t_empty[tb], ((scs / NBUF) & 1) ^ 1);
+                BF_TRACE(lane == 0 && sb == kTrB, sc);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint64_t bd = make_desc(smem_u32(s.B0 + (size_t)sl * chk_bytes), 128, sbo);
+                    const uint32_t dt = tbase + YC + tb * TCOLS;
+                    if (kZ) {  // the score and cotangent chains interleave (independent accumulators)
+                        const uint64_t bd2 = make_desc(smem_u32(s.B1 + (size_t)sl2 * chk_bytes), 128, sbo);
+#pragma unroll
+                        for (int kk = 0; kk < ksteps; ++kk) {
+                            if (kk > 0 && (a.dbg & 2)) break;
                             mma_bf16(dt, ad + (uint64_t)(kk * 16), bd + (uint64_t)(kk * 16), idesc_s, kk > 0);
-                        if (kZ) {
-                            const uint64_t ad2 = make_desc(smem_u32(s.A + (size_t)ab * a_stride + blk_bytes), 128, sbo);
-                            const uint64_t bd2 = make_desc(smem_u32(s.B + (size_t)sl * b_stride + chk_bytes), 128, sbo);
-                            for (int kk = 0; kk < ksteps; ++kk)
-                                mma_bf16(dt + kCR, ad2 + (uint64_t)(kk * 16), bd2 + (uint64_t)(kk * 16), idesc_s, kk > 0);
+                            mma_bf16(dt + kCR, ad2 + (uint64_t)(kk * 16), bd2 + (uint64_t)(kk * 16), idesc_s, kk > 0);
                         }
-                        tc_commit(&s.t_full[tb]);
-                        if (sc == s_nch - 1) tc_commit(&s.a_empty[ab]);
-                        if (!kGemm) tc_commit(&s.k_empty[sl]);
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < ksteps; ++kk) {
+                            if (kk > 0 && (a.dbg & 2)) break;
+                            mma_bf16(dt, ad + (uint64_t)(kk * 16), bd + (uint64_t)(kk * 16), idesc_s, kk > 0);
+                        }
                     }
-                    __syncwarp();
-                    ++scs;
-                    if (++sc == s_nch) {
-                        sc = 0;
-                        ++sb;
-                        if (sb < nb) s_nch = s.bd[sb].w - s.bd[sb].z + 1;
-                    }
+                    tc_commit(&s.t_full[tb]);
+                    if (sc == s_nch - 1) tc_commit(&s.a_empty[ab]);
+                    if (!kLong0) tc_commit(&s.k_empty[sl]);
+                    if (kZ) tc_commit(&s.k2_empty[sl2]);
                 }
+                __syncwarp();
+                BF_TRACE(lane == 0 && sb == kTrB, 56 + sc);
             }
-            if (kGemm && yb < nb && ycs < scs) {
-                const uint32_t wb = ycs & 1, sl = ycs % a.NSK, ybuf = yb & 1;
-                bool ok = mbar_test(&s.w_full[wb], (ycs >> 1) & 1) &&
-                          (yc > 0 || mbar_test(&s.y_empty[ybuf], ((yb >> 1) & 1) ^ 1));
-                ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
-                if (ok) {
+        }
+    } else if (warp == 2 + kEW) {
+        // ------------------------------------------------------------ Y accumulation issuer (its own warp:
+        // tcgen05.mma issue is the scarce resource of the sweep, two issuers double it)
+        if (kGemm) {
+            const uint32_t idesc_y = make_idesc_bmn(128, D);
+            const uint32_t sbo = (uint32_t)a.row_bytes * 8u;
+            uint32_t ycs = 0;
+            for (int yb = 0; yb < nb; ++yb) {
+                const int y_nch = s.bd[yb].w - s.bd[yb].z + 1;
+                const uint32_t ybuf = kYB == 2 ? (yb & 1) : 0;
+                mbar_wait(&s.y_empty[ybuf], ((yb / (kYB == 2 ? 2 : 1)) & 1) ^ 1);
+                for (int yc = 0; yc < y_nch; ++yc, ++ycs) {
+                    const uint32_t wb = ycs % NBUF, sl = kLong1 ? ycs % a.NS1 : ycs % a.NS0;
+                    if (kLong1) mbar_wait(&s.k2_full[sl], (ycs / a.NS1) & 1);  // the V chunk (X_c)
+                    mbar_wait(&s.w_full[wb], (ycs / NBUF) & 1);
+                    BF_TRACE(lane == 0 && yb == kTrB, 8 + yc);
                     tc_fence_after();
                     if (elect_one()) {
                         const uint32_t dy = tbase + ybuf * D;
-                        const uint8_t* xs = s.B + (size_t)sl * b_stride + (MODE == M_PV ? chk_bytes : 0);
+                        const uint8_t* xs = (kLong1 ? s.B1 : s.B0) + (size_t)sl * chk_bytes;
                         const uint64_t xd = make_desc(smem_u32(xs), sbo, 128);
+                        // weights: warp half hf of the chunk left plane p of its K = 16 kk .. 16 kk + 15 at
+                        // columns 32 hf + 16 p + 8 kk of the score tile (two bf16 per column)
+                        const uint32_t wa = tbase + YC + wb * TCOLS;
+                        if (!(a.dbg & 1)) {
 #pragma unroll
-                        for (int p = 0; p < 2; ++p) {
-                            const uint64_t wd = make_desc(smem_u32(s.W + (size_t)(wb * 2 + p) * kWPlane), 2048, 128);
+                            for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
-                            for (int kk = 0; kk < kCR / 16; ++kk)
-                                mma_bf16(dy, wd + (uint64_t)(kk * 256), xd + (uint64_t)(kk * a.row_bytes), idesc_y,
-                                         (yc > 0 || p > 0 || kk > 0) ? 1u : 0u);
+                                for (int p = 0; p < 2; ++p)
+#pragma unroll
+                                    for (int kk = 0; kk < 2; ++kk)
+                                        mma_bf16_ts(dy, wa + 32 * hf + 16 * p + 8 * kk,
+                                                    xd + (uint64_t)((2 * hf + kk) * a.row_bytes), idesc_y,
+                                                    (yc > 0 || hf > 0 || p > 0 || kk > 0) ? 1u : 0u);
                         }
-                        tc_commit(&s.w_empty[wb]);
-                        tc_commit(&s.k_empty[sl]);
+                        tc_commit(&s.t_empty[wb]);
+                        tc_commit(kLong1 ? &s.k2_empty[sl] : &s.k_empty[sl]);
                         if (yc == y_nch - 1) tc_commit(&s.y_full[ybuf]);
                     }
                     __syncwarp();
-                    ++ycs;
-                    if (++yc == y_nch) {
-                        yc = 0;
-                        ++yb;
-                        if (yb < nb) y_nch = s.bd[yb].w - s.bd[yb].z + 1;
-                    }
+                    BF_TRACE(lane == 0 && yb == kTrB, 48 + yc);
                 }
             }
         }
@@ -343,39 +513,44 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_bsweep(SweepArgs a) {
             const int i = i0 + r;
             const int lo = i - a.w - wbase;                  // band start of this row, window coordinates
             const int lo_min = i0 + qd * 32 - a.w - wbase;   // of the warp's first row
+            BF_TRACE(lane == 0 && warp == 2 && bi == kTrB, 44);
             mbar_wait(&s.v_full[vs], (bi / kNV) & 1);
+            BF_TRACE(lane == 0 && warp == 2 && bi == kTrB, 45);
             const float* vwp = s.vw + (size_t)vs * NW * a.maxwin;
             float O[NO];
 #pragma unroll
             for (int k = 0; k < NO; ++k) O[k] = s.vo[((size_t)vs * NO + k) * 128 + r];
-            float acc = 0.f;
+            float fown = 1.f;  // PX: the own-side factor, fetched ahead of the block-end combine
+            if (MODE == M_PX && part == 0 && a.fvec) fown = a.fvec[(size_t)b.x * a.Lp_own + i];
+            float2 acc2 = make_float2(0.f, 0.f);
             for (int c = 0; c < nch; ++c, ++cs) {
                 if ((int)(cs & 1) != gidx) continue;
-                const uint32_t tb = cs & 1;
+                const uint32_t tb = cs % NBUF, tpar = (cs / NBUF) & 1;
                 const int c0 = c * kCR + 32 * hf;  // first window column of this warp's slice
-                const bool outside = c0 + 31 < lo_min || c0 > lo_min + 31 + (int)bw;
+                const bool outside = c0 + 31 < lo_min || c0 > lo_min + 31 + (int)bw || (a.dbg & 4);
                 const bool edge = !(c0 >= lo_min + 31 && c0 + 31 <= lo_min + (int)bw);
-                uint8_t* wrow = s.W + (size_t)(tb * 2) * kWPlane + (size_t)(4 * hf) * 2048 + (size_t)r * 16;
-                mbar_wait(&s.t_full[tb], (cs >> 1) & 1);
+                const uint32_t ta = tl + YC + tb * TCOLS + 32 * hf;
+                mbar_wait(&s.t_full[tb], tpar);
+                BF_TRACE(lane == 0 && (warp == 2 || warp == 6) && bi == kTrB, 16 + c);
+                BF_TRACE(lane == 0 && bi == kTrB && (c == 2 || c == 3), 64 + (warp - 2) * 3);
                 if (outside) {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&s.t_empty[tb]);
                     if (kGemm) {
-                        mbar_wait(&s.w_empty[tb], ((cs >> 1) & 1) ^ 1);
+                        tc_fence_after();
+                        const uint32_t zero8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-                        for (int kg = 0; kg < 4; ++kg) {
-                            *reinterpret_cast<uint4*>(wrow + kg * 2048) = make_uint4(0, 0, 0, 0);
-                            *reinterpret_cast<uint4*>(wrow + kWPlane + kg * 2048) = make_uint4(0, 0, 0, 0);
-                        }
-                        fence_proxy_async_smem();
+                        for (int q = 0; q < 4; ++q) tc_st8(ta + 8 * q, zero8);
+                        tc_wait_st();
+                        tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&s.w_full[tb]);
+                    } else {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&s.t_empty[tb]);
                     }
                     continue;
                 }
                 tc_fence_after();
                 float sv[2][16], zv[2][16];
-                const uint32_t ta = tl + YC + tb * TCOLS + 32 * hf;
                 tc_ld16(ta, sv[0]);
                 tc_ld16(ta + 16, sv[1]);
                 if (kZ) {
@@ -383,146 +558,111 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_bsweep(SweepArgs a) {
                     tc_ld16(ta + kCR + 16, zv[1]);
                 }
                 tc_wait_ld();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&s.t_empty[tb]);
-                if (kGemm) mbar_wait(&s.w_empty[tb], ((cs >> 1) & 1) ^ 1);
+                BF_TRACE(lane == 0 && (warp == 2 || warp == 6) && bi == kTrB, 24 + c);
+                BF_TRACE(lane == 0 && bi == kTrB && (c == 2 || c == 3), 64 + (warp - 2) * 3 + 1);
+                if (!kGemm) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&s.t_empty[tb]);
+                }
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-#pragma unroll
-                    for (int g8 = 0; g8 < 2; ++g8) {
-                        float wg[8];
-#pragma unroll
-                        for (int q4 = 0; q4 < 2; ++q4) {
-                            const int cc = c0 + 16 * h + 8 * g8 + 4 * q4;
-                            float wvv[NW][4];
-#pragma unroll
-                            for (int k = 0; k < NW; ++k) {
-                                const float4 t4 = *reinterpret_cast<const float4*>(vwp + (size_t)k * a.maxwin + cc);
-                                wvv[k][0] = t4.x;
-                                wvv[k][1] = t4.y;
-                                wvv[k][2] = t4.z;
-                                wvv[k][3] = t4.w;
-                            }
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                const int kx = 8 * g8 + 4 * q4 + e;
-                                const float sc_ = sv[h][kx];
-                                const bool inb = !edge || (unsigned)(cc + e - lo) <= bw;
-                                const float e0 = sc_ * a.c2;
-                                float zz = e0 + wvv[0][e] + O[0];
-                                zz = inb ? zz : -INFINITY;
-                                const float p = ex2(zz);
-                                float wgt = p;
-                                if constexpr (MODE == M_R12) {
-                                    acc = fmaf(p, zv[h][kx] - wvv[1][e], acc);
-                                } else if constexpr (MODE == M_PX) {
-                                    acc = fmaf(p, wvv[1][e], acc);
-                                } else if constexpr (MODE == M_SROW) {
-                                    const float z = zv[h][kx];
-                                    if constexpr (!kDirect) {
-                                        // O = (a, u2b, alpha, au1); W = (b, v2b, beta, bv1, delta)
-                                        const float m = fmaf(wvv[4][e], O[3], fmaf(wvv[3][e], O[2], fmaf(wvv[2][e], O[1], wvv[1][e])));
-                                        wgt = p * (z - m);
-                                    } else {
-                                        // O = (u2, u1, u2b, u1b); W = (v2, v1, v0, v2b, v1b)
-                                        const float em = inb ? e0 : -INFINITY;
-                                        const float p21 = ex2(em + O[0] + wvv[1][e]);
-                                        const float p11 = ex2(em + O[1] + wvv[1][e]);
-                                        const float p10 = ex2(em + O[1] + wvv[2][e]);
-                                        wgt = p * (z - wvv[3][e]) - O[2] * p21 - p11 * wvv[4][e] - O[3] * p10;
-                                    }
-                                    acc = fmaf(wgt, sc_ * c2ln2, acc);
-                                } else if constexpr (MODE == M_SCOL) {
-                                    const float z = zv[h][kx];
-                                    if constexpr (!kDirect) {
-                                        // O = (a = v2, v2b, beta, bv1, delta); W = (b = u2, u2b, alpha, au1)
-                                        const float m = fmaf(O[4], wvv[3][e], fmaf(O[3], wvv[2][e], fmaf(O[2], wvv[1][e], O[1])));
-                                        wgt = p * (z - m);
-                                        acc = fmaf(p, wvv[3][e], acc);
-                                    } else {
-                                        // O = (v2, v1, v0, v2b, v1b); W = (u2, u1, u2b, u1b)
-                                        const float em = inb ? e0 : -INFINITY;
-                                        const float p21 = ex2(em + wvv[0][e] + O[1]);
-                                        const float p11 = ex2(em + wvv[1][e] + O[1]);
-                                        const float p10 = ex2(em + wvv[1][e] + O[2]);
-                                        wgt = p * (z - O[3]) - wvv[2][e] * p21 - p11 * O[4] - wvv[3][e] * p10;
-                                        acc = fmaf(p10, wvv[3][e], acc);
-                                    }
-                                }
-                                wg[4 * q4 + e] = wgt;
-                            }
-                        }
-                        if (kGemm) {
-                            uint32_t hw[4], lw[4];
-#pragma unroll
-                            for (int k2 = 0; k2 < 4; ++k2) {
-                                const __nv_bfloat16 h0 = __float2bfloat16_rn(wg[2 * k2]), h1 = __float2bfloat16_rn(wg[2 * k2 + 1]);
-                                hw[k2] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
-                                lw[k2] = pack_bf16(wg[2 * k2] - __bfloat162float(h0), wg[2 * k2 + 1] - __bfloat162float(h1));
-                            }
-                            const int kg = 2 * h + g8;
-                            *reinterpret_cast<uint4*>(wrow + kg * 2048) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-                            *reinterpret_cast<uint4*>(wrow + kWPlane + kg * 2048) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-                        }
+                    uint32_t hw[8], lw[8];
+                    if (edge)
+                        slice_half<MODE, kDirect, true, NW, NO>(sv[h], zv[h], vwp, a.maxwin, c0 + 16 * h, lo, bw, O, a.c2, acc2, hw, lw);
+                    else
+                        slice_half<MODE, kDirect, false, NW, NO>(sv[h], zv[h], vwp, a.maxwin, c0 + 16 * h, lo, bw, O, a.c2, acc2, hw, lw);
+                    if (kGemm) {  // K = 16 h .. 16 h + 15 of this warp's slice: hi plane, lo plane
+                        tc_st8(ta + 8 * h, hw);
+                        tc_st8(ta + 16 + 8 * h, lw);
                     }
                 }
                 if (kGemm) {
-                    fence_proxy_async_smem();
+                    tc_wait_st();
+                    tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&s.w_full[tb]);
                 }
+                BF_TRACE(lane == 0 && (warp == 2 || warp == 6) && bi == kTrB, 32 + c);
+                BF_TRACE(lane == 0 && bi == kTrB && (c == 2 || c == 3), 64 + (warp - 2) * 3 + 2);
             }
+            const float acc = (acc2.x + acc2.y) * (MODE == M_SROW ? c2ln2 : 1.f);
             __syncwarp();
+            BF_TRACE(lane == 0 && warp == 2 && bi == kTrB, 40);
             if (lane == 0) mbar_arrive(&s.v_empty[vs]);
             const size_t orow = (size_t)b.x * a.Lr_own + i;
             if (kGemm) {
-                // ---- drain this block's accumulator: the warp's quarter of the D output columns
-                constexpr int QC = D / 4;
-                const uint32_t ybuf = bi & 1;
-                mbar_wait(&s.y_full[ybuf], (bi >> 1) & 1);
+                // ---- drain this block's accumulator with 16x256b loads: thread (t0, t1) holds rows t1, t1 + 8
+                // of a 16-row half and columns 8 m + 2 t0 + {0, 1} of a 32-column group, so the 4 threads of
+                // a row write one full 32-byte sector per store (D = 128: the warp's column quarter, both
+                // halves; D = 64: one column half of one row half)
+                constexpr int NH = D == 128 ? 2 : 1;
+                const int cg = D == 128 ? part : (part & 1);
+                const uint32_t ybuf = kYB == 2 ? (bi & 1) : 0;
+                const int t0 = lane & 3, t1 = lane >> 2;
+                const bool dot = MODE == M_PV && a.dot_src != nullptr;
+                mbar_wait(&s.y_full[ybuf], (bi / (kYB == 2 ? 2 : 1)) & 1);
+                BF_TRACE(lane == 0 && warp == 2 && bi == kTrB, 41);
                 tc_fence_after();
-                float y[QC];
-                tc_ldn<QC>(tl + ybuf * D + part * QC, y);
+                float y[NH][16];
+#pragma unroll
+                for (int hh = 0; hh < NH; ++hh) {
+                    const int rh = D == 128 ? hh : (part >> 1);
+                    tc_ld16x256(tbase + ((uint32_t)(qd * 32 + 16 * rh) << 16) + ybuf * D + cg * 32, y[hh]);
+                }
                 tc_wait_ld();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s.y_empty[ybuf]);
-                if (i < a.L_own) {
-                    float* dst = a.out_mat + orow * D + part * QC;
+                float* rxd = s.rowx + (size_t)par * 4 * 128 + part * 128;
 #pragma unroll
-                    for (int q = 0; q < QC / 4; ++q)
-                        *reinterpret_cast<float4*>(dst + 4 * q) =
-                            make_float4(y[4 * q] * a.scale, y[4 * q + 1] * a.scale, y[4 * q + 2] * a.scale, y[4 * q + 3] * a.scale);
-                    if (MODE == M_PV && a.dot_src) {
-                        const uint4* src = reinterpret_cast<const uint4*>(a.dot_src + orow * D + part * QC);
+                for (int hh = 0; hh < NH; ++hh) {
+                    const int rh = D == 128 ? hh : (part >> 1);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int rloc = qd * 32 + 16 * rh + t1 + 8 * h;
+                        const int ig = i0 + rloc;
                         float dsum = 0.f;
+                        if (ig < a.L_own) {
+                            const size_t eo = ((size_t)b.x * a.Lr_own + ig) * D + cg * 32 + 2 * t0;
+                            float* dst = a.out_mat + eo;
 #pragma unroll
-                        for (int q = 0; q < QC / 8; ++q) {
-                            const uint4 v8 = src[q];
-                            const uint32_t ww[4] = {v8.x, v8.y, v8.z, v8.w};
+                            for (int m = 0; m < 4; ++m)
+                                *reinterpret_cast<float2*>(dst + 8 * m) =
+                                    make_float2(y[hh][4 * m + 2 * h] * a.scale, y[hh][4 * m + 2 * h + 1] * a.scale);
+                            if (dot) {
+                                const uint32_t* src = reinterpret_cast<const uint32_t*>(a.dot_src + eo);
 #pragma unroll
-                            for (int k2 = 0; k2 < 4; ++k2) {
-                                dsum = fmaf(y[8 * q + 2 * k2], __uint_as_float(ww[k2] << 16), dsum);
-                                dsum = fmaf(y[8 * q + 2 * k2 + 1], __uint_as_float(ww[k2] & 0xffff0000u), dsum);
+                                for (int m = 0; m < 4; ++m) {
+                                    const uint32_t ww = src[4 * m];
+                                    dsum = fmaf(y[hh][4 * m + 2 * h], __uint_as_float(ww << 16), dsum);
+                                    dsum = fmaf(y[hh][4 * m + 2 * h + 1], __uint_as_float(ww & 0xffff0000u), dsum);
+                                }
                             }
                         }
-                        acc = dsum;
+                        if (dot) {  // <Y_i, src_i> over this warp's 32 columns
+                            dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
+                            dsum += __shfl_xor_sync(0xffffffffu, dsum, 2);
+                            if (t0 == 0) rxd[rloc] = dsum;
+                            if (D == 64 && t0 == 1) rxd[qd * 32 + 16 * (1 - rh) + t1 + 8 * h] = 0.f;
+                        }
                     }
                 }
             }
             if (MODE != M_PV || a.dot_src) {
                 // ---- the four parts of a row combine in a fixed order
                 float* rx = s.rowx + (size_t)par * 4 * 128;
-                rx[part * 128 + r] = acc;
+                if (MODE != M_PV) rx[part * 128 + r] = acc;
+                BF_TRACE(lane == 0 && warp == 2 && bi == kTrB, 42);
                 named_bar(1, NE);
+                BF_TRACE(lane == 0 && warp == 2 && bi == kTrB, 43);
                 if (part == 0) {
                     const float tot = (rx[r] + rx[128 + r]) + (rx[256 + r] + rx[384 + r]);
                     const size_t prow = (size_t)b.x * a.Lp_own + i;
                     if constexpr (MODE == M_PV || MODE == M_R12) {
                         a.out1[prow] = tot;
                     } else if constexpr (MODE == M_PX) {
-                        const float f = a.fvec ? a.fvec[prow] : 1.f;
+                        const float f = fown;
                         const float o = -f * tot;
                         a.out1[prow] = o;
                         if (a.out2) a.out2[prow] = f * o;
@@ -591,24 +731,65 @@ cudaError_t run_sweep(SweepArgs a, cudaStream_t st) {
     const int grid = std::min(bf_num_sms(), a.nblk);
     a.wl_cap = (a.nblk + grid - 1) / grid;
     a.row_bytes = D * 2;
+    a.dbg = getenv("ST_BF_DBG") ? atoi(getenv("ST_BF_DBG")) : 0;
     const size_t kMax = 227 * 1024;
+    using T = ModeTraits<MODE, kDirect>;
+    constexpr bool kLong0 = MODE == M_SROW || MODE == M_SCOL, kLong1 = MODE == M_PV;
+    // (A buffers, long-ring slots, short-ring slots): the ring whose chunk is also the Y operand lives until
+    // the Y accumulation retires it and needs the depth; the other is freed by the S / Z tiles
+    static const int plans[][3] = {{2, 8, 3}, {2, 6, 3}, {2, 5, 3}, {1, 6, 3}, {1, 5, 3}, {2, 4, 3}, {1, 4, 3}, {2, 4, 2}, {1, 4, 2}, {1, 3, 2}, {1, 2, 2}};
     bool ok = false;
-    for (int NA = 2; NA >= 1 && !ok; --NA)
-        for (int NSK = 4; NSK >= 2 && !ok; --NSK)
-            if (bs_bytes<MODE, kDirect>(NA, NSK, a.row_bytes, a.maxwin, a.wl_cap) <= kMax) {
-                a.NA = NA;
-                a.NSK = NSK;
-                ok = true;
-            }
+    for (const auto& pl : plans) {
+        const int lng = pl[1], sht = T::kGemm ? pl[2] : std::max(pl[1], pl[2]);
+        const int ns0 = kLong0 ? lng : sht, ns1 = !T::kB2 ? 0 : kLong1 ? lng : pl[2];
+        if (bs_bytes<MODE, kDirect>(pl[0], ns0, ns1, a.row_bytes, a.maxwin, a.wl_cap) <= kMax) {
+            a.NA = pl[0];
+            a.NS0 = ns0;
+            a.NS1 = ns1;
+            ok = true;
+            break;
+        }
+    }
     if (!ok) return cudaErrorNotSupported;
     if (getenv("ST_BF_NA")) a.NA = atoi(getenv("ST_BF_NA"));
-    if (getenv("ST_BF_NSK")) a.NSK = atoi(getenv("ST_BF_NSK"));
-    const size_t smem = bs_bytes<MODE, kDirect>(a.NA, a.NSK, a.row_bytes, a.maxwin, a.wl_cap);
+    if (getenv("ST_BF_NS0")) a.NS0 = atoi(getenv("ST_BF_NS0"));
+    if (getenv("ST_BF_NS1") && T::kB2) a.NS1 = atoi(getenv("ST_BF_NS1"));
+    const size_t smem = bs_bytes<MODE, kDirect>(a.NA, a.NS0, a.NS1, a.row_bytes, a.maxwin, a.wl_cap);
+    if (smem > kMax) return cudaErrorNotSupported;
     auto k = k_bsweep<MODE, kDirect, D>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k<<<grid, 64 + 32 * kEW, smem, st>>>(a);
+#ifdef ST_BF_TRACE
+    static unsigned long long* tbuf = nullptr;
+    if (getenv("ST_BF_TRACE")) {
+        if (!tbuf) cudaMalloc(&tbuf, 128 * 8);
+        cudaMemsetAsync(tbuf, 0, 128 * 8, st);
+        a.trace = tbuf;
+    }
+#endif
+    k<<<grid, 96 + 32 * kEW, smem, st>>>(a);
     ++g_bf_launches;
+#ifdef ST_BF_TRACE
+    if (a.trace) {
+        unsigned long long h[128];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, tbuf, sizeof(h), cudaMemcpyDeviceToHost);
+        const unsigned long long t0 = h[44];
+        auto rel = [&](int k2) { return h[k2] ? (long long)(h[k2] - t0) : -1LL; };
+        fprintf(stderr, "k_bsweep<%d,%d,%d> NA %d NS0 %d NS1 %d (ns rel. to block %d start of epilogue warp 2)\n", MODE, (int)kDirect, D, a.NA, a.NS0, a.NS1, kTrB);
+        {
+            const int o = 0;
+            fprintf(stderr, " blk %d: start %lld vfull %lld | chunks-end %lld yfull %lld pre-bar %lld post-bar %lld\n", kTrB, rel(o + 44),
+                    rel(o + 45), rel(o + 40), rel(o + 41), rel(o + 42), rel(o + 43));
+            for (int c = 0; c < 8; ++c)
+                fprintf(stderr, "   c%d: S-issue %6lld-%6lld Y-issue %6lld-%6lld | epi tfull %6lld loaded %6lld done %6lld\n", c, rel(o + c), rel(o + 56 + c),
+                        rel(o + 8 + c), rel(o + 48 + c), rel(o + 16 + c), rel(o + 24 + c), rel(o + 32 + c));
+            for (int w2 = 0; w2 < 16; ++w2)
+                fprintf(stderr, "   warp %2d (qd %d grp %d hf %d) chunk %d: tfull %6lld loaded %6lld done %6lld\n", w2 + 2, (w2 + 2) & 3, (w2 >> 2) & 1,
+                        w2 >> 3, 2 + ((w2 >> 2) & 1), rel(64 + w2 * 3), rel(64 + w2 * 3 + 1), rel(64 + w2 * 3 + 2));
+        }
+    }
+#endif
     return cudaGetLastError();
 }
 
