@@ -472,7 +472,7 @@ const char* st_last_error(void) { return g_err.c_str(); }
 
 int64_t st_launch_count(int32_t reset) {
     return (int64_t)(st::launch_count(reset != 0) + st::phase_launch_count(reset != 0) +
-                     st::fstep16_launch_count(reset != 0));
+                     st::fstep16_launch_count(reset != 0) + st::bfree_launch_count(reset != 0));
 }
 
 size_t st_saved_bytes(const st_desc* desc) {

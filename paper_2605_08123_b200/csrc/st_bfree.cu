@@ -601,6 +601,22 @@ __global__ void __launch_bounds__(96 + 32 * kEW, 1) k_bsweep(SweepArgs a) {
                 const uint32_t ybuf = kYB == 2 ? (bi & 1) : 0;
                 const int t0 = lane & 3, t1 = lane >> 2;
                 const bool dot = MODE == M_PV && a.dot_src != nullptr;
+                // <Y_i, src_i> operands (C1: the raw V rows) fetched before the accumulator is waited for
+                uint32_t dsrc[NH][2][4];
+                if (dot) {
+#pragma unroll
+                    for (int hh = 0; hh < NH; ++hh) {
+                        const int rh = D == 128 ? hh : (part >> 1);
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int ig = i0 + qd * 32 + 16 * rh + t1 + 8 * h;
+                            const uint32_t* src = reinterpret_cast<const uint32_t*>(
+                                a.dot_src + ((size_t)b.x * a.Lr_own + min(ig, a.L_own - 1)) * D + cg * 32 + 2 * t0);
+#pragma unroll
+                            for (int m = 0; m < 4; ++m) dsrc[hh][h][m] = src[4 * m];
+                        }
+                    }
+                }
                 mbar_wait(&s.y_full[ybuf], (bi / (kYB == 2 ? 2 : 1)) & 1);
                 BF_TRACE(lane == 0 && warp == 2 && bi == kTrB, 41);
                 tc_fence_after();
@@ -631,10 +647,9 @@ __global__ void __launch_bounds__(96 + 32 * kEW, 1) k_bsweep(SweepArgs a) {
                                 *reinterpret_cast<float2*>(dst + 8 * m) =
                                     make_float2(y[hh][4 * m + 2 * h] * a.scale, y[hh][4 * m + 2 * h + 1] * a.scale);
                             if (dot) {
-                                const uint32_t* src = reinterpret_cast<const uint32_t*>(a.dot_src + eo);
 #pragma unroll
                                 for (int m = 0; m < 4; ++m) {
-                                    const uint32_t ww = src[4 * m];
+                                    const uint32_t ww = dsrc[hh][h][m];
                                     dsum = fmaf(y[hh][4 * m + 2 * h], __uint_as_float(ww << 16), dsum);
                                     dsum = fmaf(y[hh][4 * m + 2 * h + 1], __uint_as_float(ww & 0xffff0000u), dsum);
                                 }
@@ -713,7 +728,8 @@ long long bfree_launch_count(bool reset) {
 }
 
 bool bfree_supported(int d, int w, int dustbin, int esz) {
-    if (getenv("ST_NO_BFREE")) return false;
+    static const bool off = getenv("ST_NO_BFREE") != nullptr;
+    if (off) return false;
     return esz == 2 && !dustbin && (d == 64 || d == 128) && w >= 64 && w % kCR == 0;
 }
 
@@ -731,7 +747,11 @@ cudaError_t run_sweep(SweepArgs a, cudaStream_t st) {
     const int grid = std::min(bf_num_sms(), a.nblk);
     a.wl_cap = (a.nblk + grid - 1) / grid;
     a.row_bytes = D * 2;
-    a.dbg = getenv("ST_BF_DBG") ? atoi(getenv("ST_BF_DBG")) : 0;
+    static const int env_dbg = getenv("ST_BF_DBG") ? atoi(getenv("ST_BF_DBG")) : 0;
+    static const int env_na = getenv("ST_BF_NA") ? atoi(getenv("ST_BF_NA")) : 0;
+    static const int env_ns0 = getenv("ST_BF_NS0") ? atoi(getenv("ST_BF_NS0")) : 0;
+    static const int env_ns1 = getenv("ST_BF_NS1") ? atoi(getenv("ST_BF_NS1")) : 0;
+    a.dbg = env_dbg;
     const size_t kMax = 227 * 1024;
     using T = ModeTraits<MODE, kDirect>;
     constexpr bool kLong0 = MODE == M_SROW || MODE == M_SCOL, kLong1 = MODE == M_PV;
@@ -751,9 +771,9 @@ cudaError_t run_sweep(SweepArgs a, cudaStream_t st) {
         }
     }
     if (!ok) return cudaErrorNotSupported;
-    if (getenv("ST_BF_NA")) a.NA = atoi(getenv("ST_BF_NA"));
-    if (getenv("ST_BF_NS0")) a.NS0 = atoi(getenv("ST_BF_NS0"));
-    if (getenv("ST_BF_NS1") && T::kB2) a.NS1 = atoi(getenv("ST_BF_NS1"));
+    if (env_na) a.NA = env_na;
+    if (env_ns0) a.NS0 = env_ns0;
+    if (env_ns1 && T::kB2) a.NS1 = env_ns1;
     const size_t smem = bs_bytes<MODE, kDirect>(a.NA, a.NS0, a.NS1, a.row_bytes, a.maxwin, a.wl_cap);
     if (smem > kMax) return cudaErrorNotSupported;
     auto k = k_bsweep<MODE, kDirect, D>;
