@@ -505,6 +505,7 @@ float step_scale(const st_desc* d, long t) {
 namespace {
 struct BandKey {
     const void *Q, *K, *rm, *cm;
+    const void* V;  // kind 3: the packed V plane is valid too
     st_desc d;
     int kind;  // 1: score band S2; 2: S2 and its transpose S2T; 3: packed Q / K planes only (band-free)
 };
@@ -516,9 +517,14 @@ bool same_desc(const st_desc& a, const st_desc& b) {
            a.dustbin == b.dustbin && a.dustbin_cost == b.dustbin_cost;
 }
 void band_record(const void* ws, const void* Q, const void* K, const void* rm, const void* cm, const st_desc* d,
-                 int kind) {
+                 int kind, const void* V = nullptr) {
     std::lock_guard<std::mutex> lk(g_band_mu);
-    g_band[ws] = BandKey{Q, K, rm, cm, *d, kind};
+    g_band[ws] = BandKey{Q, K, rm, cm, V, *d, kind};
+}
+bool band_v_valid(const void* ws, const void* V) {
+    std::lock_guard<std::mutex> lk(g_band_mu);
+    auto it = g_band.find(ws);
+    return it != g_band.end() && it->second.kind == 3 && it->second.V == V;
 }
 // 0: nothing reusable, 1: S2 band, 2: S2 and S2T, 3: packed planes
 void band_forget(const void* ws) {
@@ -710,7 +716,7 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
             ST_CUDA(st::launch_pack(desc->dtype, V, g.BH, g.Lk, g.Lrk, tp.Lpk, g.d, 0, vp, nullptr, nullptr, st));
             ST_CUDA(st::launch_bfree_output(make_bfgeo(g, tp), qp[0], kp[0], vp, u_prev, v_prev,
                                             (float*)(ws + wl.bfvec), O, st));
-            band_record(workspace, Q, K, row_mask, col_mask, desc, 3);
+            band_record(workspace, Q, K, row_mask, col_mask, desc, 3, V);
             return ST_OK;
         }
         if (tp.npl == 1 && !getenv("ST_NO_TCBAND")) {
@@ -900,7 +906,8 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
             ST_CUDA(st::launch_pack(desc->dtype, Q, g.BH, g.Lq, g.Lrq, tpl.Lpq, g.d, 0, qp0, nullptr, nullptr, st));
             ST_CUDA(st::launch_pack(desc->dtype, K, g.BH, g.Lk, g.Lrk, tpl.Lpk, g.d, 0, kp0, nullptr, nullptr, st));
         }
-        ST_CUDA(st::launch_pack(desc->dtype, V, g.BH, g.Lk, g.Lrk, tpl.Lpk, g.d, 0, vp0, nullptr, nullptr, st));
+        if (!(packed && band_v_valid(workspace, V)))  // the forward's transport sweep left the packed V plane
+            ST_CUDA(st::launch_pack(desc->dtype, V, g.BH, g.Lk, g.Lrk, tpl.Lpk, g.d, 0, vp0, nullptr, nullptr, st));
         ST_CUDA(st::launch_pack(desc->dtype, dO, g.BH, g.Lq, g.Lrq, tpl.Lpq, g.d, 0, gp0, nullptr, nullptr, st));
         b.qp = qp0;
         b.kp = kp0;

@@ -1180,15 +1180,16 @@ __global__ void __launch_bounds__(256) k_bwd_col(Geo g, BwdArgs<TIn> a, int last
 }
 
 // d_eps[bh] = -(1/eps) * sum_i deps_part[bh][i]  (fixed-order reduction)
-__global__ void __launch_bounds__(256) k_deps_reduce(Geo g, const float* __restrict__ part, float* __restrict__ out,
-                                                     int i_begin, int i_end) {
+__global__ void __launch_bounds__(1024) k_deps_reduce(Geo g, const float* __restrict__ part, float* __restrict__ out,
+                                                      int i_begin, int i_end) {
     const int bh = blockIdx.x;
     double s = 0.0;
-    for (int i = i_begin + threadIdx.x; i < i_end; i += blockDim.x) s += (double)part[(size_t)bh * g.Lrq + i];
-    __shared__ double ss[256];
+#pragma unroll 4
+    for (int i = i_begin + threadIdx.x; i < i_end; i += 1024) s += (double)part[(size_t)bh * g.Lrq + i];
+    __shared__ double ss[1024];
     ss[threadIdx.x] = s;
     __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
+    for (int o = 512; o > 0; o >>= 1) {
         if (threadIdx.x < o) ss[threadIdx.x] += ss[threadIdx.x + o];
         __syncthreads();
     }
@@ -1556,7 +1557,7 @@ cudaError_t launch_backward(const Geo& g, int dtype, const BwdPtrs& p, bool dire
 
 cudaError_t launch_deps_reduce(const Geo& g, const float* part, float* out, cudaStream_t s, int i_begin, int i_end) {
     if (i_end < 0) i_end = g.Lrq;
-    k_deps_reduce<<<g.BH, 256, 0, s>>>(g, part, out, i_begin, i_end);
+    k_deps_reduce<<<g.BH, 1024, 0, s>>>(g, part, out, i_begin, i_end);
     ++g_launches;
     return cudaGetLastError();
 }
