@@ -827,15 +827,30 @@ __global__ void __launch_bounds__(256) k_vmerge(const float* __restrict__ part, 
     if (j >= Lk) return;
     const int lcr = CR == 128 ? 7 : 6;
     float* pv = pad_v + (size_t)bh * pad_ld + pad_off + j;
+    // every load in flight together (the old dual and up to 3 partials; out-of-range slots re-read the last)
+    const int I0 = max(0, j - w) >> 7, I1 = min(Lq - 1, j + w) >> 7;
+    const float* pb = part + (size_t)bh * NB * maxwin;
     const float vold = *pv;
+    float pr[3];
+    const bool small = I1 - I0 < 3;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        const int I = min(I0 + t, I1);
+        const int q0 = max(0, (I * 128 - w + shift) >> lcr);  // first window chunk of block I
+        pr[t] = small ? pb[(size_t)I * maxwin + (j - ((q0 << lcr) - shift))] : 0.f;
+    }
     float v = 0.f;
     if (vold != -INFINITY) {  // active column (the padded buffer carries the mask)
-        const int I0 = max(0, j - w) >> 7, I1 = min(Lq - 1, j + w) >> 7;
-        const float* pb = part + (size_t)bh * NB * maxwin;
         float sum = 0.f;
-        for (int I = I0; I <= I1; ++I) {
-            const int q0 = max(0, (I * 128 - w + shift) >> lcr);  // first window chunk of block I
-            sum += pb[(size_t)I * maxwin + (j - ((q0 << lcr) - shift))];
+        if (small) {
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+                if (I0 + t <= I1) sum += pr[t];
+        } else {  // bands wider than 128: more than 3 row blocks meet a column
+            for (int I = I0; I <= I1; ++I) {
+                const int q0 = max(0, (I * 128 - w + shift) >> lcr);
+                sum += pb[(size_t)I * maxwin + (j - ((q0 << lcr) - shift))];
+            }
         }
         v = vold - lg2(sum);
         if (!(sum > 0.f) || !isfinite(v)) {

@@ -37,7 +37,10 @@ def run(cid, L, heads, mode, masked=False):
         print(f"  {k}: rel-L2 band-free vs stored = {err:.3e}  (nan: {bool(torch.isnan(bb).any())})", flush=True)
 
 
-for args in [(4, 4096, 2, "one_reference"), (4, 4096, 2, "direct_four_plan"), (5, 8192, 2, "one_reference"),
-             (4, 4000, 3, "one_reference", True), (4, 32768, 4, "one_reference"), (5, 131072, 1, "one_reference")]:
+CASES = [(4, 4096, 2, "one_reference"), (4, 4096, 2, "direct_four_plan"), (5, 8192, 2, "one_reference"),
+             (4, 4000, 3, "one_reference", True), (4, 32768, 4, "one_reference"), (5, 131072, 1, "one_reference")]
+if len(sys.argv) > 1:
+    CASES = [(4, 16384, 4, "one_reference"), (5, 16384, 4, "direct_four_plan")]
+for args in CASES:
     print("config", *args, flush=True)
     run(*args)
