@@ -10,7 +10,7 @@
 
 namespace st {
 
-// Geometry of the band-free path (bf16 planes, no dustbin, w a multiple of 64).
+// Geometry of the band-free path (bf16 planes, no dustbin, w a multiple of 128: the packed planes of the solve carry no row shift).
 struct BfGeo {
     int BH, H;
     int Lq, Lk, Lrq, Lrk;   // rows / columns; strides of the API tensors

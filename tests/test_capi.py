@@ -95,6 +95,15 @@ def test_error_contract_without_gpu():
     assert lib.st_forward(ctypes.byref(d), 1, 1, 1, None, None, 1, None, None, 0, None) == _lib.ST_WORKSPACE_TOO_SMALL
     d = _spec(head_dim=256).desc()
     assert lib.st_forward(ctypes.byref(d), 1, 1, 1, None, None, 1, None, None, 0, None) == _lib.ST_NOT_SUPPORTED
+    # band-free bf16 problems: the generic tail adjoint needs the stored-band kernels (ST_FLAG_STORED_BAND)
+    bf = dict(batch=1, heads=1, seq_q=512, seq_k=512, head_dim=64, half_band=128, dtype="bf16")
+    d = _spec(**bf).desc()
+    assert lib.st_backward(ctypes.byref(d), 1, 1, 1, 1, 1, None, None, 1, 1, 1, None, None,
+                           _lib.ST_GENERIC_TAIL, None, 0, None) == _lib.ST_NOT_SUPPORTED
+    assert b"ST_FLAG_STORED_BAND" in lib.st_last_error()
+    d = _spec(stored_band=True, **bf).desc()
+    assert lib.st_backward(ctypes.byref(d), 1, 1, 1, 1, 1, None, None, 1, 1, 1, None, None,
+                           _lib.ST_GENERIC_TAIL, None, 0, None) == _lib.ST_WORKSPACE_TOO_SMALL
     d = _spec(seq_q=0).desc()
     assert lib.st_workspace_bytes(ctypes.byref(d)) == 0
     assert b"dimensions" in lib.st_last_error() or lib.st_last_error() != b""

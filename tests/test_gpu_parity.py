@@ -179,15 +179,19 @@ def test_bf16_stored_band_kernels_parity(cid, L, mode):
 @pytest.mark.parametrize("w,d,mask,L,mode", [(128, 128, "uniform_len", 1000, "direct_four_plan"),
                                              (256, 64, "uniform_len", 1500, "one_reference"),
                                              (256, 64, "none", 1100, "direct_four_plan"),
-                                             (64, 64, "uniform_len", 650, "one_reference"),
-                                             (192, 128, "none", 128, "one_reference")])
+                                             (128, 64, "uniform_len", 650, "one_reference"),
+                                             (256, 128, "none", 300, "one_reference")])
 def test_bf16_band_free_sweeps_parity(w, d, mask, L, mode):
     """The band-free tcgen05 sweeps (st_bfree.cu: transport output, C1 / R12 / C3 / R4 / R6 / C6 with the
     score and cotangent tiles recomputed per block, weights as bf16 hi/lo planes, MN-major operand chunks):
     both adjoint schedules, masked rows / columns (-inf offsets), partial last blocks, edge windows, a
-    band wider than the sequence, d = 64 / 128, against the oracle."""
+    band nearly as wide as the sequence, d = 64 / 128, against the oracle."""
     cfg = configs.Config(0, B=2, H=2, L=L, d=d, w=w, eps=0.05, T=12, R=2, dtype="bf16", mask=mask,
                          in_scale=1 / np.sqrt(d))
+    import dataclasses
+    spec = band.BandSpec(batch=2, heads=2, seq_q=L, seq_k=L, head_dim=d, half_band=w, base_depth=12, dtype="bf16")
+    # the problem is band-free: its workspace lacks the L x W band(s) of the stored-band layout
+    assert dataclasses.replace(spec, stored_band=True).workspace_bytes() - spec.workspace_bytes() > 0.9 * 4 * L * (2 * w + 1) * 4
     check_against_oracle(cfg, configs.make_inputs(cfg), BF16_TOL, BF16_TOL, mode=mode,
                          case=f"bfree-w{w}-d{d}-{mask}-{mode}")
 
