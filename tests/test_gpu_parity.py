@@ -151,6 +151,15 @@ def test_config2_parity_full_batch():
     check_against_oracle(cfg, configs.make_inputs(cfg), FP32_TOL, FP32_GRAD_TOL)
 
 
+def test_fp32_solve_more_blocks_than_resident_tiles():
+    """Config-2 geometry with 64 heads x 16 row blocks = 1024 work items (~750 active under the masks), more
+    than the 444 band tiles the persistent fp32 solve keeps resident (3 per SM): its non-resident mode
+    (tiles restaged every step, window duals through `vpriv`, grid barrier per step) against the oracle."""
+    cfg = configs.CONFIGS[2].replace(B=16, T=12)
+    inp = configs.make_inputs(cfg)
+    check_against_oracle(cfg, inp, FP32_TOL, FP32_GRAD_TOL, case="config2-B16-nonresident")
+
+
 def test_config3_dustbin_parity_full_batch():
     cfg = configs.CONFIGS[3]
     g, r, _ = check_against_oracle(cfg, configs.make_inputs(cfg), FP32_TOL, FP32_GRAD_TOL)

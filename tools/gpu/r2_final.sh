@@ -3,7 +3,7 @@
 set -x
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out /tmp/ncu
-python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "reuse or band_free" > gpurun_out/quick_tests.log 2>&1; tail -2 gpurun_out/quick_tests.log
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "reuse or band_free" > gpurun_out/quick_tests.log 2>&1; tail -2 gpurun_out/quick_tests.log
 python tools/timing.py 1 2 3 4 5 > gpurun_out/r2_configs_timing.txt 2>&1
 BWD_MODE=direct_four_plan python tools/timing.py 2 4 5 >> gpurun_out/r2_configs_timing.txt 2>&1
 python bench.py > gpurun_out/r2_bench_config4.json 2> gpurun_out/bench.err
@@ -16,11 +16,7 @@ for c in 4 5; do
 done
 python tools/bwd_only.py 4 direct_four_plan > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/bwd_c4d.csv python tools/bwd_only.py 4 direct_four_plan > /dev/null 2>&1
 python tools/launch_table.py gpurun_out/bwd_c4d.csv > gpurun_out/r2_launches_bwd_config4_direct.txt
-for k in "k_bsweep<0" "k_bsweep<3" "k_bsweep<2" "k_bsweep<1"; do
-  n=$(echo $k | tr -d '<' )
-  timeout 600 ncu --set full --clock-control none --import-source on --kernel-name regex:"$k" --launch-skip 1 --launch-count 1 -f -o /tmp/ncu/$n python tools/bwd_only.py 4 > gpurun_out/ncu_$n.log 2>&1
-  python tools/ncu_summary.py /tmp/ncu/$n.ncu-rep > gpurun_out/r2_ncu_config4_$n.txt 2>&1
-done
+bash tools/gpu/r2_ncu_bsweep.sh > gpurun_out/ncu_bsweep_all.log 2>&1
 timeout 600 ncu --set full --clock-control none --kernel-name regex:k_fstep16 --launch-skip 4 --launch-count 1 -f -o /tmp/ncu/fstep python tools/fwd_short.py 4 > gpurun_out/ncu_fstep.log 2>&1
 python tools/ncu_summary.py /tmp/ncu/fstep.ncu-rep > gpurun_out/r2_ncu_config4_fstep16.txt 2>&1
 cat gpurun_out/r2_configs_timing.txt

@@ -8,5 +8,5 @@ for pair in "7 pv_c1" "8 r12" "9 px_c3" "11 sbar_r6"; do
   timeout 600 ncu --set full --clock-control none --import-source on --kernel-name regex:k_bsweep --launch-skip $1 --launch-count 1 -f -o /tmp/ncu/$2 python tools/bwd_only.py 4 > gpurun_out/ncu_$2.log 2>&1
   python tools/ncu_summary.py /tmp/ncu/$2.ncu-rep > gpurun_out/r2_ncu_config4_bsweep_$2.txt 2>&1
 done
-cp /tmp/ncu/sbar_r6.ncu-rep gpurun_out/ 2>/dev/null
+
 cat gpurun_out/r2_ncu_config4_bsweep_*.txt
