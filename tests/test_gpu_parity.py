@@ -247,6 +247,25 @@ def test_deterministic_and_linear_in_G():
         assert rel(r3[k], 0.5 * r1[k] - 2.0 * r2[k]) < 1e-5, k
 
 
+def test_bf16_band_free_deterministic_and_linear_in_G():
+    """The band-free sweeps are run-to-run bit-identical (fixed-order row-part combines, no atomics on the
+    data path) and the adjoint is linear in the output cotangent (config-4 geometry, several blocks per CTA)."""
+    cfg = configs.CONFIGS[4].replace(L=8192, T=10)
+    inp = configs.make_inputs(cfg, heads=range(6))
+    a = gpu_run(cfg, inp, duals=False)
+    b = gpu_run(cfg, inp, duals=False)
+    for k in ("O", "dQ", "dK", "dV", "d_eps", "eta_v"):
+        assert np.array_equal(a[k], b[k]), k
+    shp = (6, 1, cfg.rows, cfg.d)
+    G1 = _dev(inp.G, inp.bits["G"]).reshape(shp)
+    G2 = torch.flip(G1, dims=[2]).contiguous()
+    r1 = gpu_run(cfg, inp, G=G1, duals=False)
+    r2 = gpu_run(cfg, inp, G=G2, duals=False)
+    r3 = gpu_run(cfg, inp, G=(0.5 * G1 - 2.0 * G2).contiguous(), duals=False)  # exact in bf16 up to one rounding
+    for k in ("dQ", "dK", "dV"):
+        assert rel(r3[k], 0.5 * r1[k] - 2.0 * r2[k]) < 5e-3, k
+
+
 @pytest.mark.parametrize("cid,heads", [(4, (0, 1)), (5, (0,))])
 def test_bf16_full_baseline_shape_parity(cid, heads):
     """Configs 4 / 5 at their full BASELINE shapes (L = 32768 / 131072, the full band, T, eps) on a
