@@ -384,8 +384,10 @@ WsLayout ws_layout(const Dims& m, const TcPlan& tp, bool bf) {
     }
     w.vp = w.gp = w.bfvec = 0;
     if (bf) {
-        w.vp = take((size_t)m.BH * tp.Lpk * tp.row_bytes);
-        w.gp = take((size_t)m.BH * tp.Lpq * tp.row_bytes);
+        if (!st::bfree_tma_available()) {  // else V and dO stream from the raw tensors through tensor maps
+            w.vp = take((size_t)m.BH * tp.Lpk * tp.row_bytes);
+            w.gp = take((size_t)m.BH * tp.Lpq * tp.row_bytes);
+        }
         w.bfvec = take(st::bfree_vec_bytes((int)m.BH, tp.Lpq, tp.Lpk));
     }
     w.bytes = o;
@@ -712,9 +714,10 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
         }
         if (bf) {
             // band-free transport application: O = P V from the packed planes, one tcgen05 sweep
-            uint8_t* vp = (uint8_t*)(ws + wl.vp);
-            ST_CUDA(st::launch_pack(desc->dtype, V, g.BH, g.Lk, g.Lrk, tp.Lpk, g.d, 0, vp, nullptr, nullptr, st));
-            ST_CUDA(st::launch_bfree_output(make_bfgeo(g, tp), qp[0], kp[0], vp, u_prev, v_prev,
+            const bool tma = st::bfree_tma_available();
+            uint8_t* vp = tma ? nullptr : (uint8_t*)(ws + wl.vp);  // V straight from the raw tensor through a tensor map
+            if (!tma) ST_CUDA(st::launch_pack(desc->dtype, V, g.BH, g.Lk, g.Lrk, tp.Lpk, g.d, 0, vp, nullptr, nullptr, st));
+            ST_CUDA(st::launch_bfree_output(make_bfgeo(g, tp), qp[0], kp[0], vp, V, u_prev, v_prev,
                                             (float*)(ws + wl.bfvec), O, st));
             band_record(workspace, Q, K, row_mask, col_mask, desc, 3, V);
             return ST_OK;
@@ -900,15 +903,17 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
         st::BfBwd b{};
         uint8_t* qp0 = (uint8_t*)(ws + wl.qp[0]);
         uint8_t* kp0 = (uint8_t*)(ws + wl.kp[0]);
-        uint8_t* vp0 = (uint8_t*)(ws + wl.vp);
-        uint8_t* gp0 = (uint8_t*)(ws + wl.gp);
+        uint8_t* vp0 = st::bfree_tma_available() ? nullptr : (uint8_t*)(ws + wl.vp);
+        uint8_t* gp0 = st::bfree_tma_available() ? nullptr : (uint8_t*)(ws + wl.gp);
         if (!packed) {
             ST_CUDA(st::launch_pack(desc->dtype, Q, g.BH, g.Lq, g.Lrq, tpl.Lpq, g.d, 0, qp0, nullptr, nullptr, st));
             ST_CUDA(st::launch_pack(desc->dtype, K, g.BH, g.Lk, g.Lrk, tpl.Lpk, g.d, 0, kp0, nullptr, nullptr, st));
         }
-        if (!(packed && band_v_valid(workspace, V)))  // the forward's transport sweep left the packed V plane
-            ST_CUDA(st::launch_pack(desc->dtype, V, g.BH, g.Lk, g.Lrk, tpl.Lpk, g.d, 0, vp0, nullptr, nullptr, st));
-        ST_CUDA(st::launch_pack(desc->dtype, dO, g.BH, g.Lq, g.Lrq, tpl.Lpq, g.d, 0, gp0, nullptr, nullptr, st));
+        if (!st::bfree_tma_available()) {  // else V and dO stream from the raw tensors through tensor maps
+            if (!(packed && band_v_valid(workspace, V)))  // the forward's transport sweep left the packed V plane
+                ST_CUDA(st::launch_pack(desc->dtype, V, g.BH, g.Lk, g.Lrk, tpl.Lpk, g.d, 0, vp0, nullptr, nullptr, st));
+            ST_CUDA(st::launch_pack(desc->dtype, dO, g.BH, g.Lq, g.Lrq, tpl.Lpq, g.d, 0, gp0, nullptr, nullptr, st));
+        }
         b.qp = qp0;
         b.kp = kp0;
         b.vp = vp0;
@@ -919,6 +924,7 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
         b.v1 = svv + (size_t)1 * m.BH * m.Lrk;
         b.v2 = svv + (size_t)2 * m.BH * m.Lrk;
         b.V = V;
+        b.dO = dO;
         b.vec = (float*)(ws + wl.bfvec);
         b.dQ = dQ;
         b.dK = dK;

@@ -30,6 +30,8 @@
 //   warps 2-17  epilogue: TMEM lane quadrant x column half x chunk parity; a thread owns one row
 //               and 32 columns of every other chunk, so every row reduction is in-thread and the
 //               four parts of a row combine in a fixed order.
+#include <cuda.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -51,7 +53,11 @@ constexpr int kNV = 2;    // vector ring slots
 
 enum { M_PV = 0, M_R12 = 1, M_PX = 2, M_SROW = 3, M_SCOL = 4 };
 
-struct SweepArgs {
+struct alignas(64) SweepArgs {
+    // tensor maps of the raw [BH][L][d] bf16 tensors behind the A2 / B2 streams (V and dO): boxes of
+    // 64 rows x 64 columns, SWIZZLE_128B (tma2 = 1; else A2 / B2 point at packed planes)
+    CUtensorMap tmA2, tmB2;
+    int tma2;
     int NA, NS0, NS1, row_bytes, maxwin;  // A buffers; ring slots of the B1 / B2 window chunks
     int H, NB, nblk;
     int L_own, L_other, Lr_own, Lp_own, Lp_other, w;
@@ -59,6 +65,8 @@ struct SweepArgs {
     int dbg;  // development ablations (ST_BF_DBG): 1 = no Y MMAs, 2 = one S / Z K-step, 4 = no cell math, 8 = no chunk loads (results invalid)
     float c2, scale;
     const uint8_t *A1, *B1, *A2, *B2;
+    const void *rawA2, *rawB2;  // raw [BH][Lr][D] bf16 tensors behind A2 / B2 (host side: tensor maps)
+    int Lr_other;
     const float* wv[5];  // window vectors [BH][Lp_other]; wv[0] = exponent offsets (-inf when inactive)
     const float* ov[5];  // own vectors [BH][Lp_own]; ov[0] = exponent offsets
     float* out_mat;      // [BH][Lr_own][D]
@@ -273,7 +281,7 @@ __device__ __forceinline__ unsigned long long bf_gtimer() {
 constexpr int kTrB = 4;
 
 template <int MODE, bool kDirect, int D>
-__global__ void __launch_bounds__(96 + 32 * kEW, 1) k_bsweep(SweepArgs a) {
+__global__ void __launch_bounds__(96 + 32 * kEW, 1) k_bsweep(const __grid_constant__ SweepArgs a) {
     using T = ModeTraits<MODE, kDirect>;
     constexpr bool kZ = T::kZ, kGemm = T::kGemm, kB2 = T::kB2;
     constexpr int NW = T::NW, NO = T::NO;
@@ -371,7 +379,18 @@ __global__ void __launch_bounds__(96 + 32 * kEW, 1) k_bsweep(SweepArgs a) {
                         mbar_arrive_expect_tx(&s.a_full[ab], a_stride);
                         const size_t off = ((size_t)b.x * a.Lp_own + i0) * a.row_bytes;
                         bulk_g2s(s.A + (size_t)ab * a_stride, a.A1 + off, blk_bytes, &s.a_full[ab]);
-                        if (kZ) bulk_g2s(s.A + (size_t)ab * a_stride + blk_bytes, a.A2 + off, blk_bytes, &s.a_full[ab]);
+                        if (kZ) {
+                            uint8_t* dst = s.A + (size_t)ab * a_stride + blk_bytes;
+                            if (a.tma2) {  // [d half][128 rows][128 B], two 64-row boxes per half
+#pragma unroll
+                                for (int kb = 0; kb < D / 64; ++kb)
+#pragma unroll
+                                    for (int h = 0; h < 2; ++h)
+                                        tma_load_3d(dst + kb * 16384 + h * 8192, &a.tmA2, kb * 64, i0 + 64 * h, b.x, &s.a_full[ab]);
+                            } else {
+                                bulk_g2s(dst, a.A2 + off, blk_bytes, &s.a_full[ab]);
+                            }
+                        }
                     }
                     ++pb;
                     moved = true;
@@ -395,7 +414,13 @@ __global__ void __launch_bounds__(96 + 32 * kEW, 1) k_bsweep(SweepArgs a) {
                 } else {
                     mbar_arrive_expect_tx(&full[sl], chk_bytes);
                     const size_t off = ((size_t)b.x * a.Lp_other + (size_t)(b.z + rc) * kCR) * a.row_bytes;
-                    bulk_g2s((ring ? s.B1 : s.B0) + (size_t)sl * chk_bytes, (ring ? a.B2 : a.B1) + off, chk_bytes, &full[sl]);
+                    if (ring && a.tma2) {  // [d half][64 rows][128 B]
+#pragma unroll
+                        for (int kb = 0; kb < D / 64; ++kb)
+                            tma_load_3d(s.B1 + (size_t)sl * chk_bytes + kb * 8192, &a.tmB2, kb * 64, (b.z + rc) * kCR, b.x, &full[sl]);
+                    } else {
+                        bulk_g2s((ring ? s.B1 : s.B0) + (size_t)sl * chk_bytes, (ring ? a.B2 : a.B1) + off, chk_bytes, &full[sl]);
+                    }
                 }
                 moved = true;
                 ++rs;
@@ -430,12 +455,18 @@ __global__ void __launch_bounds__(96 + 32 * kEW, 1) k_bsweep(SweepArgs a) {
                     const uint64_t bd = make_desc(smem_u32(s.B0 + (size_t)sl * chk_bytes), 128, sbo);
                     const uint32_t dt = tbase + YC + tb * TCOLS;
                     if (kZ) {  // the score and cotangent chains interleave (independent accumulators)
-                        const uint64_t bd2 = make_desc(smem_u32(s.B1 + (size_t)sl2 * chk_bytes), 128, sbo);
+                        const uint32_t a2s = smem_u32(s.A + (size_t)ab * a_stride + blk_bytes);
+                        const uint32_t b2s = smem_u32(s.B1 + (size_t)sl2 * chk_bytes);
+                        const uint64_t bd2 = make_desc(b2s, 128, sbo);
 #pragma unroll
                         for (int kk = 0; kk < ksteps; ++kk) {
                             if (kk > 0 && (a.dbg & 2)) break;
                             mma_bf16(dt, ad + (uint64_t)(kk * 16), bd + (uint64_t)(kk * 16), idesc_s, kk > 0);
-                            mma_bf16(dt + kCR, ad2 + (uint64_t)(kk * 16), bd2 + (uint64_t)(kk * 16), idesc_s, kk > 0);
+                            if (a.tma2)  // swizzled tiles: d half kk / 4, 32 bytes per K step inside the 128-byte row
+                                mma_bf16(dt + kCR, make_desc_sw128(a2s + (kk / 4) * 16384 + (kk % 4) * 32, 16, 1024),
+                                         make_desc_sw128(b2s + (kk / 4) * 8192 + (kk % 4) * 32, 16, 1024), idesc_s, kk > 0);
+                            else
+                                mma_bf16(dt + kCR, ad2 + (uint64_t)(kk * 16), bd2 + (uint64_t)(kk * 16), idesc_s, kk > 0);
                         }
                     } else {
 #pragma unroll
@@ -485,8 +516,12 @@ __global__ void __launch_bounds__(96 + 32 * kEW, 1) k_bsweep(SweepArgs a) {
 #pragma unroll
                                     for (int kk = 0; kk < 2; ++kk)
                                         mma_bf16_ts(dy, wa + 32 * hf + 16 * p + 8 * kk,
-                                                    xd + (uint64_t)((2 * hf + kk) * a.row_bytes), idesc_y,
-                                                    (yc > 0 || hf > 0 || p > 0 || kk > 0) ? 1u : 0u);
+                                                    (kLong1 && a.tma2)
+                                                        // swizzled V chunk read MN-major: 64-column halves 8192 B apart,
+                                                        // 8-row K groups 1024 B apart, 16 rows per K step
+                                                        ? make_desc_sw128(smem_u32(xs) + (2 * hf + kk) * 2048, 8192, 1024)
+                                                        : xd + (uint64_t)((2 * hf + kk) * a.row_bytes),
+                                                    idesc_y, (yc > 0 || hf > 0 || p > 0 || kk > 0) ? 1u : 0u);
                         }
                         tc_commit(&s.t_empty[wb]);
                         tc_commit(kLong1 ? &s.k2_empty[sl] : &s.k_empty[sl]);
@@ -742,11 +777,48 @@ int bf_num_sms() {
     return v > 0 ? v : 148;
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                  const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {  // the driver entry point through the runtime (no -lcuda)
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (getenv("ST_BF_NO_TMA") || cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return (EncodeTiledFn)p;
+    }();
+    return fn;
+}
+// [BH][Lr][d] bf16 (raw API tensor) -> boxes of 64 rows x 64 columns (128 bytes), SWIZZLE_128B, zeros past Lr
+bool make_tmap(CUtensorMap* m, const void* base, int BH, int Lr, int d) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || !base) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)Lr, (cuuint64_t)BH};
+    const cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)Lr * d * 2};
+    const cuuint32_t box[3] = {64, 64, 1}, es[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int MODE, bool kDirect, int D>
 cudaError_t run_sweep(SweepArgs a, cudaStream_t st) {
     const int grid = std::min(bf_num_sms(), a.nblk);
     a.wl_cap = (a.nblk + grid - 1) / grid;
     a.row_bytes = D * 2;
+    {   // the V / dO streams straight from the raw tensors through tensor maps (no packed copy) when the driver has them
+        using T0 = ModeTraits<MODE, kDirect>;
+        const int BH = a.nblk / a.NB;
+        a.tma2 = 0;
+        if (T0::kB2 && a.rawB2 && (!T0::kZ || a.rawA2)) {
+            bool okm = make_tmap(&a.tmB2, a.rawB2, BH, a.Lr_other, D);
+            if (okm && T0::kZ) okm = make_tmap(&a.tmA2, a.rawA2, BH, a.Lr_own, D);
+            a.tma2 = okm ? 1 : 0;
+        }
+        if (T0::kB2 && !a.tma2 && !a.B2) return cudaErrorNotSupported;
+    }
     static const int env_dbg = getenv("ST_BF_DBG") ? atoi(getenv("ST_BF_DBG")) : 0;
     static const int env_na = getenv("ST_BF_NA") ? atoi(getenv("ST_BF_NA")) : 0;
     static const int env_ns0 = getenv("ST_BF_NS0") ? atoi(getenv("ST_BF_NS0")) : 0;
@@ -849,6 +921,7 @@ SweepArgs base_args(const BfGeo& g, bool col) {
     a.L_own = col ? g.Lk : g.Lq;
     a.L_other = col ? g.Lq : g.Lk;
     a.Lr_own = col ? g.Lrk : g.Lrq;
+    a.Lr_other = col ? g.Lrq : g.Lrk;
     a.Lp_own = col ? g.Lpk : g.Lpq;
     a.Lp_other = col ? g.Lpq : g.Lpk;
     a.NB = a.Lp_own / 128;
@@ -866,8 +939,8 @@ cudaError_t prep(const BfGeo& g, bool col, const float* d2, const float* d1, con
 }
 
 template <int D>
-cudaError_t output_t(const BfGeo& g, const uint8_t* qp, const uint8_t* kp, const uint8_t* vp, const float* u,
-                     const float* v, float* vec, float* O, cudaStream_t st) {
+cudaError_t output_t(const BfGeo& g, const uint8_t* qp, const uint8_t* kp, const uint8_t* vp, const void* Vraw,
+                     const float* u, const float* v, float* vec, float* O, cudaStream_t st) {
     const Vecs V = carve_vecs(g, vec);
     cudaError_t e;
     if ((e = prep(g, false, u, nullptr, nullptr, V.U2, nullptr, nullptr, nullptr, nullptr, st)) != cudaSuccess) return e;
@@ -876,6 +949,7 @@ cudaError_t output_t(const BfGeo& g, const uint8_t* qp, const uint8_t* kp, const
     a.A1 = qp;
     a.B1 = kp;
     a.B2 = vp;
+    a.rawB2 = Vraw;
     a.wv[0] = V.V2;
     a.ov[0] = V.U2;
     a.out_mat = O;
@@ -892,7 +966,7 @@ cudaError_t backward_t(const BfGeo& g, const BfBwd& p, cudaStream_t st) {
     BF(prep(g, true, p.v2, p.v1, p.v0, V.V2, V.V1, V.V0, V.BETA, V.DELTA, st));
     {   // C1: dV_j = sum_i P22 dO_i;  g_v_j = <V_j, dV_j> = sum_i P22 Z   (own = keys)
         SweepArgs a = base_args(g, true);
-        a.A1 = p.kp; a.B1 = p.qp; a.B2 = p.gp;
+        a.A1 = p.kp; a.B1 = p.qp; a.B2 = p.gp; a.rawB2 = p.dO;
         a.wv[0] = V.U2; a.ov[0] = V.V2;
         a.out_mat = p.dV;
         a.out1 = V.GV;
@@ -901,7 +975,7 @@ cudaError_t backward_t(const BfGeo& g, const BfBwd& p, cudaStream_t st) {
     }
     {   // R12: u2b_i = sum_j P22 (Z - g_v_j)
         SweepArgs a = base_args(g, false);
-        a.A1 = p.qp; a.B1 = p.kp; a.A2 = p.gp; a.B2 = p.vp;
+        a.A1 = p.qp; a.B1 = p.kp; a.A2 = p.gp; a.B2 = p.vp; a.rawA2 = p.dO; a.rawB2 = p.V;
         a.wv[0] = V.V2; a.wv[1] = V.GV; a.ov[0] = V.U2;
         a.out1 = V.U2B;
         BF((run_sweep<M_R12, false, D>(a, st)));
@@ -926,7 +1000,7 @@ cudaError_t backward_t(const BfGeo& g, const BfBwd& p, cudaStream_t st) {
     }
     {   // R6: dQ_i = inv sum_j Sbar K_j, d_eps partials
         SweepArgs a = base_args(g, false);
-        a.A1 = p.qp; a.B1 = p.kp; a.A2 = p.gp; a.B2 = p.vp;
+        a.A1 = p.qp; a.B1 = p.kp; a.A2 = p.gp; a.B2 = p.vp; a.rawA2 = p.dO; a.rawB2 = p.V;
         if (kDirect) {
             a.ov[0] = V.U2; a.ov[1] = V.U1; a.ov[2] = V.U2B; a.ov[3] = V.U1B;
             a.wv[0] = V.V2; a.wv[1] = V.V1; a.wv[2] = V.V0; a.wv[3] = V.GV; a.wv[4] = V.V1B;
@@ -941,7 +1015,7 @@ cudaError_t backward_t(const BfGeo& g, const BfBwd& p, cudaStream_t st) {
     }
     {   // C6 (+ C5): dK_j = inv sum_i Sbar Q_i;  v0b_j = -delta_j sum_i P22 alpha_i u1b_i
         SweepArgs a = base_args(g, true);
-        a.A1 = p.kp; a.B1 = p.qp; a.A2 = p.vp; a.B2 = p.gp;
+        a.A1 = p.kp; a.B1 = p.qp; a.A2 = p.vp; a.B2 = p.gp; a.rawA2 = p.V; a.rawB2 = p.dO;
         if (kDirect) {
             a.ov[0] = V.V2; a.ov[1] = V.V1; a.ov[2] = V.V0; a.ov[3] = V.GV; a.ov[4] = V.V1B;
             a.wv[0] = V.U2; a.wv[1] = V.U1; a.wv[2] = V.U2B; a.wv[3] = V.U1B;
@@ -960,10 +1034,12 @@ cudaError_t backward_t(const BfGeo& g, const BfBwd& p, cudaStream_t st) {
 
 }  // namespace
 
-cudaError_t launch_bfree_output(const BfGeo& g, const uint8_t* qp, const uint8_t* kp, const uint8_t* vp,
+bool bfree_tma_available() { return encode_fn() != nullptr; }
+
+cudaError_t launch_bfree_output(const BfGeo& g, const uint8_t* qp, const uint8_t* kp, const uint8_t* vp, const void* Vraw,
                                 const float* u, const float* v, float* vec, float* O, cudaStream_t s) {
-    if (g.d == 128) return output_t<128>(g, qp, kp, vp, u, v, vec, O, s);
-    if (g.d == 64) return output_t<64>(g, qp, kp, vp, u, v, vec, O, s);
+    if (g.d == 128) return output_t<128>(g, qp, kp, vp, Vraw, u, v, vec, O, s);
+    if (g.d == 64) return output_t<64>(g, qp, kp, vp, Vraw, u, v, vec, O, s);
     return cudaErrorNotSupported;
 }
 

@@ -34,13 +34,17 @@ long long bfree_launch_count(bool reset);
 
 // O = P^(T+R,T+R) V.  qp / kp / vp: packed bf16 planes [BH][Lp][d] (launch_pack, shift 0);
 // u / v: the final raw duals (base 2) in the API layout; vec: the vector workspace.
-cudaError_t launch_bfree_output(const BfGeo& g, const uint8_t* qp, const uint8_t* kp, const uint8_t* vp,
+// true when the driver exposes cuTensorMapEncodeTiled: the V / dO streams then come straight from the raw
+// tensors through tensor maps (cp.async.bulk.tensor, SWIZZLE_128B) and vp / gp may be null
+bool bfree_tma_available();
+cudaError_t launch_bfree_output(const BfGeo& g, const uint8_t* qp, const uint8_t* kp, const uint8_t* vp, const void* Vraw,
                                 const float* u, const float* v, float* vec, float* O, cudaStream_t s);
 
 struct BfBwd {
     const uint8_t *qp, *kp, *vp, *gp;     // packed Q, K, V, dO
     const float *u1, *u2, *v0, *v1, *v2;  // saved raw tail duals (base 2), API layout
-    const void* V;                        // raw V [BH][Lrk][d] bf16 (g_v = <V_j, dV_j>)
+    const void* V;                        // raw V [BH][Lrk][d] bf16 (g_v = <V_j, dV_j>; tensor-map source)
+    const void* dO;                       // raw dO [BH][Lrq][d] bf16 (tensor-map source)
     float* vec;                           // vector workspace (bfree_vec_bytes)
     float *dQ, *dK, *dV;                  // [BH][Lr][d] fp32
     float* deps_part;                     // [BH][Lrq]

@@ -68,6 +68,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// global -> shared tiled copy through a tensor map (TMA, UTMALDG): box at coordinates (c0 fastest, c1, c2)
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
 // shared -> global bulk store (bulk-group completion); SMEM writes must be fenced to the async proxy first
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
@@ -108,6 +117,13 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t smem_addr, uint32_t lbo, 
     d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
     d |= (uint64_t)1u << 46;  // descriptor version (sm_100)
     return d;                 // base offset 0, lbo mode 0, layout SWIZZLE_NONE
+}
+
+// 128-byte swizzled operand (rows of 128 bytes, 8-row atoms of 1024 bytes, as a SWIZZLE_128B tensor-map
+// box lands in SMEM).  K-major: SBO = 1024 between 8-row groups, LBO unused; MN-major: LBO = byte step
+// between 64-element groups along MN, SBO = 1024 between 8-row groups along K.
+__device__ __forceinline__ uint64_t make_desc_sw128(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+    return make_desc(smem_addr, lbo, sbo) | ((uint64_t)2u << 61);
 }
 
 // fmt: 1 = BF16 (kind::f16), 2 = TF32 (kind::tf32); D is F32; A, B K-major.
