@@ -717,7 +717,7 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
             const bool tma = st::bfree_tma_available();
             uint8_t* vp = tma ? nullptr : (uint8_t*)(ws + wl.vp);  // V straight from the raw tensor through a tensor map
             if (!tma) ST_CUDA(st::launch_pack(desc->dtype, V, g.BH, g.Lk, g.Lrk, tp.Lpk, g.d, 0, vp, nullptr, nullptr, st));
-            ST_CUDA(st::launch_bfree_output(make_bfgeo(g, tp), qp[0], kp[0], vp, V, u_prev, v_prev,
+            ST_CUDA(st::launch_bfree_output(make_bfgeo(g, tp), qp[0], kp[0], vp, Q, K, V, u_prev, v_prev,
                                             (float*)(ws + wl.bfvec), O, st));
             band_record(workspace, Q, K, row_mask, col_mask, desc, 3, V);
             return ST_OK;
@@ -905,7 +905,7 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
         uint8_t* kp0 = (uint8_t*)(ws + wl.kp[0]);
         uint8_t* vp0 = st::bfree_tma_available() ? nullptr : (uint8_t*)(ws + wl.vp);
         uint8_t* gp0 = st::bfree_tma_available() ? nullptr : (uint8_t*)(ws + wl.gp);
-        if (!packed) {
+        if (!packed && !st::bfree_tma_available()) {  // with tensor maps the sweeps read the raw Q / K
             ST_CUDA(st::launch_pack(desc->dtype, Q, g.BH, g.Lq, g.Lrq, tpl.Lpq, g.d, 0, qp0, nullptr, nullptr, st));
             ST_CUDA(st::launch_pack(desc->dtype, K, g.BH, g.Lk, g.Lrk, tpl.Lpk, g.d, 0, kp0, nullptr, nullptr, st));
         }
@@ -923,6 +923,8 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
         b.v0 = svv;
         b.v1 = svv + (size_t)1 * m.BH * m.Lrk;
         b.v2 = svv + (size_t)2 * m.BH * m.Lrk;
+        b.Q = Q;
+        b.K = K;
         b.V = V;
         b.dO = dO;
         b.vec = (float*)(ws + wl.bfvec);

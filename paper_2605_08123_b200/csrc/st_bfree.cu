@@ -58,6 +58,8 @@ struct alignas(64) SweepArgs {
     // 64 rows x 64 columns, SWIZZLE_128B (tma2 = 1; else A2 / B2 point at packed planes)
     CUtensorMap tmA2, tmB2;
     int tma2;
+    CUtensorMap tmA1, tmB1;  // the same for the A1 / B1 streams (Q and K): tma1
+    int tma1;
     int NA, NS0, NS1, row_bytes, maxwin;  // A buffers; ring slots of the B1 / B2 window chunks
     int H, NB, nblk;
     int L_own, L_other, Lr_own, Lp_own, Lp_other, w;
@@ -65,7 +67,7 @@ struct alignas(64) SweepArgs {
     int dbg;  // development ablations (ST_BF_DBG): 1 = no Y MMAs, 2 = one S / Z K-step, 4 = no cell math, 8 = no chunk loads (results invalid)
     float c2, scale;
     const uint8_t *A1, *B1, *A2, *B2;
-    const void *rawA2, *rawB2;  // raw [BH][Lr][D] bf16 tensors behind A2 / B2 (host side: tensor maps)
+    const void *rawA1, *rawB1, *rawA2, *rawB2;  // raw [BH][Lr][D] bf16 tensors behind the streams (host side: tensor maps)
     int Lr_other;
     const float* wv[5];  // window vectors [BH][Lp_other]; wv[0] = exponent offsets (-inf when inactive)
     const float* ov[5];  // own vectors [BH][Lp_own]; ov[0] = exponent offsets
@@ -378,7 +380,15 @@ __global__ void __launch_bounds__(96 + 32 * kEW, 1) k_bsweep(const __grid_consta
                                      &s.v_full[vs]);
                         mbar_arrive_expect_tx(&s.a_full[ab], a_stride);
                         const size_t off = ((size_t)b.x * a.Lp_own + i0) * a.row_bytes;
-                        bulk_g2s(s.A + (size_t)ab * a_stride, a.A1 + off, blk_bytes, &s.a_full[ab]);
+                        if (a.tma1) {  // [d half][128 rows][128 B], two 64-row boxes per half
+#pragma unroll
+                            for (int kb = 0; kb < D / 64; ++kb)
+#pragma unroll
+                                for (int h = 0; h < 2; ++h)
+                                    tma_load_3d(s.A + (size_t)ab * a_stride + kb * 16384 + h * 8192, &a.tmA1, kb * 64, i0 + 64 * h, b.x, &s.a_full[ab]);
+                        } else {
+                            bulk_g2s(s.A + (size_t)ab * a_stride, a.A1 + off, blk_bytes, &s.a_full[ab]);
+                        }
                         if (kZ) {
                             uint8_t* dst = s.A + (size_t)ab * a_stride + blk_bytes;
                             if (a.tma2) {  // [d half][128 rows][128 B], two 64-row boxes per half
@@ -414,10 +424,11 @@ __global__ void __launch_bounds__(96 + 32 * kEW, 1) k_bsweep(const __grid_consta
                 } else {
                     mbar_arrive_expect_tx(&full[sl], chk_bytes);
                     const size_t off = ((size_t)b.x * a.Lp_other + (size_t)(b.z + rc) * kCR) * a.row_bytes;
-                    if (ring && a.tma2) {  // [d half][64 rows][128 B]
+                    if (ring ? a.tma2 : a.tma1) {  // [d half][64 rows][128 B]
 #pragma unroll
                         for (int kb = 0; kb < D / 64; ++kb)
-                            tma_load_3d(s.B1 + (size_t)sl * chk_bytes + kb * 8192, &a.tmB2, kb * 64, (b.z + rc) * kCR, b.x, &full[sl]);
+                            tma_load_3d((ring ? s.B1 : s.B0) + (size_t)sl * chk_bytes + kb * 8192, ring ? &a.tmB2 : &a.tmB1, kb * 64,
+                                        (b.z + rc) * kCR, b.x, &full[sl]);
                     } else {
                         bulk_g2s((ring ? s.B1 : s.B0) + (size_t)sl * chk_bytes, (ring ? a.B2 : a.B1) + off, chk_bytes, &full[sl]);
                     }
@@ -452,8 +463,17 @@ __global__ void __launch_bounds__(96 + 32 * kEW, 1) k_bsweep(const __grid_consta
                 BF_TRACE(lane == 0 && sb == kTrB, sc);
                 tc_fence_after();
                 if (elect_one()) {
-                    const uint64_t bd = make_desc(smem_u32(s.B0 + (size_t)sl * chk_bytes), 128, sbo);
+                    const uint32_t a1s = smem_u32(s.A + (size_t)ab * a_stride), b1s = smem_u32(s.B0 + (size_t)sl * chk_bytes);
+                    const uint64_t bd = make_desc(b1s, 128, sbo);
                     const uint32_t dt = tbase + YC + tb * TCOLS;
+                    // score tile K step kk: packed planes (core-matrix order) or 128B-swizzled tensor-map tiles
+                    auto s_mma = [&](int kk) {
+                        if (a.tma1)
+                            mma_bf16(dt, make_desc_sw128(a1s + (kk / 4) * 16384 + (kk % 4) * 32, 16, 1024),
+                                     make_desc_sw128(b1s + (kk / 4) * 8192 + (kk % 4) * 32, 16, 1024), idesc_s, kk > 0);
+                        else
+                            mma_bf16(dt, ad + (uint64_t)(kk * 16), bd + (uint64_t)(kk * 16), idesc_s, kk > 0);
+                    };
                     if (kZ) {  // the score and cotangent chains interleave (independent accumulators)
                         const uint32_t a2s = smem_u32(s.A + (size_t)ab * a_stride + blk_bytes);
                         const uint32_t b2s = smem_u32(s.B1 + (size_t)sl2 * chk_bytes);
@@ -461,7 +481,7 @@ __global__ void __launch_bounds__(96 + 32 * kEW, 1) k_bsweep(const __grid_consta
 #pragma unroll
                         for (int kk = 0; kk < ksteps; ++kk) {
                             if (kk > 0 && (a.dbg & 2)) break;
-                            mma_bf16(dt, ad + (uint64_t)(kk * 16), bd + (uint64_t)(kk * 16), idesc_s, kk > 0);
+                            s_mma(kk);
                             if (a.tma2)  // swizzled tiles: d half kk / 4, 32 bytes per K step inside the 128-byte row
                                 mma_bf16(dt + kCR, make_desc_sw128(a2s + (kk / 4) * 16384 + (kk % 4) * 32, 16, 1024),
                                          make_desc_sw128(b2s + (kk / 4) * 8192 + (kk % 4) * 32, 16, 1024), idesc_s, kk > 0);
@@ -472,7 +492,7 @@ __global__ void __launch_bounds__(96 + 32 * kEW, 1) k_bsweep(const __grid_consta
 #pragma unroll
                         for (int kk = 0; kk < ksteps; ++kk) {
                             if (kk > 0 && (a.dbg & 2)) break;
-                            mma_bf16(dt, ad + (uint64_t)(kk * 16), bd + (uint64_t)(kk * 16), idesc_s, kk > 0);
+                            s_mma(kk);
                         }
                     }
                     tc_commit(&s.t_full[tb]);
@@ -516,9 +536,9 @@ __global__ void __launch_bounds__(96 + 32 * kEW, 1) k_bsweep(const __grid_consta
 #pragma unroll
                                     for (int kk = 0; kk < 2; ++kk)
                                         mma_bf16_ts(dy, wa + 32 * hf + 16 * p + 8 * kk,
-                                                    (kLong1 && a.tma2)
-                                                        // swizzled V chunk read MN-major: 64-column halves 8192 B apart,
-                                                        // 8-row K groups 1024 B apart, 16 rows per K step
+                                                    (kLong1 ? a.tma2 : a.tma1)
+                                                        // swizzled operand chunk read MN-major: 64-column halves 8192 B
+                                                        // apart, 8-row K groups 1024 B apart, 16 rows per K step
                                                         ? make_desc_sw128(smem_u32(xs) + (2 * hf + kk) * 2048, 8192, 1024)
                                                         : xd + (uint64_t)((2 * hf + kk) * a.row_bytes),
                                                     idesc_y, (yc > 0 || hf > 0 || p > 0 || kk > 0) ? 1u : 0u);
@@ -818,6 +838,8 @@ cudaError_t run_sweep(SweepArgs a, cudaStream_t st) {
             a.tma2 = okm ? 1 : 0;
         }
         if (T0::kB2 && !a.tma2 && !a.B2) return cudaErrorNotSupported;
+        a.tma1 = (a.rawA1 && a.rawB1 && make_tmap(&a.tmA1, a.rawA1, BH, a.Lr_own, D) && make_tmap(&a.tmB1, a.rawB1, BH, a.Lr_other, D)) ? 1 : 0;
+        if (!a.tma1 && (!a.A1 || !a.B1)) return cudaErrorNotSupported;
     }
     static const int env_dbg = getenv("ST_BF_DBG") ? atoi(getenv("ST_BF_DBG")) : 0;
     static const int env_na = getenv("ST_BF_NA") ? atoi(getenv("ST_BF_NA")) : 0;
@@ -939,8 +961,8 @@ cudaError_t prep(const BfGeo& g, bool col, const float* d2, const float* d1, con
 }
 
 template <int D>
-cudaError_t output_t(const BfGeo& g, const uint8_t* qp, const uint8_t* kp, const uint8_t* vp, const void* Vraw,
-                     const float* u, const float* v, float* vec, float* O, cudaStream_t st) {
+cudaError_t output_t(const BfGeo& g, const uint8_t* qp, const uint8_t* kp, const uint8_t* vp, const void* Qraw,
+                     const void* Kraw, const void* Vraw, const float* u, const float* v, float* vec, float* O, cudaStream_t st) {
     const Vecs V = carve_vecs(g, vec);
     cudaError_t e;
     if ((e = prep(g, false, u, nullptr, nullptr, V.U2, nullptr, nullptr, nullptr, nullptr, st)) != cudaSuccess) return e;
@@ -950,6 +972,8 @@ cudaError_t output_t(const BfGeo& g, const uint8_t* qp, const uint8_t* kp, const
     a.B1 = kp;
     a.B2 = vp;
     a.rawB2 = Vraw;
+    a.rawA1 = Qraw;
+    a.rawB1 = Kraw;
     a.wv[0] = V.V2;
     a.ov[0] = V.U2;
     a.out_mat = O;
@@ -966,7 +990,7 @@ cudaError_t backward_t(const BfGeo& g, const BfBwd& p, cudaStream_t st) {
     BF(prep(g, true, p.v2, p.v1, p.v0, V.V2, V.V1, V.V0, V.BETA, V.DELTA, st));
     {   // C1: dV_j = sum_i P22 dO_i;  g_v_j = <V_j, dV_j> = sum_i P22 Z   (own = keys)
         SweepArgs a = base_args(g, true);
-        a.A1 = p.kp; a.B1 = p.qp; a.B2 = p.gp; a.rawB2 = p.dO;
+        a.A1 = p.kp; a.B1 = p.qp; a.B2 = p.gp; a.rawB2 = p.dO; a.rawA1 = p.K; a.rawB1 = p.Q;
         a.wv[0] = V.U2; a.ov[0] = V.V2;
         a.out_mat = p.dV;
         a.out1 = V.GV;
@@ -975,14 +999,14 @@ cudaError_t backward_t(const BfGeo& g, const BfBwd& p, cudaStream_t st) {
     }
     {   // R12: u2b_i = sum_j P22 (Z - g_v_j)
         SweepArgs a = base_args(g, false);
-        a.A1 = p.qp; a.B1 = p.kp; a.A2 = p.gp; a.B2 = p.vp; a.rawA2 = p.dO; a.rawB2 = p.V;
+        a.A1 = p.qp; a.B1 = p.kp; a.A2 = p.gp; a.B2 = p.vp; a.rawA2 = p.dO; a.rawB2 = p.V; a.rawA1 = p.Q; a.rawB1 = p.K;
         a.wv[0] = V.V2; a.wv[1] = V.GV; a.ov[0] = V.U2;
         a.out1 = V.U2B;
         BF((run_sweep<M_R12, false, D>(a, st)));
     }
     {   // C3: v1b_j = -beta_j sum_i P22 u2b_i   (direct: -sum_i P21 u2b_i, P21 = ex2(s + u2_i + v1_j))
         SweepArgs a = base_args(g, true);
-        a.A1 = p.kp; a.B1 = p.qp;
+        a.A1 = p.kp; a.B1 = p.qp; a.rawA1 = p.K; a.rawB1 = p.Q;
         a.wv[0] = V.U2; a.wv[1] = V.U2B; a.ov[0] = kDirect ? V.V1 : V.V2;
         a.fvec = kDirect ? nullptr : V.BETA;
         a.out1 = V.V1B;
@@ -991,7 +1015,7 @@ cudaError_t backward_t(const BfGeo& g, const BfBwd& p, cudaStream_t st) {
     }
     {   // R4: u1b_i = -alpha_i sum_j P22 beta_j v1b_j   (direct: -sum_j P11 v1b_j)
         SweepArgs a = base_args(g, false);
-        a.A1 = p.qp; a.B1 = p.kp;
+        a.A1 = p.qp; a.B1 = p.kp; a.rawA1 = p.Q; a.rawB1 = p.K;
         a.wv[0] = kDirect ? V.V1 : V.V2; a.wv[1] = kDirect ? V.V1B : V.BV1; a.ov[0] = kDirect ? V.U1 : V.U2;
         a.fvec = kDirect ? nullptr : V.ALPHA;
         a.out1 = V.U1B;
@@ -1000,7 +1024,7 @@ cudaError_t backward_t(const BfGeo& g, const BfBwd& p, cudaStream_t st) {
     }
     {   // R6: dQ_i = inv sum_j Sbar K_j, d_eps partials
         SweepArgs a = base_args(g, false);
-        a.A1 = p.qp; a.B1 = p.kp; a.A2 = p.gp; a.B2 = p.vp; a.rawA2 = p.dO; a.rawB2 = p.V;
+        a.A1 = p.qp; a.B1 = p.kp; a.A2 = p.gp; a.B2 = p.vp; a.rawA2 = p.dO; a.rawB2 = p.V; a.rawA1 = p.Q; a.rawB1 = p.K;
         if (kDirect) {
             a.ov[0] = V.U2; a.ov[1] = V.U1; a.ov[2] = V.U2B; a.ov[3] = V.U1B;
             a.wv[0] = V.V2; a.wv[1] = V.V1; a.wv[2] = V.V0; a.wv[3] = V.GV; a.wv[4] = V.V1B;
@@ -1015,7 +1039,7 @@ cudaError_t backward_t(const BfGeo& g, const BfBwd& p, cudaStream_t st) {
     }
     {   // C6 (+ C5): dK_j = inv sum_i Sbar Q_i;  v0b_j = -delta_j sum_i P22 alpha_i u1b_i
         SweepArgs a = base_args(g, true);
-        a.A1 = p.kp; a.B1 = p.qp; a.A2 = p.vp; a.B2 = p.gp; a.rawA2 = p.V; a.rawB2 = p.dO;
+        a.A1 = p.kp; a.B1 = p.qp; a.A2 = p.vp; a.B2 = p.gp; a.rawA2 = p.V; a.rawB2 = p.dO; a.rawA1 = p.K; a.rawB1 = p.Q;
         if (kDirect) {
             a.ov[0] = V.V2; a.ov[1] = V.V1; a.ov[2] = V.V0; a.ov[3] = V.GV; a.ov[4] = V.V1B;
             a.wv[0] = V.U2; a.wv[1] = V.U1; a.wv[2] = V.U2B; a.wv[3] = V.U1B;
@@ -1036,10 +1060,11 @@ cudaError_t backward_t(const BfGeo& g, const BfBwd& p, cudaStream_t st) {
 
 bool bfree_tma_available() { return encode_fn() != nullptr; }
 
-cudaError_t launch_bfree_output(const BfGeo& g, const uint8_t* qp, const uint8_t* kp, const uint8_t* vp, const void* Vraw,
-                                const float* u, const float* v, float* vec, float* O, cudaStream_t s) {
-    if (g.d == 128) return output_t<128>(g, qp, kp, vp, Vraw, u, v, vec, O, s);
-    if (g.d == 64) return output_t<64>(g, qp, kp, vp, Vraw, u, v, vec, O, s);
+cudaError_t launch_bfree_output(const BfGeo& g, const uint8_t* qp, const uint8_t* kp, const uint8_t* vp, const void* Qraw,
+                                const void* Kraw, const void* Vraw, const float* u, const float* v, float* vec, float* O,
+                                cudaStream_t s) {
+    if (g.d == 128) return output_t<128>(g, qp, kp, vp, Qraw, Kraw, Vraw, u, v, vec, O, s);
+    if (g.d == 64) return output_t<64>(g, qp, kp, vp, Qraw, Kraw, Vraw, u, v, vec, O, s);
     return cudaErrorNotSupported;
 }
 

@@ -37,12 +37,14 @@ long long bfree_launch_count(bool reset);
 // true when the driver exposes cuTensorMapEncodeTiled: the V / dO streams then come straight from the raw
 // tensors through tensor maps (cp.async.bulk.tensor, SWIZZLE_128B) and vp / gp may be null
 bool bfree_tma_available();
-cudaError_t launch_bfree_output(const BfGeo& g, const uint8_t* qp, const uint8_t* kp, const uint8_t* vp, const void* Vraw,
-                                const float* u, const float* v, float* vec, float* O, cudaStream_t s);
+cudaError_t launch_bfree_output(const BfGeo& g, const uint8_t* qp, const uint8_t* kp, const uint8_t* vp, const void* Qraw,
+                                const void* Kraw, const void* Vraw, const float* u, const float* v, float* vec, float* O,
+                                cudaStream_t s);
 
 struct BfBwd {
     const uint8_t *qp, *kp, *vp, *gp;     // packed Q, K, V, dO
     const float *u1, *u2, *v0, *v1, *v2;  // saved raw tail duals (base 2), API layout
+    const void *Q, *K;                    // raw Q, K [BH][Lr][d] bf16 (tensor-map sources)
     const void* V;                        // raw V [BH][Lrk][d] bf16 (g_v = <V_j, dV_j>; tensor-map source)
     const void* dO;                       // raw dO [BH][Lrq][d] bf16 (tensor-map source)
     float* vec;                           // vector workspace (bfree_vec_bytes)
