@@ -310,7 +310,15 @@ bool bfree_plan(const st_desc* d, const Dims& m, const TcPlan& tp) {
     return st::bfree_supported((int)m.d, (int)m.w, d->dustbin, m.esz);
 }
 
-WsLayout ws_layout(const Dims& m, const TcPlan& tp, bool bf) {
+// planes = false: the packed Q / K planes are not needed (band-free problem whose solve and sweeps load
+// their operand tiles from the raw tensors through tensor maps)
+// the packed planes are still read unless the problem is band-free, the full-step solve runs it and the
+// driver provides tensor maps
+bool need_planes(const st_desc* d, const Dims& m, const TcPlan& tp, bool bf) {
+    return !(bf && st::bfree_tma_available() && fstep_plan(d, tp, m).ok && !getenv("ST_FSTEP_NO_TMA"));
+}
+
+WsLayout ws_layout(const Dims& m, const TcPlan& tp, bool bf, bool planes = true) {
     WsLayout w;
     w.bfree = bf;
     size_t o = 0;
@@ -367,7 +375,7 @@ WsLayout ws_layout(const Dims& m, const TcPlan& tp, bool bf) {
         w.fs_partm = take(2 * np);
     }
     if (tp.ok) {
-        for (int p = 0; p < tp.npl; ++p) {
+        for (int p = 0; planes && p < tp.npl; ++p) {
             w.qp[p] = take((size_t)m.BH * tp.Lpq * tp.row_bytes);
             w.kp[p] = take((size_t)m.BH * tp.Lpk * tp.row_bytes);
         }
@@ -487,7 +495,8 @@ size_t st_workspace_bytes(const st_desc* desc) {
     Dims m;
     if (check_desc(desc, m) != ST_OK) return 0;
     const TcPlan tp = tc_plan(desc, m);
-    return ws_layout(m, tp, bfree_plan(desc, m, tp)).bytes;
+    const bool bf = bfree_plan(desc, m, tp);
+    return ws_layout(m, tp, bf, need_planes(desc, m, tp, bf)).bytes;
 }
 
 // Score scale of full step t (1-based) relative to the final temperature: the band is stored at
@@ -561,7 +570,8 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
     const bool bf = bfree_plan(desc, m, tp);
     if (bf && hook)
         return fail(ST_NOT_SUPPORTED, "sequence sharding runs on the stored-band kernels: set ST_FLAG_STORED_BAND");
-    const WsLayout wl = ws_layout(m, tp, bf);
+    const bool planes = need_planes(desc, m, tp, bf);
+    const WsLayout wl = ws_layout(m, tp, bf, planes);
     if (workspace == nullptr || workspace_bytes < wl.bytes)
         return fail(ST_WORKSPACE_TOO_SMALL, "workspace smaller than st_workspace_bytes()");
     cudaStream_t st = (cudaStream_t)stream;
@@ -597,7 +607,7 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
         // ---- tensor-core path: pack Q/K once, then 2 tcgen05 half-step launches per step
         uint8_t* qp[3] = {nullptr, nullptr, nullptr};
         uint8_t* kp[3] = {nullptr, nullptr, nullptr};
-        for (int p = 0; p < tp.npl; ++p) {
+        for (int p = 0; planes && p < tp.npl; ++p) {
             qp[p] = (uint8_t*)(ws + wl.qp[p]);
             kp[p] = (uint8_t*)(ws + wl.kp[p]);
         }
@@ -605,8 +615,10 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
         int* work_q = (int*)(ws + wl.work_q);
         int* work_k = (int*)(ws + wl.work_k);
         int* cnt = (int*)(ws + wl.cnt);
-        ST_CUDA(st::launch_pack(desc->dtype, Q, g.BH, g.Lq, g.Lrq, tp.Lpq, g.d, tp.shift, qp[0], qp[1], qp[2], st));
-        ST_CUDA(st::launch_pack(desc->dtype, K, g.BH, g.Lk, g.Lrk, tp.Lpk, g.d, tp.shift, kp[0], kp[1], kp[2], st));
+        if (planes) {
+            ST_CUDA(st::launch_pack(desc->dtype, Q, g.BH, g.Lq, g.Lrq, tp.Lpq, g.d, tp.shift, qp[0], qp[1], qp[2], st));
+            ST_CUDA(st::launch_pack(desc->dtype, K, g.BH, g.Lk, g.Lrk, tp.Lpk, g.d, tp.shift, kp[0], kp[1], kp[2], st));
+        }
         ST_CUDA(st::launch_worklist(row_mask, g.H, g.BH, g.Lq, tp.NBq, flags, work_q, cnt, st));
         ST_CUDA(st::launch_worklist(col_mask, g.H, g.BH, g.Lk, tp.NBk, flags, work_k, cnt + 1, st));
         // masked padded dual buffers (the producer bulk-copies dual windows from them): cold start
@@ -664,6 +676,11 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
             st::PhaseArgs pf = pr;
             pf.NA = fp.NA;
             pf.NSK = fp.NSK;
+            if (desc->dtype == ST_BF16 && st::bfree_tma_available() && !getenv("ST_FSTEP_NO_TMA") &&
+                st::bfree_make_tmap(&pf.tmA, Q, g.BH, g.Lrq, g.d, 128) && st::bfree_make_tmap(&pf.tmB, K, g.BH, g.Lrk, g.d, 128))
+                pf.tma = 1;  // operand tiles straight from the raw Q / K through tensor maps
+            else if (!planes)
+                return fail(ST_CUDA_ERROR, "tensor-map encode failed");
             for (long t = 1; t <= T + R; ++t) {
                 const long r = t - T;
                 float* u_out = (sv && r >= 0 && r < sl.ns) ? slot_u(r) : u_ws;
@@ -887,7 +904,7 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
     if (bf && (hook || generic_tail))
         return fail(ST_NOT_SUPPORTED,
                     "the generic tail adjoint and sequence sharding run on the stored-band kernels: set ST_FLAG_STORED_BAND");
-    const WsLayout wl = ws_layout(m, tpl, bf);
+    const WsLayout wl = ws_layout(m, tpl, bf, need_planes(desc, m, tpl, bf));
     if (workspace == nullptr || workspace_bytes < wl.bytes)
         return fail(ST_WORKSPACE_TOO_SMALL, "workspace smaller than st_workspace_bytes()");
     cudaStream_t st = (cudaStream_t)stream;
@@ -901,8 +918,9 @@ static st_status backward_impl(const st_desc* desc, const void* saved, const voi
         const bool packed = (desc->flags & ST_FLAG_REUSE_BAND) && !getenv("ST_NO_REUSE") &&
                             band_valid(workspace, Q, K, row_mask, col_mask, desc) == 3;
         st::BfBwd b{};
-        uint8_t* qp0 = (uint8_t*)(ws + wl.qp[0]);
-        uint8_t* kp0 = (uint8_t*)(ws + wl.kp[0]);
+        const bool bplanes = need_planes(desc, m, tpl, bf);
+        uint8_t* qp0 = bplanes ? (uint8_t*)(ws + wl.qp[0]) : nullptr;
+        uint8_t* kp0 = bplanes ? (uint8_t*)(ws + wl.kp[0]) : nullptr;
         uint8_t* vp0 = st::bfree_tma_available() ? nullptr : (uint8_t*)(ws + wl.vp);
         uint8_t* gp0 = st::bfree_tma_available() ? nullptr : (uint8_t*)(ws + wl.gp);
         if (!packed && !st::bfree_tma_available()) {  // with tensor maps the sweeps read the raw Q / K

@@ -812,14 +812,14 @@ EncodeTiledFn encode_fn() {  // the driver entry point through the runtime (no -
     return fn;
 }
 // [BH][Lr][d] bf16 (raw API tensor) -> boxes of 64 rows x 64 columns (128 bytes), SWIZZLE_128B, zeros past Lr
-bool make_tmap(CUtensorMap* m, const void* base, int BH, int Lr, int d) {
+bool make_tmap(CUtensorMap* m, const void* base, int BH, int Lr, int d, int box_rows = 64) {
     EncodeTiledFn fn = encode_fn();
     if (!fn || !base) return false;
     const cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)Lr, (cuuint64_t)BH};
     const cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)Lr * d * 2};
-    const cuuint32_t box[3] = {64, 64, 1}, es[3] = {1, 1, 1};
+    const cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1}, es[3] = {1, 1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1059,6 +1059,9 @@ cudaError_t backward_t(const BfGeo& g, const BfBwd& p, cudaStream_t st) {
 }  // namespace
 
 bool bfree_tma_available() { return encode_fn() != nullptr; }
+bool bfree_make_tmap(CUtensorMap* m, const void* base, int BH, int Lr, int d, int box_rows) {
+    return make_tmap(m, base, BH, Lr, d, box_rows);
+}
 
 cudaError_t launch_bfree_output(const BfGeo& g, const uint8_t* qp, const uint8_t* kp, const uint8_t* vp, const void* Qraw,
                                 const void* Kraw, const void* Vraw, const float* u, const float* v, float* vec, float* O,

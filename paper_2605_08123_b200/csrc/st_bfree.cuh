@@ -5,6 +5,7 @@
 // it) per 128-row block on the tensor cores, straight from the packed O(L d) operand planes.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -37,6 +38,8 @@ long long bfree_launch_count(bool reset);
 // true when the driver exposes cuTensorMapEncodeTiled: the V / dO streams then come straight from the raw
 // tensors through tensor maps (cp.async.bulk.tensor, SWIZZLE_128B) and vp / gp may be null
 bool bfree_tma_available();
+// tensor map of a raw [BH][Lr][d] bf16 tensor: boxes of 64 rows x 64 columns (128 bytes), SWIZZLE_128B, zero fill
+bool bfree_make_tmap(CUtensorMap* m, const void* base, int BH, int Lr, int d, int box_rows = 64);
 cudaError_t launch_bfree_output(const BfGeo& g, const uint8_t* qp, const uint8_t* kp, const uint8_t* vp, const void* Qraw,
                                 const void* Kraw, const void* Vraw, const float* u, const float* v, float* vec, float* O,
                                 cudaStream_t s);

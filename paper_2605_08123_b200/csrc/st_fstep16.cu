@@ -152,8 +152,8 @@ __device__ __forceinline__ float colsum32(float (&x)[32], int lane) {
 
 }  // namespace
 
-template <bool kFirst, bool kRecompute>
-__global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float* __restrict__ part_out) {
+template <bool kFirst, bool kRecompute, bool kTma>
+__global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(const __grid_constant__ PhaseArgs a, float* __restrict__ part_out) {
     constexpr int NE = 32 * kEW;
     constexpr int kCR = 128;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -227,8 +227,13 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float
             mbar_wait(&s.a_empty[ab], (an & 1) ^ 1);
             if (elect_one()) {
                 mbar_arrive_expect_tx(&s.a_full[ab], blk_bytes);
-                bulk_g2s(s.A + (size_t)ab * blk_bytes, a.A_pack[0] + ((size_t)b.bh * a.Lp_own + b.i0 + a.shift) * a.row_bytes,
-                         blk_bytes, &s.a_full[ab]);
+                if constexpr (kTma) {  // raw rows i0 .. i0 + 127 as [d half][128 rows][128 B] swizzled boxes
+                    for (int kb = 0; kb < a.row_bytes / 128; ++kb)  // one 128-row box per d half
+                        tma_load_3d(s.A + (size_t)ab * blk_bytes + kb * 16384, &a.tmA, kb * 64, b.i0, b.bh, &s.a_full[ab]);
+                } else {
+                    bulk_g2s(s.A + (size_t)ab * blk_bytes, a.A_pack[0] + ((size_t)b.bh * a.Lp_own + b.i0 + a.shift) * a.row_bytes,
+                             blk_bytes, &s.a_full[ab]);
+                }
             }
             __syncwarp();
             const int qstart = (b.bh == last_bh) ? max(b.q0, last_q + 1) : b.q0;
@@ -238,9 +243,15 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float
                 mbar_wait(&s.k_empty[sl], (kn & 1) ^ 1);
                 if (elect_one()) {
                     mbar_arrive_expect_tx(&s.k_full[sl], chk_bytes);
-                    bulk_g2s(s.K + (size_t)sl * chk_bytes,
-                             a.B_pack[0] + ((size_t)b.bh * a.Lp_other + (size_t)q * kCR) * a.row_bytes, chk_bytes,
-                             &s.k_full[sl]);
+                    if constexpr (kTma) {  // chunk q = raw rows q * 128 - shift .. (out-of-range rows arrive as zeros)
+                        for (int kb = 0; kb < a.row_bytes / 128; ++kb)
+                            tma_load_3d(s.K + (size_t)sl * chk_bytes + kb * 16384, &a.tmB, kb * 64, q * kCR - a.shift, b.bh,
+                                        &s.k_full[sl]);
+                    } else {
+                        bulk_g2s(s.K + (size_t)sl * chk_bytes,
+                                 a.B_pack[0] + ((size_t)b.bh * a.Lp_other + (size_t)q * kCR) * a.row_bytes, chk_bytes,
+                                 &s.k_full[sl]);
+                    }
                 }
                 __syncwarp();
                 ++kseq;
@@ -263,7 +274,8 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float
             const uint32_t an = (gi - g_begin) / a.NA;
             mbar_wait(&s.a_full[ab], an & 1);
             tc_fence_after();
-            const uint64_t ad0 = make_desc(smem_u32(s.A + (size_t)ab * blk_bytes), 128, sbo);
+            const uint32_t as_ = smem_u32(s.A + (size_t)ab * blk_bytes);
+            const uint64_t ad0 = make_desc(as_, 128, sbo);
             const bool same = have && b.bh == last_bh;
             const int new_start = same ? max(b.q0, last_q + 1) : b.q0;
             const uint32_t next_seq = have ? last_seq + 1 : 0;
@@ -287,11 +299,12 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float
                     if (ok) ng = 2;
                 }
                 uint64_t bd[2];
-                uint32_t dt[2];
+                uint32_t dt[2], bs_[2];
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     const uint32_t sq = seq_of(q + c);
-                    bd[c] = make_desc(smem_u32(s.K + (size_t)(sq % a.NSK) * chk_bytes), 128, sbo);
+                    bs_[c] = smem_u32(s.K + (size_t)(sq % a.NSK) * chk_bytes);
+                    bd[c] = make_desc(bs_[c], 128, sbo);
                     dt[c] = tbase + (uint32_t)(((tseq + c) % NST) * kCR);
                 }
                 tc_fence_after();
@@ -299,8 +312,15 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(PhaseArgs a, float
                     for (int kk = 0; kk < ksteps; ++kk) {
 #pragma unroll
                         for (int c = 0; c < 2; ++c)
-                            if (c < ng && (kk == 0 || !(a.dbg & 2)))
-                                mma_bf16(dt[c], ad0 + (uint64_t)(kk * 16), bd[c] + (uint64_t)(kk * 16), idesc, kk > 0);
+                            if (c < ng && (kk == 0 || !(a.dbg & 2))) {
+                                if constexpr (kTma) {  // 128B-swizzled tiles: d half kk / 4, 32 bytes per K step inside the row
+                                    const uint32_t ko = (uint32_t)((kk >> 2) * 16384 + (kk & 3) * 32);
+                                    mma_bf16(dt[c], make_desc_sw128(as_ + ko, 16, 1024), make_desc_sw128(bs_[c] + ko, 16, 1024), idesc,
+                                             kk > 0);
+                                } else {
+                                    mma_bf16(dt[c], ad0 + (uint64_t)(kk * 16), bd[c] + (uint64_t)(kk * 16), idesc, kk > 0);
+                                }
+                            }
                     }
 #pragma unroll
                     for (int c = 0; c < 2; ++c)
@@ -876,10 +896,10 @@ size_t fstep16_smem_bytes(const PhaseArgs& a) {
            (size_t)(2 * kNV + 2 * a.NA + 2 * a.NSK + 2 * nst) * 8 + 16 + (size_t)a.wl_cap * 16;
 }
 
-template <bool kFirst, bool kRec>
+template <bool kFirst, bool kRec, bool kTma>
 static cudaError_t launch_fstep16_t(const PhaseArgs& a, float* part, int grid, cudaStream_t s) {
     const size_t smem = fstep16_smem_bytes(a);
-    auto k = k_fstep16<kFirst, kRec>;
+    auto k = k_fstep16<kFirst, kRec, kTma>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k<<<grid, 64 + 32 * kEW, smem, s>>>(a, part);
@@ -890,8 +910,12 @@ static cudaError_t launch_fstep16_t(const PhaseArgs& a, float* part, int grid, c
 cudaError_t launch_fstep16(const PhaseArgs& a, float* part, bool first, int grid, cudaStream_t s) {
     static const bool rec = getenv("ST_FSTEP_RECOMPUTE") != nullptr;
     if (a.npl != 1 || a.CR != 128 || a.dustbin) return cudaErrorNotSupported;
-    if (first) return rec ? launch_fstep16_t<true, true>(a, part, grid, s) : launch_fstep16_t<true, false>(a, part, grid, s);
-    return rec ? launch_fstep16_t<false, true>(a, part, grid, s) : launch_fstep16_t<false, false>(a, part, grid, s);
+    if (a.tma) {  // operand tiles through tensor maps (no packed planes)
+        if (first) return rec ? launch_fstep16_t<true, true, true>(a, part, grid, s) : launch_fstep16_t<true, false, true>(a, part, grid, s);
+        return rec ? launch_fstep16_t<false, true, true>(a, part, grid, s) : launch_fstep16_t<false, false, true>(a, part, grid, s);
+    }
+    if (first) return rec ? launch_fstep16_t<true, true, false>(a, part, grid, s) : launch_fstep16_t<true, false, false>(a, part, grid, s);
+    return rec ? launch_fstep16_t<false, true, false>(a, part, grid, s) : launch_fstep16_t<false, false, false>(a, part, grid, s);
 }
 
 cudaError_t launch_vmerge(const float* part, float* pad_v, float* v_out, int BH, int H, int Lq, int Lk, int Lrk, int NB,

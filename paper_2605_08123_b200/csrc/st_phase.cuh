@@ -1,6 +1,7 @@
 // st_phase.cuh -- host interface of the tcgen05 half-step kernels (st_phase.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -8,7 +9,11 @@ namespace st {
 
 // One half-step.  "own" = the side whose dual is updated (rows of the MMA
 // tile, one TMEM lane each); "other" = the window side (MMA N dimension).
-struct PhaseArgs {
+struct alignas(64) PhaseArgs {
+    // tensor maps of the raw [BH][L][d] bf16 tensors of the own / other side (tma = 1: the operand tiles are
+    // loaded from them as 64-row x 128-byte SWIZZLE_128B boxes and no packed plane is read)
+    CUtensorMap tmA, tmB;
+    int tma;
     int npl;            // operand planes: 1 (bf16 inputs) or 3 (fp32 inputs split into bf16 hi/mid/lo)
     int CR;             // window chunk rows = MMA N (64 or 128)
     int shift;          // packed row = row + shift: aligns the chunk grid with every band window
