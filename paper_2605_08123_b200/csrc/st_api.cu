@@ -315,7 +315,10 @@ bool bfree_plan(const st_desc* d, const Dims& m, const TcPlan& tp) {
 // the packed planes are still read unless the problem is band-free, the full-step solve runs it and the
 // driver provides tensor maps
 bool need_planes(const st_desc* d, const Dims& m, const TcPlan& tp, bool bf) {
-    return !(bf && st::bfree_tma_available() && fstep_plan(d, tp, m).ok && !getenv("ST_FSTEP_NO_TMA"));
+    (void)d;
+    (void)m;
+    (void)tp;
+    return !(bf && st::bfree_tma_available() && !getenv("ST_FSTEP_NO_TMA"));
 }
 
 WsLayout ws_layout(const Dims& m, const TcPlan& tp, bool bf, bool planes = true) {
@@ -695,6 +698,12 @@ static st_status forward_impl(const st_desc* desc, const void* Q, const void* K,
                 u_prev = u_out;
                 v_prev = v_out;
             }
+        }
+        if (!fp.ok && !planes) {  // half-step kernels: operand tiles through tensor maps (own side 128-row boxes)
+            if (!(st::bfree_make_tmap(&pr.tmA, Q, g.BH, g.Lrq, g.d, 128) && st::bfree_make_tmap(&pr.tmB, K, g.BH, g.Lrk, g.d, tp.CR) &&
+                  st::bfree_make_tmap(&pc.tmA, K, g.BH, g.Lrk, g.d, 128) && st::bfree_make_tmap(&pc.tmB, Q, g.BH, g.Lrq, g.d, tp.CR)))
+                return fail(ST_CUDA_ERROR, "tensor-map encode failed");
+            pr.tma = pc.tma = 1;
         }
         for (long t = 1; !fp.ok && t <= T + R; ++t) {
             const long r = t - T;

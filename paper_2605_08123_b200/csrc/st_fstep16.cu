@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(const __grid_const
             tc_fence_after();
             const uint32_t as_ = smem_u32(s.A + (size_t)ab * blk_bytes);
             const uint64_t ad0 = make_desc(as_, 128, sbo);
+            const uint64_t ad_sw = make_desc_sw128(as_, 16, 1024);
             const bool same = have && b.bh == last_bh;
             const int new_start = same ? max(b.q0, last_q + 1) : b.q0;
             const uint32_t next_seq = have ? last_seq + 1 : 0;
@@ -298,13 +299,14 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(const __grid_const
                     ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
                     if (ok) ng = 2;
                 }
-                uint64_t bd[2];
+                uint64_t bd[2], bd_sw[2];
                 uint32_t dt[2], bs_[2];
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     const uint32_t sq = seq_of(q + c);
                     bs_[c] = smem_u32(s.K + (size_t)(sq % a.NSK) * chk_bytes);
                     bd[c] = make_desc(bs_[c], 128, sbo);
+                    bd_sw[c] = make_desc_sw128(bs_[c], 16, 1024);
                     dt[c] = tbase + (uint32_t)(((tseq + c) % NST) * kCR);
                 }
                 tc_fence_after();
@@ -314,9 +316,8 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_fstep16(const __grid_const
                         for (int c = 0; c < 2; ++c)
                             if (c < ng && (kk == 0 || !(a.dbg & 2))) {
                                 if constexpr (kTma) {  // 128B-swizzled tiles: d half kk / 4, 32 bytes per K step inside the row
-                                    const uint32_t ko = (uint32_t)((kk >> 2) * 16384 + (kk & 3) * 32);
-                                    mma_bf16(dt[c], make_desc_sw128(as_ + ko, 16, 1024), make_desc_sw128(bs_[c] + ko, 16, 1024), idesc,
-                                             kk > 0);
+                                    const uint64_t ko = (uint64_t)((kk >> 2) * 1024 + (kk & 3) * 2);  // 16-byte units
+                                    mma_bf16(dt[c], ad_sw + ko, bd_sw[c] + ko, idesc, kk > 0);
                                 } else {
                                     mma_bf16(dt[c], ad0 + (uint64_t)(kk * 16), bd[c] + (uint64_t)(kk * 16), idesc, kk > 0);
                                 }

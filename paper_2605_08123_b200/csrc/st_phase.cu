@@ -116,8 +116,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // kWrite = 0: the half-step.  kWrite = 1 / 2: the same tiles written out as the stored score band
 // (s2 = q.k c2, -inf off the support) / cotangent band (dO.v, 0 off the support) of the own side,
 // [BH][band_ld][Wf] (the transposed band from the column geometry); activity from the padded duals.
-template <int kNPL, int kCR, bool kFirst, int kEW, int kWrite = 0>
-__global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
+// kTma: the operand tiles come from the raw tensors through tensor maps (128B-swizzled boxes) instead of
+// the packed planes (bf16, one plane).
+template <int kNPL, int kCR, bool kFirst, int kEW, int kWrite = 0, bool kTma = false>
+__global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(const __grid_constant__ PhaseArgs a) {
     constexpr int kParts = kEW / 4;         // epilogue warps per TMEM lane quadrant (column parts)
     constexpr int NE = 32 * kEW;            // epilogue threads
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -188,11 +190,16 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
             if (elect_one()) {
                 ST_TRACE(1 + min(gi - g_begin, 7));
                 mbar_arrive_expect_tx(&s.a_full[ab], blk_bytes * kNPL);
+                if constexpr (kTma) {  // raw rows i0 .. i0 + 127: one 128-row swizzled box per d half
+                    for (int kb = 0; kb < a.row_bytes / 128; ++kb)
+                        tma_load_3d(s.A + (size_t)ab * blk_bytes + kb * 16384, &a.tmA, kb * 64, b.i0, b.bh, &s.a_full[ab]);
+                } else {
 #pragma unroll
-                for (int p = 0; p < kNPL; ++p)
-                    bulk_g2s(s.A + ((size_t)ab * kNPL + p) * blk_bytes,
-                             a.A_pack[p] + ((size_t)b.bh * a.Lp_own + b.i0 + a.shift) * a.row_bytes, blk_bytes,
-                             &s.a_full[ab]);
+                    for (int p = 0; p < kNPL; ++p)
+                        bulk_g2s(s.A + ((size_t)ab * kNPL + p) * blk_bytes,
+                                 a.A_pack[p] + ((size_t)b.bh * a.Lp_own + b.i0 + a.shift) * a.row_bytes, blk_bytes,
+                                 &s.a_full[ab]);
+                }
             }
             __syncwarp();
             const int qstart = (b.bh == last_bh) ? max(b.q0, last_q + 1) : b.q0;
@@ -202,11 +209,17 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
                 mbar_wait(&s.k_empty[sl], (kn & 1) ^ 1);
                 if (elect_one()) {
                     mbar_arrive_expect_tx(&s.k_full[sl], chk_bytes * kNPL);
+                    if constexpr (kTma) {  // chunk q = raw rows q * kCR - shift .. (zeros outside the tensor)
+                        for (int kb = 0; kb < a.row_bytes / 128; ++kb)
+                            tma_load_3d(s.K + (size_t)sl * chk_bytes + kb * (kCR * 128), &a.tmB, kb * 64, q * kCR - a.shift, b.bh,
+                                        &s.k_full[sl]);
+                    } else {
 #pragma unroll
-                    for (int p = 0; p < kNPL; ++p)
-                        bulk_g2s(s.K + ((size_t)sl * kNPL + p) * chk_bytes,
-                                 a.B_pack[p] + ((size_t)b.bh * a.Lp_other + (size_t)q * kCR) * a.row_bytes, chk_bytes,
-                                 &s.k_full[sl]);
+                        for (int p = 0; p < kNPL; ++p)
+                            bulk_g2s(s.K + ((size_t)sl * kNPL + p) * chk_bytes,
+                                     a.B_pack[p] + ((size_t)b.bh * a.Lp_other + (size_t)q * kCR) * a.row_bytes, chk_bytes,
+                                     &s.k_full[sl]);
+                    }
                 }
                 __syncwarp();
                 ++kseq;
@@ -236,15 +249,17 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
             mbar_wait(&s.a_full[ab], an & 1);
             if (lane == 0) ST_TRACE(9 + min(gi - g_begin, 7));
             tc_fence_after();
-            const uint64_t ad0 = make_desc(smem_u32(s.A + (size_t)ab * kNPL * blk_bytes), 128, sbo);
+            const uint32_t as_ = smem_u32(s.A + (size_t)ab * kNPL * blk_bytes);
+            const uint64_t ad0 = make_desc(as_, 128, sbo);
+            const uint64_t ad_sw = make_desc_sw128(as_, 16, 1024);
             const bool same = have && b.bh == last_bh;
             const int new_start = same ? max(b.q0, last_q + 1) : b.q0;
             const uint32_t next_seq = have ? last_seq + 1 : 0;
             constexpr int kG = 2;  // chunks per MMA group (independent accumulators)
             for (int q0 = b.q0; q0 <= b.q1; q0 += kG) {
                 const int ng = min(kG, b.q1 - q0 + 1);
-                uint64_t bd[kG];
-                uint32_t dt[kG];
+                uint64_t bd[kG], bd_sw[kG];
+                uint32_t dt[kG], bs_[kG];
 #pragma unroll
                 for (int c = 0; c < kG; ++c) {
                     if (c < ng) {
@@ -255,7 +270,9 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
                         mbar_wait(&s.k_full[sl], (seq / a.NSK) & 1);
                         const uint32_t tq = tseq + c;
                         mbar_wait(&s.t_empty[tq % NST], ((tq / NST) & 1) ^ 1);
-                        bd[c] = make_desc(smem_u32(s.K + (size_t)sl * kNPL * chk_bytes), 128, sbo);
+                        bs_[c] = smem_u32(s.K + (size_t)sl * kNPL * chk_bytes);
+                        bd[c] = make_desc(bs_[c], 128, sbo);
+                        bd_sw[c] = make_desc_sw128(bs_[c], 16, 1024);
                         dt[c] = tbase + (uint32_t)((tq % NST) * kCR);
                     }
                 }
@@ -267,9 +284,14 @@ __global__ void __launch_bounds__(64 + 32 * kEW, 1) k_phase(PhaseArgs a) {
                             const uint64_t adk = ad0 + (uint64_t)pa_[pr] * a_plane + (uint64_t)(kk * 16);
 #pragma unroll
                             for (int c = 0; c < kG; ++c)
-                                if (c < ng)
-                                    mma_bf16(dt[c], adk, bd[c] + (uint64_t)pb_[pr] * b_plane + (uint64_t)(kk * 16),
-                                             idesc, (pr | kk) > 0);
+                                if (c < ng) {
+                                    if constexpr (kTma)  // swizzled tiles: d half kk / 4, 32 bytes per K step inside the row
+                                        mma_bf16(dt[c], ad_sw + (uint64_t)((kk >> 2) * 1024 + (kk & 3) * 2),
+                                                 bd_sw[c] + (uint64_t)((kk >> 2) * (kCR * 8) + (kk & 3) * 2), idesc, kk > 0);
+                                    else
+                                        mma_bf16(dt[c], adk, bd[c] + (uint64_t)pb_[pr] * b_plane + (uint64_t)(kk * 16),
+                                                 idesc, (pr | kk) > 0);
+                                }
                         }
 #pragma unroll
                     for (int c = 0; c < kG; ++c)
@@ -687,6 +709,7 @@ template <int kNPL, int kCR, int kEW>
 static cudaError_t launch_phase_t(const PhaseArgs& a, bool first, int grid, cudaStream_t s) {
     const size_t smem = phase_smem_bytes(a);
     auto k = first ? k_phase<kNPL, kCR, true, kEW> : k_phase<kNPL, kCR, false, kEW>;
+    if (kNPL == 1 && a.tma) k = first ? k_phase<kNPL, kCR, true, kEW, 0, kNPL == 1> : k_phase<kNPL, kCR, false, kEW, 0, kNPL == 1>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k<<<grid, 64 + 32 * kEW, smem, s>>>(a);
