@@ -97,7 +97,8 @@ typedef struct st_desc {
 /* bf16 problems whose band lines up with 64-column chunks (no dustbin, seq_q == seq_k, half_band a
  * multiple of 128, head_dim 64 or 128 -- BASELINE configs 4 and 5) run band-free by default: the
  * transport output and the R=2 backward recompute their score / cotangent tiles on the tensor cores
- * and st_workspace_bytes() is O(L d), with no L x W band.  ST_FLAG_STORED_BAND selects the
+ * and st_workspace_bytes() is O(L): no L x W band and (with a driver that provides
+ * tensor maps) no packed O(L d) operand plane either.  ST_FLAG_STORED_BAND selects the
  * stored-band kernels (and their O(L W) workspace) instead; mode ST_GENERIC_TAIL and the *_halo
  * entry points need it on such problems and return ST_NOT_SUPPORTED without it. */
 #define ST_FLAG_STORED_BAND 4

@@ -6,7 +6,8 @@
 // One kernel, k_bsweep<MODE>, streams the band of a 128-row block ("own" side, one TMEM lane
 // per row) through its 64-column window chunks ("other" side):
 //   tile   S_c = A1_blk B1_c^T  (and Z_c = A2_blk B2_c^T where the stage needs the cotangent
-//          tile) on tcgen05 (kind::f16, fp32 accumulation in TMEM) from the packed operand planes
+//          tile) on tcgen05 (kind::f16, fp32 accumulation in TMEM); the operand tiles are tensor-map
+//          TMA boxes of the raw [B, H, L, d] tensors (128B-swizzled), or packed planes as a fallback
 //   cell   p = ex2(c2 S + a_i + b_j) on the band (a, b = -inf padded duals), then per stage
 //            PV    weight = p                      -> Y += W X_c       (O = P V; dV = P^T dO, g_v)
 //            R12   acc_i += p (z - g_v_j)                              (u2_bar)
@@ -19,7 +20,7 @@
 //          core matrices), so Y[128][d] (+)= W X_c is two tcgen05.mma per 16 window columns into a
 //          TMEM accumulator -- no SMEM staging of the weights.
 // Column stages are the same kernel on the transposed geometry (own = keys: A1 = K, B1 = Q).
-// Nothing of size L x W is written or read: HBM holds the packed planes (O(L d)), the padded
+// Nothing of size L x W is written or read: beyond the caller's tensors HBM holds only the padded
 // dual / cotangent vectors (O(L)) and the outputs.
 //
 // Roles (persistent CTA, one per SM):

@@ -247,6 +247,18 @@ def test_deterministic_and_linear_in_G():
         assert rel(r3[k], 0.5 * r1[k] - 2.0 * r2[k]) < 1e-5, k
 
 
+def test_bf16_workspace_is_O_of_L():
+    """With a GPU driver (tensor maps available) BASELINE configs 4 / 5 need only O(L) scratch: no L x W band
+    and no packed O(L d) operand plane (north_star: "O(L d) inputs plus O(L) extra HBM")."""
+    for cid in (4, 5):
+        cfg = configs.CONFIGS[cid]
+        spec = band.BandSpec(batch=cfg.B, heads=cfg.H, seq_q=cfg.L, seq_k=cfg.L, head_dim=cfg.d, half_band=cfg.w,
+                             base_depth=cfg.T, tail_depth=cfg.R, epsilon=cfg.eps, dtype=cfg.dtype)
+        per_row = spec.workspace_bytes() / (cfg.B * cfg.H * cfg.L)
+        one_plane = cfg.d * 2
+        assert per_row < 48 * 4 and per_row < 1.5 * one_plane, (cid, per_row)  # ~37 fp32 words per row; < 1.5 planes
+
+
 def test_bf16_band_free_deterministic_and_linear_in_G():
     """The band-free sweeps are run-to-run bit-identical (fixed-order row-part combines, no atomics on the
     data path) and the adjoint is linear in the output cotangent (config-4 geometry, several blocks per CTA)."""
