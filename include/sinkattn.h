@@ -95,7 +95,7 @@ typedef struct st_desc {
  * or Q/K in between.  Otherwise the band is recomputed. */
 #define ST_FLAG_REUSE_BAND 2
 /* bf16 problems whose band lines up with 64-column chunks (no dustbin, seq_q == seq_k, half_band a
- * multiple of 128, head_dim 64 or 128 -- BASELINE configs 4 and 5) run band-free by default: the
+ * multiple of 64, head_dim 64 or 128 -- BASELINE configs 4 and 5) run band-free by default: the
  * transport output and the R=2 backward recompute their score / cotangent tiles on the tensor cores
  * and st_workspace_bytes() is O(L): no L x W band and (with a driver that provides
  * tensor maps) no packed O(L d) operand plane either.  ST_FLAG_STORED_BAND selects the

@@ -305,7 +305,9 @@ void fstep_trace_dump(const unsigned long long* dbuf) {
 // lines up with every band window; square problems, no dustbin.  ST_FLAG_STORED_BAND keeps the
 // stored-band kernels (generic-R tail adjoint, base_solve_vjp and the sequence-sharded variants need them).
 bool bfree_plan(const st_desc* d, const Dims& m, const TcPlan& tp) {
-    if (!tp.ok || tp.npl != 1 || tp.shift != 0 || m.Lq != m.Lk) return false;
+    if (!tp.ok || tp.npl != 1 || m.Lq != m.Lk) return false;
+    // packed planes carry the solve's row shift (half_band % 128); tensor-map boxes take it as a coordinate
+    if (tp.shift != 0 && (!st::bfree_tma_available() || getenv("ST_FSTEP_NO_TMA") || getenv("ST_BF_NO_TMA"))) return false;
     if (d->flags & (ST_FLAG_GENERIC | ST_FLAG_STORED_BAND)) return false;
     return st::bfree_supported((int)m.d, (int)m.w, d->dustbin, m.esz);
 }

@@ -786,7 +786,7 @@ long long bfree_launch_count(bool reset) {
 bool bfree_supported(int d, int w, int dustbin, int esz) {
     static const bool off = getenv("ST_NO_BFREE") != nullptr;
     if (off) return false;
-    return esz == 2 && !dustbin && (d == 64 || d == 128) && w >= 128 && w % 128 == 0;
+    return esz == 2 && !dustbin && (d == 64 || d == 128) && w >= 64 && w % kCR == 0;
 }
 
 namespace {

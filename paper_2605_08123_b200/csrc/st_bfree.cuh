@@ -11,7 +11,7 @@
 
 namespace st {
 
-// Geometry of the band-free path (bf16 planes, no dustbin, w a multiple of 128: the packed planes of the solve carry no row shift).
+// Geometry of the band-free path (bf16 planes, no dustbin, w a multiple of 64).
 struct BfGeo {
     int BH, H;
     int Lq, Lk, Lrq, Lrk;   // rows / columns; strides of the API tensors

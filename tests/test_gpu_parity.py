@@ -189,6 +189,8 @@ def test_bf16_stored_band_kernels_parity(cid, L, mode):
                                              (256, 64, "uniform_len", 1500, "one_reference"),
                                              (256, 64, "none", 1100, "direct_four_plan"),
                                              (128, 64, "uniform_len", 650, "one_reference"),
+                                             (64, 64, "uniform_len", 650, "one_reference"),
+                                             (192, 128, "none", 900, "direct_four_plan"),
                                              (256, 128, "none", 300, "one_reference")])
 def test_bf16_band_free_sweeps_parity(w, d, mask, L, mode):
     """The band-free tcgen05 sweeps (st_bfree.cu: transport output, C1 / R12 / C3 / R4 / R6 / C6 with the
